@@ -1,0 +1,665 @@
+/*
+ * lapssd_oracle.c -- plain, slow, sequential CPU ORACLE for the LAPS-SD
+ * batched speculative-decoding step (arXiv 2505.17074).
+ *
+ * TEST INFRASTRUCTURE.  See lapssd_oracle.h for who may call it and which pin
+ * fixes each function.  Nothing here is shared with the CUDA path.
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fPIC -shared (no -ffast-math):
+ * every float/double operation below is one IEEE round-to-nearest operation in
+ * the written order, so results are reproducible bit for bit.
+ *
+ * Notation (PAPER.md, with the letters of BASELINE.json north_star, AMB-1):
+ *   p = target (LLM) distribution, q = draft (SSM) distribution,
+ *   k = drafts per round (the paper's n), r = first rejected position,
+ *   L_i = output length, A_i = predicted acceptance rate, E_i = attained
+ *   service, T~_i = estimated execution time (Eq. 6),
+ *   K queues with thresholds S_j^up = M^{j-1} S_1^up, gamma/delta.
+ */
+#include "lapssd_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef unsigned __int128 u128;
+
+/* ------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11; Random123 reference).  */
+/* ------------------------------------------------------------------------ */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int round = 0; round < 10; round++) {
+        if (round > 0) {                 /* key schedule: bump before rounds 2..10 */
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t prod0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t prod1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(prod0 >> 32), lo0 = (uint32_t)prod0;
+        uint32_t hi1 = (uint32_t)(prod1 >> 32), lo1 = (uint32_t)prod1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Counter layout (AMB-21): c0 = request id, c1 = round, c2 = (tag << 8) | block,
+ * c3 = trace; key = (seed low 32, seed high 32).  tag 0 = acceptance uniforms,
+ * tag 1 = the 64-bit sampling uniform. */
+static void draw(uint64_t seed, uint32_t req_id, uint32_t round_idx, uint32_t tag,
+                 uint32_t block, uint32_t trace, uint32_t out[4])
+{
+    uint32_t ctr[4] = { req_id, round_idx, (tag << 8) | block, trace };
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    orc_philox4x32_10(ctr, key, out);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Reading one stored probability.                                          */
+/* ------------------------------------------------------------------------ */
+static float load_prob(const void *rows, int32_t dtype, int64_t idx)
+{
+    if (dtype == ORC_BF16) {
+        uint16_t b = ((const uint16_t *)rows)[idx];
+        uint32_t bits = (uint32_t)b << 16;          /* bf16 is the top half of fp32 */
+        float f;
+        memcpy(&f, &bits, sizeof f);
+        return f;
+    }
+    return ((const float *)rows)[idx];
+}
+
+/* Q4.60 residual mass of one vocabulary entry (AMB-2, AMB-27):
+ *   R = floor( max(0, fl32(p - q)) * 2^60 ).
+ * The difference is taken in fp32 (the kernel's precision), the scaling by 2^60
+ * and the truncation are exact in fp64. */
+static uint64_t q460(float p, float q)
+{
+    float d = p - q;                                 /* one fp32 RN subtraction */
+    if (!(d > 0.0f)) return 0;
+    double x = (double)d * 0x1p60;                   /* exact: power-of-two scale */
+    if (x >= 0x1p64) return UINT64_MAX;
+    return (uint64_t)x;                              /* truncation = floor (x >= 0) */
+}
+
+/* ------------------------------------------------------------------------ */
+/* (1) Verification, P:57-64 (Eq. 1 with p/q as in north_star).      */
+/* ------------------------------------------------------------------------ */
+int32_t orc_verify_request(const void *p_rows, const void *q_rows, int32_t dtype,
+                           int64_t V, int32_t k, const int32_t *draft,
+                           uint32_t req_id, uint32_t round_idx, uint64_t seed,
+                           uint32_t trace, int32_t *tokens, orc_verify_out *out)
+{
+    /* Step 1: sequential acceptance test, stop at the first rejection.
+     * Draft x_j is accepted with probability min(1, p_j(x_j) / q_j(x_j)):
+     * u_j = u24 / 2^24 and accept iff u_j < p/q, evaluated as u24*q < p*2^24,
+     * which is exact in fp64 (24-bit integer times 24-bit significand). */
+    int32_t r = k;
+    for (int32_t j = 0; j < k; j++) {
+        uint32_t u4[4];
+        draw(seed, req_id, round_idx, 0, (uint32_t)(j / 4), trace, u4);
+        uint32_t u24 = u4[j % 4] >> 8;
+        int32_t x = draft[j];
+        float pj = load_prob(p_rows, dtype, (int64_t)j * V + x);
+        float qj = load_prob(q_rows, dtype, (int64_t)j * V + x);
+        int accept = (double)u24 * (double)qj < (double)pj * 16777216.0;
+        if (!accept) { r = j; break; }
+    }
+
+    /* Step 2: the distribution of the token emitted at position r.
+     * r < k: residual norm(max(0, p_r - q_r)) over the full vocabulary.
+     * r = k: the bonus token from the (k+1)-th target row p_k.      */
+    const int64_t p_off = (int64_t)r * V;
+    const int64_t q_off = (int64_t)r * V;
+    int use_q = (r < k);
+    u128 Z = 0;
+    long double z_real = 0.0L;
+    for (int64_t v = 0; v < V; v++) {
+        float p = load_prob(p_rows, dtype, p_off + v);
+        float q = use_q ? load_prob(q_rows, dtype, q_off + v) : 0.0f;
+        Z += q460(p, q);
+        long double d = (long double)p - (long double)q;
+        if (d > 0) z_real += d;
+    }
+    int fallback = 0, invalid = 0;
+    if (Z == 0 && use_q) {                /* AMB-20: no residual mass -> sample p_r */
+        fallback = 1;
+        use_q = 0;
+        z_real = 0.0L;
+        for (int64_t v = 0; v < V; v++) {
+            float p = load_prob(p_rows, dtype, p_off + v);
+            Z += q460(p, 0.0f);
+            if (p > 0) z_real += (long double)p;
+        }
+    }
+
+    /* Step 3: inverse-CDF sample.  U is a 64-bit Philox uniform,
+     * t = floor(U * Z / 2^64) in [0, Z), y = min{ v : sum_{w<=v} R_w > t }. */
+    uint32_t u4[4];
+    draw(seed, req_id, round_idx, 1, 0, trace, u4);
+    uint64_t U = ((uint64_t)u4[0] << 32) | u4[1];
+    int32_t y;
+    uint64_t t = 0;
+    double margin = 0.0;
+    if (Z == 0) {
+        invalid = 1;                       /* cannot happen for probability rows */
+        y = (r < k) ? draft[r] : 0;
+    } else {
+        t = (uint64_t)(((u128)U * Z) >> 64);
+        u128 c = 0;
+        y = (int32_t)(V - 1);
+        for (int64_t v = 0; v < V; v++) {
+            float p = load_prob(p_rows, dtype, p_off + v);
+            float q = use_q ? load_prob(q_rows, dtype, q_off + v) : 0.0f;
+            uint64_t Rv = q460(p, q);
+            if (c + Rv > t) {
+                y = (int32_t)v;
+                u128 lo = t - c, hi = c + Rv - t;     /* distance to both edges */
+                u128 m = lo < hi ? lo : hi;
+                margin = (double)m / (double)Z;
+                break;
+            }
+            c += Rv;
+        }
+    }
+
+    for (int32_t j = 0; j < r; j++) tokens[j] = draft[j];
+    tokens[r] = y;
+    for (int32_t j = r + 1; j <= k; j++) tokens[j] = -1;
+
+    if (out) {
+        out->r = r;
+        out->y = y;
+        out->fallback = fallback;
+        out->invalid = invalid;
+        out->Z = (uint64_t)Z;
+        out->t = t;
+        out->z_real = (double)z_real;
+        double zq = (double)(uint64_t)Z * 0x1p-60;
+        out->z_rel_err = z_real > 0 ? fabs(zq - (double)z_real) / (double)z_real : 0.0;
+        out->margin_rel = margin;
+    }
+    return r;
+}
+
+/* Many independent trials of the same rows (statistical pins): trial i uses
+ * drafts[i*k..], request id req_ids[i] and round rounds[i]. */
+void orc_verify_many(const void *p_rows, const void *q_rows, int32_t dtype, int64_t V,
+                     int32_t k, int32_t n_trials, const int32_t *drafts,
+                     const uint32_t *req_ids, const uint32_t *rounds, uint64_t seed,
+                     int32_t *tokens_out, int32_t *r_out)
+{
+    for (int32_t i = 0; i < n_trials; i++)
+        r_out[i] = orc_verify_request(p_rows, q_rows, dtype, V, k, drafts + (size_t)i * k,
+                                      req_ids[i], rounds[i], seed, 0,
+                                      tokens_out + (size_t)i * (k + 1), NULL);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Scheduler pieces.                                                         */
+/* ------------------------------------------------------------------------ */
+
+/* S_j^up = M^{j-1} * S_1^up.  Queue 1 holds [0, S_1^up), queue j holds
+ * [S_{j-1}^up, S_j^up), queue K is unbounded (AMB-11).  Zero-based here:
+ * S_up[j] = floor(s1_up * M^j) for j = 0..K-2, M^j by iterative multiply. */
+int32_t orc_thresholds(int32_t K, int64_t s1_up_us, double M, int64_t *S_up_out)
+{
+    if (K < 1 || K > 16 || s1_up_us <= 0 || !(M > 1.0)) return -1;
+    double m = 1.0;
+    for (int32_t j = 0; j < K - 1; j++) {
+        double s = (double)s1_up_us * m;
+        S_up_out[j] = s >= 9.2e18 ? INT64_MAX : (int64_t)floor(s);
+        m = m * M;
+    }
+    return 0;
+}
+
+/* Index of the queue whose interval contains x (0-based). */
+static int32_t level_of(const int64_t *S_up, int32_t K, int64_t x)
+{
+    int32_t lev = 0;
+    while (lev < K - 1 && x >= S_up[lev]) lev++;
+    return lev;
+}
+
+/* Eq. (6): T~ = n L T_SSM/(nA+1) + L T_LLM/(nA+1), evaluated as
+ * floor( (L * (k T_SSM + T_LLM)) / (k A + 1) ) in fp64, in this order (AMB-10). */
+uint64_t orc_eq6(int64_t L, double A, int32_t k, int64_t t_ssm_us, int64_t t_llm_us)
+{
+    double c_round = (double)((int64_t)k * t_ssm_us + t_llm_us);
+    double num = (double)L * c_round;
+    double den = (double)k * A + 1.0;
+    double T = num / den;
+    if (!(T > 0.0)) return 0;
+    if (T >= 1.8e19) return UINT64_MAX;
+    return (uint64_t)T;                              /* floor, T >= 0 */
+}
+
+struct orc_sim {
+    orc_config cfg;
+    int32_t n, rank, world;
+    uint32_t trace;
+    int64_t *arrival;
+    int32_t *L_true, *L_pred;
+    int64_t S_up[16];
+    int64_t c_round;
+    /* state, one entry per local request */
+    int32_t *acc_tok, *acc_draft, *rounds, *ring;
+    int64_t *E, *T_total, *C, *x;
+    uint8_t *admitted, *done, *perceptible, *pinned, *level, *running;
+    double *A;
+    uint64_t *key;
+    int64_t now;
+    int32_t cursor, prev_count;
+    /* scratch */
+    int32_t *order;
+};
+
+orc_sim *orc_sim_create(const orc_config *cfg, int32_t n_local, const int64_t *arrival_us,
+                        const int32_t *L_true, const int32_t *L_pred,
+                        int32_t rank, int32_t world)
+{
+    if (cfg->K < 1 || cfg->K > 16 || cfg->gamma < 2 || !(cfg->delta >= 0.0) ||
+        cfg->k < 1 || cfg->k > 16 || n_local < 0 || world < 1 || rank < 0 || rank >= world)
+        return NULL;
+    orc_sim *s = (orc_sim *)calloc(1, sizeof *s);
+    s->cfg = *cfg;
+    s->n = n_local; s->rank = rank; s->world = world;
+    if (orc_thresholds(cfg->K, cfg->s1_up_us, cfg->M, s->S_up) != 0) { free(s); return NULL; }
+    s->c_round = (int64_t)cfg->k * cfg->t_ssm_us + cfg->t_llm_us;
+    size_t n = (size_t)(n_local > 0 ? n_local : 1);
+    s->arrival = (int64_t *)malloc(n * sizeof(int64_t));
+    s->L_true = (int32_t *)malloc(n * sizeof(int32_t));
+    s->L_pred = (int32_t *)malloc(n * sizeof(int32_t));
+    if (n_local > 0) {
+        memcpy(s->arrival, arrival_us, (size_t)n_local * sizeof(int64_t));
+        memcpy(s->L_true, L_true, (size_t)n_local * sizeof(int32_t));
+        memcpy(s->L_pred, L_pred, (size_t)n_local * sizeof(int32_t));
+    }
+    s->acc_tok = (int32_t *)calloc(n, sizeof(int32_t));
+    s->acc_draft = (int32_t *)calloc(n, sizeof(int32_t));
+    s->rounds = (int32_t *)calloc(n, sizeof(int32_t));
+    s->ring = (int32_t *)calloc(n * (size_t)cfg->gamma, sizeof(int32_t));
+    s->E = (int64_t *)calloc(n, sizeof(int64_t));
+    s->T_total = (int64_t *)calloc(n, sizeof(int64_t));
+    s->C = (int64_t *)malloc(n * sizeof(int64_t));
+    s->x = (int64_t *)malloc(n * sizeof(int64_t));
+    for (size_t i = 0; i < n; i++) { s->C[i] = -1; s->x[i] = -1; }
+    s->admitted = (uint8_t *)calloc(n, 1);
+    s->done = (uint8_t *)calloc(n, 1);
+    s->perceptible = (uint8_t *)calloc(n, 1);
+    s->pinned = (uint8_t *)calloc(n, 1);
+    s->level = (uint8_t *)calloc(n, 1);
+    s->running = (uint8_t *)calloc(n, 1);
+    s->A = (double *)calloc(n, sizeof(double));
+    s->key = (uint64_t *)calloc(n, sizeof(uint64_t));
+    s->order = (int32_t *)malloc(n * sizeof(int32_t));
+    s->now = 0; s->cursor = 0; s->prev_count = 0; s->trace = 0;
+    return s;
+}
+
+void orc_sim_set_trace(orc_sim *s, uint32_t trace) { s->trace = trace; }
+
+void orc_sim_destroy(orc_sim *s)
+{
+    if (!s) return;
+    free(s->arrival); free(s->L_true); free(s->L_pred);
+    free(s->acc_tok); free(s->acc_draft); free(s->rounds); free(s->ring);
+    free(s->E); free(s->T_total); free(s->C); free(s->x);
+    free(s->admitted); free(s->done); free(s->perceptible); free(s->pinned);
+    free(s->level); free(s->running); free(s->A); free(s->key); free(s->order);
+    free(s);
+}
+
+/* The priority of one request as separate fields, compared field by field
+ * (smaller = scheduled sooner).  P:129-133: highest non-empty queue first;
+ * within a queue perceptible requests first, by SJF on the estimate;
+ * non-perceptible by FCFS; perceptible requests are not preempted
+ * (pinned, AMB-15); a running non-perceptible request is only preempted
+ * by a higher queue, a perceptible request, or its own demotion (AMB-16).
+ * Ties by request id, which encodes arrival order (AMB-19). */
+typedef struct {
+    uint32_t inelig, unpinned, level, nonperc, notrun;
+    uint64_t secondary;      /* saturated to 32 bits */
+    uint32_t id;
+} prio;
+
+static uint64_t sat32(uint64_t v) { return v > 0xFFFFFFFFull ? 0xFFFFFFFFull : v; }
+
+static prio prio_of(const orc_sim *s, int32_t i)
+{
+    prio f;
+    memset(&f, 0, sizeof f);
+    f.id = (uint32_t)(i * s->world + s->rank);
+    f.inelig = !(s->admitted[i] && !s->done[i]);
+    switch (s->cfg.policy) {
+    case ORC_POL_FCFS:                           /* P:26, non-preemptive (AMB-25) */
+        f.unpinned = !s->pinned[i];
+        break;
+    case ORC_POL_LPSJF:                          /* SJF on predicted length */
+        f.unpinned = !s->pinned[i];
+        f.secondary = sat32((uint64_t)s->L_pred[i]);
+        break;
+    case ORC_POL_LAS:                            /* P:102, multi-level, preemptive */
+        f.unpinned = 1;
+        f.level = s->level[i];
+        f.nonperc = 1;
+        f.notrun = !s->running[i];
+        break;
+    default: {                                   /* LAPS-SD, Alg. 1 */
+        f.unpinned = !s->pinned[i];
+        f.level = s->level[i];
+        f.nonperc = !s->perceptible[i];
+        if (s->perceptible[i]) {
+            int64_t L_rem = (int64_t)s->L_pred[i] - s->acc_tok[i];   /* AMB-12 */
+            if (L_rem < 0) L_rem = 0;
+            f.secondary = sat32(orc_eq6(L_rem, s->A[i], s->cfg.k, s->cfg.t_ssm_us,
+                                        s->cfg.t_llm_us));
+            f.notrun = 0;
+        } else {
+            f.notrun = !s->running[i];
+        }
+    } }
+    return f;
+}
+
+static int prio_cmp(const prio *a, const prio *b)
+{
+#define CMPF(fld) if (a->fld != b->fld) return a->fld < b->fld ? -1 : 1;
+    CMPF(inelig) CMPF(unpinned) CMPF(level) CMPF(nonperc) CMPF(notrun)
+    CMPF(secondary) CMPF(id)
+#undef CMPF
+    return 0;
+}
+
+static uint64_t pack_key(const prio *f)
+{
+    return ((uint64_t)f->inelig << 63) | ((uint64_t)f->unpinned << 62) |
+           ((uint64_t)(f->level & 15u) << 58) | ((uint64_t)f->nonperc << 57) |
+           ((uint64_t)f->notrun << 56) | (f->secondary << 24) | (uint64_t)(f->id & 0xFFFFFFu);
+}
+
+/* qsort has no context pointer in C11; the simulation is single-threaded. */
+static const orc_sim *g_sort_sim;
+static int cmp_idx(const void *pa, const void *pb)
+{
+    prio a = prio_of(g_sort_sim, *(const int32_t *)pa);
+    prio b = prio_of(g_sort_sim, *(const int32_t *)pb);
+    return prio_cmp(&a, &b);
+}
+
+/* a7 + a4: the clock advances by the cost of the step that just ran, then
+ * every request with r_i <= now is admitted (Eq. (3) x_i >= r_i). */
+static void advance_and_admit(orc_sim *s)
+{
+    if (s->prev_count > 0) s->now += s->c_round;                /* AMB-17 */
+    while (s->cursor < s->n && s->arrival[s->cursor] <= s->now) {
+        s->admitted[s->cursor] = 1;
+        s->cursor++;
+    }
+}
+
+/* Eligible requests sorted by priority; returns how many are eligible. */
+static int32_t sort_eligible(orc_sim *s)
+{
+    int32_t m = 0;
+    for (int32_t i = 0; i < s->n; i++) {
+        prio f = prio_of(s, i);
+        s->key[i] = pack_key(&f);
+        if (!f.inelig) s->order[m++] = i;
+    }
+    g_sort_sim = s;
+    qsort(s->order, (size_t)m, sizeof(int32_t), cmp_idx);
+    return m;
+}
+
+static void commit_selection(orc_sim *s, const int32_t *sel, int32_t B, int32_t global_count,
+                             int64_t next_arrival)
+{
+    for (int32_t b = 0; b < B; b++) {
+        int32_t i = sel[b];
+        if (i < 0) continue;
+        if (s->x[i] < 0) s->x[i] = s->now;                   /* x_i */
+        switch (s->cfg.policy) {
+        case ORC_POL_FCFS: case ORC_POL_LPSJF: s->pinned[i] = 1; break;
+        case ORC_POL_LAPSSD:
+            if (s->cfg.pin_rule == ORC_PIN_ON_SELECT && s->perceptible[i]) s->pinned[i] = 1;
+            break;
+        default: break;
+        }
+    }
+    for (int32_t i = 0; i < s->n; i++) s->running[i] = 0;
+    if (global_count == 0 && next_arrival != INT64_MAX && next_arrival > s->now)
+        s->now = next_arrival;                                  /* idle: jump */
+    s->prev_count = global_count;
+}
+
+int32_t orc_sim_select(orc_sim *s, int32_t B, int32_t *sel_out)
+{
+    advance_and_admit(s);
+    int32_t m = sort_eligible(s);
+    int32_t count = m < B ? m : B;
+    for (int32_t b = 0; b < B; b++) sel_out[b] = b < count ? s->order[b] : -1;
+    int64_t next = s->cursor < s->n ? s->arrival[s->cursor] : INT64_MAX;
+    commit_selection(s, sel_out, B, count, next);
+    return count;
+}
+
+void orc_sim_candidates(orc_sim *s, int32_t C, uint64_t *keys_out, int64_t *next_arrival_out)
+{
+    advance_and_admit(s);
+    int32_t m = sort_eligible(s);
+    for (int32_t c = 0; c < C; c++)
+        keys_out[c] = c < m ? s->key[s->order[c]] : UINT64_MAX;
+    *next_arrival_out = s->cursor < s->n ? s->arrival[s->cursor] : INT64_MAX;
+}
+
+static int cmp_u64(const void *a, const void *b)
+{
+    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return x < y ? -1 : x > y ? 1 : 0;
+}
+
+int32_t orc_sim_merge(orc_sim *s, const uint64_t *all_keys, int32_t C,
+                      const int64_t *all_next_arrival, int32_t B, int32_t *sel_out,
+                      int32_t *global_count_out)
+{
+    int32_t total = s->world * C;
+    uint64_t *tmp = (uint64_t *)malloc((size_t)(total > 0 ? total : 1) * sizeof(uint64_t));
+    memcpy(tmp, all_keys, (size_t)total * sizeof(uint64_t));
+    qsort(tmp, (size_t)total, sizeof(uint64_t), cmp_u64);
+    int32_t gcount = 0, own = 0;
+    for (int32_t c = 0; c < total && gcount < B; c++) {
+        if (tmp[c] == UINT64_MAX || (tmp[c] >> 63)) break;
+        uint32_t id = (uint32_t)(tmp[c] & 0xFFFFFFu);
+        if ((int32_t)(id % (uint32_t)s->world) == s->rank)
+            sel_out[own++] = (int32_t)(id / (uint32_t)s->world);
+        gcount++;
+    }
+    for (int32_t b = own; b < B; b++) sel_out[b] = -1;
+    free(tmp);
+    int64_t next = INT64_MAX;
+    for (int32_t g = 0; g < s->world; g++)
+        if (all_next_arrival[g] < next) next = all_next_arrival[g];
+    commit_selection(s, sel_out, B, gcount, next);
+    if (global_count_out) *global_count_out = gcount;
+    return own;
+}
+
+/* a3: the LAPS-SD state update after one round. */
+void orc_sim_update(orc_sim *s, const int32_t *sel, const int32_t *n_accept, int32_t B)
+{
+    const int32_t k = s->cfg.k, gamma = s->cfg.gamma, K = s->cfg.K;
+    for (int32_t b = 0; b < B; b++) {
+        int32_t i = sel[b];
+        if (i < 0) continue;
+        int32_t r = n_accept[b];
+        /* tokens: r accepted drafts + 1 resampled/bonus token, clipped at L (AMB-18) */
+        int32_t emitted = r + 1;
+        int32_t rem = s->L_true[i] - s->acc_tok[i];
+        s->acc_tok[i] += emitted < rem ? emitted : rem;
+        s->acc_draft[i] += r;                                 /* AMB-4 */
+        s->rounds[i] += 1;
+        int32_t t = s->rounds[i];
+        s->E[i] += s->c_round;                                /* E_i */
+        s->ring[(size_t)i * gamma + (t % gamma)] = s->acc_draft[i];
+        int demoted = 0;
+        if (s->cfg.policy == ORC_POL_LAPSSD && !s->perceptible[i]) {
+            /* Stabilized event: the max difference of the acceptance
+             * rate over gamma consecutive rounds is below delta.  The
+             * rate after round s is accepted / proposed = a_s / (k s) (AMB-5/6). */
+            int stable = 0;
+            double mean = 0.0;
+            if (t >= gamma) {
+                double mx = -1.0, mn = 2.0, sum = 0.0;
+                for (int32_t sr = t - gamma + 1; sr <= t; sr++) {       /* oldest first */
+                    int32_t a = s->ring[(size_t)i * gamma + (sr % gamma)];
+                    double rate = (double)a / (double)((int64_t)k * sr);
+                    if (rate > mx) mx = rate;
+                    if (rate < mn) mn = rate;
+                    sum = sum + rate;
+                }
+                if (mx - mn < s->cfg.delta) { stable = 1; mean = sum / (double)gamma; }
+            }
+            if (stable) {
+                s->perceptible[i] = 1;
+                s->A[i] = mean;                                         /* P:194, AMB-8 */
+                s->T_total[i] = (int64_t)orc_eq6(s->L_pred[i], mean, k, s->cfg.t_ssm_us,
+                                                 s->cfg.t_llm_us);      /* P:139, Eq. 6 */
+                if (s->cfg.placement == ORC_PLACE_BY_ESTIMATE)          /* P:148, AMB-14 */
+                    s->level[i] = (uint8_t)level_of(s->S_up, K, s->T_total[i]);
+                if (s->cfg.pin_rule == ORC_PIN_ON_STABLE) s->pinned[i] = 1;
+            } else {
+                int32_t lev = level_of(s->S_up, K, s->E[i]);
+                if (lev > s->level[i]) { s->level[i] = (uint8_t)lev; demoted = 1; }
+            }
+        } else if (s->cfg.policy == ORC_POL_LAS) {
+            int32_t lev = level_of(s->S_up, K, s->E[i]);
+            if (lev > s->level[i]) { s->level[i] = (uint8_t)lev; demoted = 1; }
+        }
+        if (s->acc_tok[i] >= s->L_true[i]) {
+            s->done[i] = 1;
+            s->C[i] = s->now + s->c_round;                              /* C_i */
+        }
+        s->running[i] = (uint8_t)(!s->done[i] && !demoted);
+    }
+}
+
+static int32_t slab_round_index(int32_t round_idx, int32_t R)
+{
+    int32_t h = R / 2;
+    if (round_idx < R || h == 0) return round_idx < R ? round_idx : R - 1;
+    return h + (round_idx - h) % h;
+}
+
+int32_t orc_sim_step(orc_sim *s, const void *p_pool, const void *q_pool,
+                     const int32_t *draft_pool, int32_t dtype, int64_t V,
+                     const int32_t *slab_tab, int32_t R, int32_t B, int32_t *sel_inout,
+                     int32_t *tokens_out, int32_t *n_accept_out, uint64_t *z_out)
+{
+    const int32_t k = s->cfg.k;
+    const size_t es = dtype == ORC_BF16 ? 2 : 4;
+    int32_t *nacc = (int32_t *)malloc((size_t)(B > 0 ? B : 1) * sizeof(int32_t));
+    int32_t *tok = (int32_t *)malloc((size_t)(B > 0 ? B : 1) * (size_t)(k + 1) * sizeof(int32_t));
+    for (int32_t b = 0; b < B; b++) {
+        int32_t i = sel_inout[b];
+        nacc[b] = -1;
+        for (int32_t j = 0; j <= k; j++) tok[(size_t)b * (k + 1) + j] = -1;
+        if (z_out) z_out[b] = 0;
+        if (i < 0) continue;
+        int32_t slab = slab_tab[(size_t)i * R + slab_round_index(s->rounds[i], R)];
+        const char *p = (const char *)p_pool + (size_t)slab * (size_t)(k + 1) * (size_t)V * es;
+        const char *q = (const char *)q_pool + (size_t)slab * (size_t)k * (size_t)V * es;
+        orc_verify_out o;
+        nacc[b] = orc_verify_request(p, q, dtype, V, k, draft_pool + (size_t)slab * k,
+                                     (uint32_t)(i * s->world + s->rank), (uint32_t)s->rounds[i],
+                                     s->cfg.seed, s->trace, tok + (size_t)b * (k + 1), &o);
+        if (z_out) z_out[b] = o.Z;
+    }
+    orc_sim_update(s, sel_inout, nacc, B);
+    if (tokens_out) memcpy(tokens_out, tok, (size_t)B * (k + 1) * sizeof(int32_t));
+    if (n_accept_out) memcpy(n_accept_out, nacc, (size_t)B * sizeof(int32_t));
+    free(nacc); free(tok);
+    return orc_sim_select(s, B, sel_inout);
+}
+
+void orc_sim_view(orc_sim *s, orc_state_view *v)
+{
+    v->now_us = s->now; v->cursor = s->cursor; v->prev_count = s->prev_count;
+    v->acc_tok = s->acc_tok; v->acc_draft = s->acc_draft; v->rounds = s->rounds;
+    v->E_us = s->E; v->T_total_us = s->T_total; v->C_us = s->C; v->x_us = s->x;
+    v->admitted = s->admitted; v->done = s->done; v->perceptible = s->perceptible;
+    v->pinned = s->pinned; v->level = s->level; v->running = s->running;
+    v->A = s->A; v->key = s->key; v->ring = s->ring;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Job-level scheduling (Fig. 1; objective and constraints P:86-93) */
+/* ------------------------------------------------------------------------ */
+int64_t orc_jobs_schedule(int32_t policy, int32_t n, const int64_t *arrival_us,
+                          const int64_t *service_us, const int64_t *L_pred,
+                          const int64_t *est_us, int32_t *order_out, int64_t *C_out)
+{
+    uint8_t *served = (uint8_t *)calloc((size_t)(n > 0 ? n : 1), 1);
+    int64_t now = 0, sum = 0;
+    for (int32_t pos = 0; pos < n; pos++) {
+        int32_t best = -1;
+        int64_t earliest = INT64_MAX;
+        for (int32_t i = 0; i < n; i++)
+            if (!served[i] && arrival_us[i] < earliest) earliest = arrival_us[i];
+        if (earliest > now) now = earliest;                     /* x_i >= r_i, Eq. (3) */
+        for (int32_t i = 0; i < n; i++) {
+            if (served[i] || arrival_us[i] > now) continue;
+            if (best < 0) { best = i; continue; }
+            int64_t a, b;
+            switch (policy) {
+            case 1: a = arrival_us[i]; b = arrival_us[best]; break;   /* FCFS */
+            case 2: a = L_pred[i]; b = L_pred[best]; break;           /* LP-SJF */
+            default: a = est_us[i]; b = est_us[best]; break;          /* SJF on T~ */
+            }
+            if (a < b) best = i;                                      /* ties: lower id */
+        }
+        served[best] = 1;
+        now += service_us[best];                                /* C_i = x_i + T_i, Eq. (4) */
+        if (order_out) order_out[pos] = best;
+        if (C_out) C_out[best] = now;
+        sum += now - arrival_us[best];                          /* C_i - r_i, Eq. (2) */
+    }
+    free(served);
+    return sum;
+}
+
+int64_t orc_brute_force(int32_t n, const int64_t *service_us, int32_t *best_order_out,
+                        int64_t *all_sums_out)
+{
+    if (n < 1 || n > 8) return -1;
+    int32_t perm[8];
+    for (int32_t i = 0; i < n; i++) perm[i] = i;
+    int64_t best = INT64_MAX;
+    int64_t idx = 0;
+    for (;;) {
+        int64_t now = 0, sum = 0;
+        for (int32_t pos = 0; pos < n; pos++) { now += service_us[perm[pos]]; sum += now; }
+        if (all_sums_out) all_sums_out[idx] = sum;
+        idx++;
+        if (sum < best) {                  /* strict: first (lexicographic) optimum kept */
+            best = sum;
+            for (int32_t i = 0; i < n; i++) best_order_out[i] = perm[i];
+        }
+        /* next permutation in lexicographic order */
+        int32_t a = n - 2;
+        while (a >= 0 && perm[a] > perm[a + 1]) a--;
+        if (a < 0) break;
+        int32_t b = n - 1;
+        while (perm[b] < perm[a]) b--;
+        int32_t tmp = perm[a]; perm[a] = perm[b]; perm[b] = tmp;
+        for (int32_t l = a + 1, h = n - 1; l < h; l++, h--) { tmp = perm[l]; perm[l] = perm[h]; perm[h] = tmp; }
+    }
+    return best;
+}

@@ -1,0 +1,155 @@
+/*
+ * lapssd_oracle.h -- CPU ORACLE for the LAPS-SD batched speculative-decoding step.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or helper with the CUDA product path (paper_2505_17074_b200/csrc,
+ * include/lapssd.h); both are written independently from PAPER.md (arXiv 2505.17074)
+ * and the readings listed in DESIGN.md section 3.
+ *
+ * Citations: P:NN = PAPER.md line NN.  AMB-n = DESIGN.md reading n.
+ *
+ * Parity pins (tests/test_oracle_*.py, -m "not gpu"):
+ *   orc_philox4x32_10 ...... Random123 known-answer vectors (tests/golden/philox_kat.txt)
+ *   orc_verify_request ..... closed form E[tokens/step] (Leviathan et al., cited P:11),
+ *                            accepted-count law, chi-square "first token ~ p" on V=16,
+ *                            special cases p=q / disjoint / one-hot / mixture family
+ *   orc_thresholds ......... P:169 formula hand values
+ *   orc_eq6 ................ P:196-200 hand values
+ *   orc_sim_* .............. Fig. 1 token-level expectations (renewal DP),
+ *                            stability deadline (P:194 + 1/t bound), degeneracies,
+ *                            invariants
+ *   orc_jobs_schedule ...... Fig. 1 printed averages 583 / 683 ms,
+ *                            brute-force optimum (orc_brute_force)
+ *   orc_brute_force ........ exhaustive enumeration (definition of the optimum)
+ */
+#ifndef LAPSSD_ORACLE_H
+#define LAPSSD_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- counter-based RNG: Philox4x32-10 (Salmon et al., SC'11) ---- */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+/* ---- (1) verification by rejection sampling, P:57-64, P:200 ---- */
+enum { ORC_F32 = 0, ORC_BF16 = 1 };
+
+typedef struct {
+    int32_t  r;            /* first rejected position, or k if all accepted        */
+    int32_t  y;            /* token emitted at position r                          */
+    int32_t  fallback;     /* 1: residual mass was 0, sampled from p_r (AMB-20)     */
+    int32_t  invalid;      /* 1: no mass at all (contract violation)                */
+    uint64_t Z;            /* Q4.60 total residual mass                            */
+    uint64_t t;            /* sampled target in [0, Z)                             */
+    double   z_real;       /* exact residual mass sum(max(0,p-q)) in long double   */
+    double   z_rel_err;    /* |Z*2^-60 - z_real| / z_real                          */
+    double   margin_rel;   /* distance of t to nearest CDF boundary / Z            */
+} orc_verify_out;
+
+/* p_rows: (k+1) rows of V values; q_rows: k rows of V values; both in `dtype`
+ * (bf16 stored as uint16 bit patterns).  draft: k token ids.
+ * tokens: k+1 outputs (draft[0..r-1], y, then -1).  Returns r. */
+int32_t orc_verify_request(const void *p_rows, const void *q_rows, int32_t dtype,
+                           int64_t V, int32_t k, const int32_t *draft,
+                           uint32_t req_id, uint32_t round_idx, uint64_t seed,
+                           uint32_t trace, int32_t *tokens, orc_verify_out *out);
+
+/* Many independent trials over the same rows (statistical pins). */
+void orc_verify_many(const void *p_rows, const void *q_rows, int32_t dtype, int64_t V,
+                     int32_t k, int32_t n_trials, const int32_t *drafts,
+                     const uint32_t *req_ids, const uint32_t *rounds, uint64_t seed,
+                     int32_t *tokens_out, int32_t *r_out);
+
+/* ---- scheduler pieces, P:161-202 ---- */
+enum { ORC_POL_LAPSSD = 0, ORC_POL_FCFS = 1, ORC_POL_LPSJF = 2, ORC_POL_LAS = 3 };
+enum { ORC_PLACE_BY_ESTIMATE = 0, ORC_PLACE_STAY = 1 };
+enum { ORC_PIN_ON_SELECT = 0, ORC_PIN_ON_STABLE = 1 };
+
+typedef struct {
+    int32_t  policy;
+    int32_t  K;            /* number of priority queues, 1..16                      */
+    int64_t  s1_up_us;     /* S_1^up                                                */
+    double   M;            /* threshold ratio, > 1                                  */
+    int32_t  gamma;        /* stability window (rounds), >= 2                       */
+    double   delta;        /* stability threshold, >= 0                             */
+    int32_t  k;            /* drafts per round (paper's n)                          */
+    int64_t  t_ssm_us;     /* T_SSM per drafted token                               */
+    int64_t  t_llm_us;     /* T_LLM per verification pass                           */
+    int32_t  placement;    /* ORC_PLACE_*                                           */
+    int32_t  pin_rule;     /* ORC_PIN_*                                             */
+    uint64_t seed;
+} orc_config;
+
+/* S_up[j] = floor(s1_up * M^j), j = 0..K-2, iterative fp64 multiply. */
+int32_t  orc_thresholds(int32_t K, int64_t s1_up_us, double M, int64_t *S_up_out);
+/* Eq. (6): floor(L (k T_SSM + T_LLM) / (k A + 1)) in microseconds. */
+uint64_t orc_eq6(int64_t L, double A, int32_t k, int64_t t_ssm_us, int64_t t_llm_us);
+
+/* ---- the resident-request simulation (a3-a8) ---- */
+typedef struct orc_sim orc_sim;
+
+orc_sim *orc_sim_create(const orc_config *cfg, int32_t n_local, const int64_t *arrival_us,
+                        const int32_t *L_true, const int32_t *L_pred,
+                        int32_t rank, int32_t world);
+void     orc_sim_destroy(orc_sim *s);
+/* Monte-Carlo traces: Philox counter word c3 (AMB-21). */
+void     orc_sim_set_trace(orc_sim *s, uint32_t trace);
+
+/* Single-rank select: advance clock, admit, build keys, take top-B.  Returns count;
+ * sel_out[B] holds local indices in key order, -1 padded. */
+int32_t  orc_sim_select(orc_sim *s, int32_t B, int32_t *sel_out);
+/* Multi-rank select, phase 1: advance clock, admit, build keys, write this rank's
+ * C smallest eligible keys (ascending, UINT64_MAX padded) and its next arrival. */
+void     orc_sim_candidates(orc_sim *s, int32_t C, uint64_t *keys_out, int64_t *next_arrival_out);
+/* Multi-rank select, phase 2: given the gathered candidates of all ranks
+ * (world*C keys, world next arrivals), take the global top-B and keep own ids. */
+int32_t  orc_sim_merge(orc_sim *s, const uint64_t *all_keys, int32_t C,
+                       const int64_t *all_next_arrival, int32_t B, int32_t *sel_out,
+                       int32_t *global_count_out);
+
+/* State update after verification (a3): sel[B] local indices (-1 = empty slot),
+ * n_accept[B] = r per slot. */
+void     orc_sim_update(orc_sim *s, const int32_t *sel, const int32_t *n_accept, int32_t B);
+
+/* One full step over pooled rows: verify every selected request on its slab,
+ * update, select the next batch.  slab_tab[n_local*R] maps (request, round) to a
+ * slab: idx = round < R ? round : R/2 + (round - R/2) % (R/2).
+ * tokens_out[B*(k+1)] and n_accept_out[B] may be NULL. */
+int32_t  orc_sim_step(orc_sim *s, const void *p_pool, const void *q_pool,
+                      const int32_t *draft_pool, int32_t dtype, int64_t V,
+                      const int32_t *slab_tab, int32_t R, int32_t B, int32_t *sel_inout,
+                      int32_t *tokens_out, int32_t *n_accept_out, uint64_t *z_out);
+
+typedef struct {
+    int64_t now_us;
+    int32_t cursor, prev_count;
+    int32_t *acc_tok, *acc_draft, *rounds;
+    int64_t *E_us, *T_total_us, *C_us, *x_us;
+    uint8_t *admitted, *done, *perceptible, *pinned, *level, *running;
+    double  *A;
+    uint64_t *key;
+    int32_t *ring;         /* n_local * gamma */
+} orc_state_view;
+void     orc_sim_view(orc_sim *s, orc_state_view *v);
+/* keys exactly as the last select built them (ineligible ones included) */
+
+/* ---- job-level scheduling with known service times (Fig. 1; Eqs. 2-5) ---- */
+/* policy: 0 = SJF by est (LAPS-SD, every request perceptible at arrival), 1 = FCFS,
+ * 2 = LP-SJF (by L_pred).  Non-preemptive single server.  Returns sum of (C_i - r_i). */
+int64_t  orc_jobs_schedule(int32_t policy, int32_t n, const int64_t *arrival_us,
+                           const int64_t *service_us, const int64_t *L_pred,
+                           const int64_t *est_us, int32_t *order_out, int64_t *C_out);
+/* Exhaustive search over all n! orders (n <= 8), simultaneous arrivals at 0.
+ * Returns the minimum sum of completion times; best_order_out gets the
+ * lexicographically smallest optimal order; all_sums_out (nullable) gets the
+ * sum for every permutation in lexicographic order. */
+int64_t  orc_brute_force(int32_t n, const int64_t *service_us, int32_t *best_order_out,
+                         int64_t *all_sums_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
