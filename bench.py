@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""bench.py -- the LAPS-SD batched speculative-decoding step on B200.
+
+One STEP = one pass of the whole hot path over one batch: spec_verify of every
+selected request (rejection sampling) with the fused LAPS-SD
+state update, then admission + priority keys + top-B selection of the
+next batch -- the C-ABI call laps_step (laps_step_dist for N>1).
+
+Workload = BASELINE.json configs[3] ("16,384 concurrent requests, V=128,256, k=8,
+bf16, batch 512, sharded over 8 B200"): 2,048 resident requests and B=512 per GPU
+(weak scaling, DESIGN.md s.7), all arriving at t=0, acceptance ~ Beta(7,3), output
+lengths ~ U[512, 4096], probability rows from a 4.5 GB F2 slab pool (inputs larger than
+L2; every step reads ~255 MB of rows it did not read in the previous step).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "verified draft tokens/s at V=128k,k=8 on 1/2/4/8 B200; % of HBM peak"
+UNIT = "verified draft tokens/s"
+WORKLOAD = ("configs[3]: 16,384 concurrent requests over 8 GPUs -> 2,048 resident + batch 512 "
+            "per GPU (weak scaling), V=128,256, k=8, bf16 p/q, Beta(7,3) acceptance, "
+            "L~U[512,4096], all arrive at t=0, global top-B all-gather for N>1")
+SCHED = dict(K=4, s1_up_us=4 * (8 * 1000 + 10_000), M=2.0, gamma=5, delta=0.05, k=8,
+             t_ssm_us=1000, t_llm_us=10_000, placement=0, pin_rule=0)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n-per-gpu", type=int, default=2048)
+    ap.add_argument("--batch", type=int, default=512)
+    ap.add_argument("--V", type=int, default=128256)
+    ap.add_argument("--k", type=int, default=8)
+    ap.add_argument("--buckets", type=int, default=64)
+    ap.add_argument("--variants", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "verify_dram.json"))
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.rows, self.proc = [], None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(gpu_index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                self.rows.append(f)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm, smax = [], []
+        for f in self.rows:
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- workload
+def build_workload(args, rank, world, device, pool_slabs=None):
+    n_total = args.n_per_gpu * world
+    tr = synth.make_trace(n_total, synth.CONFIGS["c4"]["seed"], arrival="zero", length="uniform",
+                          len_min=512, len_max=4096, beta_ab=(7, 3))
+    local = tr.shard(rank, world)
+    buckets, variants = args.buckets, args.variants
+    if pool_slabs is not None:
+        variants = max(1, pool_slabs // buckets)
+    pool = synth.make_pool("f2", V=args.V, k=args.k, dtype="bf16", n_buckets=buckets,
+                           variants=variants, seed=synth.CONFIGS["c4"]["seed"], device=device)
+    tab_full = synth.slab_table(tr, buckets, variants, R=64, seed=synth.CONFIGS["c4"]["seed"])
+    tab = np.ascontiguousarray(tab_full[rank::world])
+    return tr, local, pool, tab
+
+
+def algorithmic_bytes(n_acc: np.ndarray, V: int, k: int, s: int = 2) -> float:
+    """SURVEY s.8(d): per verified slot (r<k ? 2 : 1) V s row bytes + 2 s min(r+1,k)
+    gathered scalars + 4k draft bytes.  n_acc holds r per slot (-1 = empty)."""
+    r = n_acc[n_acc >= 0].astype(np.int64)
+    rows = np.where(r < k, 2, 1) * V * s
+    gathers = 2 * s * np.minimum(r + 1, k)
+    return float((rows + gathers + 4 * k).sum())
+
+
+# --------------------------------------------------------------------------- ours
+def run_ours(args):
+    import paper_2505_17074_b200 as L
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    B_local = args.batch
+    B = B_local * world                        # global batch (weak scaling)
+    tr, local, pool, tab = build_workload(args, rank, world, dev)
+    cfg = L.SchedConfig(**SCHED, seed=synth.CONFIGS["c4"]["seed"])
+    h = L.Handle(cfg, local.arrival_us, local.L_true, local.L_pred, max_batch=B, V=args.V,
+                 rank=rank, world=world)
+    tab_d = torch.as_tensor(tab, device=dev)
+    rows = L.Rows(pool.p, pool.q, pool.draft, tab_d)
+    comm = cand = None
+    Cn = min(B, args.n_per_gpu)
+    if world > 1:
+        comm = L.nccl_comm()
+        cand = torch.zeros((world + 1) * (Cn + 1), dtype=torch.int64, device=dev)
+        h.laps_candidates(Cn, cand[: Cn + 1])
+        dist.all_gather_into_tensor(cand[Cn + 1:], cand[: Cn + 1])
+        h.laps_merge(cand[Cn + 1:], Cn, B)
+    else:
+        h.laps_select(B)
+    hist = torch.full((args.warmup + args.steps, B), -1, dtype=torch.int32, device=dev)
+
+    def step(t):
+        if world > 1:
+            h.laps_step_dist(comm, rows, B, Cn, cand)
+        else:
+            h.laps_step(rows, B, n_accept=hist[t])
+
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank if "CUDA_VISIBLE_DEVICES" not in os.environ else local_rank)
+    for t in range(args.warmup):
+        step(t)
+    torch.cuda.synchronize()
+    st0 = h.state()
+    if world == 1:
+        h.profile(args.steps)
+    launches0 = L.launch_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for t in range(args.warmup, args.warmup + args.steps):
+        step(t)
+    e1.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = L.launch_count() - launches0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st1 = h.state()
+    verified_local = int((st1["rounds"] - st0["rounds"]).sum())
+    ms_t = torch.tensor([ms, float(verified_local)], dtype=torch.float64, device=dev)
+    if dist:
+        mx = ms_t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = ms_t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, verified = float(mx[0]), int(sm[1])
+    else:
+        ms_max, verified = ms, verified_local
+    value = verified * args.k / (ms_max * 1e-3)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16 rows; fp32 residual + exact "
+           "Q4.60 integer CDF; fp64 scheduler", "data": "synthetic",
+           "config": {"workload": WORKLOAD, "N_resident_per_gpu": args.n_per_gpu,
+                      "B_per_gpu": B_local, "B_global": B, "V": args.V, "k": args.k,
+                      "pool": f"F2 zipf, {pool.S} slabs x {(2 * args.k + 1) * args.V * 2 / 1e6:.2f} MB",
+                      "l2": "inputs larger than L2 (4.5 GB slab pool, ~255 MB of rows per step)",
+                      "parallelism": f"dp{world}: requests sharded by id mod {world}"
+                      + ("; global top-B via NCCL all-gather of candidate keys" if world > 1 else "")},
+           "verified_per_step": verified / args.steps, "gpu_launches": launches, "clocks": clk}
+    if world == 1:
+        v_ms, s_ms, n_prof = h.profile_read()
+        n_acc = hist[args.warmup:].cpu().numpy()
+        alg = algorithmic_bytes(n_acc, args.V, args.k)
+        per_launch = alg / args.steps
+        avg_v = v_ms / n_prof
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        peak = peaks.get("hbm_gbs")
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if peak else "fallback (B200_PROFILING.md)"
+        peak = peak or 6650.0
+        achieved = per_launch / (avg_v * 1e-3) / 1e9
+        traffic = None
+        if os.path.exists(args.traffic_file):
+            try:
+                traffic = json.load(open(args.traffic_file)).get("dram_bytes_per_launch")
+            except (OSError, ValueError):
+                traffic = None
+        out["roofline"] = {"kernel": "verify_kernel<bf16> (laps_step)", "bound": "hbm",
+                           "achieved": achieved, "peak": peak, "unit": "GB/s",
+                           "frac": achieved / peak, "peak_source": peak_src,
+                           "frac_of_8TBs": achieved / 8000.0,
+                           "algorithmic_bytes_per_launch": per_launch, "traffic": traffic,
+                           "verify_ms_avg": avg_v, "select_ms_avg": s_ms / n_prof,
+                           "verify_share_of_step": v_ms / ms}
+        if not args.no_e2e:
+            out["e2e"] = run_e2e(args, L, local, pool, cfg, dev)
+        if not args.no_cpu_baseline:
+            out["cpu_baseline"] = run_cpu_baseline(args, local, pool, tab, cfg)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        L.nccl_comm_destroy(comm)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, L, local, pool, cfg, dev):
+    """The same metric through the C-ABI with HOST buffers: every step copies that
+    step's batch rows (batch layout p[B,k+1,V], q[B,k,V], draft[B,k]) from pinned host
+    memory, runs laps_step, and reads back the batch, accepted counts and tokens."""
+    B, k, V = args.batch, args.k, args.V
+    h = L.Handle(cfg, local.arrival_us, local.L_true, local.L_pred, max_batch=B, V=V)
+    host = []
+    for j in range(2):
+        idx = (torch.arange(B) + j * B) % pool.S
+        host.append((pool.p[idx.to(dev)].cpu().pin_memory(), pool.q[idx.to(dev)].cpu().pin_memory(),
+                     pool.draft[idx.to(dev)].cpu().pin_memory()))
+    dp = torch.empty_like(pool.p[:B])
+    dq = torch.empty_like(pool.q[:B])
+    dd = torch.empty_like(pool.draft[:B])
+    rows = L.Rows(dp, dq, dd, None)
+    tok = torch.empty(B, k + 1, dtype=torch.int32, device=dev)
+    nacc = torch.empty(B, dtype=torch.int32, device=dev)
+    out_sel = torch.empty(B, dtype=torch.int32).pin_memory()
+    out_nacc = torch.empty(B, dtype=torch.int32).pin_memory()
+    out_tok = torch.empty(B, k + 1, dtype=torch.int32).pin_memory()
+    h.laps_select(B)
+    s = torch.cuda.current_stream()
+    h2d = sum(t.numel() * t.element_size() for t in host[0])
+    d2h = out_sel.numel() * 4 + out_nacc.numel() * 4 + out_tok.numel() * 4
+
+    def one(j):
+        hp, hq, hd = host[j % 2]
+        dp.copy_(hp, non_blocking=True)
+        dq.copy_(hq, non_blocking=True)
+        dd.copy_(hd, non_blocking=True)
+        h.laps_step(rows, B, tokens=tok, n_accept=nacc)
+        out_sel.copy_(h.sel[:B], non_blocking=True)
+        out_nacc.copy_(nacc, non_blocking=True)
+        out_tok.copy_(tok, non_blocking=True)
+        s.synchronize()
+
+    one(0)
+    st0 = h.state()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for j in range(args.e2e_steps):
+        one(j + 1)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    verified = int((h.state()["rounds"] - st0["rounds"]).sum())
+    h.close()
+    return {"value": verified * k / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": args.e2e_steps, "ms_per_step": ms / args.e2e_steps,
+            "path": "laps_step C-ABI, batch-layout rows H2D from pinned host each step"}
+
+
+def run_cpu_baseline(args, local, pool, tab, cfg_gpu, budget_s=None, batch=None):
+    """The oracle as it stands (single thread, plain C) on a bounded sample of the same
+    workload: the first steps of the same request set, same rows, same config."""
+    import oracle
+
+    budget_s = budget_s or args.cpu_seconds
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, tab.shape[1]
+    ocfg = oracle.SchedConfig(**SCHED, seed=cfg_gpu.seed)
+    B = batch or args.batch
+    sim = oracle.Sim(ocfg, local.arrival_us, local.L_true, local.L_pred)
+    sel, _ = sim.select(B)
+    t0 = time.perf_counter()
+    steps = verified = 0
+    while time.perf_counter() - t0 < budget_s:
+        verified += int((sel >= 0).sum())
+        sim.step(P, sel)
+        steps += 1
+    el = time.perf_counter() - t0
+    return {"value": verified * args.k / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {steps} steps of the bench workload ({B} verifications per step, "
+                      f"V={args.V}, k={args.k}, bf16), oracle/lapssd_oracle.c single thread, "
+                      f"{el:.1f} s"}
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """--impl reference: the CPU oracle, as it stands, timed on this host's cores on the
+    same config / metric; each step a bounded sample (a smaller batch) of the workload."""
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if rank != 0:
+        return
+    import oracle
+
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    # inputs: same generator and recipe; a 128-slab pool is enough for the oracle
+    tr, local, pool, tab = build_workload(args, 0, 1, dev, pool_slabs=128)
+    # each step is a bounded sample: pick the batch so the whole run takes ~2 minutes
+    probe = oracle.Sim(oracle.SchedConfig(**SCHED, seed=1), local.arrival_us, local.L_true,
+                       local.L_pred)
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, tab.shape[1]
+    sel, _ = probe.select(8)
+    t0 = time.perf_counter()
+    probe.step(P, sel)
+    per_verify = (time.perf_counter() - t0) / 8
+    total_steps = args.warmup + args.steps
+    b_ref = int(max(1, min(args.batch, 100.0 / (total_steps * per_verify))))
+    sim = oracle.Sim(oracle.SchedConfig(**SCHED, seed=synth.CONFIGS["c4"]["seed"]),
+                     local.arrival_us, local.L_true, local.L_pred)
+    sel, _ = sim.select(b_ref)
+    for _ in range(args.warmup):
+        sim.step(P, sel)
+    verified = 0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        verified += int((sel >= 0).sum())
+        sim.step(P, sel)
+    el = time.perf_counter() - t0
+    value = verified * args.k / el
+    sample = (f"oracle/lapssd_oracle.c single thread; each step verifies a batch of {b_ref} "
+              f"(of {args.batch}) requests of the same workload, V={args.V}, k={args.k}, bf16")
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16 rows; fp32/fp64/int128 oracle",
+           "data": "synthetic", "impl": "reference",
+           "config": {"workload": WORKLOAD, "N_resident_per_gpu": args.n_per_gpu,
+                      "B_per_step": b_ref, "V": args.V, "k": args.k},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,266 @@
+/*
+ * lapssd.h -- C-ABI of liblapssd.so: the B200 (sm_100a) hot path of LAPS-SD
+ * (arXiv 2505.17074), the per-iteration batched speculative-decoding step over
+ * every resident request:
+ *
+ *   (a1-a2) spec_verify  -- verify k drafts per request by rejection sampling
+ *                           (Eq. 1; bonus token P:200)
+ *   (a3)    laps_update  -- the LAPS-SD per-request state update
+ *                           (P:170-178 lifecycle, P:194 stability, Eq. 6)
+ *   (a4-a7) laps_select  -- admission, priority keys, top-B batch, clock
+ *                           (P:129-133 inter-queue, P:135-142 / P:202 intra-queue)
+ *   laps_step            -- (a1..a7) fused: verify + update + select
+ *   (a8)    laps_candidates / laps_merge / laps_step_dist -- request sharding over
+ *                           G GPUs with one all-gather of candidate keys per step
+ *
+ * The scheduling problem the calls follow: requests i arrive at r_i,
+ * their execution time is unknown in advance, the system chooses when each runs
+ * (x_i) and whether it is preempted at round boundaries; the objective is the mean
+ * of C_i - r_i.  "P:NN" is PAPER.md line NN; "AMB-n" is a reading in DESIGN.md s.3.
+ *
+ * Conventions for every call:
+ *  - Pointers marked [device] are CUDA device pointers; [host] are host pointers.
+ *    All device buffers are CALLER-OWNED (PyTorch tensors).  The library never
+ *    allocates device memory and never frees caller memory.
+ *  - Every call is asynchronous on the given stream, enqueues only kernels (no
+ *    host synchronisation, no allocation) and may be captured in a CUDA graph,
+ *    except lapssd_create (H2D copies of the request arrays), lapssd_read_state
+ *    (D2H copies, synchronises the stream) and lapssd_check (synchronises).
+ *  - Argument validation is synchronous: a bad argument returns LAPSSD_EINVAL and
+ *    enqueues nothing.  A failed launch returns LAPSSD_ECUDA.  The text of the
+ *    last error of the calling thread is returned by lapssd_last_error().
+ *  - Contract violations detected on the device (e.g. a selected request that is
+ *    already complete, a row with no probability mass) set a sticky device flag
+ *    that lapssd_check() reports as LAPSSD_ESTATE.
+ *  - A handle is bound to one stream at a time and is not thread-safe.
+ *  - Times are integer microseconds (int64).  Probabilities are float32 or bf16
+ *    in [0, 1]; each stored row of p is expected to sum to about 1.
+ */
+#ifndef LAPSSD_H
+#define LAPSSD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *lapssd_stream;   /* == cudaStream_t */
+
+typedef enum {
+    LAPSSD_OK = 0,
+    LAPSSD_EINVAL = -1,   /* invalid argument, nothing enqueued                      */
+    LAPSSD_ECUDA = -2,    /* CUDA launch / copy failure                              */
+    LAPSSD_ENCCL = -3,    /* NCCL unavailable or failed                              */
+    LAPSSD_ESTATE = -4,   /* device-detected contract violation (sticky flag)        */
+    LAPSSD_ENOMEM = -5    /* caller-provided workspace too small                     */
+} lapssd_status;
+
+typedef enum { LAPSSD_F32 = 0, LAPSSD_BF16 = 1 } lapssd_dtype;
+
+typedef enum {
+    LAPSSD_POL_LAPSSD = 0,  /* Alg. 1                                       */
+    LAPSSD_POL_FCFS = 1,    /* first-come-first-serve, non-preemptive            */
+    LAPSSD_POL_LPSJF = 2,   /* SJF on predicted output length, non-preemptive   */
+    LAPSSD_POL_LAS = 3      /* least attained service on the same K queues      */
+} lapssd_policy;
+
+/* Scheduler parameters.  Validation (EINVAL):
+ * 1 <= K <= 16, s1_up_us > 0, M > 1, gamma >= 2, delta >= 0, 1 <= k <= 16,
+ * t_ssm_us >= 0, t_llm_us >= 0.  delta == 0 disables stabilisation. */
+typedef struct {
+    int32_t policy;        /* lapssd_policy                                            */
+    int32_t K;             /* number of priority queues Q_1..Q_K                       */
+    int64_t s1_up_us;      /* S_1^up; S_j^up = floor(s1_up * M^(j-1)) (AMB-11)  */
+    double M;              /* threshold ratio                                          */
+    int32_t gamma;         /* stability window in rounds (AMB-7)                */
+    double delta;          /* stability threshold on max-min of the window (AMB-6)     */
+    int32_t k;             /* drafts per round, the paper's n                  */
+    int64_t t_ssm_us;      /* T_SSM per drafted token (Eq. 6, AMB-9)                   */
+    int64_t t_llm_us;      /* T_LLM per verification pass (Eq. 6)                      */
+    int32_t placement;     /* 0 = queue of T~_total on stabilisation, 1 = stay (AMB-14) */
+    int32_t pin_rule;      /* 0 = pin perceptible requests when selected, 1 = when
+                              stable (AMB-15)                                          */
+    uint64_t seed;         /* Philox key for every draw of the method (AMB-21)         */
+} lapssd_config;
+
+/* The resident requests of this rank.  [host] arrays of n entries, copied at
+ * create.  Local request l has global id l*world + rank; arrival_us must be
+ * non-decreasing in l (ids encode arrival order, AMB-19).  L_true >= 1 is the
+ * output length that ends the request, L_pred >= 1 the predicted length L_i
+ * used by Eq. 6 and LP-SJF.  Global ids must be < 2^24. */
+typedef struct {
+    const int64_t *arrival_us;
+    const int32_t *L_true;
+    const int32_t *L_pred;
+    int32_t n;
+    int32_t rank, world;
+} lapssd_requests;
+
+/* Where a step's probability rows live.  Two layouts:
+ *  - slab_tab == NULL: batch layout.  Slot b (0 <= b < B) reads
+ *      p[b, 0..k, 0..V), q[b, 0..k-1, 0..V), draft[b, 0..k-1].
+ *  - slab_tab != NULL: pooled layout.  p/q/draft are pools of n_slabs slabs of the
+ *      same shapes; the request in slot b, local index i, in its round t reads slab
+ *      slab_tab[i*R + (t < R ? t : R/2 + (t - R/2) % (R/2))].
+ * p: [device] (k+1) x V per slab, q: [device] k x V per slab, row-major, dtype
+ * elements; draft: [device] int32 k per slab, drafts x_j sampled from q_j.
+ * V*sizeof(dtype) must be a multiple of 16 and p, q 16-byte aligned. */
+typedef struct {
+    const void *p;
+    const void *q;
+    const int32_t *draft;
+    int32_t dtype;         /* lapssd_dtype                                             */
+    int32_t k;
+    int64_t V;
+    const int32_t *slab_tab;  /* [device] n_local x R, or NULL                         */
+    int32_t R;
+    int64_t n_slabs;
+} lapssd_rows;
+
+typedef struct lapssd_handle lapssd_handle;
+
+/* ---------------------------------------------------------------------------
+ * spec_verify -- stateless batched verification (AMB-1,2,20,21,27)
+ *
+ * For every slot b < B (rows as in lapssd_rows with slab_tab == NULL, or slab
+ * index slab[b] into pools when slab != NULL):
+ *   for j = 0..k-1: u24_j = Philox4x32-10(key = seed, ctr = (req_id[b], round_idx[b],
+ *     j/4, trace))[j%4] >> 8; accept x_j iff u24_j * q_j(x_j) < p_j(x_j) * 2^24 (fp64,
+ *     exact); r = first rejected position, or k.
+ *   R_v = floor(max(0, fl32(p_r[v] - q_r[v])) * 2^60) if r < k, else floor(p_k[v]*2^60);
+ *   if r < k and sum R = 0 the row p_r is used (AMB-20).  Z = sum_v R_v (exact uint64).
+ *   U = 64-bit Philox draw (ctr = (req_id, round, 1<<8, trace)), t = floor(U*Z/2^64),
+ *   y = min{ v : sum_{w<=v} R_w > t }.
+ * Outputs [device]: tokens[B, k+1] = (x_0..x_{r-1}, y, -1...), n_accept[B] = r,
+ * z_fixed[B] = Z (nullable).  req_id, round_idx: [device] uint32 [B].
+ * workspace: [device] >= spec_verify_workspace_bytes(B, V), ZERO-FILLED once by the
+ * caller before first use; every call leaves it zero-filled again.
+ * Errors: EINVAL (k, V, dtype, alignment, B < 0), ENOMEM (workspace), ECUDA. */
+size_t spec_verify_workspace_bytes(int32_t B, int64_t V);
+lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V, int32_t k,
+                          const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
+                          const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,
+                          int32_t *tokens, int32_t *n_accept, uint64_t *z_fixed,
+                          void *workspace, size_t workspace_bytes, lapssd_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * Handle: resident-request state (SoA, ~64 B/request + gamma*4 B ring) in a
+ * caller-owned device workspace.  lapssd_create copies the request arrays (H2D on
+ * `stream`), zero-initialises state, computes the thresholds of P:169, and sets
+ * now = 0.  The first batch comes from laps_select.  max_batch bounds B of every
+ * later call; V bounds the rows' vocabulary.
+ * Errors: EINVAL (config, n, ids >= 2^24, max_batch < 1), ENOMEM, ECUDA. */
+size_t lapssd_workspace_bytes(const lapssd_config *cfg, int32_t n_local, int32_t max_batch,
+                              int64_t V, int32_t world);
+lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req,
+                            int32_t max_batch, int64_t V, void *workspace,
+                            size_t workspace_bytes, lapssd_stream stream, lapssd_handle **out);
+lapssd_status lapssd_destroy(lapssd_handle *h);
+
+/* laps_update -- (a3) state update of the B verified slots:
+ * tokens += min(r+1, L_true - tokens) (AMB-18); accepted drafts += r; rounds += 1;
+ * E_i += k*T_SSM + T_LLM; ring of cumulative accepted drafts; if the request
+ * is non-perceptible and the cumulative acceptance rates a_s/(k s) of the last gamma
+ * rounds span < delta: A_i = their mean, perceptible, T~_i = Eq. 6 at
+ * L_pred, placement (AMB-14); otherwise demotion to the queue of E_i;
+ * completion when tokens >= L_true with C_i = now + round cost.
+ * sel: [device] int32 [B] local indices (-1 = empty slot); n_accept: [device] [B].
+ * Errors: EINVAL, ECUDA; updating a complete request sets the ESTATE flag. */
+lapssd_status laps_update(lapssd_handle *h, const int32_t *sel, const int32_t *n_accept,
+                          int32_t B, lapssd_stream stream);
+
+/* laps_select -- (a4-a7): if the previous batch was non-empty, now += k*T_SSM +
+ * T_LLM; admit every request with arrival <= now; build every resident
+ * request's 64-bit priority key (smaller = sooner; AMB-15/16/19):
+ *   [63] ineligible | [62] not pinned | [61:58] queue level | [57] non-perceptible |
+ *   [56] not running (non-perceptible) | [55:24] T~_rem us saturated (perceptible) or
+ *   policy secondary | [23:0] global id
+ * and write the B smallest eligible keys' local indices in ascending key order to
+ * sel_out [device int32 B] (-1 padded), their count to count_out [device int32,
+ * nullable].  Selected requests get x_i = now on first selection and are pinned per
+ * pin_rule.  If nothing is eligible, now jumps to the next arrival.
+ * Errors: EINVAL (B > max_batch), ECUDA. */
+lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t *count_out,
+                          lapssd_stream stream);
+
+/* laps_step -- one fused step: spec_verify on the current batch sel_inout[B]
+ * (from the previous laps_select/laps_step), the laps_update of each verified
+ * request by the last CTA that finishes its row, then laps_select into sel_inout.
+ * rows: pooled or batch layout (lapssd_rows).  tokens_out [device, B x (k+1)],
+ * n_accept_out [device, B] are nullable.  count_out as in laps_select.
+ * Errors: EINVAL, ECUDA. */
+lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel_inout,
+                        int32_t *count_out, int32_t *tokens_out, int32_t *n_accept_out,
+                        lapssd_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU (a8): requests are sharded by global id mod world; every rank keeps the
+ * same global clock.  laps_candidates does laps_select's clock/admission/keys and
+ * writes this rank's C smallest eligible keys (ascending, UINT64_MAX padded) into
+ * cand_out[device u64, C+1]; cand_out[C] = this rank's next arrival time (as u64,
+ * UINT64_MAX if none).  After an all-gather of the world*(C+1) words,
+ * laps_merge takes the global top-B keys, keeps the ids with id % world == rank as
+ * this rank's batch (sel_out, key order) and advances the clock by the GLOBAL batch.
+ * laps_step_dist = verify + update + candidates + ncclAllGather (on `nccl_comm`, a
+ * ncclComm_t created by the caller) + merge.  NCCL is resolved at run time with
+ * dlopen("libnccl.so.2"); if unavailable the call returns ENCCL. */
+lapssd_status laps_candidates(lapssd_handle *h, int32_t C, uint64_t *cand_out,
+                              lapssd_stream stream);
+lapssd_status laps_merge(lapssd_handle *h, const uint64_t *all_cand, int32_t C, int32_t B,
+                         int32_t *sel_out, int32_t *count_out, lapssd_stream stream);
+lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_rows *rows,
+                             int32_t B_global, int32_t C, int32_t *sel_inout, int32_t *count_out,
+                             uint64_t *cand_scratch /* [device] (world+1)*(C+1) words */,
+                             lapssd_stream stream);
+/* C must be the same on every rank and world*C <= 16384: the caller passes
+ * C = min(B_global, max over ranks of n_local).  sel_inout has B_global slots.
+ * NCCL plumbing without torch internals: rank 0 calls lapssd_nccl_unique_id, the
+ * 128 bytes are broadcast over torch.distributed, every rank calls
+ * lapssd_nccl_comm_init. */
+lapssd_status lapssd_nccl_unique_id(uint8_t id_out[128]);
+lapssd_status lapssd_nccl_comm_init(void **comm_out, int32_t nranks, const uint8_t id[128],
+                                    int32_t rank);
+lapssd_status lapssd_nccl_comm_destroy(void *comm);
+
+/* ---------------------------------------------------------------------------
+ * State snapshot for parity and replay: D2H copies into caller-allocated [host]
+ * arrays (any pointer may be NULL to skip), then synchronises the stream. */
+typedef struct {
+    int64_t now_us;
+    int32_t cursor, prev_count;
+    int32_t *acc_tok, *acc_draft, *rounds;        /* n each            */
+    int64_t *E_us, *T_total_us, *C_us, *x_us;     /* n each            */
+    uint8_t *admitted, *done, *perceptible, *pinned, *level, *running; /* n each */
+    double *A;                                    /* n                 */
+    uint64_t *key;                                /* n: last select's keys */
+    int32_t *ring;                                /* n * gamma         */
+} lapssd_state_view;
+lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *host_out,
+                                lapssd_stream stream);
+
+/* Synchronises the handle's last stream; returns LAPSSD_ESTATE if the device flag
+ * is set (and the flag bits in *flags_out, nullable), else LAPSSD_OK. */
+lapssd_status lapssd_check(lapssd_handle *h, uint32_t *flags_out);
+
+/* Per-kernel timing of laps_step for the next max_steps calls: the library records
+ * CUDA events (host objects, created here) immediately before the verify kernel,
+ * between verify and select, and after select, on the call's stream.
+ * lapssd_profile_read synchronises and returns the summed verify / select times (ms)
+ * and the number of steps recorded; it also ends the profiling window.
+ * max_steps <= 0 disables profiling. */
+lapssd_status lapssd_profile(lapssd_handle *h, int32_t max_steps);
+lapssd_status lapssd_profile_read(lapssd_handle *h, double *verify_ms, double *select_ms,
+                                  int32_t *steps);
+
+/* Thread-local text of the last error ("" if none). */
+const char *lapssd_last_error(void);
+
+/* Number of kernel launches the library enqueued since load (evidence counter). */
+uint64_t lapssd_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAPSSD_H */

@@ -530,8 +530,9 @@ void orc_sim_update(orc_sim *s, const int32_t *sel, const int32_t *n_accept, int
             if (stable) {
                 s->perceptible[i] = 1;                                  /* P:137 */
                 s->A[i] = mean;                                         /* P:194, AMB-8 */
-                s->T_total[i] = (int64_t)orc_eq6(s->L_pred[i], mean, k, s->cfg.t_ssm_us,
-                                                 s->cfg.t_llm_us);      /* P:139, Eq. 6 */
+                uint64_t T = orc_eq6(s->L_pred[i], mean, k, s->cfg.t_ssm_us,
+                                     s->cfg.t_llm_us);                  /* P:139, Eq. 6 */
+                s->T_total[i] = T > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)T;
                 if (s->cfg.placement == ORC_PLACE_BY_ESTIMATE)          /* P:148, AMB-14 */
                     s->level[i] = (uint8_t)level_of(s->S_up, K, s->T_total[i]);
                 if (s->cfg.pin_rule == ORC_PIN_ON_STABLE) s->pinned[i] = 1;

@@ -1,0 +1,317 @@
+"""paper_2505_17074_b200 -- B200-native LAPS-SD batched speculative-decoding step.
+
+Thin Python binding of ``liblapssd.so`` (C-ABI in ``include/lapssd.h``): argument
+marshalling only.  Every step of the hot path -- verification by rejection sampling
+(PAPER.md P:57-64), the LAPS-SD state update and the top-B
+selection -- runs in the library's sm_100a kernels.  PyTorch
+supplies device memory, streams and process groups.  There is no CPU fallback: if
+the library cannot be loaded, importing the binding raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liblapssd.so")
+
+F32, BF16 = 0, 1
+POL_LAPSSD, POL_FCFS, POL_LPSJF, POL_LAS = 0, 1, 2, 3
+STATUS = {0: "OK", -1: "EINVAL", -2: "ECUDA", -3: "ENCCL", -4: "ESTATE", -5: "ENOMEM"}
+
+
+class LapssdError(RuntimeError):
+    def __init__(self, call, status, msg):
+        super().__init__(f"{call}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Config(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("K", C.c_int32), ("s1_up_us", C.c_int64),
+                ("M", C.c_double), ("gamma", C.c_int32), ("delta", C.c_double),
+                ("k", C.c_int32), ("t_ssm_us", C.c_int64), ("t_llm_us", C.c_int64),
+                ("placement", C.c_int32), ("pin_rule", C.c_int32), ("seed", C.c_uint64)]
+
+
+class _Requests(C.Structure):
+    _fields_ = [("arrival_us", C.c_void_p), ("L_true", C.c_void_p), ("L_pred", C.c_void_p),
+                ("n", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32)]
+
+
+class _Rows(C.Structure):
+    _fields_ = [("p", C.c_void_p), ("q", C.c_void_p), ("draft", C.c_void_p),
+                ("dtype", C.c_int32), ("k", C.c_int32), ("V", C.c_int64),
+                ("slab_tab", C.c_void_p), ("R", C.c_int32), ("n_slabs", C.c_int64)]
+
+
+class _StateView(C.Structure):
+    _fields_ = [("now_us", C.c_int64), ("cursor", C.c_int32), ("prev_count", C.c_int32)] + [
+        (n, C.c_void_p) for n in ("acc_tok", "acc_draft", "rounds", "E_us", "T_total_us", "C_us",
+                                  "x_us", "admitted", "done", "perceptible", "pinned", "level",
+                                  "running", "A", "key", "ring")]
+
+
+def _load():
+    if not os.path.exists(_SO):
+        raise ImportError(f"{_SO} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`"
+                          " (nvcc sm_100a build).  There is no CPU fallback.")
+    lib = C.CDLL(_SO)
+    vp, i32, i64, u32, u64, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_size_t
+    sigs = {
+        "spec_verify_workspace_bytes": ([i32, i64], sz),
+        "spec_verify": ([vp, vp, i32, i64, i32, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp, vp, sz, vp], i32),
+        "lapssd_workspace_bytes": ([vp, i32, i32, i64, i32], sz),
+        "lapssd_create": ([vp, vp, i32, i64, vp, sz, vp, vp], i32),
+        "lapssd_destroy": ([vp], i32),
+        "laps_update": ([vp, vp, vp, i32, vp], i32),
+        "laps_select": ([vp, i32, vp, vp, vp], i32),
+        "laps_step": ([vp, vp, i32, vp, vp, vp, vp, vp], i32),
+        "laps_candidates": ([vp, i32, vp, vp], i32),
+        "laps_merge": ([vp, vp, i32, i32, vp, vp, vp], i32),
+        "laps_step_dist": ([vp, vp, vp, i32, i32, vp, vp, vp, vp], i32),
+        "lapssd_nccl_unique_id": ([vp], i32),
+        "lapssd_nccl_comm_init": ([vp, i32, vp, i32], i32),
+        "lapssd_nccl_comm_destroy": ([vp], i32),
+        "lapssd_read_state": ([vp, vp, vp], i32),
+        "lapssd_check": ([vp, vp], i32),
+        "lapssd_profile": ([vp, i32], i32),
+        "lapssd_profile_read": ([vp, vp, vp, vp], i32),
+        "lapssd_last_error": ([], C.c_char_p),
+        "lapssd_launch_count": ([], u64),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+_lib = _load()
+
+
+def library_path() -> str:
+    return _SO
+
+
+def launch_count() -> int:
+    """Kernel launches the library has enqueued in this process."""
+    return int(_lib.lapssd_launch_count())
+
+
+def _check(call, rc):
+    if rc != 0:
+        raise LapssdError(call, rc, _lib.lapssd_last_error().decode())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "device tensors must be contiguous CUDA tensors"
+    return C.c_void_p(t.data_ptr())
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return F32
+    raise TypeError(f"rows must be bf16 or fp32, got {t.dtype}")
+
+
+# --------------------------------------------------------------------------- stateless
+def spec_verify_workspace_bytes(B: int, V: int) -> int:
+    return int(_lib.spec_verify_workspace_bytes(B, V))
+
+
+def spec_verify(p, q, draft, req_id, round_idx, seed, *, slab=None, trace=0, tokens=None,
+                n_accept=None, z=None, workspace=None, stream=None):
+    """Batched verification (include/lapssd.h spec_verify).  p [S,k+1,V], q [S,k,V]
+    (bf16/fp32), draft [S,k] int32, req_id / round_idx [B] int32 (uint32 values);
+    slab [B] int32 selects rows (None: slot b reads rows b).  Returns
+    (tokens [B,k+1], n_accept [B], z [B] uint64-as-int64)."""
+    k, V = q.shape[-2], q.shape[-1]
+    B = req_id.numel()
+    dev = p.device
+    if tokens is None:
+        tokens = torch.empty(B, k + 1, dtype=torch.int32, device=dev)
+    if n_accept is None:
+        n_accept = torch.empty(B, dtype=torch.int32, device=dev)
+    if z is None:
+        z = torch.empty(B, dtype=torch.int64, device=dev)
+    ws_bytes = spec_verify_workspace_bytes(B, V)
+    if workspace is None:
+        workspace = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
+    rc = _lib.spec_verify(_dptr(p), _dptr(q), _dtype_code(p), V, k, _dptr(draft), _dptr(slab),
+                          _dptr(req_id), _dptr(round_idx), B, seed & (2**64 - 1), trace,
+                          _dptr(tokens), _dptr(n_accept), _dptr(z), _dptr(workspace),
+                          workspace.numel(), _stream(stream))
+    _check("spec_verify", rc)
+    return tokens, n_accept, z
+
+
+# --------------------------------------------------------------------------- handle
+@dataclass
+class SchedConfig:
+    """lapssd_config; defaults are DESIGN.md readings (K=4, M=2, gamma=5, delta=.05)."""
+    policy: int = POL_LAPSSD
+    K: int = 4
+    s1_up_us: int = 56_000
+    M: float = 2.0
+    gamma: int = 5
+    delta: float = 0.05
+    k: int = 4
+    t_ssm_us: int = 1_000
+    t_llm_us: int = 10_000
+    placement: int = 0
+    pin_rule: int = 0
+    seed: int = 0
+
+    def c(self):
+        return _Config(self.policy, self.K, self.s1_up_us, self.M, self.gamma, self.delta,
+                       self.k, self.t_ssm_us, self.t_llm_us, self.placement, self.pin_rule,
+                       self.seed & (2**64 - 1))
+
+
+class Rows:
+    """lapssd_rows: pooled (slab_tab given) or batch layout, device tensors."""
+
+    def __init__(self, p, q, draft, slab_tab=None):
+        self.p, self.q, self.draft, self.slab_tab = p, q, draft, slab_tab
+        self.k, self.V = q.shape[-2], q.shape[-1]
+        self.c = _Rows(p.data_ptr(), q.data_ptr(), draft.data_ptr(), _dtype_code(p), self.k, self.V,
+                       slab_tab.data_ptr() if slab_tab is not None else None,
+                       slab_tab.shape[1] if slab_tab is not None else 0, p.shape[0])
+
+
+class Handle:
+    """A LAPS-SD resident-request state on one GPU (lapssd_create)."""
+
+    def __init__(self, cfg: SchedConfig, arrival_us, L_true, L_pred, *, max_batch: int, V: int,
+                 rank: int = 0, world: int = 1, device="cuda", stream=None):
+        self.cfg = cfg
+        self._cc = cfg.c()
+        a = np.ascontiguousarray(arrival_us, np.int64)
+        lt = np.ascontiguousarray(L_true, np.int32)
+        lp = np.ascontiguousarray(L_pred, np.int32)
+        self.n = len(a)
+        self.max_batch, self.V, self.rank, self.world = max_batch, V, rank, world
+        req = _Requests(a.ctypes.data, lt.ctypes.data, lp.ctypes.data, self.n, rank, world)
+        nbytes = int(_lib.lapssd_workspace_bytes(C.byref(self._cc), self.n, max_batch, V, world))
+        if nbytes == 0:
+            raise LapssdError("lapssd_workspace_bytes", -1, "invalid sizes")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        h = C.c_void_p()
+        rc = _lib.lapssd_create(C.byref(self._cc), C.byref(req), max_batch, V,
+                                _dptr(self.workspace), nbytes, _stream(stream), C.byref(h))
+        _check("lapssd_create", rc)
+        self.h = h
+        self.sel = torch.full((max_batch,), -1, dtype=torch.int32, device=device)
+        self.count = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lapssd_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    # -- the four hot-path calls --------------------------------------------------
+    def laps_update(self, sel, n_accept, stream=None):
+        _check("laps_update", _lib.laps_update(self.h, _dptr(sel), _dptr(n_accept), sel.numel(),
+                                               _stream(stream)))
+
+    def laps_select(self, B, sel=None, count=None, stream=None):
+        sel = self.sel if sel is None else sel
+        count = self.count if count is None else count
+        _check("laps_select", _lib.laps_select(self.h, B, _dptr(sel), _dptr(count), _stream(stream)))
+        return sel, count
+
+    def laps_step(self, rows: Rows, B, sel=None, count=None, tokens=None, n_accept=None, stream=None):
+        sel = self.sel if sel is None else sel
+        count = self.count if count is None else count
+        _check("laps_step", _lib.laps_step(self.h, C.byref(rows.c), B, _dptr(sel), _dptr(count),
+                                           _dptr(tokens), _dptr(n_accept), _stream(stream)))
+        return sel, count
+
+    # -- multi-GPU halves ------------------------------------------------------
+    def laps_candidates(self, Cn, cand_out, stream=None):
+        _check("laps_candidates", _lib.laps_candidates(self.h, Cn, _dptr(cand_out), _stream(stream)))
+
+    def laps_merge(self, all_cand, Cn, B, sel=None, count=None, stream=None):
+        sel = self.sel if sel is None else sel
+        count = self.count if count is None else count
+        _check("laps_merge", _lib.laps_merge(self.h, _dptr(all_cand), Cn, B, _dptr(sel),
+                                             _dptr(count), _stream(stream)))
+        return sel, count
+
+    def laps_step_dist(self, comm, rows: Rows, B_global, Cn, cand_scratch, sel=None, count=None,
+                       stream=None):
+        sel = self.sel if sel is None else sel
+        count = self.count if count is None else count
+        _check("laps_step_dist", _lib.laps_step_dist(self.h, comm, C.byref(rows.c), B_global, Cn,
+                                                     _dptr(sel), _dptr(count), _dptr(cand_scratch),
+                                                     _stream(stream)))
+        return sel, count
+
+    # -- snapshot -----------------------------------------------------------------
+    def state(self, stream=None) -> dict:
+        n, g = self.n, self.cfg.gamma
+        arrs = dict(acc_tok=np.zeros(n, np.int32), acc_draft=np.zeros(n, np.int32),
+                    rounds=np.zeros(n, np.int32), E_us=np.zeros(n, np.int64),
+                    T_total_us=np.zeros(n, np.int64), C_us=np.zeros(n, np.int64),
+                    x_us=np.zeros(n, np.int64), admitted=np.zeros(n, np.uint8),
+                    done=np.zeros(n, np.uint8), perceptible=np.zeros(n, np.uint8),
+                    pinned=np.zeros(n, np.uint8), level=np.zeros(n, np.uint8),
+                    running=np.zeros(n, np.uint8), A=np.zeros(n, np.float64),
+                    key=np.zeros(n, np.uint64), ring=np.zeros((n, g), np.int32))
+        v = _StateView(0, 0, 0, *[arrs[f].ctypes.data for f, _ in _StateView._fields_[3:]])
+        _check("lapssd_read_state", _lib.lapssd_read_state(self.h, C.byref(v), _stream(stream)))
+        arrs.update(now_us=v.now_us, cursor=v.cursor, prev_count=v.prev_count)
+        return arrs
+
+    def profile(self, max_steps: int):
+        """Record verify / select kernel times for the next max_steps laps_step calls."""
+        _check("lapssd_profile", _lib.lapssd_profile(self.h, max_steps))
+
+    def profile_read(self):
+        v, s, n = C.c_double(), C.c_double(), C.c_int32()
+        _check("lapssd_profile_read", _lib.lapssd_profile_read(self.h, C.byref(v), C.byref(s),
+                                                               C.byref(n)))
+        return v.value, s.value, n.value
+
+    def check(self):
+        flags = C.c_uint32()
+        rc = _lib.lapssd_check(self.h, C.byref(flags))
+        _check("lapssd_check", rc)
+        return flags.value
+
+
+# --------------------------------------------------------------------------- NCCL plumbing
+def nccl_comm(group=None):
+    """Create a NCCL communicator for the library's all-gather: rank 0 draws the
+    unique id, torch.distributed broadcasts it, every rank initialises."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    buf = (C.c_uint8 * 128)()
+    if rank == 0:
+        _check("lapssd_nccl_unique_id", _lib.lapssd_nccl_unique_id(buf))
+    t = torch.tensor(list(bytes(buf)), dtype=torch.uint8,
+                     device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+    dist.broadcast(t, 0, group=group)
+    ids = (C.c_uint8 * 128)(*t.cpu().tolist())
+    comm = C.c_void_p()
+    _check("lapssd_nccl_comm_init", _lib.lapssd_nccl_comm_init(C.byref(comm), world, ids, rank))
+    return comm
+
+
+def nccl_comm_destroy(comm):
+    _check("lapssd_nccl_comm_destroy", _lib.lapssd_nccl_comm_destroy(comm))

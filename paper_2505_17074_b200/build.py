@@ -1,0 +1,51 @@
+"""Build liblapssd.so (sm_100a) in-tree with nvcc.  No JIT, no torch extension."""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+SO = os.path.join(HERE, "liblapssd.so")
+SOURCES = ["api.cu", "verify.cu", "sched.cu"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-fmad=false",            # scheduler fp64 must not contract; verify uses _rn intrinsics
+    "-Xcompiler", "-fPIC,-O2",
+    "-Xptxas", "-v",
+    "-shared",
+]
+
+
+def sources():
+    return [os.path.join(CSRC, s) for s in SOURCES]
+
+
+def stale() -> bool:
+    if not os.path.exists(SO):
+        return True
+    t = os.path.getmtime(SO)
+    deps = sources() + [os.path.join(CSRC, "lapssd_internal.cuh"),
+                        os.path.join(HERE, "..", "include", "lapssd.h")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not stale():
+        return SO
+    cmd = [NVCC, *FLAGS, "-o", SO, *sources(), "-ldl"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building liblapssd.so")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    return SO
+
+
+if __name__ == "__main__":
+    build(force=True, verbose=True)
+    print(SO)

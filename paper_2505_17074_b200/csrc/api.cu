@@ -1,0 +1,524 @@
+// api.cu -- the C-ABI of liblapssd.so (include/lapssd.h): validation, workspace
+// carving, kernel orchestration, state snapshot, errors, and the NCCL all-gather of
+// the multi-GPU step (resolved at run time with dlopen).
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lapssd_internal.cuh"
+
+using namespace lapssd;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+lapssd_status fail(lapssd_status st, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+lapssd_status fail(lapssd_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+lapssd_status cuda_status(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return LAPSSD_OK;
+    return fail(LAPSSD_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int32_t n_chunks_of(int64_t V) { return (int32_t)((V + kTile - 1) / kTile); }
+
+bool rows_ok(int32_t dtype, int64_t V, int32_t k, const void *p, const void *q) {
+    if (dtype != LAPSSD_F32 && dtype != LAPSSD_BF16) return false;
+    const int64_t esz = dtype == LAPSSD_BF16 ? 2 : 4;
+    if (V < 1 || (V * esz) % 16 != 0 || V > (int64_t)kMaxChunks * kTile) return false;
+    if (k < 1 || k > 16) return false;
+    if (((uintptr_t)p | (uintptr_t)q) & 15) return false;
+    return true;
+}
+
+// Carves a workspace in a fixed order; used both to size and to place.
+struct Carver {
+    char *base;
+    size_t off = 0;
+    template <typename T>
+    T *take(size_t count) {
+        off = align256(off);
+        T *ptr = base ? reinterpret_cast<T *>(base + off) : nullptr;
+        off += count * sizeof(T);
+        return ptr;
+    }
+};
+
+}  // namespace
+
+namespace lapssd {
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+}  // namespace lapssd
+
+struct lapssd_handle {
+    State st;
+    Sched sc;
+    int32_t max_batch;
+    int64_t V;
+    int32_t n_chunks;
+    uint64_t *part;
+    uint32_t *counter;
+    int32_t *tokens;       // internal outputs when the caller passes NULL
+    int32_t *n_accept;
+    cudaStream_t last_stream;
+    // profiling window (lapssd_profile): 3 events per recorded step
+    std::vector<cudaEvent_t> prof_events;
+    int32_t prof_max = 0, prof_used = 0;
+    ~lapssd_handle() {
+        for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
+    }
+};
+
+static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma, int32_t max_batch,
+                         int32_t n_chunks, int32_t k) {
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    State &st = h->st;
+    st.g = cv.take<Globals>(1);
+    st.arrival = cv.take<int64_t>(nn);
+    st.L_true = cv.take<int32_t>(nn);
+    st.L_pred = cv.take<int32_t>(nn);
+    st.acc_tok = cv.take<int32_t>(nn);
+    st.acc_draft = cv.take<int32_t>(nn);
+    st.rounds = cv.take<int32_t>(nn);
+    st.ring = cv.take<int32_t>(nn * (size_t)gamma);
+    st.E = cv.take<int64_t>(nn);
+    st.T_total = cv.take<int64_t>(nn);
+    st.A = cv.take<double>(nn);
+    st.flags = cv.take<uint32_t>(nn);
+    st.key = cv.take<uint64_t>(nn);
+    st.C = cv.take<int64_t>(nn);   // C and x are initialised to -1 (contiguous)
+    st.x = cv.take<int64_t>(nn);
+    h->part = cv.take<uint64_t>((size_t)max_batch * n_chunks * kPartWords);
+    h->counter = cv.take<uint32_t>((size_t)max_batch);
+    h->tokens = cv.take<int32_t>((size_t)max_batch * (k + 1));
+    h->n_accept = cv.take<int32_t>((size_t)max_batch);
+}
+
+static lapssd_status check_config(const lapssd_config *c) {
+    if (!c) return fail(LAPSSD_EINVAL, "config is NULL");
+    if (c->policy < 0 || c->policy > 3) return fail(LAPSSD_EINVAL, "policy %d", c->policy);
+    if (c->K < 1 || c->K > 16) return fail(LAPSSD_EINVAL, "K=%d outside 1..16", c->K);
+    if (c->s1_up_us <= 0) return fail(LAPSSD_EINVAL, "s1_up_us must be > 0");
+    if (!(c->M > 1.0)) return fail(LAPSSD_EINVAL, "M must be > 1");
+    if (c->gamma < 2) return fail(LAPSSD_EINVAL, "gamma must be >= 2");
+    if (!(c->delta >= 0.0)) return fail(LAPSSD_EINVAL, "delta must be >= 0");
+    if (c->k < 1 || c->k > 16) return fail(LAPSSD_EINVAL, "k=%d outside 1..16", c->k);
+    if (c->t_ssm_us < 0 || c->t_llm_us < 0) return fail(LAPSSD_EINVAL, "negative round cost");
+    if (c->placement < 0 || c->placement > 1 || c->pin_rule < 0 || c->pin_rule > 1)
+        return fail(LAPSSD_EINVAL, "placement / pin_rule");
+    return LAPSSD_OK;
+}
+
+extern "C" {
+
+const char *lapssd_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t lapssd_launch_count(void) { return g_launches.load(); }
+
+// ---------------------------------------------------------------- spec_verify
+size_t spec_verify_workspace_bytes(int32_t B, int64_t V) {
+    if (B < 0 || V < 1) return 0;
+    Carver cv{nullptr};
+    cv.take<uint64_t>((size_t)(B > 0 ? B : 1) * n_chunks_of(V) * kPartWords);
+    cv.take<uint32_t>((size_t)(B > 0 ? B : 1));
+    return align256(cv.off);
+}
+
+lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V, int32_t k,
+                          const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
+                          const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,
+                          int32_t *tokens, int32_t *n_accept, uint64_t *z_fixed, void *workspace,
+                          size_t workspace_bytes, lapssd_stream stream) {
+    g_last_error.clear();
+    if (B < 0) return fail(LAPSSD_EINVAL, "B < 0");
+    if (!rows_ok(dtype, V, k, p, q)) return fail(LAPSSD_EINVAL, "rows: dtype/V/k/alignment");
+    if (B == 0) return LAPSSD_OK;
+    if (!p || !q || !draft || !req_id || !round_idx || !tokens || !n_accept || !workspace)
+        return fail(LAPSSD_EINVAL, "NULL pointer argument");
+    if (workspace_bytes < spec_verify_workspace_bytes(B, V))
+        return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes,
+                    spec_verify_workspace_bytes(B, V));
+    VerifyArgs a{};
+    a.p = p; a.q = q; a.draft = draft; a.V = V; a.k = k; a.n_chunks = n_chunks_of(V);
+    a.slab = slab; a.req_id = req_id; a.round_idx = round_idx;
+    a.seed = seed; a.trace = trace;
+    a.tokens = tokens; a.n_accept = n_accept; a.z = z_fixed;
+    Carver cv{(char *)workspace};
+    a.part = cv.take<uint64_t>((size_t)B * a.n_chunks * kPartWords);
+    a.counter = cv.take<uint32_t>((size_t)B);
+    a.fuse_update = 0;
+    return cuda_status(launch_verify(a, dtype, B, (cudaStream_t)stream), "spec_verify launch");
+}
+
+// ---------------------------------------------------------------- handle
+size_t lapssd_workspace_bytes(const lapssd_config *cfg, int32_t n_local, int32_t max_batch, int64_t V,
+                              int32_t world) {
+    (void)world;
+    if (!cfg || n_local < 0 || max_batch < 1 || V < 1) return 0;
+    lapssd_handle tmp{};
+    Carver cv{nullptr};
+    carve_handle(cv, &tmp, n_local, cfg->gamma > 0 ? cfg->gamma : 1, max_batch, n_chunks_of(V),
+                 cfg->k > 0 ? cfg->k : 1);
+    return align256(cv.off);
+}
+
+lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req, int32_t max_batch,
+                            int64_t V, void *workspace, size_t workspace_bytes, lapssd_stream stream,
+                            lapssd_handle **out) {
+    g_last_error.clear();
+    if (!out) return fail(LAPSSD_EINVAL, "out is NULL");
+    *out = nullptr;
+    lapssd_status st = check_config(cfg);
+    if (st != LAPSSD_OK) return st;
+    if (!req || req->n < 0 || req->world < 1 || req->rank < 0 || req->rank >= req->world)
+        return fail(LAPSSD_EINVAL, "requests: n / rank / world");
+    if (req->n > 0 && (!req->arrival_us || !req->L_true || !req->L_pred))
+        return fail(LAPSSD_EINVAL, "requests: NULL arrays");
+    if ((int64_t)req->n * req->world + req->rank > (1 << 24))
+        return fail(LAPSSD_EINVAL, "global ids must be < 2^24");
+    if (req->n > sort_capacity())
+        return fail(LAPSSD_EINVAL, "n_local=%d exceeds the single-CTA select capacity %d", req->n,
+                    sort_capacity());
+    if (max_batch < 1) return fail(LAPSSD_EINVAL, "max_batch < 1");
+    if (V < 1 || V > (int64_t)kMaxChunks * kTile) return fail(LAPSSD_EINVAL, "V out of range");
+    for (int32_t i = 0; i < req->n; ++i) {
+        if (req->L_true[i] < 1 || req->L_pred[i] < 1) return fail(LAPSSD_EINVAL, "L < 1 at %d", i);
+        if (i > 0 && req->arrival_us[i] < req->arrival_us[i - 1])
+            return fail(LAPSSD_EINVAL, "arrivals not sorted at %d", i);
+    }
+    const size_t need = lapssd_workspace_bytes(cfg, req->n, max_batch, V, req->world);
+    if (!workspace || workspace_bytes < need)
+        return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes, need);
+
+    lapssd_handle *h = new lapssd_handle{};
+    Carver cv{(char *)workspace};
+    carve_handle(cv, h, req->n, cfg->gamma, max_batch, n_chunks_of(V), cfg->k);
+    h->max_batch = max_batch;
+    h->V = V;
+    h->n_chunks = n_chunks_of(V);
+    Sched &sc = h->sc;
+    sc.policy = cfg->policy; sc.K = cfg->K; sc.gamma = cfg->gamma; sc.k = cfg->k;
+    sc.placement = cfg->placement; sc.pin_rule = cfg->pin_rule;
+    sc.n = req->n; sc.rank = req->rank; sc.world = req->world;
+    sc.delta = cfg->delta;
+    sc.t_ssm_us = cfg->t_ssm_us; sc.t_llm_us = cfg->t_llm_us;
+    sc.c_round_us = (int64_t)cfg->k * cfg->t_ssm_us + cfg->t_llm_us;   // S:194, Eq. 6 denominators
+    sc.seed = cfg->seed;
+    // S_j^up = M^(j-1) S_1^up; zero-based S_up[j] = floor(s1_up * M^j), M^j by
+    // iterative fp64 multiplication (AMB-11).
+    double m = 1.0;
+    for (int j = 0; j < 16; ++j) {
+        if (j < cfg->K - 1) {
+            const double s = (double)cfg->s1_up_us * m;
+            sc.S_up[j] = s >= 9.2e18 ? INT64_MAX : (int64_t)std::floor(s);
+            m = m * cfg->M;
+        } else {
+            sc.S_up[j] = INT64_MAX;
+        }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last_stream = s;
+    cudaError_t e = cudaMemsetAsync(workspace, 0, need, s);
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(h->st.C, 0xFF, (size_t)((char *)(h->st.x + (req->n > 0 ? req->n : 1)) -
+                                                   (char *)h->st.C), s);
+    if (e == cudaSuccess && req->n > 0) {
+        e = cudaMemcpyAsync((void *)h->st.arrival, req->arrival_us, sizeof(int64_t) * req->n,
+                            cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync((void *)h->st.L_true, req->L_true, sizeof(int32_t) * req->n,
+                                cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync((void *)h->st.L_pred, req->L_pred, sizeof(int32_t) * req->n,
+                                cudaMemcpyHostToDevice, s);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host arrays may be freed on return
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_status(e, "lapssd_create");
+    }
+    *out = h;
+    return LAPSSD_OK;
+}
+
+lapssd_status lapssd_destroy(lapssd_handle *h) {
+    delete h;
+    return LAPSSD_OK;
+}
+
+// ---------------------------------------------------------------- a3 / a4-a7
+lapssd_status laps_update(lapssd_handle *h, const int32_t *sel, const int32_t *n_accept, int32_t B,
+                          lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || B < 0 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
+    if (B > 0 && (!sel || !n_accept)) return fail(LAPSSD_EINVAL, "NULL sel / n_accept");
+    h->last_stream = (cudaStream_t)stream;
+    return cuda_status(launch_update(h->st, h->sc, sel, n_accept, B, (cudaStream_t)stream), "laps_update");
+}
+
+lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t *count_out,
+                          lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || B < 1 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
+    if (!sel_out) return fail(LAPSSD_EINVAL, "sel_out is NULL");
+    h->last_stream = (cudaStream_t)stream;
+    return cuda_status(launch_select(h->st, h->sc, B, sel_out, count_out, (cudaStream_t)stream),
+                       "laps_select");
+}
+
+static lapssd_status fill_step_verify(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel,
+                                      int32_t *tokens_out, int32_t *n_accept_out, VerifyArgs &a) {
+    if (!rows) return fail(LAPSSD_EINVAL, "rows is NULL");
+    if (rows->k != h->sc.k) return fail(LAPSSD_EINVAL, "rows.k=%d != config k=%d", rows->k, h->sc.k);
+    if (!rows_ok(rows->dtype, rows->V, rows->k, rows->p, rows->q) || rows->V > h->V)
+        return fail(LAPSSD_EINVAL, "rows: dtype/V/alignment");
+    if (!rows->p || !rows->q || !rows->draft) return fail(LAPSSD_EINVAL, "rows: NULL pointer");
+    if (rows->slab_tab && rows->R < 1) return fail(LAPSSD_EINVAL, "rows.R < 1");
+    if (!sel) return fail(LAPSSD_EINVAL, "sel is NULL");
+    a = VerifyArgs{};
+    a.p = rows->p; a.q = rows->q; a.draft = rows->draft; a.V = rows->V; a.k = rows->k;
+    a.n_chunks = n_chunks_of(rows->V);
+    a.sel = sel; a.slab_tab = rows->slab_tab; a.R = rows->R;
+    a.seed = h->sc.seed; a.trace = 0;
+    a.tokens = tokens_out ? tokens_out : h->tokens;
+    a.n_accept = n_accept_out ? n_accept_out : h->n_accept;
+    a.z = nullptr;
+    a.part = h->part; a.counter = h->counter;
+    a.fuse_update = 1;
+    a.st = h->st; a.sc = h->sc;
+    (void)B;
+    return LAPSSD_OK;
+}
+
+lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel_inout,
+                        int32_t *count_out, int32_t *tokens_out, int32_t *n_accept_out,
+                        lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || B < 1 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
+    VerifyArgs a;
+    lapssd_status st = fill_step_verify(h, rows, B, sel_inout, tokens_out, n_accept_out, a);
+    if (st != LAPSSD_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last_stream = s;
+    cudaEvent_t *ev = nullptr;
+    if (h->prof_used < h->prof_max) ev = &h->prof_events[3 * (size_t)h->prof_used++];
+    if (ev) cudaEventRecord(ev[0], s);
+    st = cuda_status(launch_verify(a, rows->dtype, B, s), "laps_step verify");
+    if (st != LAPSSD_OK) return st;
+    if (ev) cudaEventRecord(ev[1], s);
+    st = cuda_status(launch_select(h->st, h->sc, B, sel_inout, count_out, s), "laps_step select");
+    if (ev) cudaEventRecord(ev[2], s);
+    return st;
+}
+
+lapssd_status lapssd_profile(lapssd_handle *h, int32_t max_steps) {
+    g_last_error.clear();
+    if (!h) return fail(LAPSSD_EINVAL, "handle is NULL");
+    for (cudaEvent_t e : h->prof_events) cudaEventDestroy(e);
+    h->prof_events.clear();
+    h->prof_used = 0;
+    h->prof_max = max_steps > 0 ? max_steps : 0;
+    h->prof_events.resize(3 * (size_t)h->prof_max);
+    for (auto &e : h->prof_events) {
+        const cudaError_t err = cudaEventCreate(&e);
+        if (err != cudaSuccess) { h->prof_max = 0; return cuda_status(err, "cudaEventCreate"); }
+    }
+    return LAPSSD_OK;
+}
+
+lapssd_status lapssd_profile_read(lapssd_handle *h, double *verify_ms, double *select_ms, int32_t *steps) {
+    g_last_error.clear();
+    if (!h) return fail(LAPSSD_EINVAL, "handle is NULL");
+    double v = 0.0, sl = 0.0;
+    for (int32_t i = 0; i < h->prof_used; ++i) {
+        cudaEvent_t *ev = &h->prof_events[3 * (size_t)i];
+        float a = 0.f, b = 0.f;
+        cudaError_t e = cudaEventSynchronize(ev[2]);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&a, ev[0], ev[1]);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&b, ev[1], ev[2]);
+        if (e != cudaSuccess) return cuda_status(e, "lapssd_profile_read");
+        v += a;
+        sl += b;
+    }
+    if (verify_ms) *verify_ms = v;
+    if (select_ms) *select_ms = sl;
+    if (steps) *steps = h->prof_used;
+    h->prof_max = h->prof_used;   // close the window
+    return LAPSSD_OK;
+}
+
+// ---------------------------------------------------------------- a8
+lapssd_status laps_candidates(lapssd_handle *h, int32_t C, uint64_t *cand_out, lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || C < 1 || !cand_out) return fail(LAPSSD_EINVAL, "handle / C / cand_out");
+    h->last_stream = (cudaStream_t)stream;
+    return cuda_status(launch_candidates(h->st, h->sc, C, cand_out, (cudaStream_t)stream),
+                       "laps_candidates");
+}
+
+lapssd_status laps_merge(lapssd_handle *h, const uint64_t *all_cand, int32_t C, int32_t B, int32_t *sel_out,
+                         int32_t *count_out, lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || C < 1 || !all_cand || !sel_out || B < 1 || B > h->max_batch)
+        return fail(LAPSSD_EINVAL, "handle / C / B / pointers");
+    if ((int64_t)h->sc.world * C > sort_capacity())
+        return fail(LAPSSD_EINVAL, "world*C=%lld exceeds %d", (long long)h->sc.world * C, sort_capacity());
+    h->last_stream = (cudaStream_t)stream;
+    return cuda_status(launch_merge(h->st, h->sc, all_cand, C, B, sel_out, count_out, (cudaStream_t)stream),
+                       "laps_merge");
+}
+
+}  // extern "C"
+
+// NCCL entry points resolved at run time (the process's already-loaded libnccl --
+// torch's -- is preferred, so one NCCL serves both).
+namespace {
+typedef int (*nccl_allgather_t)(const void *, void *, size_t, int, void *, cudaStream_t);
+typedef int (*nccl_get_id_t)(void *);
+struct NcclId { char internal[128]; };
+typedef int (*nccl_init_rank_t)(void **, int, NcclId, int);
+typedef int (*nccl_destroy_t)(void *);
+typedef const char *(*nccl_errstr_t)(int);
+
+void *nccl_lib() {
+    static void *h = nullptr;
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    return h;
+}
+template <typename F>
+F nccl_sym(const char *name) {
+    void *l = nccl_lib();
+    return l ? reinterpret_cast<F>(dlsym(l, name)) : nullptr;
+}
+lapssd_status nccl_status(int rc, const char *what) {
+    if (rc == 0) return LAPSSD_OK;
+    auto es = nccl_sym<nccl_errstr_t>("ncclGetErrorString");
+    return fail(LAPSSD_ENCCL, "%s: %s", what, es ? es(rc) : "nccl error");
+}
+constexpr int kNcclUint64 = 5;
+}  // namespace
+
+extern "C" {
+
+lapssd_status lapssd_nccl_unique_id(uint8_t id_out[128]) {
+    auto f = nccl_sym<nccl_get_id_t>("ncclGetUniqueId");
+    if (!f) return fail(LAPSSD_ENCCL, "libnccl.so.2 not loadable");
+    NcclId id;
+    const int rc = f(&id);
+    if (rc == 0) memcpy(id_out, id.internal, 128);
+    return nccl_status(rc, "ncclGetUniqueId");
+}
+
+lapssd_status lapssd_nccl_comm_init(void **comm_out, int32_t nranks, const uint8_t id[128], int32_t rank) {
+    auto f = nccl_sym<nccl_init_rank_t>("ncclCommInitRank");
+    if (!f) return fail(LAPSSD_ENCCL, "libnccl.so.2 not loadable");
+    NcclId nid;
+    memcpy(nid.internal, id, 128);
+    return nccl_status(f(comm_out, nranks, nid, rank), "ncclCommInitRank");
+}
+
+lapssd_status lapssd_nccl_comm_destroy(void *comm) {
+    auto f = nccl_sym<nccl_destroy_t>("ncclCommDestroy");
+    if (!f) return fail(LAPSSD_ENCCL, "libnccl.so.2 not loadable");
+    return nccl_status(f(comm), "ncclCommDestroy");
+}
+
+lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_rows *rows, int32_t B_global,
+                             int32_t C, int32_t *sel_inout, int32_t *count_out, uint64_t *cand_scratch,
+                             lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || !nccl_comm || !cand_scratch || B_global < 1 || B_global > h->max_batch || C < 1)
+        return fail(LAPSSD_EINVAL, "handle / comm / scratch / B_global / C");
+    if ((int64_t)h->sc.world * C > sort_capacity())
+        return fail(LAPSSD_EINVAL, "world*C exceeds %d", sort_capacity());
+    auto allgather = nccl_sym<nccl_allgather_t>("ncclAllGather");
+    if (!allgather) return fail(LAPSSD_ENCCL, "ncclAllGather not found");
+    VerifyArgs a;
+    lapssd_status st = fill_step_verify(h, rows, B_global, sel_inout, nullptr, nullptr, a);
+    if (st != LAPSSD_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last_stream = s;
+    st = cuda_status(launch_verify(a, rows->dtype, B_global, s), "step_dist verify");
+    if (st != LAPSSD_OK) return st;
+    uint64_t *local = cand_scratch;
+    uint64_t *all = cand_scratch + (C + 1);
+    st = cuda_status(launch_candidates(h->st, h->sc, C, local, s), "step_dist candidates");
+    if (st != LAPSSD_OK) return st;
+    st = nccl_status(allgather(local, all, (size_t)(C + 1), kNcclUint64, nccl_comm, s), "ncclAllGather");
+    if (st != LAPSSD_OK) return st;
+    return cuda_status(launch_merge(h->st, h->sc, all, C, B_global, sel_inout, count_out, s), "step_dist merge");
+}
+
+// ---------------------------------------------------------------- snapshot / check
+lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *v, lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || !v) return fail(LAPSSD_EINVAL, "handle / view");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n = (size_t)h->sc.n;
+    Globals g{};
+    std::vector<uint32_t> flags(n);
+    cudaError_t e = cudaMemcpyAsync(&g, h->st.g, sizeof g, cudaMemcpyDeviceToHost, s);
+#define CP(dst, src, cnt)                                                                          \
+    if (e == cudaSuccess && (dst)) e = cudaMemcpyAsync((dst), (src), sizeof(*(dst)) * (cnt), cudaMemcpyDeviceToHost, s);
+    CP(v->acc_tok, h->st.acc_tok, n)
+    CP(v->acc_draft, h->st.acc_draft, n)
+    CP(v->rounds, h->st.rounds, n)
+    CP(v->E_us, h->st.E, n)
+    CP(v->T_total_us, h->st.T_total, n)
+    CP(v->C_us, h->st.C, n)
+    CP(v->x_us, h->st.x, n)
+    CP(v->A, h->st.A, n)
+    CP(v->key, h->st.key, n)
+    CP(v->ring, h->st.ring, n * h->sc.gamma)
+#undef CP
+    if (e == cudaSuccess && n) e = cudaMemcpyAsync(flags.data(), h->st.flags, 4 * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "lapssd_read_state");
+    v->now_us = g.now_us;
+    v->cursor = g.cursor;
+    v->prev_count = g.prev_count;
+    for (size_t i = 0; i < n; ++i) {
+        const uint32_t f = flags[i];
+        if (v->admitted) v->admitted[i] = (int32_t)i < g.cursor;
+        if (v->done) v->done[i] = (f & F_DONE) != 0;
+        if (v->perceptible) v->perceptible[i] = (f & F_PERC) != 0;
+        if (v->pinned) v->pinned[i] = (f & F_PINNED) != 0;
+        if (v->running) v->running[i] = (f & F_RUNNING) != 0;
+        if (v->level) v->level[i] = (uint8_t)((f & F_LEVEL_MASK) >> F_LEVEL_SHIFT);
+    }
+    return LAPSSD_OK;
+}
+
+lapssd_status lapssd_check(lapssd_handle *h, uint32_t *flags_out) {
+    g_last_error.clear();
+    if (!h) return fail(LAPSSD_EINVAL, "handle is NULL");
+    Globals g{};
+    cudaError_t e = cudaStreamSynchronize(h->last_stream);
+    if (e == cudaSuccess) e = cudaMemcpy(&g, h->st.g, sizeof g, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_status(e, "lapssd_check");
+    if (flags_out) *flags_out = g.err;
+    if (g.err) return fail(LAPSSD_ESTATE, "device contract violation flags 0x%x", g.err);
+    return LAPSSD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+// lapssd_internal.cuh -- device-side layout and helpers of liblapssd.so (sm_100a).
+//
+// Product code.  Written from PAPER.md (arXiv 2505.17074) and include/lapssd.h; it
+// shares nothing with oracle/.  "P:NN" = PAPER.md line NN, "AMB-n" = DESIGN.md s.3.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/lapssd.h"
+
+namespace lapssd {
+
+// ---------------------------------------------------------------- verify tiling
+// One CTA streams a TILE of one row (pair): 256 threads = 8 warps, each warp owns a
+// contiguous segment of 1024 elements; lane l of warp w loads the 16-byte vectors
+// w*SEG + j*32 + l (j = 0..J-1), so every warp-wide load is 512 contiguous bytes.
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSegElems = 1024;                 // elements per warp segment
+constexpr int kTile = kWarps * kSegElems;       // 8192 elements per CTA
+constexpr int kMaxChunks = 64;                  // V <= 524288
+constexpr int kPartWords = 1 + kWarps;          // chunk sum + 8 warp sums (u64)
+
+// ---------------------------------------------------------------- state flags
+enum : uint32_t {
+    F_DONE = 1u, F_PERC = 2u, F_PINNED = 4u, F_RUNNING = 8u,
+    F_LEVEL_SHIFT = 8u, F_LEVEL_MASK = 0xF00u,
+};
+enum : uint32_t {
+    E_UPDATE_DONE = 1u,    // update on a completed request
+    E_NO_MASS = 2u,        // a row with no probability mass at all
+    E_BAD_SLOT = 4u,       // slot refers to an out-of-range request
+};
+
+struct Globals {
+    int64_t now_us;
+    int32_t cursor;        // requests [0, cursor) are admitted (arrivals sorted)
+    int32_t prev_count;    // size of the batch that ran last (global for G > 1)
+    int32_t count;         // size of the batch just selected (this rank)
+    uint32_t err;          // sticky contract-violation flags
+    int32_t pad[2];
+};
+
+// Scheduler constants, passed by value to every kernel.
+struct Sched {
+    int32_t policy, K, gamma, k;
+    int32_t placement, pin_rule;
+    int32_t n, rank, world;
+    double delta;
+    int64_t t_ssm_us, t_llm_us, c_round_us;
+    int64_t S_up[16];
+    uint64_t seed;
+};
+
+// Resident-request SoA in the caller's workspace.
+struct State {
+    const int64_t *arrival;
+    const int32_t *L_true, *L_pred;
+    int32_t *acc_tok, *acc_draft, *rounds, *ring;
+    int64_t *E, *T_total, *C, *x;
+    double *A;
+    uint32_t *flags;
+    uint64_t *key;
+    Globals *g;
+};
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Salmon et al., SC'11.  Counter (c0..c3) = (request id, round, (tag<<8)|block,
+// trace), key = (seed lo, seed hi) (AMB-21).
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    }
+    return c;
+}
+
+// ---------------------------------------------------------------- Eq. (6)
+// floor( (L * (k T_SSM + T_LLM)) / (k A + 1) ), fp64 round-to-nearest ops in this
+// order (AMB-10).  Explicit _rn intrinsics: never contracted into an FMA.
+__device__ __forceinline__ uint64_t eq6_us(int64_t L, double A, const Sched &s) {
+    const double num = __dmul_rn((double)L, (double)s.c_round_us);
+    const double den = __dadd_rn(__dmul_rn((double)s.k, A), 1.0);
+    const double T = __ddiv_rn(num, den);
+    if (!(T > 0.0)) return 0;
+    if (T >= 1.8e19) return ~0ull;
+    return (uint64_t)T;
+}
+
+// Queue index of attained service / estimate x (AMB-11).
+__device__ __forceinline__ int32_t level_of(int64_t x, const Sched &s) {
+    int32_t lev = 0;
+    while (lev < s.K - 1 && x >= s.S_up[lev]) ++lev;
+    return lev;
+}
+
+__device__ __forceinline__ uint64_t sat32(uint64_t v) { return v > 0xFFFFFFFFull ? 0xFFFFFFFFull : v; }
+
+// The 64-bit priority key (include/lapssd.h, laps_select).  Smaller = sooner.
+__device__ __forceinline__ uint64_t build_key(const State &st, const Sched &s, int32_t i,
+                                              int32_t cursor, uint32_t fl) {
+    const uint64_t id = (uint64_t)(i * s.world + s.rank) & 0xFFFFFFull;
+    const uint64_t inelig = (i >= cursor || (fl & F_DONE)) ? 1 : 0;
+    const uint64_t pinned = (fl & F_PINNED) ? 1 : 0;
+    const uint64_t perc = (fl & F_PERC) ? 1 : 0;
+    const uint64_t running = (fl & F_RUNNING) ? 1 : 0;
+    const uint64_t level = (fl & F_LEVEL_MASK) >> F_LEVEL_SHIFT;
+    uint64_t unpinned = 0, lev = 0, nonperc = 0, notrun = 0, sec = 0;
+    switch (s.policy) {
+    case LAPSSD_POL_FCFS:                           // P:26, non-preemptive
+        unpinned = !pinned;
+        break;
+    case LAPSSD_POL_LPSJF:                          // P:276, SJF on L_pred
+        unpinned = !pinned;
+        sec = sat32((uint64_t)st.L_pred[i]);
+        break;
+    case LAPSSD_POL_LAS:
+        unpinned = 1; lev = level; nonperc = 1; notrun = !running;
+        break;
+    default:                                        // LAPS-SD
+        unpinned = !pinned; lev = level; nonperc = !perc;
+        if (perc) {
+            int64_t L_rem = (int64_t)st.L_pred[i] - st.acc_tok[i];     // AMB-12
+            if (L_rem < 0) L_rem = 0;
+            sec = sat32(eq6_us(L_rem, st.A[i], s));
+        } else {
+            notrun = !running;
+        }
+    }
+    return (inelig << 63) | (unpinned << 62) | ((lev & 15) << 58) | (nonperc << 57) |
+           (notrun << 56) | (sec << 24) | id;
+}
+
+// a3: the state update of local request i after a round with r accepted drafts.
+// P:170 (E_i), P:175 (demotion), P:176 + P:194 (stability, A_i), P:139 + P:198
+// (T~_i), P:148 (placement, AMB-14), P:177 (completion).  One thread per request.
+__device__ __forceinline__ void update_one(const State &st, const Sched &s, int32_t i, int32_t r,
+                                           int64_t now) {
+    uint32_t fl = st.flags[i];
+    if (fl & F_DONE) { atomicOr(&st.g->err, E_UPDATE_DONE); return; }
+    const int32_t Lt = st.L_true[i];
+    int32_t tok = st.acc_tok[i];
+    const int32_t emitted = r + 1;                  // r drafts + 1 resampled / bonus
+    const int32_t rem = Lt - tok;
+    tok += emitted < rem ? emitted : rem;           // clipped at L (AMB-18)
+    const int32_t acc = st.acc_draft[i] + r;        // AMB-4
+    const int32_t t = st.rounds[i] + 1;
+    const int64_t E = st.E[i] + s.c_round_us;
+    int32_t *ring = st.ring + (int64_t)i * s.gamma;
+    ring[t % s.gamma] = acc;
+    int32_t level = (int32_t)((fl & F_LEVEL_MASK) >> F_LEVEL_SHIFT);
+    bool demoted = false;
+    if (s.policy == LAPSSD_POL_LAPSSD && !(fl & F_PERC)) {
+        bool stable = false;
+        double mean = 0.0;
+        if (t >= s.gamma) {
+            double mx = -1.0, mn = 2.0, sum = 0.0;
+            for (int32_t sr = t - s.gamma + 1; sr <= t; ++sr) {          // oldest first
+                const double rate = __ddiv_rn((double)ring[sr % s.gamma],
+                                              (double)((int64_t)s.k * sr));
+                mx = rate > mx ? rate : mx;
+                mn = rate < mn ? rate : mn;
+                sum = __dadd_rn(sum, rate);
+            }
+            if (__dsub_rn(mx, mn) < s.delta) { stable = true; mean = __ddiv_rn(sum, (double)s.gamma); }
+        }
+        if (stable) {
+            fl |= F_PERC;
+            st.A[i] = mean;
+            const uint64_t T = eq6_us(st.L_pred[i], mean, s);
+            const int64_t Ts = T > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)T;
+            st.T_total[i] = Ts;
+            if (s.placement == 0) level = level_of(Ts, s);
+            if (s.pin_rule == 1) fl |= F_PINNED;
+        } else {
+            const int32_t lev = level_of(E, s);
+            if (lev > level) { level = lev; demoted = true; }
+        }
+    } else if (s.policy == LAPSSD_POL_LAS) {
+        const int32_t lev = level_of(E, s);
+        if (lev > level) { level = lev; demoted = true; }
+    }
+    if (tok >= Lt) {
+        fl |= F_DONE;
+        st.C[i] = now + s.c_round_us;
+    }
+    fl = (fl & ~(F_LEVEL_MASK | F_RUNNING)) | ((uint32_t)level << F_LEVEL_SHIFT);
+    if (!(fl & F_DONE) && !demoted) fl |= F_RUNNING;
+    st.acc_tok[i] = tok;
+    st.acc_draft[i] = acc;
+    st.rounds[i] = t;
+    st.E[i] = E;
+    st.flags[i] = fl;
+}
+
+__host__ __device__ __forceinline__ int32_t slab_round_index(int32_t t, int32_t R) {
+    const int32_t h = R / 2;
+    if (t < R) return t;
+    if (h == 0) return R - 1;
+    return h + (t - h) % h;
+}
+
+// ---------------------------------------------------------------- verify launch
+struct VerifyArgs {
+    const void *p;
+    const void *q;
+    const int32_t *draft;
+    int64_t V;
+    int32_t k;
+    int32_t n_chunks;
+    // slot addressing: stateless (sel == nullptr) or handle-driven
+    const int32_t *slab;        // stateless: slab per slot, nullable (identity)
+    const uint32_t *req_id;     // stateless
+    const uint32_t *round_idx;  // stateless
+    const int32_t *sel;         // handle: local request per slot (-1 empty)
+    const int32_t *slab_tab;    // handle: pooled rows (nullable: batch layout)
+    int32_t R;
+    uint64_t seed;
+    uint32_t trace;
+    int32_t *tokens;
+    int32_t *n_accept;
+    uint64_t *z;
+    uint64_t *part;             // [B][n_chunks][kPartWords]
+    uint32_t *counter;          // [B]
+    int32_t fuse_update;
+    State st;
+    Sched sc;
+};
+
+// host-side launchers (verify.cu / sched.cu)
+cudaError_t launch_verify(const VerifyArgs &a, int32_t dtype, int32_t B, cudaStream_t s);
+cudaError_t launch_update(const State &st, const Sched &sc, const int32_t *sel,
+                          const int32_t *n_accept, int32_t B, cudaStream_t s);
+cudaError_t launch_select(const State &st, const Sched &sc, int32_t B, int32_t *sel_out,
+                          int32_t *count_out, cudaStream_t s);
+cudaError_t launch_candidates(const State &st, const Sched &sc, int32_t C, uint64_t *cand_out,
+                              cudaStream_t s);
+cudaError_t launch_merge(const State &st, const Sched &sc, const uint64_t *all_cand, int32_t C,
+                         int32_t B, int32_t *sel_out, int32_t *count_out, cudaStream_t s);
+int sort_capacity();            // largest key count one select CTA can sort
+void count_launch(int n = 1);
+
+}  // namespace lapssd

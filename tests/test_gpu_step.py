@@ -1,0 +1,133 @@
+"""GPU parity of the fused step (laps_select + laps_step through the C-ABI) against the
+oracle simulation, step by step on the same seeded workload: the selected batch (in
+key order), every priority key, and every field of the per-request state are compared
+bit-exactly; A_i (fp64) is compared as bits."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ["acc_tok", "acc_draft", "rounds", "E_us", "T_total_us", "C_us", "x_us", "admitted",
+          "done", "perceptible", "pinned", "level", "running", "key", "ring"]
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2505_17074_b200 as lib
+    return lib
+
+
+def workload(n, V, k, dtype, seed, drift, R=16, arrival="poisson", rate=80.0, len_mu=np.log(40),
+             family="f2", n_buckets=8, variants=3):
+    tr = synth.make_trace(n, seed, arrival=arrival, rate_per_s=rate, len_mu=len_mu, len_sigma=0.6,
+                          len_min=4, len_max=400, beta_ab=(4, 2), drift=drift)
+    pool = synth.make_pool(family, V=V, k=k, dtype=dtype, n_buckets=n_buckets, variants=variants,
+                           seed=seed, device="cuda")
+    tab = synth.slab_table(tr, n_buckets, variants, R=R, seed=seed)
+    return tr, pool, tab
+
+
+def compare_state(g, o, step):
+    for f in FIELDS:
+        a, b = np.asarray(g[f]), np.asarray(o[f])
+        assert a.shape == b.shape and (a == b).all(), f"step {step}: field {f} differs"
+    assert (g["A"].view(np.uint64) == o["A"].view(np.uint64)).all(), f"step {step}: A differs"
+    for f in ("now_us", "cursor", "prev_count"):
+        assert g[f] == o[f], f"step {step}: {f} {g[f]} != {o[f]}"
+
+
+def run_lockstep(L, cfg_kw, tr, pool, tab, B, max_steps=5000, check_every=1):
+    gcfg = L.SchedConfig(**cfg_kw)
+    ocfg = oracle.SchedConfig(**cfg_kw)
+    h = L.Handle(gcfg, tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=pool.V)
+    sim = oracle.Sim(ocfg, tr.arrival_us, tr.L_true, tr.L_pred)
+    rows = L.Rows(pool.p, pool.q, pool.draft,
+                  torch.as_tensor(tab, dtype=torch.int32, device="cuda"))
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, tab.shape[1]
+    sel_o, _ = sim.select(B)
+    h.laps_select(B)
+    tokens = torch.empty(B, cfg_kw["k"] + 1, dtype=torch.int32, device="cuda")
+    nacc = torch.empty(B, dtype=torch.int32, device="cuda")
+    steps = 0
+    while True:
+        sel_g = h.sel[:B].cpu().numpy()
+        assert (sel_g == sel_o).all(), f"step {steps}: batch differs\n{sel_g}\n{sel_o}"
+        if steps % check_every == 0:
+            compare_state(h.state(), sim.state(), steps)
+        if sim.state()["done"].all():
+            break
+        h.laps_step(rows, B, tokens=tokens, n_accept=nacc)
+        cnt, tok_o, na_o, _ = sim.step(P, sel_o)
+        live = sel_g >= 0
+        assert (nacc.cpu().numpy()[live] == na_o[live]).all(), f"step {steps}: r differs"
+        assert (tokens.cpu().numpy()[live] == tok_o[live]).all(), f"step {steps}: tokens differ"
+        steps += 1
+        assert steps < max_steps
+    assert h.check() == 0
+    compare_state(h.state(), sim.state(), steps)
+    return steps
+
+
+BASE = dict(K=4, s1_up_us=56_000, M=2.0, gamma=5, delta=0.05, t_ssm_us=1000, t_llm_us=10_000)
+
+
+@pytest.mark.parametrize("policy", [0, 1, 2, 3])
+def test_step_parity_config2_shape(L, policy):
+    """configs[1] shape, scaled: Poisson arrivals, Beta acceptance, fp32, V=32000, k=4."""
+    tr, pool, tab = workload(160, 32000, 4, "f32", seed=0x5D0002 + policy, drift=False)
+    run_lockstep(L, dict(BASE, policy=policy, k=4, seed=11), tr, pool, tab, B=16)
+
+
+@pytest.mark.parametrize("B", [1, 8])
+def test_step_parity_config3_drift(L, B):
+    """configs[2] shape, scaled: drifting acceptance, bf16, V=32000, k=6, K=4."""
+    tr, pool, tab = workload(96, 32000, 6, "bf16", seed=0x5D0003 + B, drift=True)
+    run_lockstep(L, dict(BASE, k=6, seed=5), tr, pool, tab, B=B, check_every=3)
+
+
+@pytest.mark.parametrize("kw", [dict(placement=1), dict(pin_rule=1), dict(K=1, delta=0.0),
+                                dict(gamma=3, delta=0.2), dict(K=16, M=1.5, s1_up_us=5000)])
+def test_step_parity_variants(L, kw):
+    tr, pool, tab = workload(80, 2048, 4, "bf16", seed=77, drift=True)
+    run_lockstep(L, dict(BASE, k=4, seed=3, **kw), tr, pool, tab, B=6)
+
+
+def test_step_parity_idle_gaps(L):
+    """Sparse arrivals: empty batches make the clock jump to the next arrival."""
+    tr, pool, tab = workload(40, 1024, 4, "bf16", seed=8, drift=False, rate=2.0,
+                             len_mu=np.log(10))
+    run_lockstep(L, dict(BASE, k=4, seed=1), tr, pool, tab, B=4)
+
+
+def test_step_parity_config4_full_size(L):
+    """configs[3] at the bench's launch configuration: N=2048 resident, B=512, V=128256,
+    k=8, bf16, all arrive at 0.  A few steps, every slot and every request compared."""
+    c = synth.CONFIGS["c4"]
+    tr = synth.make_trace(2048, c["seed"], arrival="zero", length="uniform", len_min=512,
+                          len_max=4096, beta_ab=(7, 3))
+    pool = synth.make_pool("f2", V=128256, k=8, dtype="bf16", n_buckets=16, variants=2,
+                           seed=c["seed"], device="cuda")
+    tab = synth.slab_table(tr, 16, 2, R=16, seed=c["seed"])
+    gcfg = L.SchedConfig(**dict(BASE, k=8, seed=c["seed"]))
+    h = L.Handle(gcfg, tr.arrival_us, tr.L_true, tr.L_pred, max_batch=512, V=128256)
+    sim = oracle.Sim(oracle.SchedConfig(**dict(BASE, k=8, seed=c["seed"])), tr.arrival_us,
+                     tr.L_true, tr.L_pred)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, 16
+    sel_o, _ = sim.select(512)
+    h.laps_select(512)
+    nacc = torch.empty(512, dtype=torch.int32, device="cuda")
+    for step in range(6):
+        assert (h.sel.cpu().numpy() == sel_o).all()
+        h.laps_step(rows, 512, n_accept=nacc)
+        _, _, na_o, _ = sim.step(P, sel_o)
+        assert (nacc.cpu().numpy() == na_o).all()
+        compare_state(h.state(), sim.state(), step)
