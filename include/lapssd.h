@@ -67,7 +67,7 @@ typedef enum {
 } lapssd_policy;
 
 /* Scheduler parameters.  Validation (EINVAL):
- * 1 <= K <= 16, s1_up_us > 0, M > 1, gamma >= 2, delta >= 0, 1 <= k <= 16,
+ * 1 <= K <= 16, s1_up_us > 0, M > 1, 2 <= gamma <= 32, delta >= 0, 1 <= k <= 16,
  * t_ssm_us >= 0, t_llm_us >= 0.  delta == 0 disables stabilisation. */
 typedef struct {
     int32_t policy;        /* lapssd_policy                                            */

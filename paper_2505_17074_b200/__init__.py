@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "liblapssd.so")
+_SO = os.environ.get("LAPSSD_LIBRARY") or os.path.join(_HERE, "liblapssd.so")  # override: diagnostic builds
 
 F32, BF16 = 0, 1
 POL_LAPSSD, POL_FCFS, POL_LPSJF, POL_LAS = 0, 1, 2, 3

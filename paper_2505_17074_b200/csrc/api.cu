@@ -78,12 +78,22 @@ struct lapssd_handle {
     uint32_t *counter;
     int32_t *tokens;       // internal outputs when the caller passes NULL
     int32_t *n_accept;
+    SlotDesc *desc;        // a1 results for the current batch (valid if desc_valid)
+    bool desc_valid = false;
+    lapssd_rows last_rows{};  // rows of the previous laps_step (epoch changes with them)
+    uint32_t rows_epoch = 1;
+    PreSelect *pre = nullptr;    // presort output (side stream)
+    cudaStream_t side = nullptr; // side stream for the presort, fork/join events
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t last_stream;
     // profiling window (lapssd_profile): 3 events per recorded step
     std::vector<cudaEvent_t> prof_events;
     int32_t prof_max = 0, prof_used = 0;
     ~lapssd_handle() {
         for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);
     }
 };
 
@@ -104,12 +114,18 @@ static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma,
     st.A = cv.take<double>(nn);
     st.flags = cv.take<uint32_t>(nn);
     st.key = cv.take<uint64_t>(nn);
-    st.C = cv.take<int64_t>(nn);   // C and x are initialised to -1 (contiguous)
+    st.C = cv.take<int64_t>(nn);   // C, x, next_tag are initialised to all-ones (contiguous)
     st.x = cv.take<int64_t>(nn);
+    st.next_tag = cv.take<uint64_t>(nn);
+    st.next_sr = cv.take<int2>(nn);
     h->part = cv.take<uint64_t>((size_t)max_batch * n_chunks * kPartWords);
     h->counter = cv.take<uint32_t>((size_t)max_batch);
     h->tokens = cv.take<int32_t>((size_t)max_batch * (k + 1));
     h->n_accept = cv.take<int32_t>((size_t)max_batch);
+    h->desc = cv.take<SlotDesc>((size_t)max_batch);
+    int bp = 1;
+    while (bp < max_batch) bp <<= 1;
+    h->pre = reinterpret_cast<PreSelect *>(cv.take<uint64_t>(2 + (size_t)bp));
 }
 
 static lapssd_status check_config(const lapssd_config *c) {
@@ -118,7 +134,7 @@ static lapssd_status check_config(const lapssd_config *c) {
     if (c->K < 1 || c->K > 16) return fail(LAPSSD_EINVAL, "K=%d outside 1..16", c->K);
     if (c->s1_up_us <= 0) return fail(LAPSSD_EINVAL, "s1_up_us must be > 0");
     if (!(c->M > 1.0)) return fail(LAPSSD_EINVAL, "M must be > 1");
-    if (c->gamma < 2) return fail(LAPSSD_EINVAL, "gamma must be >= 2");
+    if (c->gamma < 2 || c->gamma > 32) return fail(LAPSSD_EINVAL, "gamma must be in 2..32");
     if (!(c->delta >= 0.0)) return fail(LAPSSD_EINVAL, "delta must be >= 0");
     if (c->k < 1 || c->k > 16) return fail(LAPSSD_EINVAL, "k=%d outside 1..16", c->k);
     if (c->t_ssm_us < 0 || c->t_llm_us < 0) return fail(LAPSSD_EINVAL, "negative round cost");
@@ -139,7 +155,16 @@ size_t spec_verify_workspace_bytes(int32_t B, int64_t V) {
     Carver cv{nullptr};
     cv.take<uint64_t>((size_t)(B > 0 ? B : 1) * n_chunks_of(V) * kPartWords);
     cv.take<uint32_t>((size_t)(B > 0 ? B : 1));
+    cv.take<SlotDesc>((size_t)(B > 0 ? B : 1));
     return align256(cv.off);
+}
+
+static RowsDev rows_dev(const void *p, const void *q, const int32_t *draft, const int32_t *slab_tab,
+                        int64_t V, int32_t k, int32_t R, int32_t dtype) {
+    RowsDev rw{};
+    rw.p = p; rw.q = q; rw.draft = draft; rw.slab_tab = slab_tab;
+    rw.V = V; rw.k = k; rw.R = R; rw.dtype = dtype; rw.valid = 1;
+    return rw;
 }
 
 lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V, int32_t k,
@@ -157,15 +182,24 @@ lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V
         return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes,
                     spec_verify_workspace_bytes(B, V));
     VerifyArgs a{};
-    a.p = p; a.q = q; a.draft = draft; a.V = V; a.k = k; a.n_chunks = n_chunks_of(V);
-    a.slab = slab; a.req_id = req_id; a.round_idx = round_idx;
+    a.rows = rows_dev(p, q, draft, nullptr, V, k, 0, dtype);
+    a.n_chunks = n_chunks_of(V);
+    a.cpb = verify_cpb(V);
     a.seed = seed; a.trace = trace;
     a.tokens = tokens; a.n_accept = n_accept; a.z = z_fixed;
     Carver cv{(char *)workspace};
     a.part = cv.take<uint64_t>((size_t)B * a.n_chunks * kPartWords);
     a.counter = cv.take<uint32_t>((size_t)B);
+    SlotDesc *desc = cv.take<SlotDesc>((size_t)B);
+    a.desc = desc;
+    a.sel = nullptr;
+    a.err = nullptr;
     a.fuse_update = 0;
-    return cuda_status(launch_verify(a, dtype, B, (cudaStream_t)stream), "spec_verify launch");
+    cudaStream_t s = (cudaStream_t)stream;
+    lapssd_status st = cuda_status(launch_accept(a.rows, nullptr, nullptr, nullptr, slab, req_id, round_idx,
+                                                 seed, trace, B, desc, s), "spec_verify accept");
+    if (st != LAPSSD_OK) return st;
+    return cuda_status(launch_verify(a, B, s), "spec_verify launch");
 }
 
 // ---------------------------------------------------------------- handle
@@ -238,7 +272,7 @@ lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req
     h->last_stream = s;
     cudaError_t e = cudaMemsetAsync(workspace, 0, need, s);
     if (e == cudaSuccess)
-        e = cudaMemsetAsync(h->st.C, 0xFF, (size_t)((char *)(h->st.x + (req->n > 0 ? req->n : 1)) -
+        e = cudaMemsetAsync(h->st.C, 0xFF, (size_t)((char *)(h->st.next_tag + (req->n > 0 ? req->n : 1)) -
                                                    (char *)h->st.C), s);
     if (e == cudaSuccess && req->n > 0) {
         e = cudaMemcpyAsync((void *)h->st.arrival, req->arrival_us, sizeof(int64_t) * req->n,
@@ -250,6 +284,9 @@ lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req
             e = cudaMemcpyAsync((void *)h->st.L_pred, req->L_pred, sizeof(int32_t) * req->n,
                                 cudaMemcpyHostToDevice, s);
     }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // host arrays may be freed on return
     if (e != cudaSuccess) {
         delete h;
@@ -271,6 +308,7 @@ lapssd_status laps_update(lapssd_handle *h, const int32_t *sel, const int32_t *n
     if (!h || B < 0 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
     if (B > 0 && (!sel || !n_accept)) return fail(LAPSSD_EINVAL, "NULL sel / n_accept");
     h->last_stream = (cudaStream_t)stream;
+    h->desc_valid = false;
     return cuda_status(launch_update(h->st, h->sc, sel, n_accept, B, (cudaStream_t)stream), "laps_update");
 }
 
@@ -280,7 +318,9 @@ lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t
     if (!h || B < 1 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
     if (!sel_out) return fail(LAPSSD_EINVAL, "sel_out is NULL");
     h->last_stream = (cudaStream_t)stream;
-    return cuda_status(launch_select(h->st, h->sc, B, sel_out, count_out, (cudaStream_t)stream),
+    h->desc_valid = false;
+    const RowsDev none{};
+    return cuda_status(launch_select(h->st, h->sc, none, h->desc, B, sel_out, count_out, (cudaStream_t)stream),
                        "laps_select");
 }
 
@@ -293,10 +333,17 @@ static lapssd_status fill_step_verify(lapssd_handle *h, const lapssd_rows *rows,
     if (!rows->p || !rows->q || !rows->draft) return fail(LAPSSD_EINVAL, "rows: NULL pointer");
     if (rows->slab_tab && rows->R < 1) return fail(LAPSSD_EINVAL, "rows.R < 1");
     if (!sel) return fail(LAPSSD_EINVAL, "sel is NULL");
+    if (memcmp(&h->last_rows, rows, sizeof *rows) != 0) {
+        h->last_rows = *rows;
+        h->rows_epoch++;            // cached next-round acceptance tests are for other rows
+    }
     a = VerifyArgs{};
-    a.p = rows->p; a.q = rows->q; a.draft = rows->draft; a.V = rows->V; a.k = rows->k;
+    a.rows = rows_dev(rows->p, rows->q, rows->draft, rows->slab_tab, rows->V, rows->k, rows->R, rows->dtype);
+    a.rows.epoch = h->rows_epoch;
     a.n_chunks = n_chunks_of(rows->V);
-    a.sel = sel; a.slab_tab = rows->slab_tab; a.R = rows->R;
+    a.cpb = verify_cpb(rows->V);
+    a.desc = h->desc;
+    a.sel = sel;
     a.seed = h->sc.seed; a.trace = 0;
     a.tokens = tokens_out ? tokens_out : h->tokens;
     a.n_accept = n_accept_out ? n_accept_out : h->n_accept;
@@ -304,8 +351,22 @@ static lapssd_status fill_step_verify(lapssd_handle *h, const lapssd_rows *rows,
     a.part = h->part; a.counter = h->counter;
     a.fuse_update = 1;
     a.st = h->st; a.sc = h->sc;
+    a.err = &h->st.g->err;
     (void)B;
     return LAPSSD_OK;
+}
+
+// Verification of the current batch: the descriptors come from the previous select
+// (fused a1); if that select had no rows (or the state changed since), run a1 first.
+static lapssd_status step_verify(lapssd_handle *h, const VerifyArgs &a, int32_t *sel, int32_t B,
+                                 cudaStream_t s) {
+    if (!h->desc_valid) {
+        lapssd_status st = cuda_status(launch_accept(a.rows, sel, &h->st, &h->sc, nullptr, nullptr, nullptr,
+                                                     h->sc.seed, 0, B, h->desc, s), "accept");
+        if (st != LAPSSD_OK) return st;
+    }
+    h->desc_valid = false;
+    return cuda_status(launch_verify(a, B, s), "verify");
 }
 
 lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel_inout,
@@ -321,10 +382,28 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
     cudaEvent_t *ev = nullptr;
     if (h->prof_used < h->prof_max) ev = &h->prof_events[3 * (size_t)h->prof_used++];
     if (ev) cudaEventRecord(ev[0], s);
-    st = cuda_status(launch_verify(a, rows->dtype, B, s), "laps_step verify");
+    // fork: the presort of the next selection runs beside the verify kernel
+    cudaError_t ce = cudaEventRecord(h->ev_fork, s);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork");
+    st = cuda_status(launch_presort(h->st, h->sc, sel_inout, B, h->pre, h->side), "laps_step presort");
+    if (st != LAPSSD_OK) return st;
+    ce = cudaEventRecord(h->ev_join, h->side);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step join");
+    if (!h->desc_valid) {
+        st = cuda_status(launch_accept(a.rows, sel_inout, &h->st, &h->sc, nullptr, nullptr, nullptr, h->sc.seed, 0,
+                                       B, h->desc, s), "accept");
+        if (st != LAPSSD_OK) return st;
+    }
+    h->desc_valid = false;
+    st = cuda_status(launch_verify_grid(a, B, 1, s), "laps_step verify");
     if (st != LAPSSD_OK) return st;
     if (ev) cudaEventRecord(ev[1], s);
-    st = cuda_status(launch_select(h->st, h->sc, B, sel_inout, count_out, s), "laps_step select");
+    ce = cudaStreamWaitEvent(s, h->ev_join, 0);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step join wait");
+    st = cuda_status(launch_select_final(h->st, h->sc, a.rows, h->desc, B, sel_inout, count_out, h->pre, s),
+                     "laps_step select");
+    if (st == LAPSSD_OK) h->desc_valid = true;
     if (ev) cudaEventRecord(ev[2], s);
     return st;
 }
@@ -370,6 +449,7 @@ lapssd_status laps_candidates(lapssd_handle *h, int32_t C, uint64_t *cand_out, l
     g_last_error.clear();
     if (!h || C < 1 || !cand_out) return fail(LAPSSD_EINVAL, "handle / C / cand_out");
     h->last_stream = (cudaStream_t)stream;
+    h->desc_valid = false;
     return cuda_status(launch_candidates(h->st, h->sc, C, cand_out, (cudaStream_t)stream),
                        "laps_candidates");
 }
@@ -382,7 +462,10 @@ lapssd_status laps_merge(lapssd_handle *h, const uint64_t *all_cand, int32_t C, 
     if ((int64_t)h->sc.world * C > sort_capacity())
         return fail(LAPSSD_EINVAL, "world*C=%lld exceeds %d", (long long)h->sc.world * C, sort_capacity());
     h->last_stream = (cudaStream_t)stream;
-    return cuda_status(launch_merge(h->st, h->sc, all_cand, C, B, sel_out, count_out, (cudaStream_t)stream),
+    h->desc_valid = false;
+    const RowsDev none{};
+    return cuda_status(launch_merge(h->st, h->sc, none, h->desc, all_cand, C, B, sel_out, count_out,
+                                    (cudaStream_t)stream),
                        "laps_merge");
 }
 
@@ -458,7 +541,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
     if (st != LAPSSD_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
     h->last_stream = s;
-    st = cuda_status(launch_verify(a, rows->dtype, B_global, s), "step_dist verify");
+    st = step_verify(h, a, sel_inout, B_global, s);
     if (st != LAPSSD_OK) return st;
     uint64_t *local = cand_scratch;
     uint64_t *all = cand_scratch + (C + 1);
@@ -466,7 +549,10 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
     if (st != LAPSSD_OK) return st;
     st = nccl_status(allgather(local, all, (size_t)(C + 1), kNcclUint64, nccl_comm, s), "ncclAllGather");
     if (st != LAPSSD_OK) return st;
-    return cuda_status(launch_merge(h->st, h->sc, all, C, B_global, sel_inout, count_out, s), "step_dist merge");
+    st = cuda_status(launch_merge(h->st, h->sc, a.rows, h->desc, all, C, B_global, sel_inout, count_out, s),
+                     "step_dist merge");
+    if (st == LAPSSD_OK) h->desc_valid = true;
+    return st;
 }
 
 // ---------------------------------------------------------------- snapshot / check

@@ -20,7 +20,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kSegElems = 1024;                 // elements per warp segment
 constexpr int kTile = kWarps * kSegElems;       // 8192 elements per CTA
 constexpr int kMaxChunks = 64;                  // V <= 524288
-constexpr int kPartWords = 1 + kWarps;          // chunk sum + 8 warp sums (u64)
+constexpr int kPartWords = kWarps;              // 8 warp residual sums (u64) per chunk
 
 // ---------------------------------------------------------------- state flags
 enum : uint32_t {
@@ -63,6 +63,10 @@ struct State {
     uint32_t *flags;
     uint64_t *key;
     Globals *g;
+    // a1 of the request's NEXT round, computed by the verify finisher off the critical
+    // path: valid iff next_tag == (rows_epoch << 32 | rounds[i]).
+    uint64_t *next_tag;
+    int2 *next_sr;         // (slab, r)
 };
 
 // ---------------------------------------------------------------- Philox4x32-10
@@ -101,8 +105,9 @@ __device__ __forceinline__ int32_t level_of(int64_t x, const Sched &s) {
 __device__ __forceinline__ uint64_t sat32(uint64_t v) { return v > 0xFFFFFFFFull ? 0xFFFFFFFFull : v; }
 
 // The 64-bit priority key (include/lapssd.h, laps_select).  Smaller = sooner.
-__device__ __forceinline__ uint64_t build_key(const State &st, const Sched &s, int32_t i,
-                                              int32_t cursor, uint32_t fl) {
+// All state fields are passed in (loaded together by the caller: one memory round trip).
+__device__ __forceinline__ uint64_t build_key(const Sched &s, int32_t i, int32_t cursor, uint32_t fl,
+                                              int32_t L_pred, int32_t acc_tok, double A) {
     const uint64_t id = (uint64_t)(i * s.world + s.rank) & 0xFFFFFFull;
     const uint64_t inelig = (i >= cursor || (fl & F_DONE)) ? 1 : 0;
     const uint64_t pinned = (fl & F_PINNED) ? 1 : 0;
@@ -116,7 +121,7 @@ __device__ __forceinline__ uint64_t build_key(const State &st, const Sched &s, i
         break;
     case LAPSSD_POL_LPSJF:                          // P:276, SJF on L_pred
         unpinned = !pinned;
-        sec = sat32((uint64_t)st.L_pred[i]);
+        sec = sat32((uint64_t)L_pred);
         break;
     case LAPSSD_POL_LAS:
         unpinned = 1; lev = level; nonperc = 1; notrun = !running;
@@ -124,9 +129,9 @@ __device__ __forceinline__ uint64_t build_key(const State &st, const Sched &s, i
     default:                                        // LAPS-SD
         unpinned = !pinned; lev = level; nonperc = !perc;
         if (perc) {
-            int64_t L_rem = (int64_t)st.L_pred[i] - st.acc_tok[i];     // AMB-12
+            int64_t L_rem = (int64_t)L_pred - acc_tok;                  // AMB-12
             if (L_rem < 0) L_rem = 0;
-            sec = sat32(eq6_us(L_rem, st.A[i], s));
+            sec = sat32(eq6_us(L_rem, A, s));
         } else {
             notrun = !running;
         }
@@ -197,6 +202,92 @@ __device__ __forceinline__ void update_one(const State &st, const Sched &s, int3
     st.flags[i] = fl;
 }
 
+// Inputs of update_one for request i, loaded by the whole warp in one round trip
+// (scalars broadcast, ring slot l in lane l).  gamma <= 32.
+struct UpdIn {
+    uint32_t fl;
+    int32_t Lt, Lp, tok, acc, t;
+    int64_t E;
+    int32_t ring;  // this lane's ring slot
+};
+__device__ __forceinline__ UpdIn load_update_inputs(const State &st, const Sched &s, int32_t i, int lane) {
+    UpdIn u;
+    u.fl = st.flags[i];
+    u.Lt = st.L_true[i];
+    u.Lp = st.L_pred[i];
+    u.tok = st.acc_tok[i];
+    u.acc = st.acc_draft[i];
+    u.t = st.rounds[i];
+    u.E = st.E[i];
+    u.ring = lane < s.gamma ? st.ring[(int64_t)i * s.gamma + lane] : 0;
+    return u;
+}
+
+// update_one with preloaded inputs, executed by a full warp (uniform control flow,
+// lane 0 stores).  Same arithmetic, same order as update_one.
+__device__ __forceinline__ void update_warp(const State &st, const Sched &s, int32_t i, int32_t r, int64_t now,
+                                            const UpdIn &u, int lane) {
+    uint32_t fl = u.fl;
+    if (fl & F_DONE) {
+        if (lane == 0) atomicOr(&st.g->err, E_UPDATE_DONE);
+        return;
+    }
+    int32_t tok = u.tok;
+    const int32_t emitted = r + 1;                  // r drafts + 1 resampled / bonus
+    const int32_t rem = u.Lt - tok;
+    tok += emitted < rem ? emitted : rem;           // clipped at L (AMB-18)
+    const int32_t acc = u.acc + r;                  // AMB-4
+    const int32_t t = u.t + 1;
+    const int64_t E = u.E + s.c_round_us;
+    const int slot_new = t % s.gamma;
+    const int32_t ring_lane = lane == slot_new ? acc : u.ring;   // ring after this round
+    int32_t level = (int32_t)((fl & F_LEVEL_MASK) >> F_LEVEL_SHIFT);
+    bool demoted = false;
+    if (s.policy == LAPSSD_POL_LAPSSD && !(fl & F_PERC)) {
+        bool stable = false;
+        double mean = 0.0;
+        if (t >= s.gamma) {
+            double mx = -1.0, mn = 2.0, sum = 0.0;
+            for (int32_t sr = t - s.gamma + 1; sr <= t; ++sr) {          // oldest first
+                const int32_t a_s = __shfl_sync(0xFFFFFFFFu, ring_lane, sr % s.gamma);
+                const double rate = __ddiv_rn((double)a_s, (double)((int64_t)s.k * sr));
+                mx = rate > mx ? rate : mx;
+                mn = rate < mn ? rate : mn;
+                sum = __dadd_rn(sum, rate);
+            }
+            if (__dsub_rn(mx, mn) < s.delta) { stable = true; mean = __ddiv_rn(sum, (double)s.gamma); }
+        }
+        if (stable) {
+            fl |= F_PERC;
+            const uint64_t T = eq6_us(u.Lp, mean, s);
+            const int64_t Ts = T > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)T;
+            if (lane == 0) { st.A[i] = mean; st.T_total[i] = Ts; }
+            if (s.placement == 0) level = level_of(Ts, s);
+            if (s.pin_rule == 1) fl |= F_PINNED;
+        } else {
+            const int32_t lev = level_of(E, s);
+            if (lev > level) { level = lev; demoted = true; }
+        }
+    } else if (s.policy == LAPSSD_POL_LAS) {
+        const int32_t lev = level_of(E, s);
+        if (lev > level) { level = lev; demoted = true; }
+    }
+    if (tok >= u.Lt) {
+        fl |= F_DONE;
+        if (lane == 0) st.C[i] = now + s.c_round_us;
+    }
+    fl = (fl & ~(F_LEVEL_MASK | F_RUNNING)) | ((uint32_t)level << F_LEVEL_SHIFT);
+    if (!(fl & F_DONE) && !demoted) fl |= F_RUNNING;
+    if (lane == slot_new) st.ring[(int64_t)i * s.gamma + slot_new] = acc;
+    if (lane == 0) {
+        st.acc_tok[i] = tok;
+        st.acc_draft[i] = acc;
+        st.rounds[i] = t;
+        st.E[i] = E;
+        st.flags[i] = fl;
+    }
+}
+
 __host__ __device__ __forceinline__ int32_t slab_round_index(int32_t t, int32_t R) {
     const int32_t h = R / 2;
     if (t < R) return t;
@@ -204,44 +295,161 @@ __host__ __device__ __forceinline__ int32_t slab_round_index(int32_t t, int32_t 
     return h + (t - h) % h;
 }
 
-// ---------------------------------------------------------------- verify launch
-struct VerifyArgs {
+// ---------------------------------------------------------------- rows + slot descriptors
+// Where the probability rows live (device copy of lapssd_rows).
+struct RowsDev {
     const void *p;
     const void *q;
     const int32_t *draft;
+    const int32_t *slab_tab;    // nullable: batch layout (slot b reads slab b)
     int64_t V;
-    int32_t k;
+    int32_t k, R, dtype, valid;
+    uint32_t epoch;        // host counter: changes whenever the rows descriptor changes
+};
+
+// Per-slot result of the acceptance test (a1), produced by accept_kernel or by the
+// tail of select / merge, consumed by verify_kernel.  r < 0 marks an empty slot.
+struct __align__(16) SlotDesc {
+    int32_t i;        // local request index (-1 for stateless calls)
+    int32_t slab;     // slab whose rows this slot reads
+    uint32_t req;     // global request id (Philox c0)
+    uint32_t round;   // round index (Philox c1)
+    int32_t r;        // first rejected position, k if all accepted, -1 empty
+    int32_t pad[3];
+};
+
+// a1 for one slot: x_j = draft[slab][j]; accept iff u24_j * q_j(x_j) < p_j(x_j) * 2^24
+// (fp64, exact), u24_j = Philox(req, round, j/4, trace)[j%4] >> 8 (AMB-21).
+// Returns the first rejected position, or k.  The k gathers are independent loads.
+template <typename LoadF>
+__device__ __forceinline__ int32_t accept_test(const RowsDev &rw, int64_t slab, uint32_t req,
+                                               uint32_t rnd, uint32_t trace, uint64_t seed,
+                                               LoadF load1) {
+    const int k = rw.k;
+    const int64_t V = rw.V;
+    const int esz = rw.dtype == LAPSSD_BF16 ? 2 : 4;
+    const char *pb = (const char *)rw.p + slab * (int64_t)(k + 1) * V * esz;
+    const char *qb = (const char *)rw.q + slab * (int64_t)k * V * esz;
+    const int32_t *db = rw.draft + slab * k;
+    // positions in blocks of 8: within a block the 8 draft loads, then the 16 gathers,
+    // are independent (two dependent memory round trips per block)
+    for (int j0 = 0; j0 < k; j0 += 8) {
+        int32_t x[8];
+        float pj[8], qj[8];
+#pragma unroll
+        for (int l = 0; l < 8; ++l) x[l] = (j0 + l < k) ? db[j0 + l] : 0;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+            if (j0 + l < k) {
+                pj[l] = load1(pb, (int64_t)(j0 + l) * V + x[l]);
+                qj[l] = load1(qb, (int64_t)(j0 + l) * V + x[l]);
+            } else {
+                pj[l] = 1.0f; qj[l] = 0.0f;
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint4 u = philox4x32_10(make_uint4(req, rnd, (uint32_t)(j0 / 4 + h), trace),
+                                          (uint32_t)seed, (uint32_t)(seed >> 32));
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const int j = j0 + h * 4 + l;
+                if (j < k) {
+                    const uint32_t u24 = w[l] >> 8;
+                    if (!(__dmul_rn((double)u24, (double)qj[h * 4 + l]) <
+                          __dmul_rn((double)pj[h * 4 + l], 16777216.0)))
+                        return j;
+                }
+            }
+        }
+    }
+    return k;
+}
+
+__device__ __forceinline__ float load_prob_bf16(const void *base, int64_t idx) {
+    return __uint_as_float((uint32_t)reinterpret_cast<const uint16_t *>(base)[idx] << 16);
+}
+__device__ __forceinline__ float load_prob_f32(const void *base, int64_t idx) {
+    return reinterpret_cast<const float *>(base)[idx];
+}
+
+// Fill desc for slot b of a handle batch (local request i, or -1): the cached a1 of
+// request i's current round if the finisher computed it for these rows, else a1 now.
+__device__ __forceinline__ SlotDesc make_desc(const RowsDev &rw, const State &st, const Sched &sc,
+                                              int32_t b, int32_t i) {
+    SlotDesc d;
+    d.i = i; d.slab = 0; d.req = 0; d.round = 0; d.r = -1;
+    d.pad[0] = d.pad[1] = d.pad[2] = 0;
+    if (i < 0) return d;
+    const int32_t rnd = st.rounds[i];
+    const uint64_t tag = st.next_tag[i];
+    const int2 sr = st.next_sr[i];
+    d.req = (uint32_t)(i * sc.world + sc.rank);
+    d.round = (uint32_t)rnd;
+    if (rw.slab_tab && tag == (((uint64_t)rw.epoch << 32) | (uint32_t)rnd)) {
+        d.slab = sr.x;
+        d.r = sr.y;
+        return d;
+    }
+    int64_t slab = b;
+    if (rw.slab_tab) slab = rw.slab_tab[(int64_t)i * rw.R + slab_round_index(rnd, rw.R)];
+    d.slab = (int32_t)slab;
+    d.r = rw.dtype == LAPSSD_BF16 ? accept_test(rw, slab, d.req, d.round, 0, sc.seed, load_prob_bf16)
+                                  : accept_test(rw, slab, d.req, d.round, 0, sc.seed, load_prob_f32);
+    return d;
+}
+
+// ---------------------------------------------------------------- verify launch
+struct VerifyArgs {
+    RowsDev rows;
     int32_t n_chunks;
-    // slot addressing: stateless (sel == nullptr) or handle-driven
-    const int32_t *slab;        // stateless: slab per slot, nullable (identity)
-    const uint32_t *req_id;     // stateless
-    const uint32_t *round_idx;  // stateless
-    const int32_t *sel;         // handle: local request per slot (-1 empty)
-    const int32_t *slab_tab;    // handle: pooled rows (nullable: batch layout)
-    int32_t R;
+    int32_t cpb;                // vocabulary chunks per CTA
+    const SlotDesc *desc;       // [B]
+    const int32_t *sel;         // handle mode: must match desc[b].i (nullable: stateless)
     uint64_t seed;
     uint32_t trace;
     int32_t *tokens;
     int32_t *n_accept;
     uint64_t *z;
-    uint64_t *part;             // [B][n_chunks][kPartWords]
+    uint64_t *part;             // [B][n_chunks][kWarps] warp residual sums
     uint32_t *counter;          // [B]
     int32_t fuse_update;
-    State st;
+    State st;                   // handle mode only
     Sched sc;
+    uint32_t *err;              // sticky device flags (nullable in stateless mode)
 };
 
+enum : uint32_t { E_STALE_DESC = 8u };
+
 // host-side launchers (verify.cu / sched.cu)
-cudaError_t launch_verify(const VerifyArgs &a, int32_t dtype, int32_t B, cudaStream_t s);
+cudaError_t launch_accept(const RowsDev &rw, const int32_t *sel, const State *st, const Sched *sc,
+                          const int32_t *slab, const uint32_t *req_id, const uint32_t *round_idx,
+                          uint64_t seed, uint32_t trace, int32_t B, SlotDesc *desc, cudaStream_t s);
+cudaError_t launch_verify(const VerifyArgs &a, int32_t B, cudaStream_t s);
 cudaError_t launch_update(const State &st, const Sched &sc, const int32_t *sel,
                           const int32_t *n_accept, int32_t B, cudaStream_t s);
-cudaError_t launch_select(const State &st, const Sched &sc, int32_t B, int32_t *sel_out,
-                          int32_t *count_out, cudaStream_t s);
+cudaError_t launch_select(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc,
+                          int32_t B, int32_t *sel_out, int32_t *count_out, cudaStream_t s);
 cudaError_t launch_candidates(const State &st, const Sched &sc, int32_t C, uint64_t *cand_out,
                               cudaStream_t s);
-cudaError_t launch_merge(const State &st, const Sched &sc, const uint64_t *all_cand, int32_t C,
-                         int32_t B, int32_t *sel_out, int32_t *count_out, cudaStream_t s);
+cudaError_t launch_merge(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc,
+                         const uint64_t *all_cand, int32_t C, int32_t B, int32_t *sel_out,
+                         int32_t *count_out, cudaStream_t s);
+// Output of presort_kernel: the clock / admission of the coming select and the sorted
+// top-B keys of the requests outside the current batch.
+struct PreSelect {
+    int64_t now_us;
+    int32_t cursor, pad;
+    uint64_t cand[1];   // [next_pow2(max_batch)], flexible
+};
+cudaError_t launch_presort(const State &st, const Sched &sc, const int32_t *sel, int32_t B, PreSelect *out,
+                           cudaStream_t s);
+cudaError_t launch_select_final(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc, int32_t B,
+                                int32_t *sel, int32_t *count_out, const PreSelect *pre, cudaStream_t s);
+cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_sms, cudaStream_t s);
 int sort_capacity();            // largest key count one select CTA can sort
+int verify_cpb(int64_t V);      // chunks per CTA chosen for V (env LAPSSD_CPB overrides)
 void count_launch(int n = 1);
 
 }  // namespace lapssd

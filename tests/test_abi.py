@@ -47,7 +47,7 @@ def test_library_is_sm100a():
 
 def test_workspace_sizes():
     import paper_2505_17074_b200 as L
-    assert L.spec_verify_workspace_bytes(512, 128256) >= 512 * 16 * 9 * 8 + 512 * 4
+    assert L.spec_verify_workspace_bytes(512, 128256) >= 512 * 16 * 8 * 8 + 512 * 4 + 512 * 32
     assert L.spec_verify_workspace_bytes(0, 16) > 0
     cfg = L.SchedConfig(k=8)
     n = L._lib.lapssd_workspace_bytes(C.byref(cfg.c()), 2048, 512, 128256, 1)
