@@ -252,7 +252,9 @@ lapssd_status lapssd_check(lapssd_handle *h, uint32_t *flags_out);
  * max_steps <= 0 disables profiling. */
 lapssd_status lapssd_profile(lapssd_handle *h, int32_t max_steps);
 lapssd_status lapssd_profile_read(lapssd_handle *h, double *verify_ms, double *select_ms,
-                                  int32_t *steps);
+                                  double *presort_ms, int32_t *steps);
+/* presort_ms: summed time from the step's start to the end of the side-stream presort
+ * (it overlaps the verify kernel; if it exceeds verify_ms the select waits for it). */
 
 /* Thread-local text of the last error ("" if none). */
 const char *lapssd_last_error(void);

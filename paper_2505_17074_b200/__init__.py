@@ -79,7 +79,7 @@ def _load():
         "lapssd_read_state": ([vp, vp, vp], i32),
         "lapssd_check": ([vp, vp], i32),
         "lapssd_profile": ([vp, i32], i32),
-        "lapssd_profile_read": ([vp, vp, vp, vp], i32),
+        "lapssd_profile_read": ([vp, vp, vp, vp, vp], i32),
         "lapssd_last_error": ([], C.c_char_p),
         "lapssd_launch_count": ([], u64),
     }
@@ -283,10 +283,11 @@ class Handle:
         _check("lapssd_profile", _lib.lapssd_profile(self.h, max_steps))
 
     def profile_read(self):
-        v, s, n = C.c_double(), C.c_double(), C.c_int32()
+        """(verify_ms, select_ms, presort_ms, steps) summed over the profiled steps."""
+        v, s, p, n = C.c_double(), C.c_double(), C.c_double(), C.c_int32()
         _check("lapssd_profile_read", _lib.lapssd_profile_read(self.h, C.byref(v), C.byref(s),
-                                                               C.byref(n)))
-        return v.value, s.value, n.value
+                                                               C.byref(p), C.byref(n)))
+        return v.value, s.value, p.value, n.value
 
     def check(self):
         flags = C.c_uint32()

@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
@@ -66,6 +67,13 @@ struct Carver {
 
 namespace lapssd {
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+void prepare_all() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        verify_prepare();
+        sched_prepare();
+    });
+}
 }  // namespace lapssd
 
 struct lapssd_handle {
@@ -83,10 +91,13 @@ struct lapssd_handle {
     lapssd_rows last_rows{};  // rows of the previous laps_step (epoch changes with them)
     uint32_t rows_epoch = 1;
     PreSelect *pre = nullptr;    // presort output (side stream)
+    SelRec *fin = nullptr;       // finisher records, one per slot (fused select)
+    uint32_t *done_ctas = nullptr;
+    uint32_t *pubq = nullptr;    // slot publication queue (incremental select)
     cudaStream_t side = nullptr; // side stream for the presort, fork/join events
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t last_stream;
-    // profiling window (lapssd_profile): 3 events per recorded step
+    // profiling window (lapssd_profile): 4 events per recorded step
     std::vector<cudaEvent_t> prof_events;
     int32_t prof_max = 0, prof_used = 0;
     ~lapssd_handle() {
@@ -125,7 +136,10 @@ static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma,
     h->desc = cv.take<SlotDesc>((size_t)max_batch);
     int bp = 1;
     while (bp < max_batch) bp <<= 1;
-    h->pre = reinterpret_cast<PreSelect *>(cv.take<uint64_t>(2 + (size_t)bp));
+    h->pre = reinterpret_cast<PreSelect *>(cv.take<uint64_t>(preselect_words(bp)));
+    h->fin = cv.take<SelRec>((size_t)max_batch);
+    h->done_ctas = cv.take<uint32_t>(1);
+    h->pubq = cv.take<uint32_t>(1 + (size_t)max_batch);
 }
 
 static lapssd_status check_config(const lapssd_config *c) {
@@ -181,6 +195,7 @@ lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V
     if (workspace_bytes < spec_verify_workspace_bytes(B, V))
         return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes,
                     spec_verify_workspace_bytes(B, V));
+    prepare_all();
     VerifyArgs a{};
     a.rows = rows_dev(p, q, draft, nullptr, V, k, 0, dtype);
     a.n_chunks = n_chunks_of(V);
@@ -242,6 +257,7 @@ lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req
     if (!workspace || workspace_bytes < need)
         return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes, need);
 
+    prepare_all();
     lapssd_handle *h = new lapssd_handle{};
     Carver cv{(char *)workspace};
     carve_handle(cv, h, req->n, cfg->gamma, max_batch, n_chunks_of(V), cfg->k);
@@ -358,6 +374,16 @@ static lapssd_status fill_step_verify(lapssd_handle *h, const lapssd_rows *rows,
 
 // Verification of the current batch: the descriptors come from the previous select
 // (fused a1); if that select had no rows (or the state changed since), run a1 first.
+// Profiling event record: an external event node when the stream is being captured.
+static void prof_record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+        cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else
+        cudaEventRecord(e, s);
+}
+
 static lapssd_status step_verify(lapssd_handle *h, const VerifyArgs &a, int32_t *sel, int32_t B,
                                  cudaStream_t s) {
     if (!h->desc_valid) {
@@ -380,31 +406,56 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
     cudaStream_t s = (cudaStream_t)stream;
     h->last_stream = s;
     cudaEvent_t *ev = nullptr;
-    if (h->prof_used < h->prof_max) ev = &h->prof_events[3 * (size_t)h->prof_used++];
-    if (ev) cudaEventRecord(ev[0], s);
-    // fork: the presort of the next selection runs beside the verify kernel
-    cudaError_t ce = cudaEventRecord(h->ev_fork, s);
-    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
-    if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork");
-    st = cuda_status(launch_presort(h->st, h->sc, sel_inout, B, h->pre, h->side), "laps_step presort");
-    if (st != LAPSSD_OK) return st;
-    ce = cudaEventRecord(h->ev_join, h->side);
-    if (ce != cudaSuccess) return cuda_status(ce, "laps_step join");
-    if (!h->desc_valid) {
+    if (h->prof_used < h->prof_max) ev = &h->prof_events[4 * (size_t)h->prof_used++];
+    if (ev) prof_record(ev[0], s);
+    int bp = 1;
+    while (bp < B) bp <<= 1;
+    // pooled rows: incremental select on the side stream (presort, then merge the batch
+    // slots as the verify finishers publish them); batch layout: presort + final select
+    const bool incremental = rows->slab_tab != nullptr && bp <= 4096;
+    if (!h->desc_valid) {  // a1 for the current batch, before the fork: both streams read it
         st = cuda_status(launch_accept(a.rows, sel_inout, &h->st, &h->sc, nullptr, nullptr, nullptr, h->sc.seed, 0,
                                        B, h->desc, s), "accept");
         if (st != LAPSSD_OK) return st;
     }
+    // fork: the next selection's side-stream work runs beside the verify kernel (the
+    // verify kernel is launched first so it takes its SMs without waiting)
+    cudaError_t ce = cudaEventRecord(h->ev_fork, s);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork");
     h->desc_valid = false;
+    if (incremental) {
+        a.fuse_select = 1;
+        a.fin = h->fin;
+        a.pre = h->pre;
+        a.pubq = h->pubq;
+        a.count_out = count_out;
+    }
     st = cuda_status(launch_verify_grid(a, B, 1, s), "laps_step verify");
     if (st != LAPSSD_OK) return st;
-    if (ev) cudaEventRecord(ev[1], s);
+    if (ev) prof_record(ev[1], s);
+    ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork wait");
+    if (incremental) {
+        st = cuda_status(launch_select_side(h->st, h->sc, a.rows, sel_inout, h->desc, B, h->pre, h->fin, h->pubq,
+                                            count_out, h->side), "laps_step select");
+    } else {
+        st = cuda_status(launch_presort(h->st, h->sc, a.rows, sel_inout, B, h->pre, h->side), "laps_step presort");
+    }
+    if (st != LAPSSD_OK) return st;
+    if (ev) prof_record(ev[3], h->side);
+    ce = cudaEventRecord(h->ev_join, h->side);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step join");
     ce = cudaStreamWaitEvent(s, h->ev_join, 0);
     if (ce != cudaSuccess) return cuda_status(ce, "laps_step join wait");
+    if (incremental) {
+        h->desc_valid = true;
+        if (ev) prof_record(ev[2], s);
+        return LAPSSD_OK;
+    }
     st = cuda_status(launch_select_final(h->st, h->sc, a.rows, h->desc, B, sel_inout, count_out, h->pre, s),
                      "laps_step select");
     if (st == LAPSSD_OK) h->desc_valid = true;
-    if (ev) cudaEventRecord(ev[2], s);
+    if (ev) prof_record(ev[2], s);
     return st;
 }
 
@@ -415,7 +466,7 @@ lapssd_status lapssd_profile(lapssd_handle *h, int32_t max_steps) {
     h->prof_events.clear();
     h->prof_used = 0;
     h->prof_max = max_steps > 0 ? max_steps : 0;
-    h->prof_events.resize(3 * (size_t)h->prof_max);
+    h->prof_events.resize(4 * (size_t)h->prof_max);
     for (auto &e : h->prof_events) {
         const cudaError_t err = cudaEventCreate(&e);
         if (err != cudaSuccess) { h->prof_max = 0; return cuda_status(err, "cudaEventCreate"); }
@@ -423,22 +474,26 @@ lapssd_status lapssd_profile(lapssd_handle *h, int32_t max_steps) {
     return LAPSSD_OK;
 }
 
-lapssd_status lapssd_profile_read(lapssd_handle *h, double *verify_ms, double *select_ms, int32_t *steps) {
+lapssd_status lapssd_profile_read(lapssd_handle *h, double *verify_ms, double *select_ms, double *presort_ms,
+                                  int32_t *steps) {
     g_last_error.clear();
     if (!h) return fail(LAPSSD_EINVAL, "handle is NULL");
-    double v = 0.0, sl = 0.0;
+    double v = 0.0, sl = 0.0, pr = 0.0;
     for (int32_t i = 0; i < h->prof_used; ++i) {
-        cudaEvent_t *ev = &h->prof_events[3 * (size_t)i];
-        float a = 0.f, b = 0.f;
+        cudaEvent_t *ev = &h->prof_events[4 * (size_t)i];
+        float a = 0.f, b = 0.f, c = 0.f;
         cudaError_t e = cudaEventSynchronize(ev[2]);
         if (e == cudaSuccess) e = cudaEventElapsedTime(&a, ev[0], ev[1]);
         if (e == cudaSuccess) e = cudaEventElapsedTime(&b, ev[1], ev[2]);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&c, ev[0], ev[3]);
         if (e != cudaSuccess) return cuda_status(e, "lapssd_profile_read");
         v += a;
         sl += b;
+        pr += c;
     }
     if (verify_ms) *verify_ms = v;
     if (select_ms) *select_ms = sl;
+    if (presort_ms) *presort_ms = pr;
     if (steps) *steps = h->prof_used;
     h->prof_max = h->prof_used;   // close the window
     return LAPSSD_OK;

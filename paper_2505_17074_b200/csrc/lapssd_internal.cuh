@@ -31,7 +31,16 @@ enum : uint32_t {
     E_UPDATE_DONE = 1u,    // update on a completed request
     E_NO_MASS = 2u,        // a row with no probability mass at all
     E_BAD_SLOT = 4u,       // slot refers to an out-of-range request
+    E_TIMEOUT = 16u,       // a device-side wait exceeded its watchdog (results invalid)
 };
+
+// Watchdog for device-side spin waits: true once `t0` is more than 2 s in the past.
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ bool waited_too_long(unsigned long long t0) { return gtimer() - t0 > 2000000000ull; }
 
 struct Globals {
     int64_t now_us;
@@ -208,7 +217,13 @@ struct UpdIn {
     uint32_t fl;
     int32_t Lt, Lp, tok, acc, t;
     int64_t E;
+    double A;
     int32_t ring;  // this lane's ring slot
+};
+struct UpdOut {    // the fields a priority key needs, after the update
+    uint32_t fl;
+    int32_t tok;
+    double A;
 };
 __device__ __forceinline__ UpdIn load_update_inputs(const State &st, const Sched &s, int32_t i, int lane) {
     UpdIn u;
@@ -219,18 +234,20 @@ __device__ __forceinline__ UpdIn load_update_inputs(const State &st, const Sched
     u.acc = st.acc_draft[i];
     u.t = st.rounds[i];
     u.E = st.E[i];
+    u.A = st.A[i];
     u.ring = lane < s.gamma ? st.ring[(int64_t)i * s.gamma + lane] : 0;
     return u;
 }
 
 // update_one with preloaded inputs, executed by a full warp (uniform control flow,
 // lane 0 stores).  Same arithmetic, same order as update_one.
-__device__ __forceinline__ void update_warp(const State &st, const Sched &s, int32_t i, int32_t r, int64_t now,
-                                            const UpdIn &u, int lane) {
+__device__ __forceinline__ UpdOut update_warp(const State &st, const Sched &s, int32_t i, int32_t r, int64_t now,
+                                              const UpdIn &u, int lane) {
     uint32_t fl = u.fl;
+    UpdOut out{fl, u.tok, u.A};
     if (fl & F_DONE) {
         if (lane == 0) atomicOr(&st.g->err, E_UPDATE_DONE);
-        return;
+        return out;
     }
     int32_t tok = u.tok;
     const int32_t emitted = r + 1;                  // r drafts + 1 resampled / bonus
@@ -259,6 +276,7 @@ __device__ __forceinline__ void update_warp(const State &st, const Sched &s, int
         }
         if (stable) {
             fl |= F_PERC;
+            out.A = mean;
             const uint64_t T = eq6_us(u.Lp, mean, s);
             const int64_t Ts = T > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)T;
             if (lane == 0) { st.A[i] = mean; st.T_total[i] = Ts; }
@@ -286,6 +304,9 @@ __device__ __forceinline__ void update_warp(const State &st, const Sched &s, int
         st.E[i] = E;
         st.flags[i] = fl;
     }
+    out.fl = fl;
+    out.tok = tok;
+    return out;
 }
 
 __host__ __device__ __forceinline__ int32_t slab_round_index(int32_t t, int32_t R) {
@@ -401,6 +422,8 @@ __device__ __forceinline__ SlotDesc make_desc(const RowsDev &rw, const State &st
 }
 
 // ---------------------------------------------------------------- verify launch
+struct SelRec;
+struct PreSelect;
 struct VerifyArgs {
     RowsDev rows;
     int32_t n_chunks;
@@ -418,6 +441,16 @@ struct VerifyArgs {
     State st;                   // handle mode only
     Sched sc;
     uint32_t *err;              // sticky device flags (nullable in stateless mode)
+    // fused final select (laps_step with pooled rows): the last CTA to retire merges
+    // the finishers' records with the presort's candidates
+    int32_t fuse_select;
+    SelRec *fin;                // [B] one record per slot, written by its finisher
+    PreSelect *pre;             // presort output (side stream)
+    uint32_t *done_ctas;        // grid-wide retire ticket
+    int32_t *count_out;         // nullable
+    // incremental select: each finisher publishes its slot here once its record is
+    // written; the side-stream merger folds it into the running top-B
+    uint32_t *pubq;             // [1 + B]: ticket, then slot+1 per entry (0 = not yet)
 };
 
 enum : uint32_t { E_STALE_DESC = 8u };
@@ -438,17 +471,43 @@ cudaError_t launch_merge(const State &st, const Sched &sc, const RowsDev &rw, Sl
                          int32_t *count_out, cudaStream_t s);
 // Output of presort_kernel: the clock / admission of the coming select and the sorted
 // top-B keys of the requests outside the current batch.
+// A selectable request as the fused final select needs it: its key at this select,
+// the acceptance-test descriptor of its next round (used if it is selected), its state
+// flags at select time and whether it has never been served (x_i < 0).
+struct __align__(16) SelRec {
+    uint64_t key;
+    uint32_t flags;
+    int32_t x_unset;
+    SlotDesc desc;
+};
 struct PreSelect {
     int64_t now_us;
-    int32_t cursor, pad;
-    uint64_t cand[1];   // [next_pow2(max_batch)], flexible
+    int32_t cursor;
+    uint32_t ready;     // set (release) by the presort, cleared by the final select
+    uint64_t cand[1];   // [next_pow2(max_batch)] sorted keys, then SelRec rec[...]
 };
-cudaError_t launch_presort(const State &st, const Sched &sc, const int32_t *sel, int32_t B, PreSelect *out,
-                           cudaStream_t s);
+__host__ __device__ inline int even_up(int x) { return (x + 1) & ~1; }  // keeps SelRec 16-byte aligned
+__host__ __device__ inline size_t preselect_words(int bp) {  // uint64 words incl. records
+    return 2 + (size_t)even_up(bp) + (size_t)bp * (sizeof(SelRec) / 8);
+}
+__device__ __forceinline__ SelRec *pre_recs(PreSelect *p, int bp) {
+    return reinterpret_cast<SelRec *>(p->cand + even_up(bp));
+}
+__device__ __forceinline__ const SelRec *pre_recs(const PreSelect *p, int bp) {
+    return reinterpret_cast<const SelRec *>(p->cand + even_up(bp));
+}
+cudaError_t launch_presort(const State &st, const Sched &sc, const RowsDev &rw, const int32_t *sel, int32_t B,
+                           PreSelect *out, cudaStream_t s);
 cudaError_t launch_select_final(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc, int32_t B,
                                 int32_t *sel, int32_t *count_out, const PreSelect *pre, cudaStream_t s);
 cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_sms, cudaStream_t s);
+cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
+                               int32_t B, PreSelect *pre, const SelRec *fin, uint32_t *pubq, int32_t *count_out,
+                               cudaStream_t s);
 int sort_capacity();            // largest key count one select CTA can sort
+void prepare_all();             // kernel attributes, once per process (api.cu)
+void verify_prepare();
+void sched_prepare();
 int verify_cpb(int64_t V);      // chunks per CTA chosen for V (env LAPSSD_CPB overrides)
 void count_launch(int n = 1);
 

@@ -9,15 +9,36 @@
 // eligible keys become the batch.  The tail of the same kernel runs the acceptance
 // test (a1) of every newly selected slot, so the next verify launch starts streaming
 // after a single descriptor load.
-#include "lapssd_internal.cuh"
+#include "select_core.cuh"
 
 namespace lapssd {
 
-constexpr int kSelThreads = 1024;
-constexpr int kSortCap = 16384;          // keys per CTA (bitonic in place above kMergeCap)
-constexpr int kMergeCap = 8192;          // keys sorted by warp-sort + merge-path (2 buffers)
+#ifdef LAPSSD_TRACE
+__device__ unsigned long long g_side_iter[128][2];
+__device__ unsigned int g_side_n;
+extern "C" int lapssd_side_trace_read(unsigned long long *out, unsigned *n) {
+    cudaMemcpyFromSymbol(out, g_side_iter, sizeof g_side_iter);
+    cudaMemcpyFromSymbol(n, g_side_n, sizeof(unsigned));
+    unsigned z = 0;
+    cudaMemcpyToSymbol(g_side_n, &z, sizeof z);
+    return 0;
+}
+#define ITRACE(m) do { if (threadIdx.x == 0) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); \
+    unsigned i = g_side_n++; if (i < 128) { g_side_iter[i][0] = t; g_side_iter[i][1] = (unsigned long long)(m); } } } while (0)
+__device__ unsigned long long g_sel_trace[16];
+#define STRACE(i) do { if (threadIdx.x == 0) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); g_sel_trace[i] = t; } } while (0)
+extern "C" int lapssd_sel_trace_read(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_sel_trace, sizeof g_sel_trace); }
+#else
+#define STRACE(i)
+#define ITRACE(m)
+#endif
+
+
 
 int sort_capacity() { return kSortCap; }
+
+static void set_smem_attr(const void *fn);
+__global__ void select_kernel(const State, const Sched, const RowsDev, SlotDesc *, int32_t, int32_t *, int32_t *);
 
 // ---------------------------------------------------------------- a3 standalone
 __global__ void update_kernel(const State st, const Sched sc, const int32_t *sel,
@@ -36,275 +57,6 @@ cudaError_t launch_update(const State &st, const Sched &sc, const int32_t *sel,
     update_kernel<<<(B + 255) / 256, 256, 0, s>>>(st, sc, sel, n_accept, B);
     count_launch();
     return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------- block sort
-__device__ void bitonic_sort(uint64_t *s, int n) {  // n power of two, ascending, in place
-    for (int k = 2; k <= n; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < n; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const uint64_t x = s[i], y = s[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((x > y) == up) { s[i] = y; s[ixj] = x; }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
-// Sort one 64-key run held as (lo = element lane, hi = element lane + 32).
-__device__ __forceinline__ void warp_sort64(uint64_t &lo, uint64_t &hi, int lane) {
-#pragma unroll
-    for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j == 32) {
-                const bool asc = true;  // k == 64: (e & 64) == 0 for every element
-                const uint64_t a = lo < hi ? lo : hi, b = lo < hi ? hi : lo;
-                lo = asc ? a : b;
-                hi = asc ? b : a;
-            } else {
-                const bool lower = (lane & j) == 0;
-                {
-                    const uint64_t p = __shfl_xor_sync(0xFFFFFFFFu, lo, j);
-                    const bool asc = ((lane & k) == 0);
-                    lo = (lower == asc) ? (lo < p ? lo : p) : (lo > p ? lo : p);
-                }
-                {
-                    const uint64_t p = __shfl_xor_sync(0xFFFFFFFFu, hi, j);
-                    const bool asc = (((lane + 32) & k) == 0);
-                    hi = (lower == asc) ? (hi < p ? hi : p) : (hi > p ? hi : p);
-                }
-            }
-        }
-    }
-}
-
-// Sorts n (power of two) keys; returns the buffer holding the result (a or b).
-__device__ uint64_t *block_sort(uint64_t *a, uint64_t *b, int n) {
-    if (n < 64 || n > kMergeCap || b == nullptr) {
-        bitonic_sort(a, n);
-        return a;
-    }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    for (int run = warp; run < n / 64; run += nwarps) {
-        uint64_t lo = a[run * 64 + lane], hi = a[run * 64 + 32 + lane];
-        warp_sort64(lo, hi, lane);
-        a[run * 64 + lane] = lo;
-        a[run * 64 + 32 + lane] = hi;
-    }
-    __syncthreads();
-    uint64_t *src = a, *dst = b;
-    const int T = blockDim.x;
-    const int per = n >= T ? n / T : 1;
-    for (int w = 64; w < n; w <<= 1) {
-        for (int o0 = threadIdx.x * per; o0 < n; o0 += T * per) {
-            const int pair = o0 / (2 * w);
-            const int d0 = o0 - pair * 2 * w;
-            const uint64_t *A = src + pair * 2 * w;
-            const uint64_t *Bv = A + w;
-            int lo = d0 - w > 0 ? d0 - w : 0, hi = d0 < w ? d0 : w;
-            while (lo < hi) {  // number of A elements among the first d0 outputs
-                const int mid = (lo + hi) >> 1;
-                if (A[mid] <= Bv[d0 - 1 - mid]) lo = mid + 1; else hi = mid;
-            }
-            int i = lo, j = d0 - lo;
-            for (int e = 0; e < per; ++e) {
-                const bool takeA = j >= w || (i < w && A[i] <= Bv[j]);
-                dst[o0 + e] = takeA ? A[i++] : Bv[j++];
-            }
-        }
-        __syncthreads();
-        uint64_t *t = src; src = dst; dst = t;
-    }
-    return src;
-}
-
-// The B smallest of n keys, sorted ascending, into out[0..bp) (bp = next_pow2(B) with
-// UINT64_MAX padding); tmp is bp words of scratch.  MSB-first radix select finds the
-// B-th smallest key T with eight 256-bin histogram passes (keys are unique: the id is
-// in the low bits), then the keys <= T are compacted and only they are sorted.
-__device__ uint64_t *select_topB(const uint64_t *keys, int n, int B, uint64_t *out, uint64_t *tmp, int bp) {
-    __shared__ int hist[256];
-    __shared__ uint64_t s_prefix, s_mask;
-    __shared__ int s_remaining, s_done;
-    __shared__ int s_scan[64];
-    const int want = B < n ? B : n;
-    if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_remaining = want; s_done = 0; }
-    __syncthreads();
-    for (int shift = 56; shift >= 0 && want > 0; shift -= 8) {
-        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-        __syncthreads();
-        if (s_done) break;
-        const uint64_t prefix = s_prefix, mask = s_mask;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint64_t key = keys[i];
-            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            const int lane = threadIdx.x;
-            int loc[8], sum = 0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) { loc[e] = hist[lane * 8 + e]; sum += loc[e]; }
-            int incl = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const int rem = s_remaining;
-            const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= rem);
-            const int src = __ffs(hit) - 1;
-            if (lane == src) {
-                int acc = incl - sum;
-                int dgt = 0;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    if (acc + loc[e] >= rem) { dgt = lane * 8 + e; break; }
-                    acc += loc[e];
-                }
-                const int cnt = hist[dgt];
-                s_prefix = prefix | ((uint64_t)dgt << shift);
-                s_mask = mask | (255ull << shift);
-                s_remaining = rem - acc;
-                if (rem - acc == cnt) s_done = 1;  // every key of this bin is needed
-            }
-        }
-        __syncthreads();
-    }
-    // threshold: all keys matching the final prefix pattern up to its mask, i.e. key <= T
-    const uint64_t T = want > 0 ? (s_prefix | ~s_mask) : 0;
-    // compact keys <= T (exactly `want` of them) in index order, then sort
-    const int per = (n + (int)blockDim.x - 1) / (int)blockDim.x;
-    const int lo = (int)threadIdx.x * per;
-    int mine = 0;
-    // keys are unique except UINT64_MAX padding: take keys < T, plus T itself unless it
-    // is the padding value (then the tail is filled with padding below)
-    const bool t_real = T != ~0ull;
-    for (int i = lo; i < lo + per && i < n; ++i) mine += want > 0 && (keys[i] < T || (t_real && keys[i] == T));
-    int total = 0;
-    {
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        int x = mine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xFFFFFFFFu, x, o);
-            if (lane >= o) x += v;
-        }
-        if (lane == 31) s_scan[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            int w = lane < (int)(blockDim.x >> 5) ? s_scan[lane] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(0xFFFFFFFFu, w, o);
-                if (lane >= o) w += v;
-            }
-            s_scan[32 + lane] = w;
-        }
-        __syncthreads();
-        int pos = (warp > 0 ? s_scan[32 + warp - 1] : 0) + x - mine;
-        total = s_scan[32 + (int)(blockDim.x >> 5) - 1];
-        for (int i = lo; i < lo + per && i < n; ++i)
-            if (want > 0 && (keys[i] < T || (t_real && keys[i] == T)) && pos < bp) out[pos++] = keys[i];
-    }
-    for (int i = total + (int)threadIdx.x; i < bp; i += blockDim.x) out[i] = ~0ull;
-    __syncthreads();
-    return block_sort(out, bp >= 64 && bp <= kMergeCap ? tmp : nullptr, bp);
-}
-
-__device__ __forceinline__ int next_pow2(int n) {
-    int p = 1;
-    while (p < n) p <<= 1;
-    return p;
-}
-
-__host__ __device__ inline size_t sort_smem_bytes(int n) {
-    int p = 1;
-    while (p < n) p <<= 1;
-    return (size_t)p * sizeof(uint64_t) * (p >= 64 && p <= kMergeCap ? 2 : 1);
-}
-
-// Block-wide exclusive scan of one int per thread.
-__device__ int block_excl_scan(int v, int *s_tmp, int *total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int n = __shfl_up_sync(0xFFFFFFFFu, x, o);
-        if (lane >= o) x += n;
-    }
-    if (lane == 31) s_tmp[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        int w = lane < (int)(blockDim.x >> 5) ? s_tmp[lane] : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int n = __shfl_up_sync(0xFFFFFFFFu, w, o);
-            if (lane >= o) w += n;
-        }
-        s_tmp[32 + lane] = w;  // inclusive warp totals
-    }
-    __syncthreads();
-    const int before = warp > 0 ? s_tmp[32 + warp - 1] : 0;
-    *total = s_tmp[32 + (int)(blockDim.x >> 5) - 1];
-    __syncthreads();
-    return before + x - v;
-}
-
-// a7 (first half) + a4: advance the clock by the round that ran, admit arrivals.
-// Arrivals are sorted, so the admitted set is the prefix [0, cursor).
-__device__ void advance_and_admit(const State &st, const Sched &sc, int64_t *s_now, int *s_cursor) {
-    if (threadIdx.x == 0) {
-        int64_t now = st.g->now_us;
-        if (st.g->prev_count > 0) now += sc.c_round_us;         // AMB-17
-        *s_now = now;
-        *s_cursor = st.g->cursor;
-    }
-    __syncthreads();
-    const int64_t now = *s_now;
-    int cursor = *s_cursor;
-    for (;;) {
-        const int idx = cursor + (int)threadIdx.x;
-        const bool adm = idx < sc.n && st.arrival[idx] <= now;
-        const int cnt = __syncthreads_count(adm);
-        cursor += cnt;
-        if (cnt < (int)blockDim.x) break;
-    }
-    if (threadIdx.x == 0) *s_cursor = cursor;
-    __syncthreads();
-}
-
-// Build every key into global and shared memory (padded to npow2 with UINT64_MAX)
-// and clear the running flags (they describe the round that just ran).
-__device__ void build_keys(const State &st, const Sched &sc, int cursor, uint64_t *s_keys, int npow2) {
-    for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
-        uint64_t key = ~0ull;
-        if (i < sc.n) {
-            const uint32_t fl = st.flags[i];
-            const int32_t lp = st.L_pred[i], tok = st.acc_tok[i];
-            const double A = st.A[i];
-            key = build_key(sc, i, cursor, fl, lp, tok, A);
-            st.key[i] = key;
-            if (fl & F_RUNNING) st.flags[i] = fl & ~F_RUNNING;
-        }
-        s_keys[i] = key;
-    }
-    __syncthreads();
-}
-
-// Commit one selected request: first-service time and pinning (AMB-15, AMB-25).
-__device__ __forceinline__ void commit_one(const State &st, const Sched &sc, int32_t i, int64_t now) {
-    if (st.x[i] < 0) st.x[i] = now;                                // x_i
-    const uint32_t fl = st.flags[i];
-    bool pin = false;
-    if (sc.policy == LAPSSD_POL_FCFS || sc.policy == LAPSSD_POL_LPSJF) pin = true;
-    else if (sc.policy == LAPSSD_POL_LAPSSD && sc.pin_rule == 0 && (fl & F_PERC)) pin = true;
-    if (pin && !(fl & F_PINNED)) st.flags[i] = fl | F_PINNED;
 }
 
 // ---------------------------------------------------------------- a4-a7 select
@@ -366,8 +118,8 @@ static void set_smem_attr(const void *fn) {
 // top-B, sorted -- on a side stream while the verify kernel streams.  After the join,
 // select_final_kernel rebuilds only the B updated keys, sorts them and merges the two
 // sorted lists: the top-B of the union is the top-B of all keys.
-__global__ void __launch_bounds__(kSelThreads) presort_kernel(const State st, const Sched sc, const int32_t *sel,
-                                                               int32_t B, PreSelect *out) {
+__global__ void __launch_bounds__(kSelThreads) presort_kernel(const State st, const Sched sc, const RowsDev rw,
+                                                               const int32_t *sel, int32_t B, PreSelect *out) {
     extern __shared__ uint64_t s_buf[];
     __shared__ int64_t s_now;
     __shared__ int s_cursor;
@@ -397,10 +149,34 @@ __global__ void __launch_bounds__(kSelThreads) presort_kernel(const State st, co
     __syncthreads();
     const int bp = next_pow2(B);
     const uint64_t *top = select_topB(s_buf, n, B, s_buf + npow2, s_buf + npow2 + bp, bp);
-    for (int b = threadIdx.x; b < bp; b += blockDim.x) out->cand[b] = top[b];
+    // records for the fused final select: flags, first-service marker, and the
+    // acceptance-test descriptor of the candidate's current round (cached or computed)
+    SelRec *rec = pre_recs(out, bp);
+    for (int b = threadIdx.x; b < bp; b += blockDim.x) {
+        const uint64_t key = top[b];
+        out->cand[b] = key;
+        SelRec r;
+        r.key = key;
+        r.flags = 0;
+        r.x_unset = 0;
+        r.desc.i = -1; r.desc.slab = 0; r.desc.req = 0; r.desc.round = 0; r.desc.r = -1;
+        r.desc.pad[0] = r.desc.pad[1] = r.desc.pad[2] = 0;
+        if (key != ~0ull) {
+            const int32_t i = (int32_t)((uint32_t)(key & 0xFFFFFFull) / (uint32_t)sc.world);
+            r.flags = st.flags[i];
+            r.x_unset = st.x[i] < 0;
+            if (rw.valid) r.desc = make_desc(rw, st, sc, 0, i);
+        }
+        rec[b] = r;
+    }
     if (threadIdx.x == 0) {
         out->now_us = s_now;
         out->cursor = s_cursor;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&out->ready), "r"(1u) : "memory");
     }
 }
 
@@ -409,6 +185,7 @@ __global__ void __launch_bounds__(kSelThreads) select_final_kernel(const State s
                                                                     int32_t *count_out, const PreSelect *pre) {
     extern __shared__ uint64_t s_buf[];
     __shared__ int s_count;
+    STRACE(0);
     const int bp = next_pow2(B);
     const int64_t now = pre->now_us;
     const int cursor = pre->cursor;
@@ -426,12 +203,15 @@ __global__ void __launch_bounds__(kSelThreads) select_final_kernel(const State s
         }
         s_buf[b] = key;
     }
+    uint64_t *cand = s_buf + 2 * bp;  // presorted candidates, staged in shared memory
+    for (int b = threadIdx.x; b < bp; b += blockDim.x) cand[b] = pre->cand[b];
     if (threadIdx.x == 0) s_count = 0;
     __syncthreads();
+    STRACE(1);
     const uint64_t *bk = block_sort(s_buf, bp >= 64 && bp <= kMergeCap ? s_buf + bp : nullptr, bp);
+    STRACE(2);
     // merge path: first B outputs of merge(batch keys, presorted candidates)
     uint64_t *merged = (bk == s_buf) ? s_buf + bp : s_buf;
-    const uint64_t *cand = pre->cand;
     for (int o = threadIdx.x; o < B; o += blockDim.x) {
         int lo = o - bp > 0 ? o - bp : 0, hi = o < bp ? o : bp;
         while (lo < hi) {
@@ -443,11 +223,13 @@ __global__ void __launch_bounds__(kSelThreads) select_final_kernel(const State s
         merged[o] = takeA ? bk[i] : cand[j];
     }
     __syncthreads();
+    STRACE(3);
     int valid = 0;
     for (int b = threadIdx.x; b < B; b += blockDim.x) valid += (merged[b] >> 63) == 0;
     if (valid) atomicAdd(&s_count, valid);
     __syncthreads();
     const int cnt = s_count;
+    STRACE(4);
     for (int b = threadIdx.x; b < B; b += blockDim.x) {
         int32_t i = -1;
         if (b < cnt) {
@@ -469,28 +251,245 @@ __global__ void __launch_bounds__(kSelThreads) select_final_kernel(const State s
         st.g->prev_count = cnt;
         st.g->count = cnt;
         if (count_out) *count_out = cnt;
+        const_cast<PreSelect *>(pre)->ready = 0;
     }
+    __syncthreads();
+    STRACE(5);
 }
 
-cudaError_t launch_presort(const State &st, const Sched &sc, const int32_t *sel, int32_t B, PreSelect *out,
-                           cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) { set_smem_attr((const void *)presort_kernel); attr = true; }
+// ---------------------------------------------------------------- incremental select
+// One CTA on the side stream, concurrent with the verify kernel (which leaves it one
+// SM).  Phase 1 = the presort above.  Phase 2: the verify finishers publish each
+// batch slot as soon as its record (new key, flags, next descriptor) is written; this
+// CTA repeatedly takes the newly published slots, sorts their keys and merges them into
+// its sorted running list, keeping only the first B (an element ranked >= B can never
+// re-enter the top B).  When every verified slot has arrived the list IS the next
+// batch, and the commit (x_i, pinning, running flags, descriptors, clock) follows.
+__global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st, const Sched sc, const RowsDev rw,
+                                                                   int32_t *sel, SlotDesc *desc, int32_t B,
+                                                                   PreSelect *pre, const SelRec *fin, uint32_t *pubq,
+                                                                   int32_t *count_out) {
+    extern __shared__ uint64_t s_buf[];
+    STRACE(8);
+    __shared__ int64_t s_now;
+    __shared__ int s_cursor, s_expected, s_head, s_m, s_count;
+    __shared__ uint32_t s_member[kSortCap / 32];
+    const int n = sc.n;
+    const int T = blockDim.x;
+    // ---------------- phase 1: presort of every request outside the batch
+    for (int w = threadIdx.x; w < (n + 31) / 32; w += T) s_member[w] = 0;
+    if (threadIdx.x == 0) { s_expected = 0; s_head = 0; s_count = 0; }
+    advance_and_admit(st, sc, &s_now, &s_cursor);   // ends with a barrier
+    int expected = 0;
+    for (int b = threadIdx.x; b < B; b += T) {
+        const int i = sel[b];
+        if (i >= 0) atomicOr(&s_member[i >> 5], 1u << (i & 31));
+        const SlotDesc d = desc[b];
+        expected += (d.r >= 0 && i >= 0 && d.i == i);   // the slots the verify kernel will finish
+    }
+    if (expected) atomicAdd(&s_expected, expected);
+    __syncthreads();
+    const int npow2 = next_pow2(n > 0 ? n : 1);
+    const int cursor = s_cursor;
+    for (int i = threadIdx.x; i < npow2; i += T) {
+        uint64_t key = ~0ull;
+        if (i < n && !((s_member[i >> 5] >> (i & 31)) & 1u)) {
+            const uint32_t fl = st.flags[i];
+            const int32_t lp = st.L_pred[i], tok = st.acc_tok[i];
+            const double A = st.A[i];
+            key = build_key(sc, i, cursor, fl, lp, tok, A);
+            st.key[i] = key;
+            if (key >> 63) key = ~0ull;   // ineligible: never selected
+        }
+        s_buf[i] = key;
+    }
+    __syncthreads();
+    const int bp = next_pow2(B);
+    const uint64_t *top = select_topB(s_buf, n, B, s_buf + npow2, s_buf + npow2 + bp, bp);
+    SelRec *crec = pre_recs(pre, bp);
+    for (int b = threadIdx.x; b < bp; b += T) {
+        const uint64_t key = top[b];
+        pre->cand[b] = key;
+        SelRec r;
+        r.key = key;
+        r.flags = 0;
+        r.x_unset = 0;
+        r.desc.i = -1; r.desc.slab = 0; r.desc.req = 0; r.desc.round = 0; r.desc.r = -1;
+        r.desc.pad[0] = r.desc.pad[1] = r.desc.pad[2] = 0;
+        if (key != ~0ull) {
+            const int32_t i = (int32_t)((uint32_t)(key & 0xFFFFFFull) / (uint32_t)sc.world);
+            r.flags = st.flags[i];
+            r.x_unset = st.x[i] < 0;
+            if (rw.valid && rw.slab_tab) r.desc = make_desc(rw, st, sc, 0, i);
+        }
+        crec[b] = r;
+    }
+    __syncthreads();
+    ITRACE(200000);
+    // ---------------- phase 2: fold in the verified batch as it is published
+    uint64_t *L = s_buf;                      // [bp] running top-B, sorted
+    uint64_t *L2 = s_buf + bp;                // [bp]
+    uint64_t *nk = s_buf + 2 * bp;            // [bp] newly published keys
+    uint64_t *ntmp = s_buf + 3 * bp;          // [bp]
+    int16_t *slot_of = reinterpret_cast<int16_t *>(s_buf + 4 * bp);   // [n]: batch slot, or -1
+    int16_t *cand_of = slot_of + ((n + 7) & ~7);                       // [n]: candidate index, or -1
+    // record copies in shared memory (bp <= 1024), so the commit needs no dependent loads
+    SelRec *brec = reinterpret_cast<SelRec *>(cand_of + ((n + 7) & ~7));
+    SelRec *srec = brec + bp;
+    const bool rec_smem = bp <= 1024;
+    if (rec_smem)
+        for (int b = threadIdx.x; b < bp; b += T) srec[b] = crec[b];
+    for (int b = threadIdx.x; b < bp; b += T) L[b] = pre->cand[b];
+    for (int i = threadIdx.x; i < n; i += T) { slot_of[i] = -1; cand_of[i] = -1; }
+    __syncthreads();
+    for (int b = threadIdx.x; b < bp; b += T) {
+        const uint64_t key = L[b];
+        if (key != ~0ull) cand_of[(uint32_t)(key & 0xFFFFFFull) / (uint32_t)sc.world] = (int16_t)b;
+        if (b < B && sel[b] >= 0) slot_of[sel[b]] = (int16_t)b;
+    }
+    __syncthreads();
+    const int need = s_expected;
+    const unsigned long long t_start = gtimer();
+    for (;;) {
+        __syncthreads();               // everyone has finished with s_m / s_head
+        const int head = s_head;
+        if (head >= need) break;
+        if (waited_too_long(t_start)) {  // watchdog: never hang the GPU
+            if (threadIdx.x == 0) atomicOr(&st.g->err, E_TIMEOUT);
+            break;
+        }
+        // published entries head .. head+m-1 (stop at the first unpublished one)
+        if (threadIdx.x == 0) s_m = bp;
+        __syncthreads();
+        for (int x = threadIdx.x; x < bp && head + x < need; x += T) {
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(pubq + 1 + head + x) : "memory");
+            if (v == 0) {
+                atomicMin(&s_m, x);
+            } else {
+                const SelRec r = fin[v - 1];
+                nk[x] = r.key;
+                if (rec_smem) brec[v - 1] = r;
+            }
+        }
+        __syncthreads();
+        int m = s_m;
+        if (head + m > need) m = need - head;
+        if (m == 0 || (m < 32 && head + m < need)) {   // merge in batches of >= 32, or the last ones
+            __nanosleep(100);
+            continue;
+        }
+        ITRACE(m);
+        const int mp = next_pow2(m);
+        for (int x = m + (int)threadIdx.x; x < mp; x += T) nk[x] = ~0ull;
+        __syncthreads();
+        const uint64_t *snk = block_sort(nk, mp >= 64 && mp <= kMergeCap ? ntmp : nullptr, mp);
+        for (int o = threadIdx.x; o < bp; o += T) {   // first bp outputs of merge(L, snk)
+            int lo = o - mp > 0 ? o - mp : 0, hi = o < bp ? o : bp;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (L[mid] <= snk[o - 1 - mid]) lo = mid + 1; else hi = mid;
+            }
+            const int i = lo, j = o - lo;
+            const bool takeA = j >= mp || (i < bp && L[i] <= snk[j]);
+            L2[o] = takeA ? L[i] : snk[j];
+        }
+        __syncthreads();
+        for (int o = threadIdx.x; o < bp; o += T) L[o] = L2[o];
+        for (int x = threadIdx.x; x < m; x += T) pubq[1 + head + x] = 0;   // consumed
+        __syncthreads();
+        if (threadIdx.x == 0) s_head = head + m;
+    }
+    __syncthreads();
+    ITRACE(100000);
+    // ---------------- commit
+    int valid = 0;
+    for (int b = threadIdx.x; b < B; b += T) valid += (L[b] >> 63) == 0;
+    if (valid) atomicAdd(&s_count, valid);
+    __syncthreads();
+    const int cnt = s_count;
+    const int64_t now = s_now;
+    uint8_t *mark = reinterpret_cast<uint8_t *>(L2);     // [bp] 1 reselected, 2 +pin
+    int32_t *old_i = reinterpret_cast<int32_t *>(nk);    // [bp] the verified batch
+    for (int b = threadIdx.x; b < bp; b += T) { mark[b] = 0; old_i[b] = b < B ? sel[b] : -1; }
+    __syncthreads();
+    for (int b = threadIdx.x; b < B; b += T) {
+        SlotDesc d;
+        d.i = -1; d.slab = 0; d.req = 0; d.round = 0; d.r = -1;
+        d.pad[0] = d.pad[1] = d.pad[2] = 0;
+        if (b < cnt) {
+            const int i = (int)((uint32_t)(L[b] & 0xFFFFFFull) / (uint32_t)sc.world);
+            const int sl = slot_of[i];
+            const SelRec &rec = sl >= 0 ? (rec_smem ? brec[sl] : fin[sl])
+                                        : (rec_smem ? srec[cand_of[i]] : crec[cand_of[i]]);
+            d = rec.desc;
+            if (!rw.slab_tab) d = make_desc(rw, st, sc, b, i);   // batch layout: slab = slot
+            bool pin = false;
+            if (sc.policy == LAPSSD_POL_FCFS || sc.policy == LAPSSD_POL_LPSJF) pin = true;
+            else if (sc.policy == LAPSSD_POL_LAPSSD && sc.pin_rule == 0 && (rec.flags & F_PERC)) pin = true;
+            if (sl >= 0) {
+                mark[sl] = pin ? 2 : 1;
+            } else {
+                if (pin && !(rec.flags & F_PINNED)) st.flags[i] = rec.flags | F_PINNED;
+                if (rec.x_unset) st.x[i] = now;      // x_i
+            }
+        }
+        sel[b] = d.i;
+        desc[b] = d;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < B; b += T) {   // the verified batch: running flags cleared
+        const int i = old_i[b];
+        if (i < 0) continue;
+        uint32_t fl = (rec_smem ? brec[b].flags : fin[b].flags) & ~F_RUNNING;
+        if (mark[b] == 2) fl |= F_PINNED;
+        st.flags[i] = fl;
+    }
+    if (threadIdx.x == 0) {
+        int64_t nnow = now;
+        if (cnt == 0 && s_cursor < n) {
+            const int64_t nxt = st.arrival[s_cursor];
+            if (nxt > nnow) nnow = nxt;
+        }
+        st.g->now_us = nnow;
+        st.g->cursor = s_cursor;
+        st.g->prev_count = cnt;
+        st.g->count = cnt;
+        if (count_out) *count_out = cnt;
+        pubq[0] = 0;
+    }
+    STRACE(9);
+}
+
+cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
+                               int32_t B, PreSelect *pre, const SelRec *fin, uint32_t *pubq, int32_t *count_out,
+                               cudaStream_t s) {
     int np = 1, bp = 1;
     while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
     while (bp < B) bp <<= 1;
-    presort_kernel<<<1, kSelThreads, (size_t)(np + 2 * bp) * sizeof(uint64_t), s>>>(st, sc, sel, B, out);
+    const size_t a = (size_t)(np + 2 * bp) * sizeof(uint64_t);
+    const size_t b = (size_t)4 * bp * sizeof(uint64_t) + 2 * (size_t)((sc.n + 7) & ~7) * sizeof(int16_t) + 64 +
+                     (bp <= 1024 ? 2 * (size_t)bp * sizeof(SelRec) : 0);
+    select_side_kernel<<<1, kSelThreads, a > b ? a : b, s>>>(st, sc, rw, sel, desc, B, pre, fin, pubq, count_out);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_presort(const State &st, const Sched &sc, const RowsDev &rw, const int32_t *sel, int32_t B,
+                           PreSelect *out, cudaStream_t s) {
+    int np = 1, bp = 1;
+    while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
+    while (bp < B) bp <<= 1;
+    presort_kernel<<<1, kSelThreads, (size_t)(np + 2 * bp) * sizeof(uint64_t), s>>>(st, sc, rw, sel, B, out);
     count_launch();
     return cudaGetLastError();
 }
 
 cudaError_t launch_select_final(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc, int32_t B,
                                 int32_t *sel, int32_t *count_out, const PreSelect *pre, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) { set_smem_attr((const void *)select_final_kernel); attr = true; }
     int bp = 1;
     while (bp < B) bp <<= 1;
-    select_final_kernel<<<1, kSelThreads, (size_t)(2 * bp) * sizeof(uint64_t), s>>>(st, sc, rw, desc, B, sel,
+    select_final_kernel<<<1, kSelThreads, (size_t)(3 * bp) * sizeof(uint64_t), s>>>(st, sc, rw, desc, B, sel,
                                                                                      count_out, pre);
     count_launch();
     return cudaGetLastError();
@@ -498,8 +497,6 @@ cudaError_t launch_select_final(const State &st, const Sched &sc, const RowsDev 
 
 cudaError_t launch_select(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc, int32_t B,
                           int32_t *sel_out, int32_t *count_out, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) { set_smem_attr((const void *)select_kernel); attr = true; }
     int np = 1, bp = 1;
     while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
     while (bp < B) bp <<= 1;
@@ -535,8 +532,6 @@ __global__ void __launch_bounds__(kSelThreads) candidates_kernel(const State st,
 
 cudaError_t launch_candidates(const State &st, const Sched &sc, int32_t C, uint64_t *cand_out,
                               cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) { set_smem_attr((const void *)candidates_kernel); attr = true; }
     candidates_kernel<<<1, kSelThreads, sort_smem_bytes(sc.n > 0 ? sc.n : 1), s>>>(st, sc, C, cand_out);
     count_launch();
     return cudaGetLastError();
@@ -614,13 +609,23 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
 cudaError_t launch_merge(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc,
                          const uint64_t *all_cand, int32_t C, int32_t B, int32_t *sel_out,
                          int32_t *count_out, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) { set_smem_attr((const void *)merge_kernel); attr = true; }
     const int total = sc.world * C;
     merge_kernel<<<1, kSelThreads, sort_smem_bytes(total > 0 ? total : 1), s>>>(st, sc, rw, desc, all_cand, C,
                                                                                 B, sel_out, count_out);
     count_launch();
     return cudaGetLastError();
+}
+
+// Kernel attributes are set once, at handle creation: cudaFuncSetAttribute may wait for
+// the device to go idle, which must never happen while a verify and a side kernel that
+// wait on each other are in flight.
+void sched_prepare() {
+    set_smem_attr((const void *)select_kernel);
+    set_smem_attr((const void *)candidates_kernel);
+    set_smem_attr((const void *)merge_kernel);
+    set_smem_attr((const void *)presort_kernel);
+    set_smem_attr((const void *)select_final_kernel);
+    set_smem_attr((const void *)select_side_kernel);
 }
 
 }  // namespace lapssd

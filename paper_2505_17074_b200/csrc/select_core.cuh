@@ -1,0 +1,516 @@
+// select_core.cuh -- block-level selection primitives shared by the select kernels
+// (sched.cu) and the fused final select at the end of the verify kernel (verify.cu):
+// warp-register bitonic sort + merge-path block sort, radix top-B selection, admission,
+// key building and commits.  PAPER.md P:129-142; DESIGN.md s.6.
+#pragma once
+
+#include "lapssd_internal.cuh"
+
+namespace lapssd {
+
+constexpr int kSelThreads = 1024;
+constexpr int kSortCap = 16384;          // keys per CTA (bitonic in place above kMergeCap)
+constexpr int kMergeCap = 8192;          // keys sorted by warp-sort + merge-path (2 buffers)
+
+// ---------------------------------------------------------------- block sort
+__device__ inline void bitonic_sort(uint64_t *s, int n) {  // n power of two, ascending, in place
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const uint64_t x = s[i], y = s[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((x > y) == up) { s[i] = y; s[ixj] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Sort one 64-key run held as (lo = element lane, hi = element lane + 32).
+__device__ __forceinline__ void warp_sort64(uint64_t &lo, uint64_t &hi, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {
+                const bool asc = true;  // k == 64: (e & 64) == 0 for every element
+                const uint64_t a = lo < hi ? lo : hi, b = lo < hi ? hi : lo;
+                lo = asc ? a : b;
+                hi = asc ? b : a;
+            } else {
+                const bool lower = (lane & j) == 0;
+                {
+                    const uint64_t p = __shfl_xor_sync(0xFFFFFFFFu, lo, j);
+                    const bool asc = ((lane & k) == 0);
+                    lo = (lower == asc) ? (lo < p ? lo : p) : (lo > p ? lo : p);
+                }
+                {
+                    const uint64_t p = __shfl_xor_sync(0xFFFFFFFFu, hi, j);
+                    const bool asc = (((lane + 32) & k) == 0);
+                    hi = (lower == asc) ? (hi < p ? hi : p) : (hi > p ? hi : p);
+                }
+            }
+        }
+    }
+}
+
+// Register-resident bitonic sort of n keys held in s (n = E * T, T = n / E threads
+// take part; the block's other threads only join the barriers).  Thread t holds the
+// elements e(m) = (t/32)*32E + 32m + lane, m < E, so a partner at distance j < 32 is a
+// warp shuffle, 32 <= j < 32E is a swap inside the thread, and only j >= 32E goes
+// through shared memory.  Ascending; result back in s.
+template <int E>
+__device__ void bitonic_reg(uint64_t *s, int n) {
+    const int T = n / E;
+    const int t = threadIdx.x;
+    const bool on = t < T;
+    const int lane = t & 31;
+    const int ebase = (t >> 5) * 32 * E + lane;   // element of v[m] is ebase + 32 m
+    uint64_t v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = on ? s[ebase + 32 * m] : ~0ull;
+    for (int k = 2; k <= n; k <<= 1) {
+        int j = k >> 1;
+        if (j >= 32 * E) {  // cross-warp distances: in shared memory
+            if (on) {
+#pragma unroll
+                for (int m = 0; m < E; ++m) s[ebase + 32 * m] = v[m];
+            }
+            __syncthreads();
+            for (; j >= 32 * E; j >>= 1) {
+                if (on) {
+#pragma unroll
+                    for (int m = 0; m < E; ++m) {
+                        const int e = ebase + 32 * m;
+                        const uint64_t b = s[e ^ j];
+                        const bool lower = (e & j) == 0, asc = (e & k) == 0;
+                        v[m] = (lower == asc) ? (v[m] < b ? v[m] : b) : (v[m] > b ? v[m] : b);
+                    }
+                }
+                __syncthreads();
+                if (on) {
+#pragma unroll
+                    for (int m = 0; m < E; ++m) s[ebase + 32 * m] = v[m];
+                }
+                __syncthreads();
+            }
+        }
+        // inside the thread: distances 32*dm for dm = E/2 .. 1 (compile-time register indices)
+#pragma unroll
+        for (int dm = E / 2; dm >= 1; dm >>= 1) {
+            if (32 * dm <= j) {
+#pragma unroll
+                for (int m = 0; m < E; ++m) {
+                    if ((m & dm) == 0) {
+                        const bool asc = ((ebase + 32 * m) & k) == 0;
+                        const uint64_t a = v[m], b = v[m | dm];
+                        const uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+                        v[m] = asc ? lo : hi;
+                        v[m | dm] = asc ? hi : lo;
+                    }
+                }
+            }
+        }
+        if (j >= 32) j = 16;
+        for (; j > 0; j >>= 1) {  // inside the warp
+            const bool lower = (lane & j) == 0;
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const uint64_t p = __shfl_xor_sync(0xFFFFFFFFu, v[m], j);
+                const bool asc = ((ebase + 32 * m) & k) == 0;
+                v[m] = (lower == asc) ? (v[m] < p ? v[m] : p) : (v[m] > p ? v[m] : p);
+            }
+        }
+    }
+    __syncthreads();
+    if (on) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) s[ebase + 32 * m] = v[m];
+    }
+    __syncthreads();
+}
+
+// Block sort front end: picks E so that n / E threads fit in the block.
+__device__ inline void block_sort_reg(uint64_t *s, int n) {
+    int T = 1;
+    while (T * 2 <= (int)blockDim.x) T <<= 1;
+    if (n < 64) {
+        bitonic_sort(s, n);
+        return;
+    }
+    const int E = n / T > 0 ? n / T : 1;
+    if (n / E < 32) { bitonic_sort(s, n); return; }
+    switch (E) {
+    case 1: bitonic_reg<1>(s, n); break;
+    case 2: bitonic_reg<2>(s, n); break;
+    case 4: bitonic_reg<4>(s, n); break;
+    case 8: bitonic_reg<8>(s, n); break;
+    default: bitonic_sort(s, n); break;
+    }
+}
+
+// Sorts n (power of two) keys; returns the buffer holding the result (a or b).
+__device__ inline uint64_t *block_sort(uint64_t *a, uint64_t *b, int n) {
+    if (n < 64 || n > kMergeCap || b == nullptr) {
+        bitonic_sort(a, n);
+        return a;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int run = warp; run < n / 64; run += nwarps) {
+        uint64_t lo = a[run * 64 + lane], hi = a[run * 64 + 32 + lane];
+        warp_sort64(lo, hi, lane);
+        a[run * 64 + lane] = lo;
+        a[run * 64 + 32 + lane] = hi;
+    }
+    __syncthreads();
+    uint64_t *src = a, *dst = b;
+    const int T = blockDim.x;
+    int per = 1;  // outputs per thread: a power of two, so no thread's range crosses a pair
+    while (per * 2 * T <= n) per *= 2;
+    for (int w = 64; w < n; w <<= 1) {
+        for (int o0 = threadIdx.x * per; o0 < n; o0 += T * per) {
+            const int pair = o0 / (2 * w);
+            const int d0 = o0 - pair * 2 * w;
+            const uint64_t *A = src + pair * 2 * w;
+            const uint64_t *Bv = A + w;
+            int lo = d0 - w > 0 ? d0 - w : 0, hi = d0 < w ? d0 : w;
+            while (lo < hi) {  // number of A elements among the first d0 outputs
+                const int mid = (lo + hi) >> 1;
+                if (A[mid] <= Bv[d0 - 1 - mid]) lo = mid + 1; else hi = mid;
+            }
+            int i = lo, j = d0 - lo;
+            for (int e = 0; e < per; ++e) {
+                const bool takeA = j >= w || (i < w && A[i] <= Bv[j]);
+                dst[o0 + e] = takeA ? A[i++] : Bv[j++];
+            }
+        }
+        __syncthreads();
+        uint64_t *t = src; src = dst; dst = t;
+    }
+    return src;
+}
+
+// The B smallest of n keys, sorted ascending, into out[0..bp) (bp = next_pow2(B) with
+// UINT64_MAX padding); tmp is bp words of scratch.  MSB-first radix select finds the
+// B-th smallest key T with eight 256-bin histogram passes (keys are unique: the id is
+// in the low bits), then the keys <= T are compacted and only they are sorted.
+__device__ inline uint64_t *select_topB(const uint64_t *keys, int n, int B, uint64_t *out, uint64_t *tmp, int bp) {
+    __shared__ int hist[256];
+    __shared__ uint64_t s_prefix, s_mask;
+    __shared__ int s_remaining, s_done;
+    __shared__ int s_scan[64];
+    const int want = B < n ? B : n;
+    if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_remaining = want; s_done = 0; }
+    __syncthreads();
+    for (int shift = 56; shift >= 0 && want > 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        if (s_done) break;
+        const uint64_t prefix = s_prefix, mask = s_mask;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint64_t key = keys[i];
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            int loc[8], sum = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { loc[e] = hist[lane * 8 + e]; sum += loc[e]; }
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int rem = s_remaining;
+            const unsigned hit = __ballot_sync(0xFFFFFFFFu, incl >= rem);
+            const int src = __ffs(hit) - 1;
+            if (lane == src) {
+                int acc = incl - sum;
+                int dgt = 0;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    if (acc + loc[e] >= rem) { dgt = lane * 8 + e; break; }
+                    acc += loc[e];
+                }
+                const int cnt = hist[dgt];
+                s_prefix = prefix | ((uint64_t)dgt << shift);
+                s_mask = mask | (255ull << shift);
+                s_remaining = rem - acc;
+                if (rem - acc == cnt) s_done = 1;  // every key of this bin is needed
+            }
+        }
+        __syncthreads();
+    }
+    // threshold: all keys matching the final prefix pattern up to its mask, i.e. key <= T
+    const uint64_t T = want > 0 ? (s_prefix | ~s_mask) : 0;
+    // compact keys <= T (exactly `want` of them) in index order, then sort
+    const int per = (n + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int lo = (int)threadIdx.x * per;
+    int mine = 0;
+    // keys are unique except UINT64_MAX padding: take keys < T, plus T itself unless it
+    // is the padding value (then the tail is filled with padding below)
+    const bool t_real = T != ~0ull;
+    for (int i = lo; i < lo + per && i < n; ++i) mine += want > 0 && (keys[i] < T || (t_real && keys[i] == T));
+    int total = 0;
+    {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        int x = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += v;
+        }
+        if (lane == 31) s_scan[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int w = lane < (int)(blockDim.x >> 5) ? s_scan[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xFFFFFFFFu, w, o);
+                if (lane >= o) w += v;
+            }
+            s_scan[32 + lane] = w;
+        }
+        __syncthreads();
+        int pos = (warp > 0 ? s_scan[32 + warp - 1] : 0) + x - mine;
+        total = s_scan[32 + (int)(blockDim.x >> 5) - 1];
+        for (int i = lo; i < lo + per && i < n; ++i)
+            if (want > 0 && (keys[i] < T || (t_real && keys[i] == T)) && pos < bp) out[pos++] = keys[i];
+    }
+    for (int i = total + (int)threadIdx.x; i < bp; i += blockDim.x) out[i] = ~0ull;
+    __syncthreads();
+    return block_sort(out, bp >= 64 && bp <= kMergeCap ? tmp : nullptr, bp);
+}
+
+__device__ __forceinline__ int next_pow2(int n) {
+    int p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+
+__host__ __device__ inline size_t sort_smem_bytes(int n) {
+    int p = 1;
+    while (p < n) p <<= 1;
+    return (size_t)p * sizeof(uint64_t) * (p >= 64 && p <= kMergeCap ? 2 : 1);
+}
+
+// Block-wide exclusive scan of one int per thread.
+__device__ inline int block_excl_scan(int v, int *s_tmp, int *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += n;
+    }
+    if (lane == 31) s_tmp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < (int)(blockDim.x >> 5) ? s_tmp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int n = __shfl_up_sync(0xFFFFFFFFu, w, o);
+            if (lane >= o) w += n;
+        }
+        s_tmp[32 + lane] = w;  // inclusive warp totals
+    }
+    __syncthreads();
+    const int before = warp > 0 ? s_tmp[32 + warp - 1] : 0;
+    *total = s_tmp[32 + (int)(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return before + x - v;
+}
+
+// a7 (first half) + a4: advance the clock by the round that ran, admit arrivals.
+// Arrivals are sorted, so the admitted set is the prefix [0, cursor).
+__device__ inline void advance_and_admit(const State &st, const Sched &sc, int64_t *s_now, int *s_cursor) {
+    if (threadIdx.x == 0) {
+        int64_t now = st.g->now_us;
+        if (st.g->prev_count > 0) now += sc.c_round_us;         // AMB-17
+        *s_now = now;
+        *s_cursor = st.g->cursor;
+    }
+    __syncthreads();
+    const int64_t now = *s_now;
+    int cursor = *s_cursor;
+    for (;;) {
+        const int idx = cursor + (int)threadIdx.x;
+        const bool adm = idx < sc.n && st.arrival[idx] <= now;
+        const int cnt = __syncthreads_count(adm);
+        cursor += cnt;
+        if (cnt < (int)blockDim.x) break;
+    }
+    if (threadIdx.x == 0) *s_cursor = cursor;
+    __syncthreads();
+}
+
+// Build every key into global and shared memory (padded to npow2 with UINT64_MAX)
+// and clear the running flags (they describe the round that just ran).
+__device__ inline void build_keys(const State &st, const Sched &sc, int cursor, uint64_t *s_keys, int npow2) {
+    for (int i = threadIdx.x; i < npow2; i += blockDim.x) {
+        uint64_t key = ~0ull;
+        if (i < sc.n) {
+            const uint32_t fl = st.flags[i];
+            const int32_t lp = st.L_pred[i], tok = st.acc_tok[i];
+            const double A = st.A[i];
+            key = build_key(sc, i, cursor, fl, lp, tok, A);
+            st.key[i] = key;
+            if (fl & F_RUNNING) st.flags[i] = fl & ~F_RUNNING;
+        }
+        s_keys[i] = key;
+    }
+    __syncthreads();
+}
+
+// Commit one selected request: first-service time and pinning (AMB-15, AMB-25).
+__device__ __forceinline__ void commit_one(const State &st, const Sched &sc, int32_t i, int64_t now) {
+    if (st.x[i] < 0) st.x[i] = now;                                // x_i
+    const uint32_t fl = st.flags[i];
+    bool pin = false;
+    if (sc.policy == LAPSSD_POL_FCFS || sc.policy == LAPSSD_POL_LPSJF) pin = true;
+    else if (sc.policy == LAPSSD_POL_LAPSSD && sc.pin_rule == 0 && (fl & F_PERC)) pin = true;
+    if (pin && !(fl & F_PINNED)) st.flags[i] = fl | F_PINNED;
+}
+
+
+// ---------------------------------------------------------------- fused final select
+// Run by the last CTA of the verify kernel (all its threads).  Inputs: the finishers'
+// records of the verified batch (new key, flags, next-round descriptor) and the
+// presort's sorted top-B candidates of every other request (with records).  The B
+// batch keys are sorted, merged with the candidates (first B outputs), and the result
+// is committed exactly as select_kernel does: batch in key order, x_i on first
+// selection, pinning, running flags cleared, clock / admission / counts.
+__device__ __forceinline__ void dbg_time(unsigned long long *tr, int i) {
+    if (tr && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tr[i] = t;
+    }
+}
+__device__ inline void fused_final_select(const State &st, const Sched &sc, int B, int32_t *sel, SlotDesc *desc,
+                                          const SelRec *fin, PreSelect *pre, int32_t *count_out, uint64_t *smem,
+                                          unsigned long long *tr = nullptr) {
+    __shared__ int s_count;
+    dbg_time(tr, 0);
+    if (threadIdx.x == 0) {
+        uint32_t ready = 0;
+        const unsigned long long t_start = gtimer();
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(ready) : "l"(&pre->ready) : "memory");
+            if (!ready) __nanosleep(64);
+            if (waited_too_long(t_start)) { atomicOr(&st.g->err, E_TIMEOUT); break; }
+        } while (!ready);
+        s_count = 0;
+    }
+    __syncthreads();
+    dbg_time(tr, 1);
+    const int bp = next_pow2(B);
+    uint64_t *bk = smem;                                  // [bp] batch keys
+    uint64_t *tmp = smem + bp;                            // [bp]
+    uint64_t *cand = smem + 2 * bp;                       // [bp] presorted candidates
+    uint64_t *merged = smem + 3 * bp;                     // [bp]
+    int32_t *msrc = reinterpret_cast<int32_t *>(smem + 4 * bp);          // [bp] origin of each output
+    int32_t *old_i = msrc + bp;                                           // [bp] batch requests
+    uint8_t *mark = reinterpret_cast<uint8_t *>(old_i + bp);            // [bp] 1 reselected, 2 +pin
+    int16_t *slot_of = reinterpret_cast<int16_t *>(mark + ((bp + 15) & ~15));  // [n] slot of a request
+    const SelRec *crec = pre_recs(pre, bp);
+    for (int b = threadIdx.x; b < bp; b += blockDim.x) {
+        const int i = b < B ? sel[b] : -1;
+        old_i[b] = i;
+        bk[b] = i >= 0 ? fin[b].key : ~0ull;
+        cand[b] = pre->cand[b];
+        mark[b] = 0;
+        if (i >= 0) slot_of[i] = (int16_t)b;
+    }
+    __syncthreads();
+    dbg_time(tr, 2);
+#ifdef LAPSSD_TRACE_SORT_TWICE
+    {   // diagnostic: sort a copy first, so the timed sort below runs with a warm I-cache
+        uint64_t *c2 = merged;
+        for (int b = threadIdx.x; b < bp; b += blockDim.x) c2[b] = bk[b];
+        __syncthreads();
+        block_sort(c2, reinterpret_cast<uint64_t *>(msrc), bp);
+        __syncthreads();
+        dbg_time(tr, 6);
+    }
+#endif
+    const uint64_t *sk = block_sort(bk, tmp, bp);
+    dbg_time(tr, 3);
+    for (int o = threadIdx.x; o < B; o += blockDim.x) {  // merge path, first B outputs
+        int lo = o - bp > 0 ? o - bp : 0, hi = o < bp ? o : bp;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sk[mid] <= cand[o - 1 - mid]) lo = mid + 1; else hi = mid;
+        }
+        const int i = lo, j = o - lo;
+        const bool takeA = j >= bp || (i < bp && sk[i] <= cand[j]);
+        const uint64_t key = takeA ? sk[i] : cand[j];
+        merged[o] = key;
+        int src = j;
+        if (takeA) {
+            const int req = (int)((uint32_t)(key & 0xFFFFFFull) / (uint32_t)sc.world);
+            src = key == ~0ull ? 0 : -(slot_of[req] + 1);
+        }
+        msrc[o] = src;
+    }
+    __syncthreads();
+    int valid = 0;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) valid += (merged[b] >> 63) == 0;
+    if (valid) atomicAdd(&s_count, valid);
+    __syncthreads();
+    const int cnt = s_count;
+    dbg_time(tr, 4);
+    const int64_t now = pre->now_us;
+    const int cursor = pre->cursor;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        SlotDesc d;
+        d.i = -1; d.slab = 0; d.req = 0; d.round = 0; d.r = -1;
+        d.pad[0] = d.pad[1] = d.pad[2] = 0;
+        if (b < cnt) {
+            const int src = msrc[b];
+            const SelRec &rec = src < 0 ? fin[-src - 1] : crec[src];
+            d = rec.desc;
+            bool pin = false;
+            if (sc.policy == LAPSSD_POL_FCFS || sc.policy == LAPSSD_POL_LPSJF) pin = true;
+            else if (sc.policy == LAPSSD_POL_LAPSSD && sc.pin_rule == 0 && (rec.flags & F_PERC)) pin = true;
+            if (src < 0) {
+                mark[-src - 1] = pin ? 2 : 1;          // batch member: flags written below
+            } else {
+                if (pin && !(rec.flags & F_PINNED)) st.flags[d.i] = rec.flags | F_PINNED;
+                if (rec.x_unset) st.x[d.i] = now;      // x_i
+            }
+        }
+        sel[b] = d.i;
+        desc[b] = d;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {  // the verified batch: running cleared
+        const int i = old_i[b];
+        if (i < 0) continue;
+        uint32_t fl = fin[b].flags & ~F_RUNNING;
+        if (mark[b] == 2) fl |= F_PINNED;
+        st.flags[i] = fl;
+    }
+    if (threadIdx.x == 0) {
+        int64_t nnow = now;
+        if (cnt == 0 && cursor < sc.n) {                             // idle: jump
+            const int64_t nxt = st.arrival[cursor];
+            if (nxt > nnow) nnow = nxt;
+        }
+        st.g->now_us = nnow;
+        st.g->cursor = cursor;
+        st.g->prev_count = cnt;
+        st.g->count = cnt;
+        if (count_out) *count_out = cnt;
+        pre->ready = 0;
+    }
+    __syncthreads();
+    dbg_time(tr, 5);
+}
+
+}  // namespace lapssd

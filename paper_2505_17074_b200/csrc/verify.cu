@@ -17,7 +17,7 @@
 // HBM bytes per slot: 2 V s (r < k) or V s (r = k), plus k gathered scalars.
 #include <cstdlib>
 
-#include "lapssd_internal.cuh"
+#include "select_core.cuh"
 
 namespace lapssd {
 
@@ -186,6 +186,24 @@ __device__ __forceinline__ void trace(int ev, int x) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_trace[slot][ev][x & 1023] = t;
 }
+__device__ unsigned long long g_cta_t[2][160];   // first / last instruction per CTA
+__device__ unsigned long long g_fs_trace[8];     // fused final select phases
+extern "C" int lapssd_fs_trace_read(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_fs_trace, sizeof g_fs_trace); }
+__device__ __forceinline__ void cta_time(int which) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 160) {
+        if (which == 0) atomicMin(&g_cta_t[0][blockIdx.x], t); else atomicMax(&g_cta_t[1][blockIdx.x], t);
+    }
+}
+extern "C" int lapssd_cta_trace_read(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_cta_t, sizeof(g_cta_t));
+    static unsigned long long init[2][160];
+    for (int i = 0; i < 160; ++i) { init[0][i] = ~0ull; init[1][i] = 0; }
+    cudaMemcpyToSymbol(g_cta_t, init, sizeof(init));
+    return 0;
+}
+#define CTA_TIME(w) cta_time(w)
 extern "C" int lapssd_trace_read(unsigned long long *out) {
     cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
     cudaMemset(nullptr, 0, 0);
@@ -196,6 +214,7 @@ extern "C" int lapssd_trace_read(unsigned long long *out) {
 #define TRACE(ev, x) trace(ev, x)
 #else
 #define TRACE(ev, x)
+#define CTA_TIME(w)
 #endif
 constexpr int kConsumerWarps = kWarps;                     // 8 per group
 constexpr int kGroups = 2;                                 // consumer groups take alternate items
@@ -288,10 +307,10 @@ __device__ __forceinline__ NextA1 next_a1_load(const VerifyArgs &a, int32_t i, u
     }
     return n;
 }
-__device__ __forceinline__ void next_a1_store(const VerifyArgs &a, int32_t i, uint32_t req, uint32_t round_next,
-                                              const NextA1 &n) {
+__device__ __forceinline__ int next_a1_store(const VerifyArgs &a, int32_t i, uint32_t req, uint32_t round_next,
+                                             const NextA1 &n) {
     const int lane = threadIdx.x & 31;
-    if (!n.live) return;
+    if (!n.live) return -1;
     const int k = a.rows.k;
     bool reject = false;
     if (lane < k) {
@@ -301,10 +320,12 @@ __device__ __forceinline__ void next_a1_store(const VerifyArgs &a, int32_t i, ui
         reject = !(__dmul_rn((double)(w >> 8), (double)n.qj) < __dmul_rn((double)n.pj, 16777216.0));
     }
     const unsigned m = __ballot_sync(0xFFFFFFFFu, reject);
+    const int r = m ? __ffs(m) - 1 : k;
     if (lane == 0) {
-        a.st.next_sr[i] = make_int2((int32_t)n.slab, m ? __ffs(m) - 1 : k);
+        a.st.next_sr[i] = make_int2((int32_t)n.slab, r);
         a.st.next_tag[i] = ((uint64_t)a.rows.epoch << 32) | round_next;
     }
+    return r;
 }
 
 // Warp-level finish of slot b: total Z, draw t, locate (chunk, warp segment), rescan
@@ -436,9 +457,30 @@ __device__ __forceinline__ void finish_slot_warp(const VerifyArgs &a, int b, con
     }
     if (lane == 0) TRACE(12, b);
     if (a.fuse_update) {
-        update_warp(a.st, a.sc, d.i, r, now, upd, lane);
+        const UpdOut uo = update_warp(a.st, a.sc, d.i, r, now, upd, lane);
         if (lane == 0) TRACE(13, b);
-        next_a1_store(a, d.i, d.req, d.round + 1, nxt);  // harmless if the request completed
+        const int r_next = next_a1_store(a, d.i, d.req, d.round + 1, nxt);  // harmless if it completed
+        if (a.fuse_select && lane == 0) {
+            // the request's record for the fused final select: new key and next descriptor
+            SelRec rec;
+            rec.key = build_key(a.sc, d.i, INT32_MAX, uo.fl, upd.Lp, uo.tok, uo.A);
+            rec.flags = uo.fl;
+            rec.x_unset = 0;
+            rec.desc.i = d.i;
+            rec.desc.slab = (int32_t)nxt.slab;
+            rec.desc.req = d.req;
+            rec.desc.round = d.round + 1;
+            rec.desc.r = r_next;
+            rec.desc.pad[0] = rec.desc.pad[1] = rec.desc.pad[2] = 0;
+            a.fin[b] = rec;
+            a.st.key[d.i] = rec.key;
+            __threadfence();
+            if (a.pubq) {  // publish: the side-stream merger may take this slot now
+                const uint32_t slot = atomicAdd(a.pubq, 1u);
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.pubq + 1 + slot), "r"((uint32_t)b + 1u)
+                             : "memory");
+            }
+        }
     }
     __syncwarp();
 }
@@ -468,6 +510,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nc = a.n_chunks;
     const int n_items = B * nc;
+    if (tid == 0) CTA_TIME(0);
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
@@ -541,8 +584,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                 __syncwarp();
             }
         }
-        return;
-    }
+    } else {
     const int grp = (warp - 1) / (kConsumerWarps + 1);
     const int gw = (warp - 1) % (kConsumerWarps + 1);  // 0..7 consumer, 8 finisher
     if (gw == kConsumerWarps) {
@@ -573,6 +615,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
             const NextA1 nxt = next_a1_load<BF16>(a, d.i, d.round + 1);
             const uint64_t *pw = a.part + (int64_t)b * nc * kPartWords;
             uint64_t w0[kWarps], w1[kWarps];
+            const unsigned long long t_start = gtimer();
             for (;;) {  // every (chunk, warp) sum of slot b published?
 #pragma unroll
                 for (int x = 0; x < kWarps; ++x) w0[x] = w1[x] = kReady;
@@ -582,14 +625,18 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
 #pragma unroll
                 for (int x = 0; x < kWarps; ++x) ready &= ((w0[x] & w1[x]) & kReady) != 0;
                 if (__all_sync(0xFFFFFFFFu, ready)) break;
+                if (waited_too_long(t_start)) {
+                    if (lane == 0 && a.err) atomicOr(a.err, E_TIMEOUT);
+                    break;
+                }
                 __nanosleep(32);
             }
             if (lane == 0) TRACE(6, b);
             finish_slot_warp<BF16>(a, b, d, s_fb[grp], w0, w1, upd, now, nxt);
             if (lane == 0) TRACE(7, b);
         }
-        return;
-    }
+        if (lane == 0) CTA_TIME(1);
+    } else {
     // ---------------------------------------------------------------- consumers of group grp
     int k = grp;
     const int warp_seg = gw;  // this warp's 1024-entry segment of every chunk
@@ -647,6 +694,30 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
         __threadfence_block();
         s_qtail[grp] = s_qtail[grp] + 1;
     }
+    }  // consumers
+    }  // consumer groups / finishers
+    if (tid == 0) CTA_TIME(1);
+    // ------------------------------------------------------------ fused final select
+    if (a.fuse_select && !a.pubq) {
+        __shared__ int s_last;
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            s_last = atomicAdd(a.done_ctas, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+#ifdef LAPSSD_TRACE
+            unsigned long long *trp = g_fs_trace;
+#else
+            unsigned long long *trp = nullptr;
+#endif
+            fused_final_select(a.st, a.sc, B, const_cast<int32_t *>(a.sel), const_cast<SlotDesc *>(a.desc), a.fin,
+                               a.pre, a.count_out, reinterpret_cast<uint64_t *>(s_tiles), trp);
+            if (tid == 0) *a.done_ctas = 0;
+        }
+    }
 }
 
 int verify_cpb(int64_t V) {
@@ -654,32 +725,45 @@ int verify_cpb(int64_t V) {
     return 1;
 }
 
+static int g_verify_grid = 0;
+
+template <bool BF16>
+static void verify_prepare_t() {
+    const size_t smem = (size_t)VerifyCfg<BF16>::kStages * 2 * VerifyCfg<BF16>::kTileBytes;
+    cudaFuncSetAttribute(verify_kernel<BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(verify_kernel<BF16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
+// Once per process, before any launch (see sched_prepare).
+void verify_prepare() {
+    verify_prepare_t<true>();
+    verify_prepare_t<false>();
+    cudaFuncSetAttribute(accept_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g_verify_grid = sms;
+}
+
 template <bool BF16>
 static cudaError_t launch_verify_t(const VerifyArgs &a, int32_t B, int32_t reserve_sms, cudaStream_t s) {
     const size_t smem = (size_t)VerifyCfg<BF16>::kStages * 2 * VerifyCfg<BF16>::kTileBytes;
-    static int grid = 0;
-    if (grid == 0) {
-        cudaFuncSetAttribute(verify_kernel<BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(verify_kernel<BF16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = sms;
-    }
+    const int grid = g_verify_grid > 0 ? g_verify_grid : 148;
     const int n_items = B * a.n_chunks;
     const int avail = grid - reserve_sms > 1 ? grid - reserve_sms : 1;  // SMs left for a concurrent kernel
     const int g = n_items < avail ? n_items : avail;
-    // co-residency is required (finishers wait on other CTAs' chunks): cooperative launch
+    // Finishers wait on other CTAs' chunks, so all CTAs must be resident together: each
+    // CTA needs an SM's shared memory (one CTA per SM) and the grid is at most the SM
+    // count minus the SMs left to the side-stream select.  No cooperative attribute: a
+    // cooperative launch is serialised against other streams' kernels, which would
+    // forbid exactly the overlap with the side kernel.  Device waits have a watchdog.
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)g);
     cfg.blockDim = dim3(kVerifyThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.attrs = nullptr;
+    cfg.numAttrs = 0;
     return cudaLaunchKernelEx(&cfg, verify_kernel<BF16>, a, B);
 }
 

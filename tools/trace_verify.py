@@ -24,10 +24,13 @@ for _ in range(8):
     h.laps_step(rows, 512)
 torch.cuda.synchronize()
 buf = np.zeros((2, 16, 1024), np.uint64)
+ct = np.zeros((2, 160), np.uint64)
 lib.lapssd_trace_read(buf.ctypes.data_as(C.c_void_p))
+lib.lapssd_cta_trace_read(ct.ctypes.data_as(C.c_void_p))
 h.laps_step(rows, 512)
 torch.cuda.synchronize()
 lib.lapssd_trace_read(buf.ctypes.data_as(C.c_void_p))
+lib.lapssd_cta_trace_read(ct.ctypes.data_as(C.c_void_p))
 names = {1: "P-wait", 2: "P-free", 8: "P-issued", 3: "C-full", 4: "C-done", 5: "F-pop", 6: "F-ready", 7: "F-done",
          9: "f-Z", 10: "f-seg", 11: "f-y", 12: "f-out", 13: "f-upd"}
 for cta in range(2):
@@ -42,3 +45,15 @@ for cta in range(2):
     print("finisher:", sorted(fin, key=lambda z: z[2])[:40])
 allb = buf.astype(np.int64)
 t0 = allb[allb > 0].min()
+sel = np.zeros(16, np.uint64)
+lib.lapssd_sel_trace_read(sel.ctypes.data_as(C.c_void_p))
+t = sel.astype(np.int64)
+print("select_final phases (us):", [(i, round((t[i] - t[0]) / 1000, 2)) for i in range(6)])
+fs = np.zeros(8, np.uint64)
+lib.lapssd_fs_trace_read(fs.ctypes.data_as(C.c_void_p))
+starts = ct[0][ct[0] < 2**63].astype(np.int64); ends = ct[1][ct[1] > 0].astype(np.int64)
+v0 = starts.min()
+print("verify CTAs: first start 0, last start %.2f us, first end %.2f, last end %.2f; select_final start %.2f end %.2f" % (
+    (starts.max() - v0) / 1000, (ends.min() - v0) / 1000, (ends.max() - v0) / 1000, (t[0] - v0) / 1000, (t[5] - v0) / 1000))
+f = fs.astype(np.int64)
+print("fused final select phases from verify start (us):", [round((f[i] - v0) / 1000, 2) for i in range(7)])
