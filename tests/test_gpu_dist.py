@@ -1,0 +1,89 @@
+"""Device side of the multi-GPU step (a8) on ONE GPU: two handles play ranks 0 and 1 of
+world 2 (requests sharded by global id mod 2).  Each step every rank verifies its own
+slots (spec_verify on its slabs) and updates them (laps_update); then each rank runs
+laps_candidates, the candidate blocks are concatenated on the device (the all-gather's
+result), and each rank runs laps_merge.  The sharded run must equal the single-rank
+oracle request by request (the global top-B of per-rank top-B lists is the global top-B)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+MS = 1000
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2505_17074_b200 as lib
+    return lib
+
+
+@pytest.mark.parametrize("policy", [0, 2])
+def test_two_handles_candidates_merge_equal_single_rank(L, policy):
+    seed, B, G, R = 41, 6, 2, 16
+    tr = synth.make_trace(40, seed, arrival="poisson", rate_per_s=50.0, len_mu=np.log(30), len_sigma=0.6,
+                          len_min=4, len_max=200, beta_ab=(3, 2), drift=True)
+    pool = synth.make_pool("f2", V=2048, k=4, dtype="bf16", n_buckets=8, variants=3, seed=seed, device="cuda")
+    tab = synth.slab_table(tr, 8, 3, R=R, seed=seed)
+    kw = dict(policy=policy, K=4, s1_up_us=30 * MS, gamma=3, delta=0.05, k=4, t_ssm_us=1 * MS,
+              t_llm_us=10 * MS, seed=12)
+    # reference: one rank, oracle
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, R
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
+    sel_o, _ = sim.select(B)
+    ref_steps = [sel_o.copy()]
+    while not sim.state()["done"].all():
+        sim.step(P, sel_o)
+        ref_steps.append(sel_o.copy())
+    ref = sim.state()
+    # two GPU handles
+    hs = []
+    for g in range(G):
+        sh = tr.shard(g, G)
+        hs.append(L.Handle(L.SchedConfig(**kw), sh.arrival_us, sh.L_true, sh.L_pred, max_batch=B, V=2048,
+                           rank=g, world=G))
+    Cn = B
+    cand = [torch.zeros(Cn + 1, dtype=torch.int64, device="cuda") for _ in range(G)]
+    sels = [torch.full((B,), -1, dtype=torch.int32, device="cuda") for _ in range(G)]
+
+    def exchange():
+        for g in range(G):
+            hs[g].laps_candidates(Cn, cand[g])
+        allc = torch.cat(cand)
+        for g in range(G):
+            hs[g].laps_merge(allc, Cn, B, sel=sels[g])
+
+    exchange()
+    for step in range(len(ref_steps) + 5):
+        got = sorted(int(i) * G + g for g in range(G) for i in sels[g].cpu().numpy() if i >= 0)
+        want = sorted(int(i) for i in ref_steps[step] if i >= 0) if step < len(ref_steps) else []
+        assert got == want, f"step {step}"
+        if all(h.state()["done"].all() for h in hs):
+            break
+        for g in range(G):
+            s = sels[g].cpu().numpy()
+            st = hs[g].state()
+            live = s >= 0
+            if not live.any():
+                continue
+            rounds = np.where(live, st["rounds"][np.maximum(s, 0)], 0)
+            idx = np.where(rounds < R, rounds, R // 2 + (rounds - R // 2) % (R // 2))
+            shard_tab = tab[g::G]
+            slab = np.where(live, shard_tab[np.maximum(s, 0), idx], 0).astype(np.int32)
+            req = np.where(live, s * G + g, 0).astype(np.int32)
+            tok, na, _ = L.spec_verify(pool.p, pool.q, pool.draft, torch.as_tensor(req, device="cuda"),
+                                       torch.as_tensor(rounds.astype(np.int32), device="cuda"), kw["seed"],
+                                       slab=torch.as_tensor(slab, device="cuda"))
+            hs[g].laps_update(sels[g], na)
+        exchange()
+    for g in range(G):
+        st = hs[g].state()
+        assert (st["C_us"] == ref["C_us"][g::G]).all()
+        assert (st["acc_draft"] == ref["acc_draft"][g::G]).all()
+        assert hs[g].check() == 0

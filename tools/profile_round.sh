@@ -1,0 +1,14 @@
+#!/bin/bash
+# ncu evidence for profiles/: per-launch list of the bench command, and one full
+# capture of the verify kernel.  Never a multi-rank command.
+mkdir -p gpurun_out
+cd "$(dirname "$0")/.."
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none \
+  -k regex:"verify_kernel|select_side_kernel|accept_kernel|presort_kernel|select_final_kernel|select_kernel" \
+  -s 30 -c 60 --csv --log-file gpurun_out/r01_launches.csv \
+  python bench.py --steps 20 --warmup 10 --graph-steps 0 --no-e2e --no-cpu-baseline > gpurun_out/r01_launch_bench.log 2>&1
+echo "launch list rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"verify_kernel" -s 12 -c 1 \
+  -o gpurun_out/r01_verify_full python bench.py --steps 4 --warmup 10 --graph-steps 0 --no-e2e --no-cpu-baseline \
+  > gpurun_out/r01_full_bench.log 2>&1
+echo "full capture rc=$?"
