@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--variants", type=int, default=16)
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--graph-steps", type=int, default=20, help="steps per captured CUDA graph (0 = eager)")
+    ap.add_argument("--no-profile", action="store_true", help="no per-kernel events at all")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -69,52 +70,51 @@ def parse():
 
 # --------------------------------------------------------------------------- clocks
 class Clocks:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled DURING the timed region (B200_PROFILING.md):
+    NVML polled every ~1 ms from a thread (nvidia-smi's 100 ms cadence would see a
+    few-ms timed region at most once).  Falls back to nvidia-smi if NVML is missing."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index: int):
-        self.rows, self.proc = [], None
+        self.samples, self.stop_flag, self.h = [], False, None
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(gpu_index)], stdout=subprocess.PIPE,
-                stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.h = None
+        self.active = False
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            f = [x.strip() for x in line.split(",")]
-            if len(f) >= 8:
-                self.rows.append(f)
+    def _poll(self):
+        while not self.stop_flag:
+            if self.h is not None and self.active:
+                try:
+                    sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                    rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.samples.append((sm, rs))
+                except Exception:  # noqa: BLE001
+                    pass
+            time.sleep(0.001)
+
+    def start(self):
+        self.active = True
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        sm, smax = [], []
-        for f in self.rows:
-            try:
-                sm.append(float(f[1]))
-                smax.append(float(f[2]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[4:8]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self.active = False
+        self.stop_flag = True
+        self.t.join(1.0)
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(sm), "source": "NVML, 1 ms poll during the timed region"}
 
 
 # --------------------------------------------------------------------------- workload
@@ -176,7 +176,7 @@ def run_ours(args):
     else:
         h.laps_select(B)
     G = min(args.graph_steps, args.steps) if args.graph_steps > 0 else 0
-    hist = torch.full((max(args.warmup, G, 1) + (0 if G else args.steps), B), -1, dtype=torch.int32,
+    hist = torch.full((max(args.warmup, G, 1) + 1 + (0 if G else args.steps), B), -1, dtype=torch.int32,
                       device=dev)
 
     def step(t):
@@ -192,16 +192,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     graphs = []
     launches_per_step = None
+    g_prof = None
     if G:
-        # the timed steps replay CUDA graphs of G captured steps (host enqueue cost removed;
-        # the fork/join of the presort side stream is part of the graph)
+        # timed steps: replays of an UNINSTRUMENTED captured graph of G steps (the host
+        # enqueue cost is removed; the presort/merge side stream's fork/join is in the graph)
         if world == 1:
-            h.profile(G)
+            h.profile(0)
         c0 = L.launch_count()
         g1 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g1):
             for t in range(G):
-                step(t)
+                step(max(args.warmup, G))  # n_accept of timed steps goes to a scratch row
         launches_per_step = (L.launch_count() - c0) / G
         graphs = [g1] * (args.steps // G)
         rem = args.steps % G
@@ -209,10 +210,19 @@ def run_ours(args):
             g2 = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g2):
                 for t in range(rem):
-                    step(t)
+                    step(max(args.warmup, G))
             graphs.append(g2)
+        if world == 1 and not args.no_profile:
+            # a second graph of G steps with the library's per-kernel CUDA events,
+            # replayed right after the timed region (events add graph nodes, so they are
+            # kept out of the timed replays)
+            h.profile(G)
+            g_prof = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_prof):
+                for t in range(G):
+                    step(t)
         torch.cuda.synchronize()
-    elif world == 1:
+    elif world == 1 and not args.no_profile:
         h.profile(args.steps)
     st0 = h.state()
     launches0 = L.launch_count()
@@ -220,6 +230,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
     e0.record()
     if G:
         for g in graphs:
@@ -234,9 +245,17 @@ def run_ours(args):
     launches = L.launch_count() - launches0
     if G:
         launches = int(round(launches_per_step * args.steps))
+    st1 = h.state()  # before the instrumented replay, which advances the state further
     clk = clocks.stop()
+    prof_ms = None
+    if g_prof is not None:
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record()
+        g_prof.replay()
+        p1.record()
+        torch.cuda.synchronize()
+        prof_ms = p0.elapsed_time(p1)
     ms = e0.elapsed_time(e1)
-    st1 = h.state()
     verified_local = int((st1["rounds"] - st0["rounds"]).sum())
     ms_t = torch.tensor([ms, float(verified_local)], dtype=torch.float64, device=dev)
     if dist:
@@ -259,7 +278,7 @@ def run_ours(args):
                       "parallelism": f"dp{world}: requests sharded by id mod {world}"
                       + ("; global top-B via NCCL all-gather of candidate keys" if world > 1 else "")},
            "verified_per_step": verified / args.steps, "gpu_launches": launches, "clocks": clk}
-    if world == 1:
+    if world == 1 and not args.no_profile:
         v_ms, s_ms, p_ms, n_prof = h.profile_read()
         # kernel times: the profiled steps (the last replay of the captured graph, or all
         # timed steps when not using graphs); algorithmic bytes from the same steps' r_b
@@ -287,9 +306,11 @@ def run_ours(args):
                            "verify_ms_avg": avg_v, "select_ms_avg": s_ms / n_prof,
                            "presort_end_ms_avg": p_ms / n_prof,
                            "verify_share_of_step": (v_ms / n_prof) / (ms / args.steps),
-                           "timing": (f"timed region = {args.steps} steps as CUDA-graph replays of {G} captured "
-                                      f"steps; kernel times from the events captured in the last replay"
-                                      if G else "eager laps_step calls")}
+                           "timing": (f"timed region = {args.steps} steps as replays of an uninstrumented "
+                                      f"CUDA graph of {G} steps; kernel times from CUDA events in a second, "
+                                      f"instrumented graph of {G} steps replayed right after "
+                                      f"({prof_ms / G * 1e3 if prof_ms else 0:.1f} us/step instrumented)"
+                                      if G else "eager laps_step calls, events on every step")}
         if not args.no_e2e:
             out["e2e"] = run_e2e(args, L, local, pool, cfg, dev)
         if not args.no_cpu_baseline:
