@@ -136,7 +136,8 @@ typedef struct lapssd_handle lapssd_handle;
  * Outputs [device]: tokens[B, k+1] = (x_0..x_{r-1}, y, -1...), n_accept[B] = r,
  * z_fixed[B] = Z (nullable).  req_id, round_idx: [device] uint32 [B].
  * workspace: [device] >= spec_verify_workspace_bytes(B, V), ZERO-FILLED once by the
- * caller before first use; every call leaves it zero-filled again.
+ * caller before first use; every call leaves it zero-filled again, so the same
+ * workspace can be reused without re-zeroing (one call at a time per workspace).
  * Errors: EINVAL (k, V, dtype, alignment, B < 0), ENOMEM (workspace), ECUDA. */
 size_t spec_verify_workspace_bytes(int32_t B, int64_t V);
 lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V, int32_t k,

@@ -39,12 +39,17 @@ lapssd_status cuda_status(cudaError_t e, const char *what) {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-int32_t n_chunks_of(int64_t V) { return (int32_t)((V + kTile - 1) / kTile); }
+int32_t n_chunks_of(int64_t V, int32_t dtype) {
+    const int64_t te = tile_elems(dtype == LAPSSD_BF16 ? 2 : 4);
+    return (int32_t)((V + te - 1) / te);
+}
+// buffers sized at create hold either dtype: the fp32 chunking has the most chunks
+int32_t n_chunks_max(int64_t V) { return n_chunks_of(V, LAPSSD_F32); }
 
 bool rows_ok(int32_t dtype, int64_t V, int32_t k, const void *p, const void *q) {
     if (dtype != LAPSSD_F32 && dtype != LAPSSD_BF16) return false;
     const int64_t esz = dtype == LAPSSD_BF16 ? 2 : 4;
-    if (V < 1 || (V * esz) % 16 != 0 || V > (int64_t)kMaxChunks * kTile) return false;
+    if (V < 1 || (V * esz) % 16 != 0 || V > (int64_t)kMaxSegs * kSegElems) return false;
     if (k < 1 || k > 16) return false;
     if (((uintptr_t)p | (uintptr_t)q) & 15) return false;
     return true;
@@ -83,7 +88,7 @@ struct lapssd_handle {
     int64_t V;
     int32_t n_chunks;
     uint64_t *part;
-    uint32_t *counter;
+    uint32_t *work;          // verify work-claim counter + retire counter (left zero)
     int32_t *tokens;       // internal outputs when the caller passes NULL
     int32_t *n_accept;
     SlotDesc *desc;        // a1 results for the current batch (valid if desc_valid)
@@ -92,7 +97,7 @@ struct lapssd_handle {
     uint32_t rows_epoch = 1;
     PreSelect *pre = nullptr;    // presort output (side stream)
     SelRec *fin = nullptr;       // finisher records, one per slot (fused select)
-    uint32_t *done_ctas = nullptr;
+    uint32_t *snap = nullptr;    // verify CTAs that have read sel/desc (incremental select)
     uint32_t *pubq = nullptr;    // slot publication queue (incremental select)
     cudaStream_t side = nullptr; // side stream for the presort, fork/join events
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -130,7 +135,7 @@ static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma,
     st.next_tag = cv.take<uint64_t>(nn);
     st.next_sr = cv.take<int2>(nn);
     h->part = cv.take<uint64_t>((size_t)max_batch * n_chunks * kPartWords);
-    h->counter = cv.take<uint32_t>((size_t)max_batch);
+    h->work = cv.take<uint32_t>(2);
     h->tokens = cv.take<int32_t>((size_t)max_batch * (k + 1));
     h->n_accept = cv.take<int32_t>((size_t)max_batch);
     h->desc = cv.take<SlotDesc>((size_t)max_batch);
@@ -138,7 +143,7 @@ static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma,
     while (bp < max_batch) bp <<= 1;
     h->pre = reinterpret_cast<PreSelect *>(cv.take<uint64_t>(preselect_words(bp)));
     h->fin = cv.take<SelRec>((size_t)max_batch);
-    h->done_ctas = cv.take<uint32_t>(1);
+    h->snap = cv.take<uint32_t>(1);
     h->pubq = cv.take<uint32_t>(1 + (size_t)max_batch);
 }
 
@@ -167,8 +172,8 @@ uint64_t lapssd_launch_count(void) { return g_launches.load(); }
 size_t spec_verify_workspace_bytes(int32_t B, int64_t V) {
     if (B < 0 || V < 1) return 0;
     Carver cv{nullptr};
-    cv.take<uint64_t>((size_t)(B > 0 ? B : 1) * n_chunks_of(V) * kPartWords);
-    cv.take<uint32_t>((size_t)(B > 0 ? B : 1));
+    cv.take<uint64_t>((size_t)(B > 0 ? B : 1) * n_chunks_max(V) * kPartWords);
+    cv.take<uint32_t>(2);
     cv.take<SlotDesc>((size_t)(B > 0 ? B : 1));
     return align256(cv.off);
 }
@@ -198,13 +203,13 @@ lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V
     prepare_all();
     VerifyArgs a{};
     a.rows = rows_dev(p, q, draft, nullptr, V, k, 0, dtype);
-    a.n_chunks = n_chunks_of(V);
+    a.n_chunks = n_chunks_of(V, dtype);
     a.cpb = verify_cpb(V);
     a.seed = seed; a.trace = trace;
     a.tokens = tokens; a.n_accept = n_accept; a.z = z_fixed;
     Carver cv{(char *)workspace};
     a.part = cv.take<uint64_t>((size_t)B * a.n_chunks * kPartWords);
-    a.counter = cv.take<uint32_t>((size_t)B);
+    a.work = cv.take<uint32_t>(2);
     SlotDesc *desc = cv.take<SlotDesc>((size_t)B);
     a.desc = desc;
     a.sel = nullptr;
@@ -214,7 +219,19 @@ lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V
     lapssd_status st = cuda_status(launch_accept(a.rows, nullptr, nullptr, nullptr, slab, req_id, round_idx,
                                                  seed, trace, B, desc, s), "spec_verify accept");
     if (st != LAPSSD_OK) return st;
-    return cuda_status(launch_verify(a, B, s), "spec_verify launch");
+    // one launch per sub-batch that fits the kernel's per-CTA snapshot (all of B at usual sizes)
+    const int32_t bmax = verify_max_batch(a.n_chunks, 0);
+    for (int32_t b0 = 0; b0 < B && st == LAPSSD_OK; b0 += bmax) {
+        VerifyArgs ab = a;
+        const int32_t nb = B - b0 < bmax ? B - b0 : bmax;
+        ab.desc = desc + b0;
+        ab.tokens = tokens + (int64_t)b0 * (k + 1);
+        ab.n_accept = n_accept + b0;
+        ab.z = z_fixed ? z_fixed + b0 : nullptr;
+        ab.part = a.part + (int64_t)b0 * a.n_chunks * kPartWords;
+        st = cuda_status(launch_verify(ab, nb, s), "spec_verify launch");
+    }
+    return st;
 }
 
 // ---------------------------------------------------------------- handle
@@ -224,7 +241,7 @@ size_t lapssd_workspace_bytes(const lapssd_config *cfg, int32_t n_local, int32_t
     if (!cfg || n_local < 0 || max_batch < 1 || V < 1) return 0;
     lapssd_handle tmp{};
     Carver cv{nullptr};
-    carve_handle(cv, &tmp, n_local, cfg->gamma > 0 ? cfg->gamma : 1, max_batch, n_chunks_of(V),
+    carve_handle(cv, &tmp, n_local, cfg->gamma > 0 ? cfg->gamma : 1, max_batch, n_chunks_max(V),
                  cfg->k > 0 ? cfg->k : 1);
     return align256(cv.off);
 }
@@ -247,7 +264,7 @@ lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req
         return fail(LAPSSD_EINVAL, "n_local=%d exceeds the single-CTA select capacity %d", req->n,
                     sort_capacity());
     if (max_batch < 1) return fail(LAPSSD_EINVAL, "max_batch < 1");
-    if (V < 1 || V > (int64_t)kMaxChunks * kTile) return fail(LAPSSD_EINVAL, "V out of range");
+    if (V < 1 || V > (int64_t)kMaxSegs * kSegElems) return fail(LAPSSD_EINVAL, "V out of range");
     for (int32_t i = 0; i < req->n; ++i) {
         if (req->L_true[i] < 1 || req->L_pred[i] < 1) return fail(LAPSSD_EINVAL, "L < 1 at %d", i);
         if (i > 0 && req->arrival_us[i] < req->arrival_us[i - 1])
@@ -258,12 +275,15 @@ lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req
         return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes, need);
 
     prepare_all();
+    if (!verify_fits(max_batch, n_chunks_max(V), 0) || !verify_fits(max_batch, n_chunks_max(V), 1))
+        return fail(LAPSSD_EINVAL, "max_batch=%d exceeds the verify kernel's per-CTA capacity (%d at this V)",
+                    max_batch, verify_max_batch(n_chunks_max(V), 1));
     lapssd_handle *h = new lapssd_handle{};
     Carver cv{(char *)workspace};
-    carve_handle(cv, h, req->n, cfg->gamma, max_batch, n_chunks_of(V), cfg->k);
+    carve_handle(cv, h, req->n, cfg->gamma, max_batch, n_chunks_max(V), cfg->k);
     h->max_batch = max_batch;
     h->V = V;
-    h->n_chunks = n_chunks_of(V);
+    h->n_chunks = n_chunks_max(V);
     Sched &sc = h->sc;
     sc.policy = cfg->policy; sc.K = cfg->K; sc.gamma = cfg->gamma; sc.k = cfg->k;
     sc.placement = cfg->placement; sc.pin_rule = cfg->pin_rule;
@@ -356,7 +376,7 @@ static lapssd_status fill_step_verify(lapssd_handle *h, const lapssd_rows *rows,
     a = VerifyArgs{};
     a.rows = rows_dev(rows->p, rows->q, rows->draft, rows->slab_tab, rows->V, rows->k, rows->R, rows->dtype);
     a.rows.epoch = h->rows_epoch;
-    a.n_chunks = n_chunks_of(rows->V);
+    a.n_chunks = n_chunks_of(rows->V, rows->dtype);
     a.cpb = verify_cpb(rows->V);
     a.desc = h->desc;
     a.sel = sel;
@@ -364,7 +384,7 @@ static lapssd_status fill_step_verify(lapssd_handle *h, const lapssd_rows *rows,
     a.tokens = tokens_out ? tokens_out : h->tokens;
     a.n_accept = n_accept_out ? n_accept_out : h->n_accept;
     a.z = nullptr;
-    a.part = h->part; a.counter = h->counter;
+    a.part = h->part; a.work = h->work;
     a.fuse_update = 1;
     a.st = h->st; a.sc = h->sc;
     a.err = &h->st.g->err;
@@ -424,11 +444,9 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
     if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork");
     h->desc_valid = false;
     if (incremental) {
-        a.fuse_select = 1;
         a.fin = h->fin;
-        a.pre = h->pre;
         a.pubq = h->pubq;
-        a.count_out = count_out;
+        a.snap = h->snap;
     }
     st = cuda_status(launch_verify_grid(a, B, 1, s), "laps_step verify");
     if (st != LAPSSD_OK) return st;
@@ -437,7 +455,8 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
     if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork wait");
     if (incremental) {
         st = cuda_status(launch_select_side(h->st, h->sc, a.rows, sel_inout, h->desc, B, h->pre, h->fin, h->pubq,
-                                            count_out, h->side), "laps_step select");
+                                            h->snap, (uint32_t)verify_grid(B, a.n_chunks, 1), count_out, h->side),
+                         "laps_step select");
     } else {
         st = cuda_status(launch_presort(h->st, h->sc, a.rows, sel_inout, B, h->pre, h->side), "laps_step presort");
     }

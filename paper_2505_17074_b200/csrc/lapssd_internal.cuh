@@ -12,15 +12,18 @@
 namespace lapssd {
 
 // ---------------------------------------------------------------- verify tiling
-// One CTA streams a TILE of one row (pair): 256 threads = 8 warps, each warp owns a
-// contiguous segment of 1024 elements; lane l of warp w loads the 16-byte vectors
-// w*SEG + j*32 + l (j = 0..J-1), so every warp-wide load is 512 contiguous bytes.
+// A work item is chunk c of one row pair: kTileBytes of p_r (and of q_r) -- 16384 bf16
+// or 8192 fp32 entries -- split into segments of 1024 entries, each reduced to one
+// published u64.  32 KB per row per item: the longest contiguous bulk copy per SM that
+// still leaves three ring stages in shared memory (tools/rows_bench.cu: 16 KB items
+// stream at 5.7 TB/s, 32 KB items at 6.4 TB/s on the same access pattern).
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kSegElems = 1024;                 // elements per warp segment
-constexpr int kTile = kWarps * kSegElems;       // 8192 elements per CTA
-constexpr int kMaxChunks = 64;                  // V <= 524288
-constexpr int kPartWords = kWarps;              // 8 warp residual sums (u64) per chunk
+constexpr int kSegElems = 1024;                 // entries per published segment sum
+constexpr int kTileBytes = 32768;               // bytes of one row per work item
+constexpr int kMaxSegs = 512;                   // segments per row: V <= 524288
+constexpr int kPartWords = 16;                  // published words per chunk (16 bf16 / 8 fp32 segments)
+__host__ __device__ constexpr int tile_elems(int esz) { return kTileBytes / esz; }
 
 // ---------------------------------------------------------------- state flags
 enum : uint32_t {
@@ -435,22 +438,19 @@ struct VerifyArgs {
     int32_t *tokens;
     int32_t *n_accept;
     uint64_t *z;
-    uint64_t *part;             // [B][n_chunks][kWarps] warp residual sums
-    uint32_t *counter;          // [B]
+    uint64_t *part;             // [B][n_chunks][kPartWords] segment residual sums
+    uint32_t *work;             // [2] item-claim counter, retired CTAs (zero between launches)
     int32_t fuse_update;
     State st;                   // handle mode only
     Sched sc;
     uint32_t *err;              // sticky device flags (nullable in stateless mode)
-    // fused final select (laps_step with pooled rows): the last CTA to retire merges
-    // the finishers' records with the presort's candidates
-    int32_t fuse_select;
-    SelRec *fin;                // [B] one record per slot, written by its finisher
-    PreSelect *pre;             // presort output (side stream)
-    uint32_t *done_ctas;        // grid-wide retire ticket
-    int32_t *count_out;         // nullable
-    // incremental select: each finisher publishes its slot here once its record is
-    // written; the side-stream merger folds it into the running top-B
-    uint32_t *pubq;             // [1 + B]: ticket, then slot+1 per entry (0 = not yet)
+    // incremental select (laps_step with pooled rows): each finisher writes its slot's
+    // record (new key, next descriptor) and publishes the slot to the side-stream merger
+    SelRec *fin;                // [B] one record per slot
+    uint32_t *pubq;             // [1 + B]: ticket, then slot+1 per entry (0 = not yet); null: no records
+    // +1 per CTA (release) once it has read all it needs of desc[] / sel[]; the side
+    // select overwrites those only after every CTA has signalled (nullable)
+    uint32_t *snap;
 };
 
 enum : uint32_t { E_STALE_DESC = 8u };
@@ -501,9 +501,12 @@ cudaError_t launch_presort(const State &st, const Sched &sc, const RowsDev &rw, 
 cudaError_t launch_select_final(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc, int32_t B,
                                 int32_t *sel, int32_t *count_out, const PreSelect *pre, cudaStream_t s);
 cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_sms, cudaStream_t s);
+int verify_grid(int32_t B, int32_t n_chunks, int32_t reserve_sms);       // CTAs of that launch
+bool verify_fits(int32_t B, int32_t n_chunks, int32_t reserve_sms);      // per-CTA snapshot capacity
+int verify_max_batch(int32_t n_chunks, int32_t reserve_sms);
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
-                               int32_t B, PreSelect *pre, const SelRec *fin, uint32_t *pubq, int32_t *count_out,
-                               cudaStream_t s);
+                               int32_t B, PreSelect *pre, const SelRec *fin, uint32_t *pubq, uint32_t *snap,
+                               uint32_t snap_target, int32_t *count_out, cudaStream_t s);
 int sort_capacity();            // largest key count one select CTA can sort
 void prepare_all();             // kernel attributes, once per process (api.cu)
 void verify_prepare();

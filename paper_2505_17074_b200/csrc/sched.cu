@@ -26,6 +26,13 @@ extern "C" int lapssd_side_trace_read(unsigned long long *out, unsigned *n) {
 #define ITRACE(m) do { if (threadIdx.x == 0) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); \
     unsigned i = g_side_n++; if (i < 128) { g_side_iter[i][0] = t; g_side_iter[i][1] = (unsigned long long)(m); } } } while (0)
 __device__ unsigned long long g_sel_trace[16];
+__device__ unsigned long long g_send[64];
+__device__ unsigned int g_scount;
+extern "C" int lapssd_send_read(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_send, sizeof g_send);
+    unsigned z = 0; cudaMemcpyToSymbol(g_scount, &z, 4);
+    return 0;
+}
 #define STRACE(i) do { if (threadIdx.x == 0) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); g_sel_trace[i] = t; } } while (0)
 extern "C" int lapssd_sel_trace_read(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_sel_trace, sizeof g_sel_trace); }
 #else
@@ -268,6 +275,7 @@ __global__ void __launch_bounds__(kSelThreads) select_final_kernel(const State s
 __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st, const Sched sc, const RowsDev rw,
                                                                    int32_t *sel, SlotDesc *desc, int32_t B,
                                                                    PreSelect *pre, const SelRec *fin, uint32_t *pubq,
+                                                                   uint32_t *snap, uint32_t snap_target,
                                                                    int32_t *count_out) {
     extern __shared__ uint64_t s_buf[];
     STRACE(8);
@@ -383,7 +391,9 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
         const int mp = next_pow2(m);
         for (int x = m + (int)threadIdx.x; x < mp; x += T) nk[x] = ~0ull;
         __syncthreads();
+        ITRACE(300000 + m);
         const uint64_t *snk = block_sort(nk, mp >= 64 && mp <= kMergeCap ? ntmp : nullptr, mp);
+        ITRACE(400000 + m);
         for (int o = threadIdx.x; o < bp; o += T) {   // first bp outputs of merge(L, snk)
             int lo = o - mp > 0 ? o - mp : 0, hi = o < bp ? o : bp;
             while (lo < hi) {
@@ -400,6 +410,19 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
         __syncthreads();
         if (threadIdx.x == 0) s_head = head + m;
     }
+    // every verify CTA has read what it needs of sel[] / desc[] (usually long ago): only
+    // now may the commit overwrite them
+    if (snap && threadIdx.x == 0) {
+        const unsigned long long t0 = gtimer();
+        for (;;) {
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(snap) : "memory");
+            if (v >= snap_target) break;
+            if (waited_too_long(t0)) { atomicOr(&st.g->err, E_TIMEOUT); break; }
+            __nanosleep(64);
+        }
+        *snap = 0;
+    }
     __syncthreads();
     ITRACE(100000);
     // ---------------- commit
@@ -408,6 +431,7 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
     if (valid) atomicAdd(&s_count, valid);
     __syncthreads();
     const int cnt = s_count;
+    ITRACE(100001);
     const int64_t now = s_now;
     uint8_t *mark = reinterpret_cast<uint8_t *>(L2);     // [bp] 1 reselected, 2 +pin
     int32_t *old_i = reinterpret_cast<int32_t *>(nk);    // [bp] the verified batch
@@ -438,6 +462,7 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
         desc[b] = d;
     }
     __syncthreads();
+    ITRACE(100002);
     for (int b = threadIdx.x; b < B; b += T) {   // the verified batch: running flags cleared
         const int i = old_i[b];
         if (i < 0) continue;
@@ -458,19 +483,25 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
         if (count_out) *count_out = cnt;
         pubq[0] = 0;
     }
+    __syncthreads();
+    ITRACE(100003);
     STRACE(9);
+#ifdef LAPSSD_TRACE
+    if (threadIdx.x == 0) { unsigned c = atomicAdd(&g_scount, 1u); if (c < 64) g_send[c] = gtimer(); }
+#endif
 }
 
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
-                               int32_t B, PreSelect *pre, const SelRec *fin, uint32_t *pubq, int32_t *count_out,
-                               cudaStream_t s) {
+                               int32_t B, PreSelect *pre, const SelRec *fin, uint32_t *pubq, uint32_t *snap,
+                               uint32_t snap_target, int32_t *count_out, cudaStream_t s) {
     int np = 1, bp = 1;
     while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
     while (bp < B) bp <<= 1;
     const size_t a = (size_t)(np + 2 * bp) * sizeof(uint64_t);
     const size_t b = (size_t)4 * bp * sizeof(uint64_t) + 2 * (size_t)((sc.n + 7) & ~7) * sizeof(int16_t) + 64 +
                      (bp <= 1024 ? 2 * (size_t)bp * sizeof(SelRec) : 0);
-    select_side_kernel<<<1, kSelThreads, a > b ? a : b, s>>>(st, sc, rw, sel, desc, B, pre, fin, pubq, count_out);
+    select_side_kernel<<<1, kSelThreads, a > b ? a : b, s>>>(st, sc, rw, sel, desc, B, pre, fin, pubq, snap,
+                                                              snap_target, count_out);
     count_launch();
     return cudaGetLastError();
 }

@@ -378,139 +378,5 @@ __device__ __forceinline__ void commit_one(const State &st, const Sched &sc, int
 }
 
 
-// ---------------------------------------------------------------- fused final select
-// Run by the last CTA of the verify kernel (all its threads).  Inputs: the finishers'
-// records of the verified batch (new key, flags, next-round descriptor) and the
-// presort's sorted top-B candidates of every other request (with records).  The B
-// batch keys are sorted, merged with the candidates (first B outputs), and the result
-// is committed exactly as select_kernel does: batch in key order, x_i on first
-// selection, pinning, running flags cleared, clock / admission / counts.
-__device__ __forceinline__ void dbg_time(unsigned long long *tr, int i) {
-    if (tr && threadIdx.x == 0) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        tr[i] = t;
-    }
-}
-__device__ inline void fused_final_select(const State &st, const Sched &sc, int B, int32_t *sel, SlotDesc *desc,
-                                          const SelRec *fin, PreSelect *pre, int32_t *count_out, uint64_t *smem,
-                                          unsigned long long *tr = nullptr) {
-    __shared__ int s_count;
-    dbg_time(tr, 0);
-    if (threadIdx.x == 0) {
-        uint32_t ready = 0;
-        const unsigned long long t_start = gtimer();
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(ready) : "l"(&pre->ready) : "memory");
-            if (!ready) __nanosleep(64);
-            if (waited_too_long(t_start)) { atomicOr(&st.g->err, E_TIMEOUT); break; }
-        } while (!ready);
-        s_count = 0;
-    }
-    __syncthreads();
-    dbg_time(tr, 1);
-    const int bp = next_pow2(B);
-    uint64_t *bk = smem;                                  // [bp] batch keys
-    uint64_t *tmp = smem + bp;                            // [bp]
-    uint64_t *cand = smem + 2 * bp;                       // [bp] presorted candidates
-    uint64_t *merged = smem + 3 * bp;                     // [bp]
-    int32_t *msrc = reinterpret_cast<int32_t *>(smem + 4 * bp);          // [bp] origin of each output
-    int32_t *old_i = msrc + bp;                                           // [bp] batch requests
-    uint8_t *mark = reinterpret_cast<uint8_t *>(old_i + bp);            // [bp] 1 reselected, 2 +pin
-    int16_t *slot_of = reinterpret_cast<int16_t *>(mark + ((bp + 15) & ~15));  // [n] slot of a request
-    const SelRec *crec = pre_recs(pre, bp);
-    for (int b = threadIdx.x; b < bp; b += blockDim.x) {
-        const int i = b < B ? sel[b] : -1;
-        old_i[b] = i;
-        bk[b] = i >= 0 ? fin[b].key : ~0ull;
-        cand[b] = pre->cand[b];
-        mark[b] = 0;
-        if (i >= 0) slot_of[i] = (int16_t)b;
-    }
-    __syncthreads();
-    dbg_time(tr, 2);
-#ifdef LAPSSD_TRACE_SORT_TWICE
-    {   // diagnostic: sort a copy first, so the timed sort below runs with a warm I-cache
-        uint64_t *c2 = merged;
-        for (int b = threadIdx.x; b < bp; b += blockDim.x) c2[b] = bk[b];
-        __syncthreads();
-        block_sort(c2, reinterpret_cast<uint64_t *>(msrc), bp);
-        __syncthreads();
-        dbg_time(tr, 6);
-    }
-#endif
-    const uint64_t *sk = block_sort(bk, tmp, bp);
-    dbg_time(tr, 3);
-    for (int o = threadIdx.x; o < B; o += blockDim.x) {  // merge path, first B outputs
-        int lo = o - bp > 0 ? o - bp : 0, hi = o < bp ? o : bp;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (sk[mid] <= cand[o - 1 - mid]) lo = mid + 1; else hi = mid;
-        }
-        const int i = lo, j = o - lo;
-        const bool takeA = j >= bp || (i < bp && sk[i] <= cand[j]);
-        const uint64_t key = takeA ? sk[i] : cand[j];
-        merged[o] = key;
-        int src = j;
-        if (takeA) {
-            const int req = (int)((uint32_t)(key & 0xFFFFFFull) / (uint32_t)sc.world);
-            src = key == ~0ull ? 0 : -(slot_of[req] + 1);
-        }
-        msrc[o] = src;
-    }
-    __syncthreads();
-    int valid = 0;
-    for (int b = threadIdx.x; b < B; b += blockDim.x) valid += (merged[b] >> 63) == 0;
-    if (valid) atomicAdd(&s_count, valid);
-    __syncthreads();
-    const int cnt = s_count;
-    dbg_time(tr, 4);
-    const int64_t now = pre->now_us;
-    const int cursor = pre->cursor;
-    for (int b = threadIdx.x; b < B; b += blockDim.x) {
-        SlotDesc d;
-        d.i = -1; d.slab = 0; d.req = 0; d.round = 0; d.r = -1;
-        d.pad[0] = d.pad[1] = d.pad[2] = 0;
-        if (b < cnt) {
-            const int src = msrc[b];
-            const SelRec &rec = src < 0 ? fin[-src - 1] : crec[src];
-            d = rec.desc;
-            bool pin = false;
-            if (sc.policy == LAPSSD_POL_FCFS || sc.policy == LAPSSD_POL_LPSJF) pin = true;
-            else if (sc.policy == LAPSSD_POL_LAPSSD && sc.pin_rule == 0 && (rec.flags & F_PERC)) pin = true;
-            if (src < 0) {
-                mark[-src - 1] = pin ? 2 : 1;          // batch member: flags written below
-            } else {
-                if (pin && !(rec.flags & F_PINNED)) st.flags[d.i] = rec.flags | F_PINNED;
-                if (rec.x_unset) st.x[d.i] = now;      // x_i
-            }
-        }
-        sel[b] = d.i;
-        desc[b] = d;
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < B; b += blockDim.x) {  // the verified batch: running cleared
-        const int i = old_i[b];
-        if (i < 0) continue;
-        uint32_t fl = fin[b].flags & ~F_RUNNING;
-        if (mark[b] == 2) fl |= F_PINNED;
-        st.flags[i] = fl;
-    }
-    if (threadIdx.x == 0) {
-        int64_t nnow = now;
-        if (cnt == 0 && cursor < sc.n) {                             // idle: jump
-            const int64_t nxt = st.arrival[cursor];
-            if (nxt > nnow) nnow = nxt;
-        }
-        st.g->now_us = nnow;
-        st.g->cursor = cursor;
-        st.g->prev_count = cnt;
-        st.g->count = cnt;
-        if (count_out) *count_out = cnt;
-        pre->ready = 0;
-    }
-    __syncthreads();
-    dbg_time(tr, 5);
-}
 
 }  // namespace lapssd

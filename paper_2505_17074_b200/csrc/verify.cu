@@ -177,33 +177,65 @@ cudaError_t launch_accept(const RowsDev &rw, const int32_t *sel, const State *st
 //            the state update, and computes that request's next-round acceptance test
 //            (cached for the next select).  Off the streaming path.
 #ifdef LAPSSD_TRACE
+#ifndef LAPSSD_TRACE_A
+#define LAPSSD_TRACE_A 0
+#endif
+#ifndef LAPSSD_TRACE_B
+#define LAPSSD_TRACE_B 74
+#endif
 // Diagnostic build only (tools/): fire-and-forget timestamps per (event, item) of two CTAs.
 __device__ unsigned long long g_trace[2][16][1024];
 __device__ __forceinline__ void trace(int ev, int x) {
-    const int slot = blockIdx.x == 0 ? 0 : blockIdx.x == 74 ? 1 : -1;
+    const int slot = blockIdx.x == LAPSSD_TRACE_A ? 0 : blockIdx.x == LAPSSD_TRACE_B ? 1 : -1;
     if (slot < 0) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_trace[slot][ev][x & 1023] = t;
 }
-__device__ unsigned long long g_cta_t[2][160];   // first / last instruction per CTA
+__device__ unsigned long long g_cta_t[10][160];   // start, end, producer last issue, consumer last, finisher last ready, bytes, f-y, f-upd, f-done
 __device__ unsigned long long g_fs_trace[8];     // fused final select phases
+__device__ unsigned long long g_vstart[64];      // verify CTA 0 start per launch
+__device__ unsigned int g_vcount;
+extern "C" int lapssd_vstart_read(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_vstart, sizeof g_vstart);
+    unsigned z = 0; cudaMemcpyToSymbol(g_vcount, &z, 4);
+    return 0;
+}
 extern "C" int lapssd_fs_trace_read(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_fs_trace, sizeof g_fs_trace); }
 __device__ __forceinline__ void cta_time(int which) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (blockIdx.x < 160) {
-        if (which == 0) atomicMin(&g_cta_t[0][blockIdx.x], t); else atomicMax(&g_cta_t[1][blockIdx.x], t);
+        if (which == 0) {
+            atomicMin(&g_cta_t[0][blockIdx.x], t);
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_cta_t[9][blockIdx.x] = smid;
+        } else {
+            atomicMax(&g_cta_t[which][blockIdx.x], t);
+        }
     }
+}
+__device__ __forceinline__ void cta_bytes(unsigned n) {
+    if (blockIdx.x < 160) atomicAdd(&g_cta_t[5][blockIdx.x], (unsigned long long)n);
 }
 extern "C" int lapssd_cta_trace_read(unsigned long long *out) {
     cudaMemcpyFromSymbol(out, g_cta_t, sizeof(g_cta_t));
-    static unsigned long long init[2][160];
-    for (int i = 0; i < 160; ++i) { init[0][i] = ~0ull; init[1][i] = 0; }
+    static unsigned long long init[10][160];
+    for (int i = 0; i < 160; ++i) { init[0][i] = ~0ull; for (int j = 1; j < 10; ++j) init[j][i] = 0; }
     cudaMemcpyToSymbol(g_cta_t, init, sizeof(init));
     return 0;
 }
 #define CTA_TIME(w) cta_time(w)
+#define CTA_BYTES(n) cta_bytes(n)
+__device__ unsigned long long g_slot_t[3][4096];   // per slot: update start, published, sampled
+extern "C" int lapssd_slot_trace_read(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_slot_t, sizeof g_slot_t);
+    static unsigned long long zero[3 * 4096];
+    cudaMemcpyToSymbol(g_slot_t, zero, sizeof zero);
+    return 0;
+}
+#define SLOT_TIME(w, b) do { if ((b) < 4096) g_slot_t[w][b] = gtimer(); } while (0)
 extern "C" int lapssd_trace_read(unsigned long long *out) {
     cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
     cudaMemset(nullptr, 0, 0);
@@ -215,12 +247,30 @@ extern "C" int lapssd_trace_read(unsigned long long *out) {
 #else
 #define TRACE(ev, x)
 #define CTA_TIME(w)
+#define CTA_BYTES(n)
+#define SLOT_TIME(w, b)
 #endif
-constexpr int kConsumerWarps = kWarps;                     // 8 per group
-constexpr int kGroups = 2;                                 // consumer groups take alternate items
-constexpr int kVerifyThreads = (1 + kGroups * (kConsumerWarps + 1)) * 32;  // producer + groups
-constexpr int kFinQ = 64;                                  // finish-queue ring
+constexpr int kConsumerWarps = 16;                         // all consume every item (one segment each)
+constexpr int kGroups = 2;                                 // finisher warps per CTA
+constexpr int kVerifyThreads = (1 + kConsumerWarps + kGroups) * 32;  // producer, consumers, finishers
+constexpr int kMaxSlots = 4096;                            // slots per launch (4-byte snapshot each)
+constexpr int kFinCap = 64;                                // slots per finisher warp
 constexpr int kStageBudget = 192 * 1024;                   // shared memory for the ring
+#ifndef LAPSSD_POLL_NS
+#define LAPSSD_POLL_NS 32
+#endif
+constexpr int kPollNs = LAPSSD_POLL_NS;                     // finisher back-off between polls
+
+template <bool BF16>
+struct VerifyCfg {
+    static constexpr int kEsz = BF16 ? 2 : 4;
+    static constexpr int kTileElems = tile_elems(kEsz);               // 16384 / 8192 entries per item
+    static constexpr int kSegs = kTileElems / kSegElems;              // 16 / 8 segments per chunk
+    static constexpr int kCPL = kPartWords / kSegs;                   // chunks per finisher lane: 1 / 2
+    static constexpr int kStages = kStageBudget / (2 * kTileBytes);   // 3
+    static_assert(kSegs * kCPL == kPartWords && kSegs <= kConsumerWarps, "tiling");
+    static_assert(kMaxSegs / kSegs <= 32 * kCPL, "a finisher lane holds at most kCPL chunks");
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -251,7 +301,7 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-// Published warp sums carry bit 63 as a ready flag (a segment's Q4.60 mass is < 2^61),
+// Published segment sums carry bit 63 as a ready flag (a segment's Q4.60 mass is < 2^61),
 // so each word is self-describing: no fence or counter orders it against other words.
 constexpr uint64_t kReady = 1ull << 63;
 __device__ __forceinline__ void st_relaxed(uint64_t *addr, uint64_t v) {
@@ -262,10 +312,12 @@ __device__ __forceinline__ ulonglong2 ld_relaxed2(const uint64_t *addr) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(addr) : "memory");
     return v;
 }
-// The 8 published warp sums of chunk c (one lane per chunk): issued together.
-__device__ __forceinline__ void load_chunk_words(const uint64_t *part, int c, uint64_t (&w)[kWarps]) {
+// The N published segment sums of chunk c (one lane per chunk), into w[off..off+N):
+// issued together.
+template <int N>
+__device__ __forceinline__ void load_chunk_words(const uint64_t *part, int c, uint64_t *w) {
 #pragma unroll
-    for (int h = 0; h < kWarps / 2; ++h) {
+    for (int h = 0; h < N / 2; ++h) {
         const ulonglong2 v = ld_relaxed2(part + (int64_t)c * kPartWords + 2 * h);
         w[2 * h] = v.x;
         w[2 * h + 1] = v.y;
@@ -328,14 +380,53 @@ __device__ __forceinline__ int next_a1_store(const VerifyArgs &a, int32_t i, uin
     return r;
 }
 
-// Warp-level finish of slot b: total Z, draw t, locate (chunk, warp segment), rescan
-// that segment (L2-hot) in vocabulary order, emit, update.  P:64, AMB-20.
+// Warp-level state update of slot b's request (a3) plus what the next select needs from
+// it, run at the START of the verify kernel.  The scheduler state depends on r (fixed by
+// a1 before any row streams) and never on the sampled token y, so the update, the new
+// priority key and the next round's acceptance test need not wait for the residual
+// stream; the record is published to the side-stream select at
+// once, which then merges the whole verified batch while the rows are still streaming.
 template <bool BF16>
-__device__ __forceinline__ void finish_slot_warp(const VerifyArgs &a, int b, const SlotDesc &d, uint64_t (*fb)[kWarps],
-                                                 uint64_t (&w0)[kWarps], uint64_t (&w1)[kWarps], const UpdIn &upd,
+__device__ __forceinline__ void update_slot_warp(const VerifyArgs &a, int b, const SlotDesc &d, const UpdIn &upd,
                                                  int64_t now, const NextA1 &nxt) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) SLOT_TIME(0, b);
+    const UpdOut uo = update_warp(a.st, a.sc, d.i, d.r, now, upd, lane);
+    if (lane == 0) TRACE(13, b);
+    const int r_next = next_a1_store(a, d.i, d.req, d.round + 1, nxt);  // harmless if it completed
+    if (a.pubq && lane == 0) {
+        // the request's record for the select: new key and next-round descriptor
+        SelRec rec;
+        rec.key = build_key(a.sc, d.i, INT32_MAX, uo.fl, upd.Lp, uo.tok, uo.A);
+        rec.flags = uo.fl;
+        rec.x_unset = 0;
+        rec.desc.i = d.i;
+        rec.desc.slab = (int32_t)nxt.slab;
+        rec.desc.req = d.req;
+        rec.desc.round = d.round + 1;
+        rec.desc.r = r_next;
+        rec.desc.pad[0] = rec.desc.pad[1] = rec.desc.pad[2] = 0;
+        a.fin[b] = rec;
+        a.st.key[d.i] = rec.key;
+        __threadfence();
+        const uint32_t slot = atomicAdd(a.pubq, 1u);  // publish: the merger may take it now
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.pubq + 1 + slot), "r"((uint32_t)b + 1u)
+                     : "memory");
+        SLOT_TIME(1, b);
+    }
+    __syncwarp();
+}
+
+// Warp-level residual draw of slot b once all its (chunk, segment) sums are published:
+// total Z, draw t, locate (chunk, segment), rescan that segment in vocabulary order,
+// emit.  P:64, AMB-20.  w[h * kSegs + s] = sum of segment s of chunk lane + 32 h.
+template <bool BF16>
+__device__ __forceinline__ void sample_slot_warp(const VerifyArgs &a, int b, const SlotDesc &d, uint64_t *fb,
+                                                 uint64_t (&w)[kPartWords]) {
     using E = Elt<BF16>;
     using S = Seg<BF16>;
+    using TC = VerifyCfg<BF16>;
+    constexpr int kSegs = TC::kSegs;
     const int lane = threadIdx.x & 31;
     const int k = a.rows.k, r = d.r, nc = a.n_chunks;
     const int64_t V = a.rows.V;
@@ -343,32 +434,28 @@ __device__ __forceinline__ void finish_slot_warp(const VerifyArgs &a, int b, con
     const char *prow = (const char *)a.rows.p + ((int64_t)d.slab * (k + 1) + r) * V * E::kEsz;
     const char *qrow = (const char *)a.rows.q + ((int64_t)d.slab * k + (use_q ? r : 0)) * V * E::kEsz;
     const uint64_t *part = a.part + (int64_t)b * nc * kPartWords;
-    // chunk sums from the words of the final poll: lane holds chunks lane and lane + 32
+    // chunk sums: cs0 for chunk lane, cs1 for chunk lane + 32 (fp32 tiling only)
     uint64_t cs0 = 0, cs1 = 0;
 #pragma unroll
-    for (int x = 0; x < kWarps; ++x) {
-        w0[x] &= ~kReady;
-        w1[x] &= ~kReady;
-        cs0 += w0[x];
-        cs1 += w1[x];
+    for (int x = 0; x < kPartWords; ++x) {
+        w[x] &= ~kReady;
+        if (x < kSegs) cs0 += w[x]; else cs1 += w[x];
     }
     uint64_t Z = warp_sum_u64(cs0 + cs1);
     if (lane == 0) TRACE(9, b);
     bool fallback = false;
     if (Z == 0 && use_q) {  // no residual mass while rejecting: the row p_r itself
         fallback = true;
-        for (int c = 0; c < nc; ++c)
-            for (int w = 0; w < kWarps; ++w) {
-                const uint64_t m = warp_sum_u64(
-                    lane_mass<BF16>(prow, qrow, false, (int64_t)c * kTile + (int64_t)w * kSegElems, V, lane));
-                if (lane == 0) fb[c][w] = m;
-            }
+        for (int g = 0; g < nc * kSegs; ++g) {
+            const uint64_t m = warp_sum_u64(lane_mass<BF16>(prow, qrow, false, (int64_t)g * kSegElems, V, lane));
+            if (lane == 0) fb[g] = m;
+        }
         __syncwarp();
         cs0 = cs1 = 0;
         if (lane < nc)
-            for (int w = 0; w < kWarps; ++w) cs0 += fb[lane][w];
+            for (int x = 0; x < kSegs; ++x) cs0 += fb[lane * kSegs + x];
         if (lane + 32 < nc)
-            for (int w = 0; w < kWarps; ++w) cs1 += fb[lane + 32][w];
+            for (int x = 0; x < kSegs; ++x) cs1 += fb[(lane + 32) * kSegs + x];
         Z = warp_sum_u64(cs0 + cs1);
     }
     int y = -1;
@@ -396,17 +483,17 @@ __device__ __forceinline__ void finish_slot_warp(const VerifyArgs &a, int b, con
                 cstar = 32 + src;
             }
         }
-        uint64_t wsum = 0;
+        uint64_t ssum = 0;
 #pragma unroll
-        for (int x = 0; x < kWarps; ++x) {  // the 8 warp sums of chunk cstar, to lanes 0..7
-            const uint64_t v = __shfl_sync(0xFFFFFFFFu, cstar < 32 ? w0[x] : w1[x], cstar & 31);
-            if (lane == x) wsum = v;
+        for (int x = 0; x < kSegs; ++x) {  // the segment sums of chunk cstar, to lanes 0..kSegs-1
+            const uint64_t v = __shfl_sync(0xFFFFFFFFu, cstar < 32 ? w[x] : w[(kSegs + x) % kPartWords], cstar & 31);
+            if (lane == x) ssum = v;
         }
-        if (fallback) wsum = lane < kWarps ? fb[cstar][lane] : 0;
-        const uint64_t wincl = warp_incl_scan_u64(wsum, lane);
-        const int wstar = __ffs(__ballot_sync(0xFFFFFFFFu, lane < kWarps && wincl > t)) - 1;
-        t -= __shfl_sync(0xFFFFFFFFu, wincl - wsum, wstar);
-        const int64_t base = (int64_t)cstar * kTile + (int64_t)wstar * kSegElems;
+        if (fallback) ssum = lane < kSegs ? fb[cstar * kSegs + lane] : 0;
+        const uint64_t sincl = warp_incl_scan_u64(ssum, lane);
+        const int sstar = __ffs(__ballot_sync(0xFFFFFFFFu, lane < kSegs && sincl > t)) - 1;
+        t -= __shfl_sync(0xFFFFFFFFu, sincl - ssum, sstar);
+        const int64_t base = (int64_t)cstar * TC::kTileElems + (int64_t)sstar * kSegElems;
         if (lane == 0) TRACE(10, b);
         const bool q_in = use_q && !fallback;
         uint4 pv[S::J], qv[S::J];
@@ -455,269 +542,246 @@ __device__ __forceinline__ void finish_slot_warp(const VerifyArgs &a, int b, con
         if (a.n_accept) a.n_accept[b] = r;
         if (a.z) a.z[b] = Z;
     }
-    if (lane == 0) TRACE(12, b);
-    if (a.fuse_update) {
-        const UpdOut uo = update_warp(a.st, a.sc, d.i, r, now, upd, lane);
-        if (lane == 0) TRACE(13, b);
-        const int r_next = next_a1_store(a, d.i, d.req, d.round + 1, nxt);  // harmless if it completed
-        if (a.fuse_select && lane == 0) {
-            // the request's record for the fused final select: new key and next descriptor
-            SelRec rec;
-            rec.key = build_key(a.sc, d.i, INT32_MAX, uo.fl, upd.Lp, uo.tok, uo.A);
-            rec.flags = uo.fl;
-            rec.x_unset = 0;
-            rec.desc.i = d.i;
-            rec.desc.slab = (int32_t)nxt.slab;
-            rec.desc.req = d.req;
-            rec.desc.round = d.round + 1;
-            rec.desc.r = r_next;
-            rec.desc.pad[0] = rec.desc.pad[1] = rec.desc.pad[2] = 0;
-            a.fin[b] = rec;
-            a.st.key[d.i] = rec.key;
-            __threadfence();
-            if (a.pubq) {  // publish: the side-stream merger may take this slot now
-                const uint32_t slot = atomicAdd(a.pubq, 1u);
-                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.pubq + 1 + slot), "r"((uint32_t)b + 1u)
-                             : "memory");
-            }
-        }
-    }
     __syncwarp();
 }
 
-template <bool BF16>
-struct VerifyCfg {
-    static constexpr int kTileBytes = kTile * Elt<BF16>::kEsz;        // one row chunk
-    static constexpr int kStages = kStageBudget / (2 * kTileBytes);   // 6 (bf16) / 3 (fp32)
-};
+// Slot b is finished (sampled) by finisher f = b mod (kGroups * grid): group f / grid of
+// CTA f % grid, so consecutive slots -- which complete together at the end of the
+// stream -- are finished by different warps of different CTAs.
+__host__ __device__ __forceinline__ int fin_slots(int B, int grid, int f0) {
+    return f0 < B ? (B - 1 - f0) / (kGroups * grid) + 1 : 0;
+}
 
 template <bool BF16>
 __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_constant__ VerifyArgs a,
                                                                     int32_t B) {
     using E = Elt<BF16>;
     using S = Seg<BF16>;
-    constexpr int kTileBytes = VerifyCfg<BF16>::kTileBytes;
+    using TC = VerifyCfg<BF16>;
     constexpr int kStages = VerifyCfg<BF16>::kStages;
     extern __shared__ __align__(128) uint8_t s_tiles[];  // kStages x (p chunk, q chunk)
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-    __shared__ SlotDesc s_desc[kStages];
-    __shared__ int s_chunk[kStages];
-    __shared__ volatile int s_q[kGroups][kFinQ];
-    __shared__ int4 s_qd[kGroups][kFinQ];      // (i, slab, req, round) of the queued slot
-    __shared__ int s_qr[kGroups][kFinQ];       // its r
-    __shared__ volatile int s_qhead[kGroups], s_qtail[kGroups];
-    __shared__ uint64_t s_fb[kGroups][kMaxChunks][kWarps];
+    __shared__ uint32_t s_slot[kMaxSlots];             // per slot: (slab << 5) | (r + 1), 0 = nothing to do
+    __shared__ int s_stage[kStages];                   // item in each ring stage (-1: no more items)
+    __shared__ SlotDesc s_fin[kGroups][kFinCap];       // the slots each finisher owns
+    __shared__ uint64_t s_fb[kGroups][kMaxSegs];       // Z = 0 fallback sums
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nc = a.n_chunks;
     const int n_items = B * nc;
+    const int grid = (int)gridDim.x;
+    // warp 0 producer; warps 1..16 consumers (gw = segment); warps 17, 18 finishers (grp)
+    const int gw = warp >= 1 && warp <= kConsumerWarps ? warp - 1 : -1;
+    const int grp = warp > kConsumerWarps ? warp - 1 - kConsumerWarps : 0;
+    const bool finisher = warp > kConsumerWarps;
     if (tid == 0) CTA_TIME(0);
+#ifdef LAPSSD_TRACE
+    if (tid == 0 && blockIdx.x == 0) { unsigned c = atomicAdd(&g_vcount, 1u); if (c < 64) g_vstart[c] = gtimer(); }
+#endif
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumerWarps);
         }
-        for (int g = 0; g < kGroups; ++g) { s_qhead[g] = 0; s_qtail[g] = 0; }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // ---- snapshot of everything this CTA reads of desc[] / sel[]: the (slab, r) of every
+    // slot (items are claimed dynamically, so any slot may come up) and the descriptors
+    // of the finishers' slots.  Once every CTA has signalled, the side-stream select may
+    // overwrite desc[] / sel[] with the next batch.
+    if (!finisher) {
+        for (int b = tid; b < B; b += (1 + kConsumerWarps) * 32) {
+            const int4 *dp = reinterpret_cast<const int4 *>(a.desc + b);
+            const int4 dh = dp[0];   // i, slab, req, round
+            int r = dp[1].x;
+            const int si = a.sel ? a.sel[b] : dh.x;
+            if (r >= 0 && si != dh.x) {
+                if (a.err) atomicOr(a.err, E_STALE_DESC);
+                r = -1;
+            }
+            if (r >= 0 && (uint32_t)dh.y >= (1u << 27)) {
+                if (a.err) atomicOr(a.err, E_BAD_SLOT);
+                r = -1;
+            }
+            s_slot[b] = r < 0 ? 0u : ((uint32_t)dh.y << 5) | (uint32_t)(r + 1);
+        }
+    } else {
+        const int f0 = grp * grid + (int)blockIdx.x;
+        const int nf = fin_slots(B, grid, f0);
+        for (int j = lane; j < nf; j += 32) {
+            const int b = f0 + j * kGroups * grid;
+            SlotDesc d = a.desc[b];
+            const int si = a.sel ? a.sel[b] : d.i;
+            if (d.r >= 0 && (si != d.i || (uint32_t)d.slab >= (1u << 27))) d.r = -1;
+            s_fin[grp][j] = d;
+        }
+    }
     __syncthreads();
+    if (tid == 0 && a.snap) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.snap) : "memory");
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
-        const int kk = a.rows.k;
-        const int64_t V = a.rows.V;
-        int k = 0;
-        for (int base = blockIdx.x; base < n_items; base += 32 * gridDim.x) {
-            // lane l prefetches the descriptor of item base + l * gridDim.x
-            const int my_n = base + lane * (int)gridDim.x;
-            SlotDesc md;
-            md.r = -1;
-            md.i = md.slab = 0;
-            md.req = md.round = 0;
-            if (my_n < n_items) {
-                const int b = my_n / nc;
-                md = a.desc[b];
-                if (md.r >= 0 && a.sel) {
-                    const int si = a.sel[b];
-                    if (si != md.i) {
-                        if (a.err) atomicOr(a.err, E_STALE_DESC);
-                        md.r = -1;
+        // Items are claimed dynamically (first item n = blockIdx.x, then grid + ticket), so
+        // SMs that stream faster take more of them; one claim is kept in flight ahead.
+        if (lane == 0) {
+            const int kk = a.rows.k;
+            const int64_t V = a.rows.V;
+            int n = (int)blockIdx.x;
+            uint32_t nxt = (uint32_t)grid + atomicAdd(a.work, 1u);
+            for (int k = 0;; ++k) {
+                const int st = k % kStages;
+                TRACE(1, k & 1023);
+                if (k >= kStages) mbar_wait(&empty[st], ((k / kStages) - 1) & 1);
+                TRACE(2, k & 1023);
+                if (n >= n_items) {  // no more items: tell the consumers
+                    s_stage[st] = -1;
+                    mbar_arrive(&full[st]);
+                    break;
+                }
+                const int cur = n;
+                n = nxt < (uint32_t)n_items ? (int)nxt : n_items;
+                if (n < n_items) nxt = (uint32_t)grid + atomicAdd(a.work, 1u);
+                s_stage[st] = cur;
+                const uint32_t it = s_slot[cur / nc];
+                if (it == 0) {
+                    mbar_arrive(&full[st]);
+                } else {
+                    const int r = (int)(it & 31u) - 1;
+                    const int64_t slab = it >> 5;
+                    const int c = cur % nc;
+                    const int64_t e0 = (int64_t)c * TC::kTileElems;
+                    const int64_t ne = V - e0 < TC::kTileElems ? V - e0 : TC::kTileElems;
+                    const uint32_t bytes = (uint32_t)(ne * E::kEsz);
+                    const char *pr = (const char *)a.rows.p + ((slab * (kk + 1) + r) * V + e0) * E::kEsz;
+                    uint8_t *dst = s_tiles + (size_t)st * 2 * kTileBytes;
+                    const bool use_q = r < kk;
+                    mbar_arrive_tx(&full[st], use_q ? 2 * bytes : bytes);
+                    CTA_BYTES(use_q ? 2 * bytes : bytes);
+                    tma_load_1d(dst, pr, bytes, &full[st]);
+                    if (use_q) {
+                        const char *qr = (const char *)a.rows.q + ((slab * kk + r) * V + e0) * E::kEsz;
+                        tma_load_1d(dst + kTileBytes, qr, bytes, &full[st]);
                     }
                 }
+                TRACE(8, k & 1023);
+                CTA_TIME(2);
             }
-            for (int j = 0; j < 32; ++j, ++k) {
-                const int n = base + j * (int)gridDim.x;
-                if (n >= n_items) break;
-                const int r = __shfl_sync(0xFFFFFFFFu, md.r, j);
-                const int slab = __shfl_sync(0xFFFFFFFFu, md.slab, j);
-                const int di = __shfl_sync(0xFFFFFFFFu, md.i, j);
-                const uint32_t req = __shfl_sync(0xFFFFFFFFu, md.req, j);
-                const uint32_t rnd = __shfl_sync(0xFFFFFFFFu, md.round, j);
-                if (lane == 0) {
-                    const int st = k % kStages;
-                    TRACE(1, k);
-                    if (k >= kStages) mbar_wait(&empty[st], ((k / kStages) - 1) & 1);
-                    TRACE(2, k);
-                    const int c = n % nc;
-                    SlotDesc d;
-                    d.i = di; d.slab = slab; d.req = req; d.round = rnd; d.r = r;
-                    d.pad[0] = d.pad[1] = d.pad[2] = 0;
-                    s_desc[st] = d;
-                    s_chunk[st] = c;
-                    if (r < 0) {
-                        mbar_arrive(&full[st]);
-                    } else {
-                        const bool use_q = r < kk;
-                        const int64_t e0 = (int64_t)c * kTile;
-                        const int64_t ne = V - e0 < kTile ? V - e0 : kTile;
-                        const uint32_t bytes = (uint32_t)(ne * E::kEsz);
-                        uint8_t *dst = s_tiles + (size_t)st * 2 * kTileBytes;
-                        const char *prow = (const char *)a.rows.p + ((int64_t)slab * (kk + 1) + r) * V * E::kEsz;
-                        mbar_arrive_tx(&full[st], use_q ? 2 * bytes : bytes);
-                        tma_load_1d(dst, prow + e0 * E::kEsz, bytes, &full[st]);
-                        if (use_q) {
-                            const char *qrow = (const char *)a.rows.q + ((int64_t)slab * kk + r) * V * E::kEsz;
-                            tma_load_1d(dst + kTileBytes, qrow + e0 * E::kEsz, bytes, &full[st]);
-                        }
-                    }
-                    TRACE(8, k);
-                }
-                __syncwarp();
+            // retire: the last CTA to stop claiming leaves the counters zero for the next launch
+            if (atomicAdd(a.work + 1, 1u) == (uint32_t)grid - 1) {
+                a.work[0] = 0;
+                a.work[1] = 0;
             }
         }
-    } else {
-    const int grp = (warp - 1) / (kConsumerWarps + 1);
-    const int gw = (warp - 1) % (kConsumerWarps + 1);  // 0..7 consumer, 8 finisher
-    if (gw == kConsumerWarps) {
-        // ------------------------------------------------------------ finisher of group grp
-        int head = 0;
-        for (;;) {
-            while (head == s_qtail[grp]) __nanosleep(32);
-            const int b = s_q[grp][head % kFinQ];
-            SlotDesc d;
-            d.i = s_qd[grp][head % kFinQ].x;
-            d.slab = s_qd[grp][head % kFinQ].y;
-            d.req = (uint32_t)s_qd[grp][head % kFinQ].z;
-            d.round = (uint32_t)s_qd[grp][head % kFinQ].w;
-            d.r = s_qr[grp][head % kFinQ];
-            ++head;
-            __syncwarp();
-            if (lane == 0) s_qhead[grp] = head;
-            if (b < 0) break;
-            if (lane == 0) TRACE(5, b);
-            // independent work first, overlapping the wait for the other CTAs' chunks:
-            // the state update's inputs and the next round's acceptance-test chain
-            UpdIn upd{};
-            int64_t now = 0;
-            if (a.fuse_update) {
-                upd = load_update_inputs(a.st, a.sc, d.i, lane);
-                now = a.st.g->now_us;
+        __syncwarp();
+    } else if (finisher) {
+        // ------------------------------------------------------------ finisher grp
+        const int f0 = grp * grid + (int)blockIdx.x;
+        const int nf = fin_slots(B, grid, f0);
+        if (a.fuse_update) {
+            // the state updates first, two slots at a time (both slots' loads in flight)
+            const int64_t now = a.st.g->now_us;
+            for (int j = 0; j < nf; j += 2) {
+                const SlotDesc d0 = s_fin[grp][j];
+                const bool has1 = j + 1 < nf;
+                const SlotDesc d1 = s_fin[grp][has1 ? j + 1 : j];
+                const bool l0 = d0.r >= 0, l1 = has1 && d1.r >= 0;
+                UpdIn u0{}, u1{};
+                if (l0) u0 = load_update_inputs(a.st, a.sc, d0.i, lane);
+                if (l1) u1 = load_update_inputs(a.st, a.sc, d1.i, lane);
+                const NextA1 x0 = next_a1_load<BF16>(a, l0 ? d0.i : -1, d0.round + 1);
+                const NextA1 x1 = next_a1_load<BF16>(a, l1 ? d1.i : -1, d1.round + 1);
+                if (l0) update_slot_warp<BF16>(a, f0 + j * kGroups * grid, d0, u0, now, x0);
+                if (l1) update_slot_warp<BF16>(a, f0 + (j + 1) * kGroups * grid, d1, u1, now, x1);
             }
-            const NextA1 nxt = next_a1_load<BF16>(a, d.i, d.round + 1);
+        }
+#if defined(LAPSSD_DIAG) && (LAPSSD_DIAG & 2)
+        if (nf >= 0) return;  // diagnostic build: no sampling
+#endif
+        for (int j = 0; j < nf; ++j) {
+            const SlotDesc d = s_fin[grp][j];
+            if (d.r < 0) continue;
+            const int b = f0 + j * kGroups * grid;
+            if (lane == 0) TRACE(5, b);
             const uint64_t *pw = a.part + (int64_t)b * nc * kPartWords;
-            uint64_t w0[kWarps], w1[kWarps];
+            uint64_t w[kPartWords];
             const unsigned long long t_start = gtimer();
-            for (;;) {  // every (chunk, warp) sum of slot b published?
+            for (;;) {  // every (chunk, segment) sum of slot b published?
 #pragma unroll
-                for (int x = 0; x < kWarps; ++x) w0[x] = w1[x] = kReady;
-                if (lane < nc) load_chunk_words(pw, lane, w0);
-                if (lane + 32 < nc) load_chunk_words(pw, lane + 32, w1);
-                bool ready = true;
+                for (int x = 0; x < kPartWords; ++x) w[x] = kReady;
 #pragma unroll
-                for (int x = 0; x < kWarps; ++x) ready &= ((w0[x] & w1[x]) & kReady) != 0;
-                if (__all_sync(0xFFFFFFFFu, ready)) break;
+                for (int h = 0; h < TC::kCPL; ++h)
+                    if (lane + 32 * h < nc) load_chunk_words<TC::kSegs>(pw, lane + 32 * h, w + h * TC::kSegs);
+                uint64_t all = kReady;
+#pragma unroll
+                for (int x = 0; x < kPartWords; ++x) all &= w[x];
+                if (__all_sync(0xFFFFFFFFu, (all & kReady) != 0)) break;
                 if (waited_too_long(t_start)) {
                     if (lane == 0 && a.err) atomicOr(a.err, E_TIMEOUT);
                     break;
                 }
-                __nanosleep(32);
+                __nanosleep(kPollNs);
             }
             if (lane == 0) TRACE(6, b);
-            finish_slot_warp<BF16>(a, b, d, s_fb[grp], w0, w1, upd, now, nxt);
+            if (lane == 0) CTA_TIME(4);
+            sample_slot_warp<BF16>(a, b, d, s_fb[grp], w);
             if (lane == 0) TRACE(7, b);
+            if (lane == 0) CTA_TIME(8);
+            if (lane == 0) SLOT_TIME(2, b);
         }
         if (lane == 0) CTA_TIME(1);
     } else {
-    // ---------------------------------------------------------------- consumers of group grp
-    int k = grp;
-    const int warp_seg = gw;  // this warp's 1024-entry segment of every chunk
-    for (int n = blockIdx.x + grp * (int)gridDim.x; n < n_items; n += kGroups * (int)gridDim.x, k += kGroups) {
-        const int st = k % kStages;
-        mbar_wait(&full[st], (k / kStages) & 1);
-        if (warp_seg == 0 && lane == 0) TRACE(3, k);
-        const SlotDesc d = s_desc[st];
-        const int c = s_chunk[st];
-        const int b = n / nc;
-        if (d.r >= 0) {
-            const uint4 qmask = d.r < a.rows.k ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
-            const uint4 *tp = reinterpret_cast<const uint4 *>(s_tiles + (size_t)st * 2 * kTileBytes);
-            const uint4 *tq = tp + kTileBytes / 16;
-            const int64_t e_base = (int64_t)c * kTile + (int64_t)warp_seg * kSegElems;
-            const int64_t V = a.rows.V;
-            uint4 pv[S::J], qv[S::J];
+        // ------------------------------------------------------------ consumers: every item, segment gw
+        // (one stage ring consumed in order by all consumer warps: a stage is refilled only
+        // after all of them released it, so no warp can run a phase ahead)
+        const int64_t V = a.rows.V;
+        for (int k = 0;; ++k) {
+            const int st = k % TC::kStages;
+            mbar_wait(&full[st], (k / TC::kStages) & 1);
+            if (gw == 0 && lane == 0) TRACE(3, k & 1023);
+            const int n = s_stage[st];
+            if (n < 0) break;
+            const uint32_t it = s_slot[n / nc];
+            if (it != 0 && gw < TC::kSegs) {
+                const int b = n / nc, c = n % nc;
+                const int r = (int)(it & 31u) - 1;
+                const uint4 qmask = r < a.rows.k ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
+                const uint4 *tp = reinterpret_cast<const uint4 *>(s_tiles + (size_t)st * 2 * kTileBytes);
+                const uint4 *tq = tp + kTileBytes / 16;
+                {
+                    const int seg = gw;
+                    const int64_t e_base = (int64_t)c * TC::kTileElems + (int64_t)seg * kSegElems;
+                    uint4 pv[S::J], qv[S::J];
 #pragma unroll
-            for (int j = 0; j < S::J; ++j) {  // branch-free: load, then mask the tail / absent q
-                const int v = warp_seg * (kSegElems / S::kVec) + j * 32 + lane;
-                pv[j] = tp[v];
-                qv[j] = tq[v];
-            }
-            uint64_t m = 0;
-#pragma unroll
-            for (int j = 0; j < S::J; ++j) {
-                const bool in = e_base + (int64_t)(j * 32 + lane) * S::kVec < V;
-                const uint4 z = make_uint4(0, 0, 0, 0);
-                const uint4 pm = in ? pv[j] : z;  // beyond V the stage holds stale bytes
-                const uint4 qm = in ? make_uint4(qv[j].x & qmask.x, qv[j].y & qmask.y, qv[j].z & qmask.z,
-                                                 qv[j].w & qmask.w)
-                                    : z;
-                m += E::mass(pm, qm);
-            }
-            m = warp_sum_u64(m);
-            if (lane == 0) st_relaxed(&a.part[((int64_t)b * nc + c) * kPartWords + warp_seg], m | kReady);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-        if (warp_seg == 0 && lane == 0) TRACE(4, k);
-        // slot b is finished by the CTA that consumed its chunk b % nc: spreads the
-        // finishing over all CTAs whatever gcd(gridDim, nc) is
-        if (d.r >= 0 && c == b % nc && warp_seg == 0 && lane == 0) {
-            while (s_qtail[grp] - s_qhead[grp] >= kFinQ) __nanosleep(32);
-            s_q[grp][s_qtail[grp] % kFinQ] = b;
-            s_qd[grp][s_qtail[grp] % kFinQ] = make_int4(d.i, d.slab, (int)d.req, (int)d.round);
-            s_qr[grp][s_qtail[grp] % kFinQ] = d.r;
-            __threadfence_block();
-            s_qtail[grp] = s_qtail[grp] + 1;
-        }
-    }
-    if (warp_seg == 0 && lane == 0) {
-        while (s_qtail[grp] - s_qhead[grp] >= kFinQ) __nanosleep(32);
-        s_q[grp][s_qtail[grp] % kFinQ] = -1;
-        __threadfence_block();
-        s_qtail[grp] = s_qtail[grp] + 1;
-    }
-    }  // consumers
-    }  // consumer groups / finishers
-    if (tid == 0) CTA_TIME(1);
-    // ------------------------------------------------------------ fused final select
-    if (a.fuse_select && !a.pubq) {
-        __shared__ int s_last;
-        __syncthreads();
-        if (tid == 0) {
-            __threadfence();
-            s_last = atomicAdd(a.done_ctas, 1u) == gridDim.x - 1;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-#ifdef LAPSSD_TRACE
-            unsigned long long *trp = g_fs_trace;
+                    for (int j = 0; j < S::J; ++j) {  // branch-free: load, then mask the tail / absent q
+                        const int v = seg * (kSegElems / S::kVec) + j * 32 + lane;
+                        pv[j] = tp[v];
+                        qv[j] = tq[v];
+                    }
+                    uint64_t m = 0;
+#if defined(LAPSSD_DIAG) && (LAPSSD_DIAG & 1)
+                    if (pv[0].x == 0x7FFFFFFFu && qv[0].y == 1u) m = 1;  // diagnostic build: no residual math
 #else
-            unsigned long long *trp = nullptr;
+#pragma unroll
+                    for (int j = 0; j < S::J; ++j) {
+                        const bool in = e_base + (int64_t)(j * 32 + lane) * S::kVec < V;
+                        const uint4 z = make_uint4(0, 0, 0, 0);
+                        const uint4 pm = in ? pv[j] : z;  // beyond V the stage holds stale bytes
+                        const uint4 qm = in ? make_uint4(qv[j].x & qmask.x, qv[j].y & qmask.y, qv[j].z & qmask.z,
+                                                         qv[j].w & qmask.w)
+                                            : z;
+                        m += E::mass(pm, qm);
+                    }
 #endif
-            fused_final_select(a.st, a.sc, B, const_cast<int32_t *>(a.sel), const_cast<SlotDesc *>(a.desc), a.fin,
-                               a.pre, a.count_out, reinterpret_cast<uint64_t *>(s_tiles), trp);
-            if (tid == 0) *a.done_ctas = 0;
+                    m = warp_sum_u64(m);
+                    if (lane == 0) st_relaxed(&a.part[((int64_t)b * nc + c) * kPartWords + seg], m | kReady);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (gw == 0 && lane == 0) TRACE(4, k & 1023);
+            if (lane == 0) CTA_TIME(3);
         }
     }
+    if (tid == 0) CTA_TIME(1);
 }
 
 int verify_cpb(int64_t V) {
@@ -725,11 +789,12 @@ int verify_cpb(int64_t V) {
     return 1;
 }
 
-static int g_verify_grid = 0;
+
+static int g_verify_grid = 0;  // SM count, set once by verify_prepare
 
 template <bool BF16>
 static void verify_prepare_t() {
-    const size_t smem = (size_t)VerifyCfg<BF16>::kStages * 2 * VerifyCfg<BF16>::kTileBytes;
+    const size_t smem = (size_t)VerifyCfg<BF16>::kStages * 2 * kTileBytes;
     cudaFuncSetAttribute(verify_kernel<BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(verify_kernel<BF16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
@@ -745,20 +810,38 @@ void verify_prepare() {
     g_verify_grid = sms;
 }
 
+int verify_grid(int32_t B, int32_t n_chunks, int32_t reserve_sms) {
+    const int sms = g_verify_grid > 0 ? g_verify_grid : 148;
+    const int64_t n_items = (int64_t)B * n_chunks;
+    const int avail = sms - reserve_sms > 1 ? sms - reserve_sms : 1;  // SMs left for a concurrent kernel
+    return n_items < avail ? (int)n_items : avail;
+}
+
+bool verify_fits(int32_t B, int32_t n_chunks, int32_t reserve_sms) {
+    if (B <= 0) return true;
+    const int g = verify_grid(B, n_chunks, reserve_sms);
+    return B <= kMaxSlots && fin_slots(B, g, 0) <= kFinCap;
+}
+
+int verify_max_batch(int32_t n_chunks, int32_t reserve_sms) {
+    int lo = 1, hi = 1 << 20;
+    while (lo < hi) {  // largest B that fits (monotone in B)
+        const int mid = lo + (hi - lo + 1) / 2;
+        if (verify_fits(mid, n_chunks, reserve_sms)) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
 template <bool BF16>
 static cudaError_t launch_verify_t(const VerifyArgs &a, int32_t B, int32_t reserve_sms, cudaStream_t s) {
-    const size_t smem = (size_t)VerifyCfg<BF16>::kStages * 2 * VerifyCfg<BF16>::kTileBytes;
-    const int grid = g_verify_grid > 0 ? g_verify_grid : 148;
-    const int n_items = B * a.n_chunks;
-    const int avail = grid - reserve_sms > 1 ? grid - reserve_sms : 1;  // SMs left for a concurrent kernel
-    const int g = n_items < avail ? n_items : avail;
+    const size_t smem = (size_t)VerifyCfg<BF16>::kStages * 2 * kTileBytes;
     // Finishers wait on other CTAs' chunks, so all CTAs must be resident together: each
     // CTA needs an SM's shared memory (one CTA per SM) and the grid is at most the SM
     // count minus the SMs left to the side-stream select.  No cooperative attribute: a
     // cooperative launch is serialised against other streams' kernels, which would
     // forbid exactly the overlap with the side kernel.  Device waits have a watchdog.
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)g);
+    cfg.gridDim = dim3((unsigned)verify_grid(B, a.n_chunks, reserve_sms));
     cfg.blockDim = dim3(kVerifyThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -769,6 +852,7 @@ static cudaError_t launch_verify_t(const VerifyArgs &a, int32_t B, int32_t reser
 
 cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_sms, cudaStream_t s) {
     if (B <= 0) return cudaSuccess;
+    if (!verify_fits(B, a.n_chunks, reserve_sms)) return cudaErrorInvalidValue;  // callers split / validate
     count_launch();
     return a.rows.dtype == LAPSSD_BF16 ? launch_verify_t<true>(a, B, reserve_sms, s)
                                        : launch_verify_t<false>(a, B, reserve_sms, s);

@@ -59,7 +59,7 @@ def check_parity(L, pool, B, seed, rng):
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
-@pytest.mark.parametrize("V", [16, 1000, 8200, 32000, 128256])
+@pytest.mark.parametrize("V", [16, 1000, 8200, 16392, 32000, 128256, 524288])
 @pytest.mark.parametrize("k", [1, 4, 8])
 def test_spec_verify_parity_grid(L, dtype, V, k):
     pool = synth.make_pool("f2", V=V, k=k, dtype=dtype, n_buckets=4, variants=2, seed=V + k,
@@ -92,7 +92,7 @@ def _pool_from(p, q, draft, dtype):
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 def test_special_cases(L, dtype):
-    V, k = 8192 + 64, 4
+    V, k = 16384 + 64, 4  # two bf16 chunks (ragged), three fp32 chunks
     rng = np.random.default_rng(2)
     base = rng.random((k + 1, V)).astype(np.float32)
     base /= base.sum(1, keepdims=True)
