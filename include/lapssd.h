@@ -89,7 +89,8 @@ typedef struct {
  * create.  Local request l has global id l*world + rank; arrival_us must be
  * non-decreasing in l (ids encode arrival order, AMB-19).  L_true >= 1 is the
  * output length that ends the request, L_pred >= 1 the predicted length L_i
- * used by Eq. 6 and LP-SJF.  Global ids must be < 2^24. */
+ * used by Eq. 6 and LP-SJF.  Global ids must be < 2^24 - 1 (the all-ones key
+ * stays unused). */
 typedef struct {
     const int64_t *arrival_us;
     const int32_t *L_true;
@@ -152,7 +153,7 @@ lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V
  * `stream`), zero-initialises state, computes the thresholds of P:169, and sets
  * now = 0.  The first batch comes from laps_select.  max_batch bounds B of every
  * later call; V bounds the rows' vocabulary.
- * Errors: EINVAL (config, n, ids >= 2^24, max_batch < 1), ENOMEM, ECUDA. */
+ * Errors: EINVAL (config, n, ids >= 2^24 - 1, max_batch < 1), ENOMEM, ECUDA. */
 size_t lapssd_workspace_bytes(const lapssd_config *cfg, int32_t n_local, int32_t max_batch,
                               int64_t V, int32_t world);
 lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req,

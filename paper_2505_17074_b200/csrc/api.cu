@@ -1,6 +1,7 @@
 // api.cu -- the C-ABI of liblapssd.so (include/lapssd.h): validation, workspace
 // carving, kernel orchestration, state snapshot, errors, and the NCCL all-gather of
 // the multi-GPU step (resolved at run time with dlopen).
+#include <cstdlib>
 #include <dlfcn.h>
 
 #include <atomic>
@@ -98,7 +99,7 @@ struct lapssd_handle {
     PreSelect *pre = nullptr;    // presort output (side stream)
     SelRec *fin = nullptr;       // finisher records, one per slot (fused select)
     uint32_t *snap = nullptr;    // verify CTAs that have read sel/desc (incremental select)
-    uint32_t *pubq = nullptr;    // slot publication queue (incremental select)
+    uint64_t *fin_key = nullptr; // per-slot published keys (~key, 0 = none) of fin[] (incremental select)
     cudaStream_t side = nullptr; // side stream for the presort, fork/join events
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t last_stream;
@@ -134,8 +135,8 @@ static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma,
     st.x = cv.take<int64_t>(nn);
     st.next_tag = cv.take<uint64_t>(nn);
     st.next_sr = cv.take<int2>(nn);
-    h->part = cv.take<uint64_t>((size_t)max_batch * n_chunks * kPartWords);
-    h->work = cv.take<uint32_t>(2);
+    h->part = cv.take<uint64_t>(2 * (size_t)max_batch * n_chunks * kPartWords);  // two parity sets
+    h->work = cv.take<uint32_t>(4);
     h->tokens = cv.take<int32_t>((size_t)max_batch * (k + 1));
     h->n_accept = cv.take<int32_t>((size_t)max_batch);
     h->desc = cv.take<SlotDesc>((size_t)max_batch);
@@ -144,7 +145,7 @@ static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma,
     h->pre = reinterpret_cast<PreSelect *>(cv.take<uint64_t>(preselect_words(bp)));
     h->fin = cv.take<SelRec>((size_t)max_batch);
     h->snap = cv.take<uint32_t>(1);
-    h->pubq = cv.take<uint32_t>(1 + (size_t)max_batch);
+    h->fin_key = cv.take<uint64_t>((size_t)max_batch);
 }
 
 static lapssd_status check_config(const lapssd_config *c) {
@@ -258,8 +259,8 @@ lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req
         return fail(LAPSSD_EINVAL, "requests: n / rank / world");
     if (req->n > 0 && (!req->arrival_us || !req->L_true || !req->L_pred))
         return fail(LAPSSD_EINVAL, "requests: NULL arrays");
-    if ((int64_t)req->n * req->world + req->rank > (1 << 24))
-        return fail(LAPSSD_EINVAL, "global ids must be < 2^24");
+    if ((int64_t)req->n * req->world + req->rank > (1 << 24) - 1)
+        return fail(LAPSSD_EINVAL, "global ids must be < 2^24 - 1");   // key ~0 stays unused
     if (req->n > sort_capacity())
         return fail(LAPSSD_EINVAL, "n_local=%d exceeds the single-CTA select capacity %d", req->n,
                     sort_capacity());
@@ -445,16 +446,20 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
     h->desc_valid = false;
     if (incremental) {
         a.fin = h->fin;
-        a.pubq = h->pubq;
+        a.fin_key = h->fin_key;
         a.snap = h->snap;
+        a.part1 = h->part + (size_t)h->max_batch * h->n_chunks * kPartWords;
+        a.work1 = h->work + 2;
+        a.vstep = &h->st.g->vstep;
     }
-    st = cuda_status(launch_verify_grid(a, B, 1, s), "laps_step verify");
+    static const bool no_pdl = getenv("LAPSSD_NO_PDL") != nullptr;  // A/B switch for measurements
+    st = cuda_status(launch_verify_grid(a, B, 1, incremental && !no_pdl, s), "laps_step verify");
     if (st != LAPSSD_OK) return st;
     if (ev) prof_record(ev[1], s);
     ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
     if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork wait");
     if (incremental) {
-        st = cuda_status(launch_select_side(h->st, h->sc, a.rows, sel_inout, h->desc, B, h->pre, h->fin, h->pubq,
+        st = cuda_status(launch_select_side(h->st, h->sc, a.rows, sel_inout, h->desc, B, h->pre, h->fin, h->fin_key,
                                             h->snap, (uint32_t)verify_grid(B, a.n_chunks, 1), count_out, h->side),
                          "laps_step select");
     } else {

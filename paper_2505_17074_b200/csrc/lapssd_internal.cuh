@@ -51,7 +51,8 @@ struct Globals {
     int32_t prev_count;    // size of the batch that ran last (global for G > 1)
     int32_t count;         // size of the batch just selected (this rank)
     uint32_t err;          // sticky contract-violation flags
-    int32_t pad[2];
+    uint32_t vstep;        // incremental steps committed: parity of the verify buffers
+    int32_t pad;
 };
 
 // Scheduler constants, passed by value to every kernel.
@@ -118,7 +119,12 @@ __device__ __forceinline__ uint64_t sat32(uint64_t v) { return v > 0xFFFFFFFFull
 
 // The 64-bit priority key (include/lapssd.h, laps_select).  Smaller = sooner.
 // All state fields are passed in (loaded together by the caller: one memory round trip).
-__device__ __forceinline__ uint64_t build_key(const Sched &s, int32_t i, int32_t cursor, uint32_t fl,
+#ifdef LAPSSD_SIDE_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+uint64_t build_key(const Sched &s, int32_t i, int32_t cursor, uint32_t fl,
                                               int32_t L_pred, int32_t acc_tok, double A) {
     const uint64_t id = (uint64_t)(i * s.world + s.rank) & 0xFFFFFFull;
     const uint64_t inelig = (i >= cursor || (fl & F_DONE)) ? 1 : 0;
@@ -400,7 +406,12 @@ __device__ __forceinline__ float load_prob_f32(const void *base, int64_t idx) {
 
 // Fill desc for slot b of a handle batch (local request i, or -1): the cached a1 of
 // request i's current round if the finisher computed it for these rows, else a1 now.
-__device__ __forceinline__ SlotDesc make_desc(const RowsDev &rw, const State &st, const Sched &sc,
+#ifdef LAPSSD_SIDE_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+SlotDesc make_desc(const RowsDev &rw, const State &st, const Sched &sc,
                                               int32_t b, int32_t i) {
     SlotDesc d;
     d.i = i; d.slab = 0; d.req = 0; d.round = 0; d.r = -1;
@@ -421,6 +432,10 @@ __device__ __forceinline__ SlotDesc make_desc(const RowsDev &rw, const State &st
     d.slab = (int32_t)slab;
     d.r = rw.dtype == LAPSSD_BF16 ? accept_test(rw, slab, d.req, d.round, 0, sc.seed, load_prob_bf16)
                                   : accept_test(rw, slab, d.req, d.round, 0, sc.seed, load_prob_f32);
+    if (rw.slab_tab) {  // memoise: a waiting request's round (hence its a1) does not change
+        st.next_sr[i] = make_int2(d.slab, d.r);
+        st.next_tag[i] = ((uint64_t)rw.epoch << 32) | (uint32_t)rnd;
+    }
     return d;
 }
 
@@ -440,6 +455,12 @@ struct VerifyArgs {
     uint64_t *z;
     uint64_t *part;             // [B][n_chunks][kPartWords] segment residual sums
     uint32_t *work;             // [2] item-claim counter, retired CTAs (zero between launches)
+    // second (part, work) set and the step counter that picks one: consecutive laps_step
+    // launches overlap (programmatic dependent launch), so step t+1 streams into the
+    // other set while step t's finishers still read theirs (nullable: one set)
+    uint64_t *part1;
+    uint32_t *work1;
+    const uint32_t *vstep;
     int32_t fuse_update;
     State st;                   // handle mode only
     Sched sc;
@@ -447,7 +468,7 @@ struct VerifyArgs {
     // incremental select (laps_step with pooled rows): each finisher writes its slot's
     // record (new key, next descriptor) and publishes the slot to the side-stream merger
     SelRec *fin;                // [B] one record per slot
-    uint32_t *pubq;             // [1 + B]: ticket, then slot+1 per entry (0 = not yet); null: no records
+    uint64_t *fin_key;          // [B] ~key, release-stored once fin[b] is written (0 = not yet); null: no records
     // +1 per CTA (release) once it has read all it needs of desc[] / sel[]; the side
     // select overwrites those only after every CTA has signalled (nullable)
     uint32_t *snap;
@@ -500,12 +521,12 @@ cudaError_t launch_presort(const State &st, const Sched &sc, const RowsDev &rw, 
                            PreSelect *out, cudaStream_t s);
 cudaError_t launch_select_final(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc, int32_t B,
                                 int32_t *sel, int32_t *count_out, const PreSelect *pre, cudaStream_t s);
-cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_sms, cudaStream_t s);
+cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_sms, bool pdl, cudaStream_t s);
 int verify_grid(int32_t B, int32_t n_chunks, int32_t reserve_sms);       // CTAs of that launch
 bool verify_fits(int32_t B, int32_t n_chunks, int32_t reserve_sms);      // per-CTA snapshot capacity
 int verify_max_batch(int32_t n_chunks, int32_t reserve_sms);
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
-                               int32_t B, PreSelect *pre, const SelRec *fin, uint32_t *pubq, uint32_t *snap,
+                               int32_t B, PreSelect *pre, const SelRec *fin, uint64_t *fin_key, uint32_t *snap,
                                uint32_t snap_target, int32_t *count_out, cudaStream_t s);
 int sort_capacity();            // largest key count one select CTA can sort
 void prepare_all();             // kernel attributes, once per process (api.cu)

@@ -23,9 +23,32 @@ extern "C" int lapssd_side_trace_read(unsigned long long *out, unsigned *n) {
     cudaMemcpyToSymbol(g_side_n, &z, sizeof z);
     return 0;
 }
+#ifdef LAPSSD_TRACE_SIDE   // per-iteration side-kernel events (perturbs the side kernel)
 #define ITRACE(m) do { if (threadIdx.x == 0) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); \
     unsigned i = g_side_n++; if (i < 128) { g_side_iter[i][0] = t; g_side_iter[i][1] = (unsigned long long)(m); } } } while (0)
+#else
+#define ITRACE(m)
+#endif
+#define SSTEP(k) do { if (threadIdx.x == 0) g_sstep_t[vstep0 & 63][k] = gtimer(); } while (0)
+__device__ unsigned long long g_siter[64][8][3];   // per step, first 8 merge passes: time, collected, merged
+extern "C" int lapssd_siter_read(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_siter, sizeof g_siter);
+    static unsigned long long zero[64][8][3];
+    cudaMemcpyToSymbol(g_siter, zero, sizeof zero);
+    return 0;
+}
+#define SITER(it, a, b) do { if (threadIdx.x == 0 && (it) < 8) { g_siter[vstep0 & 63][it][0] = gtimer(); \
+    g_siter[vstep0 & 63][it][1] = (a); g_siter[vstep0 & 63][it][2] = (b); } } while (0)
 __device__ unsigned long long g_sel_trace[16];
+__device__ unsigned long long g_dbg_rec[16][4];
+extern "C" int lapssd_dbg_rec_read(unsigned long long *out) { return (int)cudaMemcpyFromSymbol(out, g_dbg_rec, sizeof g_dbg_rec); }
+__device__ unsigned long long g_sstep_t[64][10];   // per committed step: side start, presort, merged, snap, end
+extern "C" int lapssd_sstep_trace_read(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_sstep_t, sizeof g_sstep_t);
+    static unsigned long long zero[64][10];
+    cudaMemcpyToSymbol(g_sstep_t, zero, sizeof zero);
+    return 0;
+}
 __device__ unsigned long long g_send[64];
 __device__ unsigned int g_scount;
 extern "C" int lapssd_send_read(unsigned long long *out) {
@@ -38,6 +61,8 @@ extern "C" int lapssd_sel_trace_read(unsigned long long *out) { return (int)cuda
 #else
 #define STRACE(i)
 #define ITRACE(m)
+#define SSTEP(k)
+#define SITER(it, a, b)
 #endif
 
 
@@ -272,31 +297,48 @@ __global__ void __launch_bounds__(kSelThreads) select_final_kernel(const State s
 // its sorted running list, keeping only the first B (an element ranked >= B can never
 // re-enter the top B).  When every verified slot has arrived the list IS the next
 // batch, and the commit (x_i, pinning, running flags, descriptors, clock) follows.
-__global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st, const Sched sc, const RowsDev rw,
+__global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State st, const Sched sc, const RowsDev rw,
                                                                    int32_t *sel, SlotDesc *desc, int32_t B,
-                                                                   PreSelect *pre, const SelRec *fin, uint32_t *pubq,
+                                                                   PreSelect *pre, const SelRec *fin, uint64_t *fin_key,
                                                                    uint32_t *snap, uint32_t snap_target,
                                                                    int32_t *count_out) {
     extern __shared__ uint64_t s_buf[];
     STRACE(8);
+#ifdef LAPSSD_TRACE
+    const uint32_t vstep0 = st.g->vstep;
+    if (threadIdx.x == 0) {
+        g_sstep_t[vstep0 & 63][0] = gtimer();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_sstep_t[vstep0 & 63][5] = smid;
+    }
+#endif
     __shared__ int64_t s_now;
-    __shared__ int s_cursor, s_expected, s_head, s_m, s_count;
+    __shared__ int s_cursor, s_expected, s_merged, s_m, s_count;
     __shared__ uint32_t s_member[kSortCap / 32];
+    __shared__ uint32_t s_pend[4096 / 32];    // expected slots not yet merged (B <= 4096 here)
+    __shared__ int s_snap_ok;
     const int n = sc.n;
     const int T = blockDim.x;
     // ---------------- phase 1: presort of every request outside the batch
     for (int w = threadIdx.x; w < (n + 31) / 32; w += T) s_member[w] = 0;
-    if (threadIdx.x == 0) { s_expected = 0; s_head = 0; s_count = 0; }
+    for (int w = threadIdx.x; w < 4096 / 32; w += T) s_pend[w] = 0;
+    if (threadIdx.x == 0) { s_expected = 0; s_merged = 0; s_m = 0; s_count = 0; s_snap_ok = snap == nullptr; }
     advance_and_admit(st, sc, &s_now, &s_cursor);   // ends with a barrier
+    SSTEP(6);
     int expected = 0;
     for (int b = threadIdx.x; b < B; b += T) {
         const int i = sel[b];
         if (i >= 0) atomicOr(&s_member[i >> 5], 1u << (i & 31));
         const SlotDesc d = desc[b];
-        expected += (d.r >= 0 && i >= 0 && d.i == i);   // the slots the verify kernel will finish
+        if (d.r >= 0 && i >= 0 && d.i == i) {   // the slots the verify kernel updates and publishes
+            ++expected;
+            atomicOr(&s_pend[b >> 5], 1u << (b & 31));
+        }
     }
     if (expected) atomicAdd(&s_expected, expected);
     __syncthreads();
+    SSTEP(7);
     const int npow2 = next_pow2(n > 0 ? n : 1);
     const int cursor = s_cursor;
     for (int i = threadIdx.x; i < npow2; i += T) {
@@ -305,15 +347,23 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
             const uint32_t fl = st.flags[i];
             const int32_t lp = st.L_pred[i], tok = st.acc_tok[i];
             const double A = st.A[i];
+            const int32_t rnd = st.rounds[i];
+            const uint64_t tag = st.next_tag[i];
             key = build_key(sc, i, cursor, fl, lp, tok, A);
             st.key[i] = key;
             if (key >> 63) key = ~0ull;   // ineligible: never selected
+            // a1 of a waiting request's current round, memoised once (make_desc stores it):
+            // the records below then never wait on row gathers under the verify stream
+            else if (rw.valid && rw.slab_tab && tag != (((uint64_t)rw.epoch << 32) | (uint32_t)rnd))
+                (void)make_desc(rw, st, sc, 0, i);
         }
         s_buf[i] = key;
     }
     __syncthreads();
+    SSTEP(8);
     const int bp = next_pow2(B);
     const uint64_t *top = select_topB(s_buf, n, B, s_buf + npow2, s_buf + npow2 + bp, bp);
+    SSTEP(9);
     SelRec *crec = pre_recs(pre, bp);
     for (int b = threadIdx.x; b < bp; b += T) {
         const uint64_t key = top[b];
@@ -334,6 +384,7 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
     }
     __syncthreads();
     ITRACE(200000);
+    SSTEP(1);
     // ---------------- phase 2: fold in the verified batch as it is published
     uint64_t *L = s_buf;                      // [bp] running top-B, sorted
     uint64_t *L2 = s_buf + bp;                // [bp]
@@ -345,9 +396,21 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
     SelRec *brec = reinterpret_cast<SelRec *>(cand_of + ((n + 7) & ~7));
     SelRec *srec = brec + bp;
     const bool rec_smem = bp <= 1024;
+    constexpr int kTopReg = 4096 / kSideThreads;   // bp <= 4096 on this path
+    uint64_t topv[kTopReg];   // L <- top (they may overlap: read all, barrier, write)
+#pragma unroll
+    for (int u = 0; u < kTopReg; ++u) {
+        const int b = threadIdx.x + u * T;
+        topv[u] = b < bp ? top[b] : ~0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kTopReg; ++u) {
+        const int b = threadIdx.x + u * T;
+        if (b < bp) L[b] = topv[u];
+    }
     if (rec_smem)
         for (int b = threadIdx.x; b < bp; b += T) srec[b] = crec[b];
-    for (int b = threadIdx.x; b < bp; b += T) L[b] = pre->cand[b];
     for (int i = threadIdx.x; i < n; i += T) { slot_of[i] = -1; cand_of[i] = -1; }
     __syncthreads();
     for (int b = threadIdx.x; b < bp; b += T) {
@@ -358,32 +421,34 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
     __syncthreads();
     const int need = s_expected;
     const unsigned long long t_start = gtimer();
-    for (;;) {
-        __syncthreads();               // everyone has finished with s_m / s_head
-        const int head = s_head;
-        if (head >= need) break;
+    int iter = 0;
+    for (;; ++iter) {
+        __syncthreads();               // everyone has finished with s_m / s_merged
+        if (s_merged >= need) break;
         if (waited_too_long(t_start)) {  // watchdog: never hang the GPU
             if (threadIdx.x == 0) atomicOr(&st.g->err, E_TIMEOUT);
             break;
         }
-        // published entries head .. head+m-1 (stop at the first unpublished one)
-        if (threadIdx.x == 0) s_m = bp;
-        __syncthreads();
-        for (int x = threadIdx.x; x < bp && head + x < need; x += T) {
+        // collect the slots published since the last pass: their keys (stored as ~key,
+        // 0 = not yet; release-stored after the record) -- one round trip per pass
+        for (int b = threadIdx.x; b < B; b += T) {
+            if (!((s_pend[b >> 5] >> (b & 31)) & 1u)) continue;
+            uint64_t v;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(fin_key + b) : "memory");
+            if (v == 0) continue;
+            nk[atomicAdd(&s_m, 1)] = ~v;
+            fin_key[b] = 0;   // consumed (the next step's verify starts after this kernel)
+            atomicAnd(&s_pend[b >> 5], ~(1u << (b & 31)));
+        }
+        if (threadIdx.x == 0 && !s_snap_ok) {   // verify CTAs' snapshot, polled alongside
             uint32_t v;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(pubq + 1 + head + x) : "memory");
-            if (v == 0) {
-                atomicMin(&s_m, x);
-            } else {
-                const SelRec r = fin[v - 1];
-                nk[x] = r.key;
-                if (rec_smem) brec[v - 1] = r;
-            }
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(snap) : "memory");
+            if (v >= snap_target) s_snap_ok = 1;
         }
         __syncthreads();
-        int m = s_m;
-        if (head + m > need) m = need - head;
-        if (m == 0 || (m < 32 && head + m < need)) {   // merge in batches of >= 32, or the last ones
+        const int m = s_m;
+        SITER(iter, m, s_merged);
+        if (m == 0 || (m < 32 && s_merged + m < need)) {   // merge in batches of >= 32, or the last ones
             __nanosleep(100);
             continue;
         }
@@ -406,15 +471,15 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
         }
         __syncthreads();
         for (int o = threadIdx.x; o < bp; o += T) L[o] = L2[o];
-        for (int x = threadIdx.x; x < m; x += T) pubq[1 + head + x] = 0;   // consumed
         __syncthreads();
-        if (threadIdx.x == 0) s_head = head + m;
+        if (threadIdx.x == 0) { s_merged += m; s_m = 0; }
     }
+    SSTEP(2);
     // every verify CTA has read what it needs of sel[] / desc[] (usually long ago): only
     // now may the commit overwrite them
     if (snap && threadIdx.x == 0) {
         const unsigned long long t0 = gtimer();
-        for (;;) {
+        while (!s_snap_ok) {
             uint32_t v;
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(snap) : "memory");
             if (v >= snap_target) break;
@@ -423,8 +488,20 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
         }
         *snap = 0;
     }
+    // the verified slots' records (their keys were merged above): one parallel round trip
+    if (rec_smem)
+        for (int b = threadIdx.x; b < B; b += T) brec[b] = fin[b];
     __syncthreads();
+#ifdef LAPSSD_TRACE
+    for (int b = threadIdx.x; b < B && b < 16; b += T) {
+        g_dbg_rec[b][0] = brec[b].key;
+        g_dbg_rec[b][1] = ((uint64_t)(uint32_t)brec[b].desc.i << 32) | (uint32_t)brec[b].desc.r;
+        g_dbg_rec[b][2] = (uint64_t)(uint32_t)sel[b];
+        g_dbg_rec[b][3] = L[b];
+    }
+#endif
     ITRACE(100000);
+    SSTEP(3);
     // ---------------- commit
     int valid = 0;
     for (int b = threadIdx.x; b < B; b += T) valid += (L[b] >> 63) == 0;
@@ -481,18 +558,19 @@ __global__ void __launch_bounds__(kSelThreads) select_side_kernel(const State st
         st.g->prev_count = cnt;
         st.g->count = cnt;
         if (count_out) *count_out = cnt;
-        pubq[0] = 0;
+        st.g->vstep = st.g->vstep + 1;   // the next verify launch streams into the other set
     }
     __syncthreads();
     ITRACE(100003);
     STRACE(9);
 #ifdef LAPSSD_TRACE
+    if (threadIdx.x == 0) g_sstep_t[vstep0 & 63][4] = gtimer();
     if (threadIdx.x == 0) { unsigned c = atomicAdd(&g_scount, 1u); if (c < 64) g_send[c] = gtimer(); }
 #endif
 }
 
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
-                               int32_t B, PreSelect *pre, const SelRec *fin, uint32_t *pubq, uint32_t *snap,
+                               int32_t B, PreSelect *pre, const SelRec *fin, uint64_t *fin_key, uint32_t *snap,
                                uint32_t snap_target, int32_t *count_out, cudaStream_t s) {
     int np = 1, bp = 1;
     while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
@@ -500,7 +578,7 @@ cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &
     const size_t a = (size_t)(np + 2 * bp) * sizeof(uint64_t);
     const size_t b = (size_t)4 * bp * sizeof(uint64_t) + 2 * (size_t)((sc.n + 7) & ~7) * sizeof(int16_t) + 64 +
                      (bp <= 1024 ? 2 * (size_t)bp * sizeof(SelRec) : 0);
-    select_side_kernel<<<1, kSelThreads, a > b ? a : b, s>>>(st, sc, rw, sel, desc, B, pre, fin, pubq, snap,
+    select_side_kernel<<<1, kSideThreads, a > b ? a : b, s>>>(st, sc, rw, sel, desc, B, pre, fin, fin_key, snap,
                                                               snap_target, count_out);
     count_launch();
     return cudaGetLastError();

@@ -9,6 +9,7 @@
 namespace lapssd {
 
 constexpr int kSelThreads = 1024;
+constexpr int kSideThreads = 1024;     // side-stream select (measured: 512 is slower)
 constexpr int kSortCap = 16384;          // keys per CTA (bitonic in place above kMergeCap)
 constexpr int kMergeCap = 8192;          // keys sorted by warp-sort + merge-path (2 buffers)
 
@@ -153,7 +154,12 @@ __device__ inline void block_sort_reg(uint64_t *s, int n) {
 }
 
 // Sorts n (power of two) keys; returns the buffer holding the result (a or b).
-__device__ inline uint64_t *block_sort(uint64_t *a, uint64_t *b, int n) {
+#ifdef LAPSSD_SIDE_NOINLINE
+__device__ __noinline__
+#else
+__device__ inline
+#endif
+uint64_t *block_sort(uint64_t *a, uint64_t *b, int n) {
     if (n < 64 || n > kMergeCap || b == nullptr) {
         bitonic_sort(a, n);
         return a;
@@ -197,7 +203,12 @@ __device__ inline uint64_t *block_sort(uint64_t *a, uint64_t *b, int n) {
 // UINT64_MAX padding); tmp is bp words of scratch.  MSB-first radix select finds the
 // B-th smallest key T with eight 256-bin histogram passes (keys are unique: the id is
 // in the low bits), then the keys <= T are compacted and only they are sorted.
-__device__ inline uint64_t *select_topB(const uint64_t *keys, int n, int B, uint64_t *out, uint64_t *tmp, int bp) {
+#ifdef LAPSSD_SIDE_NOINLINE
+__device__ __noinline__
+#else
+__device__ inline
+#endif
+uint64_t *select_topB(const uint64_t *keys, int n, int B, uint64_t *out, uint64_t *tmp, int bp) {
     __shared__ int hist[256];
     __shared__ uint64_t s_prefix, s_mask;
     __shared__ int s_remaining, s_done;
@@ -210,9 +221,18 @@ __device__ inline uint64_t *select_topB(const uint64_t *keys, int n, int B, uint
         __syncthreads();
         if (s_done) break;
         const uint64_t prefix = s_prefix, mask = s_mask;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint64_t key = keys[i];
-            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1);
+        // keys share their high bytes (flags, level, a zero estimate field), so most land
+        // in one bin: aggregate equal bins across the warp first (one atomic per bin per
+        // warp instead of one per key)
+        const int n32 = (n + 31) & ~31;
+        for (int i = threadIdx.x; i < n32; i += blockDim.x) {
+            int bin = 256;  // no bin: out of range or outside the prefix
+            if (i < n) {
+                const uint64_t key = keys[i];
+                if ((key & mask) == prefix) bin = (int)((key >> shift) & 255);
+            }
+            const unsigned peers = __match_any_sync(__activemask(), bin);
+            if (bin < 256 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
         }
         __syncthreads();
         if (threadIdx.x < 32) {

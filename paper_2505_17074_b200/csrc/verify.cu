@@ -1,19 +1,17 @@
 // verify.cu -- batched speculative verification by rejection sampling on sm_100a
 // (Eq. 1, bonus token P:200; AMB-1, 2, 20, 21, 27).
 //
-// a1 (accept_kernel, or fused into the tail of select/merge): one thread per slot
-//    gathers p_j(x_j), q_j(x_j) for the k drafts (independent loads) and applies the
-//    exact fp64 test u24*q < p*2^24 with Philox uniforms -> r, in a 32-byte SlotDesc.
-// a2 (verify_kernel): grid (ceil(n_chunks / cpb), B), 256 threads.  Every thread
-//    reads the slot's descriptor with one broadcast load and immediately streams the
-//    ONE row pair the algorithm needs -- (p_r, q_r), or p_k on full acceptance -- over
-//    its cpb vocabulary chunks of 8192 entries with 128-bit L1::no_allocate loads,
-//    reducing the exact Q4.60 residual mass R_v = floor(max(0, fl32(p-q)) * 2^60)
-//    to one uint64 per (chunk, warp) (integer sums: exact, order-independent).  The
-//    last CTA of the slot (threadfence + atomic ticket) totals Z, draws
-//    t = floor(U Z / 2^64), finds the (chunk, warp) segment holding t from the stored
-//    sums, rescans that one 1024-entry segment (L2-hot) with a warp inclusive scan,
-//    emits y, and -- in laps_step -- runs the state update of that request (a3).
+// a1 (accept_kernel, or memoised by the select / the previous step's update): one
+//    thread per slot gathers p_j(x_j), q_j(x_j) for the k drafts (independent loads)
+//    and applies the exact fp64 test u24*q < p*2^24 with Philox uniforms -> r, in a
+//    32-byte SlotDesc.
+// a2 (+a3) (verify_kernel): persistent, TMA-fed, one CTA per SM; streams the ONE row
+//    pair the algorithm needs -- (p_r, q_r), or p_k on full acceptance -- in 32 KB
+//    chunks, reducing the exact Q4.60 residual mass R_v = floor(max(0, fl32(p-q)) * 2^60)
+//    to one uint64 per 1024-entry segment (integer sums: exact, order-independent);
+//    the finisher of each slot totals Z, draws t = floor(U Z / 2^64), finds the segment
+//    holding t, rescans it with warp scans and emits y.  The state update of the slot's
+//    request runs first, at kernel start, since it depends on r only.
 // HBM bytes per slot: 2 V s (r < k) or V s (r = k), plus k gathered scalars.
 #include <cstdlib>
 
@@ -162,20 +160,20 @@ cudaError_t launch_accept(const RowsDev &rw, const int32_t *sel, const State *st
 }
 
 // ---------------------------------------------------------------- a2: verify kernel
-// Persistent, warp-specialised, TMA-fed; one CTA per SM.  CTA = 8 consumer warps +
-// 1 producer warp + 1 finisher warp.  Work item n = (slot b = n / n_chunks, chunk
-// c = n % n_chunks); a CTA takes items blockIdx.x, blockIdx.x + gridDim.x, ...
-//  producer: loads the descriptors of its next 32 items (one per lane), then issues
-//            cp.async.bulk of chunk c of p_r (and q_r when r < k) into a ring of
-//            shared-memory stages, completion tracked by mbarrier tx-count.
-//  consumers: each warp reduces its 1024-entry segment of the stage to one uint64 and
-//            publishes it with bit 63 as a ready flag (relaxed store); it then frees the
-//            stage (empty barrier counts 8 warp arrivals).  No block-wide barrier, no
-//            fence and no atomic on the streaming path.
-//  finisher: for every slot whose designated chunk (b % n_chunks) this CTA consumed, polls until all
-//            n_chunks*8 warp sums carry the flag, then totals, samples, emits, runs
-//            the state update, and computes that request's next-round acceptance test
-//            (cached for the next select).  Off the streaming path.
+// Persistent, warp-specialised, TMA-fed; one CTA per SM.  CTA = 1 producer warp + 16
+// consumer warps + 2 finisher warps.  Work item n = (slot b = n / n_chunks, chunk
+// c = n % n_chunks), claimed dynamically (first n = blockIdx.x, then tickets).
+//  snapshot: (slab, r) of every slot and the descriptors of the finishers' slots are
+//            copied to shared memory first; then the side select may commit the next
+//            batch over desc[] / sel[].
+//  producer: issues cp.async.bulk of chunk c of p_r (and q_r when r < k) into a ring
+//            of shared-memory stages, completion tracked by mbarrier tx-count.
+//  consumers: warp w reduces segment w of the stage to one uint64 and publishes it
+//            with bit 63 as a ready flag (relaxed store); it then frees the stage.  No
+//            block-wide barrier, no fence and no atomic on the streaming path.
+//  finishers: slot b belongs to finisher b mod (2 grid).  First the state updates of
+//            their slots (+ next-round a1, select record, release-stored tag), then,
+//            per slot, wait for all n_chunks*16 ready words, total, sample, emit.
 #ifdef LAPSSD_TRACE
 #ifndef LAPSSD_TRACE_A
 #define LAPSSD_TRACE_A 0
@@ -236,6 +234,23 @@ extern "C" int lapssd_slot_trace_read(unsigned long long *out) {
     return 0;
 }
 #define SLOT_TIME(w, b) do { if ((b) < 4096) g_slot_t[w][b] = gtimer(); } while (0)
+__device__ unsigned long long g_vstep_t[64][2];   // per committed step: first CTA start, last CTA end
+__device__ unsigned long long g_vstep_sm[64][3];  // per committed step: SMs the verify CTAs ran on
+extern "C" int lapssd_vstep_sm_read(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_vstep_sm, sizeof g_vstep_sm);
+    static unsigned long long zero[64][3];
+    cudaMemcpyToSymbol(g_vstep_sm, zero, sizeof zero);
+    return 0;
+}
+extern "C" int lapssd_vstep_trace_read(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_vstep_t, sizeof g_vstep_t);
+    static unsigned long long init[64][2];
+    for (int i = 0; i < 64; ++i) { init[i][0] = ~0ull; init[i][1] = 0; }
+    cudaMemcpyToSymbol(g_vstep_t, init, sizeof init);
+    return 0;
+}
+#define VSTEP_TIME(w, v) do { if ((w) == 0) atomicMin(&g_vstep_t[(v) & 63][0], gtimer()); \
+                              else atomicMax(&g_vstep_t[(v) & 63][1], gtimer()); } while (0)
 extern "C" int lapssd_trace_read(unsigned long long *out) {
     cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
     cudaMemset(nullptr, 0, 0);
@@ -249,6 +264,7 @@ extern "C" int lapssd_trace_read(unsigned long long *out) {
 #define CTA_TIME(w)
 #define CTA_BYTES(n)
 #define SLOT_TIME(w, b)
+#define VSTEP_TIME(w, v)
 #endif
 constexpr int kConsumerWarps = 16;                         // all consume every item (one segment each)
 constexpr int kGroups = 2;                                 // finisher warps per CTA
@@ -334,30 +350,38 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *addr) {
 // issued at the start of the finish and overlap the sampling.
 struct NextA1 {
     int64_t slab;
+    int32_t x;
     float pj, qj;
     bool live;
 };
-template <bool BF16>
-__device__ __forceinline__ NextA1 next_a1_load(const VerifyArgs &a, int32_t i, uint32_t round_next) {
-    const int lane = threadIdx.x & 31;
+// The chain in three stages (slab table -> draft -> gathers) so that the stages of
+// several slots can be issued together: one memory round trip per stage, not per slot.
+__device__ __forceinline__ NextA1 next_a1_stage1(const VerifyArgs &a, int32_t i, uint32_t round_next) {
     const RowsDev &rw = a.rows;
     NextA1 n;
     n.live = a.fuse_update && rw.slab_tab != nullptr && i >= 0;
     n.slab = 0;
+    n.x = 0;
     n.pj = 1.0f;
     n.qj = 0.0f;
-    if (!n.live) return n;
-    n.slab = rw.slab_tab[(int64_t)i * rw.R + slab_round_index((int32_t)round_next, rw.R)];
-    const int k = rw.k;
-    if (lane < k) {
-        const int64_t V = rw.V;
-        const int32_t x = rw.draft[n.slab * k + lane];
-        const char *pb = (const char *)rw.p + n.slab * (int64_t)(k + 1) * V * Elt<BF16>::kEsz;
-        const char *qb = (const char *)rw.q + n.slab * (int64_t)k * V * Elt<BF16>::kEsz;
-        n.pj = BF16 ? load_prob_bf16(pb, (int64_t)lane * V + x) : load_prob_f32(pb, (int64_t)lane * V + x);
-        n.qj = BF16 ? load_prob_bf16(qb, (int64_t)lane * V + x) : load_prob_f32(qb, (int64_t)lane * V + x);
-    }
+    if (n.live) n.slab = rw.slab_tab[(int64_t)i * rw.R + slab_round_index((int32_t)round_next, rw.R)];
     return n;
+}
+__device__ __forceinline__ void next_a1_stage2(const VerifyArgs &a, NextA1 &n) {
+    const int lane = threadIdx.x & 31;
+    if (n.live && lane < a.rows.k) n.x = a.rows.draft[n.slab * a.rows.k + lane];
+}
+template <bool BF16>
+__device__ __forceinline__ void next_a1_stage3(const VerifyArgs &a, NextA1 &n) {
+    const int lane = threadIdx.x & 31;
+    const RowsDev &rw = a.rows;
+    const int k = rw.k;
+    if (!n.live || lane >= k) return;
+    const int64_t V = rw.V;
+    const char *pb = (const char *)rw.p + n.slab * (int64_t)(k + 1) * V * Elt<BF16>::kEsz;
+    const char *qb = (const char *)rw.q + n.slab * (int64_t)k * V * Elt<BF16>::kEsz;
+    n.pj = BF16 ? load_prob_bf16(pb, (int64_t)lane * V + n.x) : load_prob_f32(pb, (int64_t)lane * V + n.x);
+    n.qj = BF16 ? load_prob_bf16(qb, (int64_t)lane * V + n.x) : load_prob_f32(qb, (int64_t)lane * V + n.x);
 }
 __device__ __forceinline__ int next_a1_store(const VerifyArgs &a, int32_t i, uint32_t req, uint32_t round_next,
                                              const NextA1 &n) {
@@ -394,7 +418,7 @@ __device__ __forceinline__ void update_slot_warp(const VerifyArgs &a, int b, con
     const UpdOut uo = update_warp(a.st, a.sc, d.i, d.r, now, upd, lane);
     if (lane == 0) TRACE(13, b);
     const int r_next = next_a1_store(a, d.i, d.req, d.round + 1, nxt);  // harmless if it completed
-    if (a.pubq && lane == 0) {
+    if (a.fin_key && lane == 0) {
         // the request's record for the select: new key and next-round descriptor
         SelRec rec;
         rec.key = build_key(a.sc, d.i, INT32_MAX, uo.fl, upd.Lp, uo.tok, uo.A);
@@ -408,10 +432,9 @@ __device__ __forceinline__ void update_slot_warp(const VerifyArgs &a, int b, con
         rec.desc.pad[0] = rec.desc.pad[1] = rec.desc.pad[2] = 0;
         a.fin[b] = rec;
         a.st.key[d.i] = rec.key;
-        __threadfence();
-        const uint32_t slot = atomicAdd(a.pubq, 1u);  // publish: the merger may take it now
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.pubq + 1 + slot), "r"((uint32_t)b + 1u)
-                     : "memory");
+        // publish the key (release: orders the record before it; nothing waits on it
+        // here).  Stored inverted so 0 means "not yet": no key is all ones (ids < 2^24-1)
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.fin_key + b), "l"(~rec.key) : "memory");
         SLOT_TIME(1, b);
     }
     __syncwarp();
@@ -421,8 +444,8 @@ __device__ __forceinline__ void update_slot_warp(const VerifyArgs &a, int b, con
 // total Z, draw t, locate (chunk, segment), rescan that segment in vocabulary order,
 // emit.  P:64, AMB-20.  w[h * kSegs + s] = sum of segment s of chunk lane + 32 h.
 template <bool BF16>
-__device__ __forceinline__ void sample_slot_warp(const VerifyArgs &a, int b, const SlotDesc &d, uint64_t *fb,
-                                                 uint64_t (&w)[kPartWords]) {
+__device__ __forceinline__ void sample_slot_warp(const VerifyArgs &a, uint64_t *part_set, int b, const SlotDesc &d,
+                                                 uint64_t *fb, uint64_t (&w)[kPartWords]) {
     using E = Elt<BF16>;
     using S = Seg<BF16>;
     using TC = VerifyCfg<BF16>;
@@ -433,7 +456,7 @@ __device__ __forceinline__ void sample_slot_warp(const VerifyArgs &a, int b, con
     const bool use_q = r < k;
     const char *prow = (const char *)a.rows.p + ((int64_t)d.slab * (k + 1) + r) * V * E::kEsz;
     const char *qrow = (const char *)a.rows.q + ((int64_t)d.slab * k + (use_q ? r : 0)) * V * E::kEsz;
-    const uint64_t *part = a.part + (int64_t)b * nc * kPartWords;
+    uint64_t *part = part_set + (int64_t)b * nc * kPartWords;
     // chunk sums: cs0 for chunk lane, cs1 for chunk lane + 32 (fp32 tiling only)
     uint64_t cs0 = 0, cs1 = 0;
 #pragma unroll
@@ -537,7 +560,7 @@ __device__ __forceinline__ void sample_slot_warp(const VerifyArgs &a, int b, con
         if (lane <= k) tok[lane] = lane < r ? dr[lane] : lane == r ? y : -1;
     }
     for (int x = lane; x < nc * kPartWords; x += 32)  // unpublish for the next launch / replay
-        st_relaxed(const_cast<uint64_t *>(part) + x, 0ull);
+        st_relaxed(part + x, 0ull);
     if (lane == 0) {
         if (a.n_accept) a.n_accept[b] = r;
         if (a.z) a.z[b] = Z;
@@ -577,7 +600,23 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
 #ifdef LAPSSD_TRACE
     if (tid == 0 && blockIdx.x == 0) { unsigned c = atomicAdd(&g_vcount, 1u); if (c < 64) g_vstart[c] = gtimer(); }
 #endif
+    // the next step's launch may start on SMs as ours retire (programmatic dependent
+    // launch): it uses the other (part, work) set, and its finishers wait for this grid
+    // before touching outputs.  The set is picked by the committed-step parity.
+    const uint32_t vstep = a.vstep ? *a.vstep : 0u;
+    const int par = (int)(vstep & 1u);
+    if (tid == 0) VSTEP_TIME(0, vstep);
+#ifdef LAPSSD_TRACE
     if (tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        atomicOr(&g_vstep_sm[vstep & 63][smid >> 6], 1ull << (smid & 63));
+    }
+#endif
+    uint64_t *const part = par ? a.part1 : a.part;
+    uint32_t *const work = par ? a.work1 : a.work;
+    if (tid == 0) {
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumerWarps);
@@ -626,7 +665,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
             const int kk = a.rows.k;
             const int64_t V = a.rows.V;
             int n = (int)blockIdx.x;
-            uint32_t nxt = (uint32_t)grid + atomicAdd(a.work, 1u);
+            uint32_t nxt = (uint32_t)grid + atomicAdd(work, 1u);
             for (int k = 0;; ++k) {
                 const int st = k % kStages;
                 TRACE(1, k & 1023);
@@ -639,7 +678,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                 }
                 const int cur = n;
                 n = nxt < (uint32_t)n_items ? (int)nxt : n_items;
-                if (n < n_items) nxt = (uint32_t)grid + atomicAdd(a.work, 1u);
+                if (n < n_items) nxt = (uint32_t)grid + atomicAdd(work, 1u);
                 s_stage[st] = cur;
                 const uint32_t it = s_slot[cur / nc];
                 if (it == 0) {
@@ -666,9 +705,9 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                 CTA_TIME(2);
             }
             // retire: the last CTA to stop claiming leaves the counters zero for the next launch
-            if (atomicAdd(a.work + 1, 1u) == (uint32_t)grid - 1) {
-                a.work[0] = 0;
-                a.work[1] = 0;
+            if (atomicAdd(work + 1, 1u) == (uint32_t)grid - 1) {
+                work[0] = 0;
+                work[1] = 0;
             }
         }
         __syncwarp();
@@ -677,7 +716,8 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
         const int f0 = grp * grid + (int)blockIdx.x;
         const int nf = fin_slots(B, grid, f0);
         if (a.fuse_update) {
-            // the state updates first, two slots at a time (both slots' loads in flight)
+            // the state updates first, two slots at a time: each stage of both slots' loads
+            // (state + slab table, drafts, gathers) is one round trip
             const int64_t now = a.st.g->now_us;
             for (int j = 0; j < nf; j += 2) {
                 const SlotDesc d0 = s_fin[grp][j];
@@ -687,8 +727,12 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                 UpdIn u0{}, u1{};
                 if (l0) u0 = load_update_inputs(a.st, a.sc, d0.i, lane);
                 if (l1) u1 = load_update_inputs(a.st, a.sc, d1.i, lane);
-                const NextA1 x0 = next_a1_load<BF16>(a, l0 ? d0.i : -1, d0.round + 1);
-                const NextA1 x1 = next_a1_load<BF16>(a, l1 ? d1.i : -1, d1.round + 1);
+                NextA1 x0 = next_a1_stage1(a, l0 ? d0.i : -1, d0.round + 1);
+                NextA1 x1 = next_a1_stage1(a, l1 ? d1.i : -1, d1.round + 1);
+                next_a1_stage2(a, x0);
+                next_a1_stage2(a, x1);
+                next_a1_stage3<BF16>(a, x0);
+                next_a1_stage3<BF16>(a, x1);
                 if (l0) update_slot_warp<BF16>(a, f0 + j * kGroups * grid, d0, u0, now, x0);
                 if (l1) update_slot_warp<BF16>(a, f0 + (j + 1) * kGroups * grid, d1, u1, now, x1);
             }
@@ -696,12 +740,15 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
 #if defined(LAPSSD_DIAG) && (LAPSSD_DIAG & 2)
         if (nf >= 0) return;  // diagnostic build: no sampling
 #endif
+        // outputs (tokens, n_accept, z) and the part words of the previous step's slots are
+        // only touched once the previous launch has completed
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int j = 0; j < nf; ++j) {
             const SlotDesc d = s_fin[grp][j];
             if (d.r < 0) continue;
             const int b = f0 + j * kGroups * grid;
             if (lane == 0) TRACE(5, b);
-            const uint64_t *pw = a.part + (int64_t)b * nc * kPartWords;
+            const uint64_t *pw = part + (int64_t)b * nc * kPartWords;
             uint64_t w[kPartWords];
             const unsigned long long t_start = gtimer();
             for (;;) {  // every (chunk, segment) sum of slot b published?
@@ -722,7 +769,12 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
             }
             if (lane == 0) TRACE(6, b);
             if (lane == 0) CTA_TIME(4);
-            sample_slot_warp<BF16>(a, b, d, s_fb[grp], w);
+#if defined(LAPSSD_DIAG) && (LAPSSD_DIAG & 4)
+            for (int x = lane; x < nc * kPartWords; x += 32)  // diagnostic build: poll, no draw
+                st_relaxed(part + (int64_t)b * nc * kPartWords + x, 0ull);
+#else
+            sample_slot_warp<BF16>(a, part, b, d, s_fb[grp], w);
+#endif
             if (lane == 0) TRACE(7, b);
             if (lane == 0) CTA_TIME(8);
             if (lane == 0) SLOT_TIME(2, b);
@@ -772,7 +824,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                     }
 #endif
                     m = warp_sum_u64(m);
-                    if (lane == 0) st_relaxed(&a.part[((int64_t)b * nc + c) * kPartWords + seg], m | kReady);
+                    if (lane == 0) st_relaxed(&part[((int64_t)b * nc + c) * kPartWords + seg], m | kReady);
                 }
             }
             __syncwarp();
@@ -782,6 +834,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
         }
     }
     if (tid == 0) CTA_TIME(1);
+    if (lane == 0) VSTEP_TIME(1, vstep);
 }
 
 int verify_cpb(int64_t V) {
@@ -833,7 +886,7 @@ int verify_max_batch(int32_t n_chunks, int32_t reserve_sms) {
 }
 
 template <bool BF16>
-static cudaError_t launch_verify_t(const VerifyArgs &a, int32_t B, int32_t reserve_sms, cudaStream_t s) {
+static cudaError_t launch_verify_t(const VerifyArgs &a, int32_t B, int32_t reserve_sms, bool pdl, cudaStream_t s) {
     const size_t smem = (size_t)VerifyCfg<BF16>::kStages * 2 * kTileBytes;
     // Finishers wait on other CTAs' chunks, so all CTAs must be resident together: each
     // CTA needs an SM's shared memory (one CTA per SM) and the grid is at most the SM
@@ -845,19 +898,24 @@ static cudaError_t launch_verify_t(const VerifyArgs &a, int32_t B, int32_t reser
     cfg.blockDim = dim3(kVerifyThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cfg.attrs = nullptr;
-    cfg.numAttrs = 0;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? attr : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, verify_kernel<BF16>, a, B);
 }
 
-cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_sms, cudaStream_t s) {
+cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_sms, bool pdl, cudaStream_t s) {
     if (B <= 0) return cudaSuccess;
     if (!verify_fits(B, a.n_chunks, reserve_sms)) return cudaErrorInvalidValue;  // callers split / validate
     count_launch();
-    return a.rows.dtype == LAPSSD_BF16 ? launch_verify_t<true>(a, B, reserve_sms, s)
-                                       : launch_verify_t<false>(a, B, reserve_sms, s);
+    return a.rows.dtype == LAPSSD_BF16 ? launch_verify_t<true>(a, B, reserve_sms, pdl, s)
+                                       : launch_verify_t<false>(a, B, reserve_sms, pdl, s);
 }
 
-cudaError_t launch_verify(const VerifyArgs &a, int32_t B, cudaStream_t s) { return launch_verify_grid(a, B, 0, s); }
+cudaError_t launch_verify(const VerifyArgs &a, int32_t B, cudaStream_t s) {
+    return launch_verify_grid(a, B, 0, false, s);
+}
 
 }  // namespace lapssd

@@ -50,6 +50,14 @@ int main() {
     std::vector<uint64_t> h(N);
     srand(1);
     for (int i = 0; i < N; ++i) h[i] = ((uint64_t)rand() << 40) ^ ((uint64_t)rand() << 20) ^ (uint64_t)i;
+    if (getenv("REALISTIC")) {  // priority-key shaped: shared high bytes, 24-bit ids in the low bits
+        for (int i = 0; i < N; ++i) {
+            const uint64_t level = (uint64_t)(rand() % 3), perc = (uint64_t)(rand() % 4 == 0);
+            const uint64_t est = perc ? (uint64_t)(rand() % 400000) : 0;
+            h[i] = (1ull << 62) | (level << 58) | ((1 - perc) << 57) | (1ull << 56) | (est << 24) | (uint64_t)(i * 8 + 3);
+        }
+        printf("realistic keys\n");
+    }
     uint64_t *din, *dout;
     long long *dc, hc[3];
     cudaMalloc(&din, N * 8); cudaMalloc(&dout, N * 8); cudaMalloc(&dc, 64);
