@@ -258,6 +258,46 @@ lapssd_status lapssd_profile_read(lapssd_handle *h, double *verify_ms, double *s
 /* presort_ms: summed time from the step's start to the end of the side-stream presort
  * (it overlaps the verify kernel; if it exceeds verify_ms the select waits for it). */
 
+/* ---------------------------------------------------------------------------
+ * Monte-Carlo replicas (SURVEY §8(d) configs[4]; §8(a) a6 "per-trace top-1").
+ * T independent traces, each a simulation of its own requests with its own clock and
+ * ONE request served at a time (batch 1).  One laps_mc_step advances every trace
+ * by one round: verify the request it runs (a1-a2, Philox c3 = the trace index t), its
+ * state update (a3), the trace clock (+ c_round after a round, next arrival when idle,
+ * P:84-93), admission, keys and the trace's top-1, x_i / pinning.
+ * Per trace the result is exactly that of a single-trace handle (and the oracle) with
+ * B = 1 and trace index t; traces share only the slab pool.
+ *
+ * trace_offsets [host, n_traces+1]: trace t owns requests [off[t], off[t+1]) of the
+ *   concatenated arrays; off[0] = 0; arrival_us sorted within each trace; local
+ *   request ids (their index within the trace, < 2^24 - 1) are the Philox c0 and the
+ *   key id.  Requests of one trace may not exceed 2^24 - 2; the total is < 2^31.
+ * rows: pooled layout only; slab_tab is indexed by the GLOBAL request index
+ *   (off[t] + local), n_total x R.
+ * laps_mc_select: the first selection of every trace (no verification).
+ * laps_mc_step: tokens_out [device, T*(k+1)] and n_accept_out [device, T] (nullable:
+ *   internal buffers) receive trace t's emitted tokens and r in slot t (r = -1, tokens
+ *   untouched for an idle trace); active_out [device int32, nullable] = the number of
+ *   traces that selected a request for the next step (0: every trace has finished).
+ * lapssd_mc_read: D2H snapshot; the view's arrays hold n_total entries (its now_us /
+ *   cursor / prev_count fields are unused), now_us / cursor / sel [host, T] per trace
+ *   (sel = local index of the request the trace runs next, or -1).  Synchronises.
+ * Errors: EINVAL (config, offsets, ids, unsorted arrivals, rows), ENOMEM, ECUDA;
+ *   lapssd_mc_check reports device contract violations as LAPSSD_ESTATE. */
+typedef struct lapssd_mc lapssd_mc;
+size_t lapssd_mc_workspace_bytes(const lapssd_config *cfg, int32_t n_traces, int64_t n_total, int64_t V);
+lapssd_status lapssd_mc_create(const lapssd_config *cfg, int32_t n_traces, const int64_t *trace_offsets,
+                               const int64_t *arrival_us, const int32_t *L_true, const int32_t *L_pred,
+                               int64_t V, void *workspace, size_t workspace_bytes, lapssd_stream stream,
+                               lapssd_mc **out);
+lapssd_status lapssd_mc_destroy(lapssd_mc *h);
+lapssd_status laps_mc_select(lapssd_mc *h, const lapssd_rows *rows, lapssd_stream stream);
+lapssd_status laps_mc_step(lapssd_mc *h, const lapssd_rows *rows, int32_t *tokens_out,
+                           int32_t *n_accept_out, int32_t *active_out, lapssd_stream stream);
+lapssd_status lapssd_mc_read(lapssd_mc *h, lapssd_state_view *view, int64_t *now_us, int32_t *cursor,
+                             int32_t *sel, lapssd_stream stream);
+lapssd_status lapssd_mc_check(lapssd_mc *h, uint32_t *flags_out);
+
 /* Thread-local text of the last error ("" if none). */
 const char *lapssd_last_error(void);
 

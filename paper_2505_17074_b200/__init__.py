@@ -80,6 +80,13 @@ def _load():
         "lapssd_check": ([vp, vp], i32),
         "lapssd_profile": ([vp, i32], i32),
         "lapssd_profile_read": ([vp, vp, vp, vp, vp], i32),
+        "lapssd_mc_workspace_bytes": ([vp, i32, i64, i64], sz),
+        "lapssd_mc_create": ([vp, i32, vp, vp, vp, vp, i64, vp, sz, vp, vp], i32),
+        "lapssd_mc_destroy": ([vp], i32),
+        "laps_mc_select": ([vp, vp, vp], i32),
+        "laps_mc_step": ([vp, vp, vp, vp, vp, vp], i32),
+        "lapssd_mc_read": ([vp, vp, vp, vp, vp, vp], i32),
+        "lapssd_mc_check": ([vp, vp], i32),
         "lapssd_last_error": ([], C.c_char_p),
         "lapssd_launch_count": ([], u64),
     }
@@ -264,15 +271,7 @@ class Handle:
 
     # -- snapshot -----------------------------------------------------------------
     def state(self, stream=None) -> dict:
-        n, g = self.n, self.cfg.gamma
-        arrs = dict(acc_tok=np.zeros(n, np.int32), acc_draft=np.zeros(n, np.int32),
-                    rounds=np.zeros(n, np.int32), E_us=np.zeros(n, np.int64),
-                    T_total_us=np.zeros(n, np.int64), C_us=np.zeros(n, np.int64),
-                    x_us=np.zeros(n, np.int64), admitted=np.zeros(n, np.uint8),
-                    done=np.zeros(n, np.uint8), perceptible=np.zeros(n, np.uint8),
-                    pinned=np.zeros(n, np.uint8), level=np.zeros(n, np.uint8),
-                    running=np.zeros(n, np.uint8), A=np.zeros(n, np.float64),
-                    key=np.zeros(n, np.uint64), ring=np.zeros((n, g), np.int32))
+        arrs = _state_arrays(self.n, self.cfg.gamma)
         v = _StateView(0, 0, 0, *[arrs[f].ctypes.data for f, _ in _StateView._fields_[3:]])
         _check("lapssd_read_state", _lib.lapssd_read_state(self.h, C.byref(v), _stream(stream)))
         arrs.update(now_us=v.now_us, cursor=v.cursor, prev_count=v.prev_count)
@@ -293,6 +292,76 @@ class Handle:
         flags = C.c_uint32()
         rc = _lib.lapssd_check(self.h, C.byref(flags))
         _check("lapssd_check", rc)
+        return flags.value
+
+
+def _state_arrays(n, gamma):
+    return dict(acc_tok=np.zeros(n, np.int32), acc_draft=np.zeros(n, np.int32),
+                rounds=np.zeros(n, np.int32), E_us=np.zeros(n, np.int64),
+                T_total_us=np.zeros(n, np.int64), C_us=np.zeros(n, np.int64),
+                x_us=np.zeros(n, np.int64), admitted=np.zeros(n, np.uint8),
+                done=np.zeros(n, np.uint8), perceptible=np.zeros(n, np.uint8),
+                pinned=np.zeros(n, np.uint8), level=np.zeros(n, np.uint8),
+                running=np.zeros(n, np.uint8), A=np.zeros(n, np.float64),
+                key=np.zeros(n, np.uint64), ring=np.zeros((n, gamma), np.int32))
+
+
+# --------------------------------------------------------------------------- Monte-Carlo replicas
+class MCHandle:
+    """T independent traces, batch 1 each (lapssd_mc_create): configs[4]'s engine.
+    Requests are concatenated trace by trace; offsets[t]..offsets[t+1] belong to trace t."""
+
+    def __init__(self, cfg: SchedConfig, offsets, arrival_us, L_true, L_pred, *, V: int, device="cuda",
+                 stream=None):
+        self.cfg = cfg
+        self._cc = cfg.c()
+        off = np.ascontiguousarray(offsets, np.int64)
+        a = np.ascontiguousarray(arrival_us, np.int64)
+        lt = np.ascontiguousarray(L_true, np.int32)
+        lp = np.ascontiguousarray(L_pred, np.int32)
+        self.T, self.n, self.V = len(off) - 1, int(off[-1]), V
+        self.offsets = off
+        nbytes = int(_lib.lapssd_mc_workspace_bytes(C.byref(self._cc), self.T, self.n, V))
+        if nbytes == 0:
+            raise LapssdError("lapssd_mc_workspace_bytes", -1, "invalid sizes")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        h = C.c_void_p()
+        rc = _lib.lapssd_mc_create(C.byref(self._cc), self.T, off.ctypes.data, a.ctypes.data, lt.ctypes.data,
+                                   lp.ctypes.data, V, _dptr(self.workspace), nbytes, _stream(stream), C.byref(h))
+        _check("lapssd_mc_create", rc)
+        self.h = h
+        self.active = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.lapssd_mc_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def select(self, rows: Rows, stream=None):
+        _check("laps_mc_select", _lib.laps_mc_select(self.h, C.byref(rows.c), _stream(stream)))
+
+    def step(self, rows: Rows, tokens=None, n_accept=None, active=None, stream=None):
+        active = self.active if active is None else active
+        _check("laps_mc_step", _lib.laps_mc_step(self.h, C.byref(rows.c), _dptr(tokens), _dptr(n_accept),
+                                                 _dptr(active), _stream(stream)))
+        return active
+
+    def state(self, stream=None):
+        """(per-request state dict over all traces, now_us[T], cursor[T], sel[T])."""
+        arrs = _state_arrays(self.n, self.cfg.gamma)
+        v = _StateView(0, 0, 0, *[arrs[f].ctypes.data for f, _ in _StateView._fields_[3:]])
+        now = np.zeros(self.T, np.int64)
+        cur = np.zeros(self.T, np.int32)
+        sel = np.zeros(self.T, np.int32)
+        _check("lapssd_mc_read", _lib.lapssd_mc_read(self.h, C.byref(v), now.ctypes.data, cur.ctypes.data,
+                                                      sel.ctypes.data, _stream(stream)))
+        return arrs, now, cur, sel
+
+    def check(self):
+        flags = C.c_uint32()
+        _check("lapssd_mc_check", _lib.lapssd_mc_check(self.h, C.byref(flags)))
         return flags.value
 
 

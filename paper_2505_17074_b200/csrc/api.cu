@@ -114,10 +114,8 @@ struct lapssd_handle {
     }
 };
 
-static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma, int32_t max_batch,
-                         int32_t n_chunks, int32_t k) {
+static void carve_state(Carver &cv, State &st, int64_t n, int32_t gamma) {
     const size_t nn = (size_t)(n > 0 ? n : 1);
-    State &st = h->st;
     st.g = cv.take<Globals>(1);
     st.arrival = cv.take<int64_t>(nn);
     st.L_true = cv.take<int32_t>(nn);
@@ -135,6 +133,11 @@ static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma,
     st.x = cv.take<int64_t>(nn);
     st.next_tag = cv.take<uint64_t>(nn);
     st.next_sr = cv.take<int2>(nn);
+}
+
+static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma, int32_t max_batch,
+                         int32_t n_chunks, int32_t k) {
+    carve_state(cv, h->st, n, gamma);
     h->part = cv.take<uint64_t>(2 * (size_t)max_batch * n_chunks * kPartWords);  // two parity sets
     h->work = cv.take<uint32_t>(4);
     h->tokens = cv.take<int32_t>((size_t)max_batch * (k + 1));
@@ -161,6 +164,45 @@ static lapssd_status check_config(const lapssd_config *c) {
     if (c->placement < 0 || c->placement > 1 || c->pin_rule < 0 || c->pin_rule > 1)
         return fail(LAPSSD_EINVAL, "placement / pin_rule");
     return LAPSSD_OK;
+}
+
+static void fill_sched(Sched &sc, const lapssd_config *cfg, int32_t n, int32_t rank, int32_t world) {
+    sc = Sched{};
+    sc.policy = cfg->policy; sc.K = cfg->K; sc.gamma = cfg->gamma; sc.k = cfg->k;
+    sc.placement = cfg->placement; sc.pin_rule = cfg->pin_rule;
+    sc.n = n; sc.rank = rank; sc.world = world;
+    sc.delta = cfg->delta;
+    sc.t_ssm_us = cfg->t_ssm_us; sc.t_llm_us = cfg->t_llm_us;
+    sc.c_round_us = (int64_t)cfg->k * cfg->t_ssm_us + cfg->t_llm_us;   // S:194, Eq. 6 denominators
+    sc.seed = cfg->seed;
+    // P:169: S_j^up = M^(j-1) S_1^up; zero-based S_up[j] = floor(s1_up * M^j), M^j by
+    // iterative fp64 multiplication (AMB-11).
+    double m = 1.0;
+    for (int j = 0; j < 16; ++j) {
+        if (j < cfg->K - 1) {
+            const double v = (double)cfg->s1_up_us * m;
+            sc.S_up[j] = v >= 9.2e18 ? INT64_MAX : (int64_t)std::floor(v);
+            m = m * cfg->M;
+        } else {
+            sc.S_up[j] = INT64_MAX;
+        }
+    }
+}
+
+// Zero-fill a state workspace, all-ones for C / x / next_tag, copy the request arrays.
+static cudaError_t init_state(void *workspace, size_t bytes, const State &st, int64_t n, const int64_t *arrival,
+                              const int32_t *L_true, const int32_t *L_pred, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(workspace, 0, bytes, s);
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(st.C, 0xFF, (size_t)((char *)(st.next_tag + (n > 0 ? n : 1)) - (char *)st.C), s);
+    if (e == cudaSuccess && n > 0) {
+        e = cudaMemcpyAsync((void *)st.arrival, arrival, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync((void *)st.L_true, L_true, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync((void *)st.L_pred, L_pred, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s);
+    }
+    return e;
 }
 
 extern "C" {
@@ -285,42 +327,10 @@ lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req
     h->max_batch = max_batch;
     h->V = V;
     h->n_chunks = n_chunks_max(V);
-    Sched &sc = h->sc;
-    sc.policy = cfg->policy; sc.K = cfg->K; sc.gamma = cfg->gamma; sc.k = cfg->k;
-    sc.placement = cfg->placement; sc.pin_rule = cfg->pin_rule;
-    sc.n = req->n; sc.rank = req->rank; sc.world = req->world;
-    sc.delta = cfg->delta;
-    sc.t_ssm_us = cfg->t_ssm_us; sc.t_llm_us = cfg->t_llm_us;
-    sc.c_round_us = (int64_t)cfg->k * cfg->t_ssm_us + cfg->t_llm_us;   // S:194, Eq. 6 denominators
-    sc.seed = cfg->seed;
-    // P:169: S_j^up = M^(j-1) S_1^up; zero-based S_up[j] = floor(s1_up * M^j), M^j by
-    // iterative fp64 multiplication (AMB-11).
-    double m = 1.0;
-    for (int j = 0; j < 16; ++j) {
-        if (j < cfg->K - 1) {
-            const double s = (double)cfg->s1_up_us * m;
-            sc.S_up[j] = s >= 9.2e18 ? INT64_MAX : (int64_t)std::floor(s);
-            m = m * cfg->M;
-        } else {
-            sc.S_up[j] = INT64_MAX;
-        }
-    }
+    fill_sched(h->sc, cfg, req->n, req->rank, req->world);
     cudaStream_t s = (cudaStream_t)stream;
     h->last_stream = s;
-    cudaError_t e = cudaMemsetAsync(workspace, 0, need, s);
-    if (e == cudaSuccess)
-        e = cudaMemsetAsync(h->st.C, 0xFF, (size_t)((char *)(h->st.next_tag + (req->n > 0 ? req->n : 1)) -
-                                                   (char *)h->st.C), s);
-    if (e == cudaSuccess && req->n > 0) {
-        e = cudaMemcpyAsync((void *)h->st.arrival, req->arrival_us, sizeof(int64_t) * req->n,
-                            cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync((void *)h->st.L_true, req->L_true, sizeof(int32_t) * req->n,
-                                cudaMemcpyHostToDevice, s);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync((void *)h->st.L_pred, req->L_pred, sizeof(int32_t) * req->n,
-                                cudaMemcpyHostToDevice, s);
-    }
+    cudaError_t e = init_state(workspace, need, h->st, req->n, req->arrival_us, req->L_true, req->L_pred, s);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
@@ -681,6 +691,221 @@ lapssd_status lapssd_check(lapssd_handle *h, uint32_t *flags_out) {
     cudaError_t e = cudaStreamSynchronize(h->last_stream);
     if (e == cudaSuccess) e = cudaMemcpy(&g, h->st.g, sizeof g, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_status(e, "lapssd_check");
+    if (flags_out) *flags_out = g.err;
+    if (g.err) return fail(LAPSSD_ESTATE, "device contract violation flags 0x%x", g.err);
+    return LAPSSD_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- Monte-Carlo replicas
+
+struct lapssd_mc {
+    State st;
+    Sched sc;
+    McDev mc{};
+    SlotDesc *desc = nullptr;   // [T] a1 of each trace's selected request
+    int32_t *sel = nullptr, *n_accept = nullptr, *tokens = nullptr, *active = nullptr;
+    uint64_t *part = nullptr;   // verify scratch for one sub-launch
+    uint32_t *work = nullptr;
+    int32_t T = 0, bmax = 0;
+    int64_t n = 0, V = 0;
+    cudaStream_t last_stream = nullptr;
+};
+
+static void carve_mc(Carver &cv, lapssd_mc *h, int32_t T, int64_t n, int32_t gamma, int32_t k, int64_t V) {
+    carve_state(cv, h->st, n, gamma);
+    const size_t tt = (size_t)(T > 0 ? T : 1);
+    h->mc.g = cv.take<Globals>(tt);
+    h->mc.off = cv.take<int64_t>(tt + 1);
+    h->desc = cv.take<SlotDesc>(tt);
+    h->sel = cv.take<int32_t>(tt);
+    h->n_accept = cv.take<int32_t>(tt);
+    h->tokens = cv.take<int32_t>(tt * (size_t)(k + 1));
+    h->active = cv.take<int32_t>(1);
+    const int32_t nc = n_chunks_max(V);
+    const int32_t bmax = verify_max_batch(nc, 0);
+    const int32_t nb = T < bmax ? (T > 0 ? T : 1) : bmax;
+    h->part = cv.take<uint64_t>((size_t)nb * nc * kPartWords);
+    h->work = cv.take<uint32_t>(2);
+}
+
+extern "C" {
+
+size_t lapssd_mc_workspace_bytes(const lapssd_config *cfg, int32_t n_traces, int64_t n_total, int64_t V) {
+    if (!cfg || n_traces < 1 || n_total < 0 || V < 1) return 0;
+    prepare_all();   // the verify sub-launch size depends on the SM count
+    lapssd_mc tmp{};
+    Carver cv{nullptr};
+    carve_mc(cv, &tmp, n_traces, n_total, cfg->gamma > 0 ? cfg->gamma : 1, cfg->k > 0 ? cfg->k : 1, V);
+    return align256(cv.off);
+}
+
+lapssd_status lapssd_mc_create(const lapssd_config *cfg, int32_t n_traces, const int64_t *trace_offsets,
+                               const int64_t *arrival_us, const int32_t *L_true, const int32_t *L_pred, int64_t V,
+                               void *workspace, size_t workspace_bytes, lapssd_stream stream, lapssd_mc **out) {
+    g_last_error.clear();
+    if (!out) return fail(LAPSSD_EINVAL, "out is NULL");
+    *out = nullptr;
+    lapssd_status st = check_config(cfg);
+    if (st != LAPSSD_OK) return st;
+    if (n_traces < 1 || !trace_offsets) return fail(LAPSSD_EINVAL, "n_traces / trace_offsets");
+    if (trace_offsets[0] != 0) return fail(LAPSSD_EINVAL, "trace_offsets[0] must be 0");
+    const int64_t n = trace_offsets[n_traces];
+    if (n > ((int64_t)1 << 31) - 1) return fail(LAPSSD_EINVAL, "more than 2^31-1 requests");
+    if (n > 0 && (!arrival_us || !L_true || !L_pred)) return fail(LAPSSD_EINVAL, "requests: NULL arrays");
+    if (V < 1 || V > (int64_t)kMaxSegs * kSegElems) return fail(LAPSSD_EINVAL, "V out of range");
+    for (int32_t t = 0; t < n_traces; ++t) {
+        const int64_t a = trace_offsets[t], b = trace_offsets[t + 1];
+        if (b < a) return fail(LAPSSD_EINVAL, "trace_offsets not non-decreasing at %d", t);
+        if (b - a > (1 << 24) - 2) return fail(LAPSSD_EINVAL, "trace %d: local ids must be < 2^24 - 1", t);
+        for (int64_t i = a; i < b; ++i) {
+            if (L_true[i] < 1 || L_pred[i] < 1) return fail(LAPSSD_EINVAL, "L < 1 at %lld", (long long)i);
+            if (i > a && arrival_us[i] < arrival_us[i - 1])
+                return fail(LAPSSD_EINVAL, "trace %d: arrivals not sorted at %lld", t, (long long)i);
+        }
+    }
+    const size_t need = lapssd_mc_workspace_bytes(cfg, n_traces, n, V);
+    if (!workspace || workspace_bytes < need)
+        return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes, need);
+    prepare_all();
+    lapssd_mc *h = new lapssd_mc{};
+    Carver cv{(char *)workspace};
+    carve_mc(cv, h, n_traces, n, cfg->gamma, cfg->k, V);
+    h->T = n_traces;
+    h->n = n;
+    h->V = V;
+    h->bmax = verify_max_batch(n_chunks_max(V), 0);
+    h->mc.T = n_traces;
+    fill_sched(h->sc, cfg, 0, 0, 1);   // every trace is its own id space (world 1, local ids)
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last_stream = s;
+    cudaError_t e = init_state(workspace, need, h->st, n, arrival_us, L_true, L_pred, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync((void *)h->mc.off, trace_offsets, sizeof(int64_t) * (n_traces + 1),
+                            cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->sel, 0xFF, sizeof(int32_t) * n_traces, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_status(e, "lapssd_mc_create");
+    }
+    *out = h;
+    return LAPSSD_OK;
+}
+
+lapssd_status lapssd_mc_destroy(lapssd_mc *h) {
+    delete h;
+    return LAPSSD_OK;
+}
+
+lapssd_status laps_mc_select(lapssd_mc *h, const lapssd_rows *rows, lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || !rows || !rows->slab_tab || rows->k != h->sc.k || rows->R < 1)
+        return fail(LAPSSD_EINVAL, "handle / rows (pooled layout with slab_tab required)");
+    if (!rows_ok(rows->dtype, rows->V, rows->k, rows->p, rows->q) || rows->V > h->V)
+        return fail(LAPSSD_EINVAL, "rows: dtype/V/alignment");
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last_stream = s;
+    const RowsDev rw = rows_dev(rows->p, rows->q, rows->draft, rows->slab_tab, rows->V, rows->k, rows->R, rows->dtype);
+    return cuda_status(launch_mc_step(h->st, h->sc, h->mc, rw, nullptr, h->desc, h->sel, nullptr, s),
+                       "laps_mc_select");
+}
+
+lapssd_status laps_mc_step(lapssd_mc *h, const lapssd_rows *rows, int32_t *tokens_out, int32_t *n_accept_out,
+                           int32_t *active_out, lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || !rows || !rows->slab_tab || rows->k != h->sc.k || rows->R < 1)
+        return fail(LAPSSD_EINVAL, "handle / rows (pooled layout with slab_tab required)");
+    if (!rows_ok(rows->dtype, rows->V, rows->k, rows->p, rows->q) || rows->V > h->V)
+        return fail(LAPSSD_EINVAL, "rows: dtype/V/alignment");
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last_stream = s;
+    const RowsDev rw = rows_dev(rows->p, rows->q, rows->draft, rows->slab_tab, rows->V, rows->k, rows->R, rows->dtype);
+    int32_t *tok = tokens_out ? tokens_out : h->tokens;
+    int32_t *na = n_accept_out ? n_accept_out : h->n_accept;
+    // a2: one verified request per trace (slot t), in sub-launches the kernel's per-CTA
+    // snapshot holds
+    VerifyArgs a{};
+    a.rows = rw;
+    a.n_chunks = n_chunks_of(rows->V, rows->dtype);
+    a.cpb = verify_cpb(rows->V);
+    a.seed = h->sc.seed;
+    a.part = h->part;
+    a.work = h->work;
+    a.fuse_update = 0;
+    a.err = &h->st.g->err;
+    lapssd_status st = LAPSSD_OK;
+    for (int32_t b0 = 0; b0 < h->T && st == LAPSSD_OK; b0 += h->bmax) {
+        VerifyArgs ab = a;
+        const int32_t nb = h->T - b0 < h->bmax ? h->T - b0 : h->bmax;
+        ab.desc = h->desc + b0;
+        ab.tokens = tok + (int64_t)b0 * (rows->k + 1);
+        ab.n_accept = na + b0;
+        st = cuda_status(launch_verify(ab, nb, s), "laps_mc_step verify");
+    }
+    if (st != LAPSSD_OK) return st;
+    if (active_out) {
+        const cudaError_t e = cudaMemsetAsync(active_out, 0, sizeof(int32_t), s);
+        if (e != cudaSuccess) return cuda_status(e, "laps_mc_step");
+    }
+    // a3 + a4-a7 + a1, one warp per trace
+    return cuda_status(launch_mc_step(h->st, h->sc, h->mc, rw, na, h->desc, h->sel, active_out, s),
+                       "laps_mc_step update/select");
+}
+
+lapssd_status lapssd_mc_read(lapssd_mc *h, lapssd_state_view *v, int64_t *now_us, int32_t *cursor, int32_t *sel,
+                             lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h) return fail(LAPSSD_EINVAL, "handle is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n = (size_t)h->n, T = (size_t)h->T;
+    std::vector<Globals> g(T);
+    std::vector<uint32_t> flags(n);
+    std::vector<int64_t> off(T + 1);
+    cudaError_t e = cudaMemcpyAsync(g.data(), h->mc.g, sizeof(Globals) * T, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(off.data(), h->mc.off, sizeof(int64_t) * (T + 1), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && sel) e = cudaMemcpyAsync(sel, h->sel, sizeof(int32_t) * T, cudaMemcpyDeviceToHost, s);
+#define CP(dst, src, cnt)                                                                          \
+    if (e == cudaSuccess && v && (dst)) e = cudaMemcpyAsync((dst), (src), sizeof(*(dst)) * (cnt), cudaMemcpyDeviceToHost, s);
+    CP(v->acc_tok, h->st.acc_tok, n)
+    CP(v->acc_draft, h->st.acc_draft, n)
+    CP(v->rounds, h->st.rounds, n)
+    CP(v->E_us, h->st.E, n)
+    CP(v->T_total_us, h->st.T_total, n)
+    CP(v->C_us, h->st.C, n)
+    CP(v->x_us, h->st.x, n)
+    CP(v->A, h->st.A, n)
+    CP(v->key, h->st.key, n)
+    CP(v->ring, h->st.ring, n * h->sc.gamma)
+#undef CP
+    if (e == cudaSuccess && n) e = cudaMemcpyAsync(flags.data(), h->st.flags, 4 * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "lapssd_mc_read");
+    for (size_t t = 0; t < T; ++t) {
+        if (now_us) now_us[t] = g[t].now_us;
+        if (cursor) cursor[t] = g[t].cursor;
+        if (!v) continue;
+        for (int64_t i = off[t]; i < off[t + 1]; ++i) {
+            const uint32_t f = flags[i];
+            if (v->admitted) v->admitted[i] = (int32_t)(i - off[t]) < g[t].cursor;
+            if (v->done) v->done[i] = (f & F_DONE) != 0;
+            if (v->perceptible) v->perceptible[i] = (f & F_PERC) != 0;
+            if (v->pinned) v->pinned[i] = (f & F_PINNED) != 0;
+            if (v->running) v->running[i] = (f & F_RUNNING) != 0;
+            if (v->level) v->level[i] = (uint8_t)((f & F_LEVEL_MASK) >> F_LEVEL_SHIFT);
+        }
+    }
+    return LAPSSD_OK;
+}
+
+lapssd_status lapssd_mc_check(lapssd_mc *h, uint32_t *flags_out) {
+    g_last_error.clear();
+    if (!h) return fail(LAPSSD_EINVAL, "handle is NULL");
+    Globals g{};
+    cudaError_t e = cudaStreamSynchronize(h->last_stream);
+    if (e == cudaSuccess) e = cudaMemcpy(&g, h->st.g, sizeof g, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_status(e, "lapssd_mc_check");
     if (flags_out) *flags_out = g.err;
     if (g.err) return fail(LAPSSD_ESTATE, "device contract violation flags 0x%x", g.err);
     return LAPSSD_OK;

@@ -345,7 +345,8 @@ struct __align__(16) SlotDesc {
     uint32_t req;     // global request id (Philox c0)
     uint32_t round;   // round index (Philox c1)
     int32_t r;        // first rejected position, k if all accepted, -1 empty
-    int32_t pad[3];
+    uint32_t trace;   // Philox c3 of the slot's draws (trace index: Monte-Carlo replicas)
+    int32_t pad[2];
 };
 
 // a1 for one slot: x_j = draft[slab][j]; accept iff u24_j * q_j(x_j) < p_j(x_j) * 2^24
@@ -415,7 +416,7 @@ SlotDesc make_desc(const RowsDev &rw, const State &st, const Sched &sc,
                                               int32_t b, int32_t i) {
     SlotDesc d;
     d.i = i; d.slab = 0; d.req = 0; d.round = 0; d.r = -1;
-    d.pad[0] = d.pad[1] = d.pad[2] = 0;
+    d.trace = 0; d.pad[0] = d.pad[1] = 0;
     if (i < 0) return d;
     const int32_t rnd = st.rounds[i];
     const uint64_t tag = st.next_tag[i];
@@ -528,6 +529,15 @@ int verify_max_batch(int32_t n_chunks, int32_t reserve_sms);
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
                                int32_t B, PreSelect *pre, const SelRec *fin, uint64_t *fin_key, uint32_t *snap,
                                uint32_t snap_target, int32_t *count_out, cudaStream_t s);
+// Monte-Carlo replicas (mc.cu): T traces over one concatenated request SoA.
+struct McDev {
+    const int64_t *off;         // [T+1] request offsets of the traces
+    Globals *g;                 // [T] per-trace clock, cursor, counts
+    int32_t T;
+};
+cudaError_t launch_mc_step(const State &st, const Sched &sc, const McDev &mc, const RowsDev &rw,
+                           const int32_t *n_accept, SlotDesc *desc, int32_t *sel_out, int32_t *active,
+                           cudaStream_t s);
 int sort_capacity();            // largest key count one select CTA can sort
 void prepare_all();             // kernel attributes, once per process (api.cu)
 void verify_prepare();

@@ -1,0 +1,106 @@
+// mc.cu -- the Monte-Carlo replica engine (SURVEY §8(d) configs[4], §8(a) a6 segmented):
+// T independent traces, each a batch-1 simulation of its own requests with its own
+// clock (one request served at a time), advanced together one round per step.
+//
+// One step = the verify kernel over T slots (slot t = the request trace t runs, rows of
+// its slab, Philox c3 = t) and mc_step_kernel: one warp per trace runs
+//   (a3) the state update of the request just verified,
+//   (a7) the trace clock (+c_round after a round, AMB-17; jump to the next arrival when
+//        idle),
+//   (a4) admission of the trace's arrivals up to its clock,
+//   (a5, a6) every request's priority key and the trace's top-1 (warp min: P:129-133),
+//        with x_i and pinning on selection (AMB-15, AMB-25),
+//   (a1) the acceptance test of the selected request's round for the next verify.
+// The per-trace result is exactly the single-trace handle's (and the oracle's) with
+// B = 1; traces share nothing but the slab pool.
+#include "select_core.cuh"
+
+namespace lapssd {
+
+__global__ void __launch_bounds__(256) mc_step_kernel(const State st, const Sched sc, const McDev mc,
+                                                      const RowsDev rw, const int32_t *n_accept, SlotDesc *desc,
+                                                      int32_t *sel_out, int32_t *active) {
+    const int lane = threadIdx.x & 31;
+    const int t = (int)((blockIdx.x * (unsigned)blockDim.x + threadIdx.x) >> 5);
+    if (t >= mc.T) return;
+    const int64_t off = mc.off[t];
+    const int n = (int)(mc.off[t + 1] - off);
+    Globals *g = mc.g + t;
+    // (a3) the round this trace just verified
+    if (n_accept && lane == 0) {
+        const SlotDesc d = desc[t];
+        const int r = n_accept[t];
+        if (d.i >= 0 && r >= 0) update_one(st, sc, d.i, r, g->now_us);
+    }
+    __syncwarp();
+    // (a7 + a4) clock and admission over the trace's sorted arrivals
+    int64_t now = g->now_us;
+    if (g->prev_count > 0) now += sc.c_round_us;
+    int cursor = g->cursor;
+    for (;;) {
+        const int j = cursor + lane;
+        const bool adm = j < n && st.arrival[off + j] <= now;
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, adm);
+        cursor += __popc(m);
+        if (m != 0xFFFFFFFFu) break;
+    }
+    // (a5 + a6) keys (local ids: the trace is its own id space) and the top-1
+    uint64_t best = ~0ull;
+    for (int j = lane; j < n; j += 32) {
+        const int64_t i = off + j;
+        const uint32_t fl = st.flags[i];
+        const uint64_t key = build_key(sc, j, cursor, fl, st.L_pred[i], st.acc_tok[i], st.A[i]);
+        st.key[i] = key;
+        if (fl & F_RUNNING) st.flags[i] = fl & ~F_RUNNING;   // they describe the round that ran
+        best = key < best ? key : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t v = __shfl_xor_sync(0xFFFFFFFFu, best, o);
+        best = v < best ? v : best;
+    }
+    const bool have = (best >> 63) == 0;
+    const int jsel = have ? (int)(best & 0xFFFFFFull) : -1;
+    if (lane == 0) {
+        SlotDesc d;
+        d.i = -1; d.slab = 0; d.req = 0; d.round = 0; d.r = -1;
+        d.trace = (uint32_t)t; d.pad[0] = d.pad[1] = 0;
+        int64_t nnow = now;
+        if (have) {
+            const int64_t i = off + jsel;
+            commit_one(st, sc, (int32_t)i, now);
+            // (a1) for the next verify: x_j ~ q_j of the slab of this round, Philox c3 = t
+            const int32_t rnd = st.rounds[i];
+            const int64_t slab = rw.slab_tab[i * rw.R + slab_round_index(rnd, rw.R)];
+            d.i = (int32_t)i;
+            d.slab = (int32_t)slab;
+            d.req = (uint32_t)jsel;
+            d.round = (uint32_t)rnd;
+            d.r = rw.dtype == LAPSSD_BF16 ? accept_test(rw, slab, d.req, d.round, (uint32_t)t, sc.seed, load_prob_bf16)
+                                          : accept_test(rw, slab, d.req, d.round, (uint32_t)t, sc.seed, load_prob_f32);
+            if (active) atomicAdd(active, 1);
+        } else if (cursor < n) {                                 // idle: jump to the next arrival
+            const int64_t nxt = st.arrival[off + cursor];
+            if (nxt > nnow) nnow = nxt;
+        }
+        desc[t] = d;
+        if (sel_out) sel_out[t] = jsel;
+        g->now_us = nnow;
+        g->cursor = cursor;
+        g->prev_count = have ? 1 : 0;
+        g->count = have ? 1 : 0;
+    }
+}
+
+cudaError_t launch_mc_step(const State &st, const Sched &sc, const McDev &mc, const RowsDev &rw,
+                           const int32_t *n_accept, SlotDesc *desc, int32_t *sel_out, int32_t *active,
+                           cudaStream_t s) {
+    if (mc.T <= 0) return cudaSuccess;
+    const int warps_per_block = 8;
+    const int blocks = (mc.T + warps_per_block - 1) / warps_per_block;
+    mc_step_kernel<<<blocks, 32 * warps_per_block, 0, s>>>(st, sc, mc, rw, n_accept, desc, sel_out, active);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace lapssd

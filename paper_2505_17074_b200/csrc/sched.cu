@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kSelThreads) presort_kernel(const State st, co
         r.flags = 0;
         r.x_unset = 0;
         r.desc.i = -1; r.desc.slab = 0; r.desc.req = 0; r.desc.round = 0; r.desc.r = -1;
-        r.desc.pad[0] = r.desc.pad[1] = r.desc.pad[2] = 0;
+        r.desc.trace = 0; r.desc.pad[0] = r.desc.pad[1] = 0;
         if (key != ~0ull) {
             const int32_t i = (int32_t)((uint32_t)(key & 0xFFFFFFull) / (uint32_t)sc.world);
             r.flags = st.flags[i];
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
         r.flags = 0;
         r.x_unset = 0;
         r.desc.i = -1; r.desc.slab = 0; r.desc.req = 0; r.desc.round = 0; r.desc.r = -1;
-        r.desc.pad[0] = r.desc.pad[1] = r.desc.pad[2] = 0;
+        r.desc.trace = 0; r.desc.pad[0] = r.desc.pad[1] = 0;
         if (key != ~0ull) {
             const int32_t i = (int32_t)((uint32_t)(key & 0xFFFFFFull) / (uint32_t)sc.world);
             r.flags = st.flags[i];
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     for (int b = threadIdx.x; b < B; b += T) {
         SlotDesc d;
         d.i = -1; d.slab = 0; d.req = 0; d.round = 0; d.r = -1;
-        d.pad[0] = d.pad[1] = d.pad[2] = 0;
+        d.trace = 0; d.pad[0] = d.pad[1] = 0;
         if (b < cnt) {
             const int i = (int)((uint32_t)(L[b] & 0xFFFFFFull) / (uint32_t)sc.world);
             const int sl = slot_of[i];

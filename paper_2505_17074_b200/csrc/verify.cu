@@ -140,7 +140,7 @@ __global__ void accept_kernel(const RowsDev rw, const int32_t *sel, const State 
     d.slab = slab ? slab[b] : b;
     d.req = req_id[b];
     d.round = round_idx[b];
-    d.pad[0] = d.pad[1] = d.pad[2] = 0;
+    d.trace = trace; d.pad[0] = d.pad[1] = 0;
     d.r = rw.dtype == LAPSSD_BF16
               ? accept_test(rw, d.slab, d.req, d.round, trace, seed, load_prob_bf16)
               : accept_test(rw, d.slab, d.req, d.round, trace, seed, load_prob_f32);
@@ -429,7 +429,7 @@ __device__ __forceinline__ void update_slot_warp(const VerifyArgs &a, int b, con
         rec.desc.req = d.req;
         rec.desc.round = d.round + 1;
         rec.desc.r = r_next;
-        rec.desc.pad[0] = rec.desc.pad[1] = rec.desc.pad[2] = 0;
+        rec.desc.trace = d.trace; rec.desc.pad[0] = rec.desc.pad[1] = 0;
         a.fin[b] = rec;
         a.st.key[d.i] = rec.key;
         // publish the key (release: orders the record before it; nothing waits on it
@@ -486,7 +486,7 @@ __device__ __forceinline__ void sample_slot_warp(const VerifyArgs &a, uint64_t *
         if (a.err && lane == 0) atomicOr(a.err, E_NO_MASS);
         y = use_q ? a.rows.draft[(int64_t)d.slab * k + r] : 0;
     } else {
-        const uint4 u = philox4x32_10(make_uint4(d.req, d.round, 1u << 8, a.trace), (uint32_t)a.seed,
+        const uint4 u = philox4x32_10(make_uint4(d.req, d.round, 1u << 8, d.trace), (uint32_t)a.seed,
                                       (uint32_t)(a.seed >> 32));
         const uint64_t U = ((uint64_t)u.x << 32) | u.y;
         uint64_t t = __umul64hi(U, Z);  // floor(U Z / 2^64) in [0, Z)
@@ -745,8 +745,11 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
         asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int j = 0; j < nf; ++j) {
             const SlotDesc d = s_fin[grp][j];
-            if (d.r < 0) continue;
             const int b = f0 + j * kGroups * grid;
+            if (d.r < 0) {  // empty slot: nothing verified
+                if (lane == 0 && a.n_accept) a.n_accept[b] = -1;
+                continue;
+            }
             if (lane == 0) TRACE(5, b);
             const uint64_t *pw = part + (int64_t)b * nc * kPartWords;
             uint64_t w[kPartWords];

@@ -265,6 +265,67 @@ CONFIGS = {
 }
 
 
+# configs[4]: Monte-Carlo sweep, 8,192 independent traces x 512 requests, batch 1 per
+# trace, V=32000, k=4, bf16, per-trace Poisson arrivals at load rho=0.8
+CONFIGS["c5"] = dict(T=8192, n=512, V=32000, k=4, dtype="bf16", arrival="poisson", length="lognormal",
+                     len_mu=math.log(128), len_sigma=0.8, len_min=8, len_max=2048, beta_ab=(4, 2),
+                     drift=False, rho=0.8, K=4, family="f2", n_buckets=64, variants=256, R=16,
+                     seed=0x5D0005)
+
+
+@dataclass
+class MCWorkload:
+    """T traces concatenated: trace t owns requests offsets[t]..offsets[t+1]."""
+    offsets: np.ndarray     # [T+1] int64
+    arrival_us: np.ndarray  # [n_total] int64, sorted within each trace
+    L_true: np.ndarray      # [n_total] int32
+    L_pred: np.ndarray      # [n_total] int32
+    slab_tab: np.ndarray    # [n_total, R] int32 (global request index)
+    alpha: np.ndarray       # [n_total] acceptance rate behind the slab buckets
+
+    @property
+    def T(self) -> int:
+        return len(self.offsets) - 1
+
+    def trace(self, t: int):
+        a, b = int(self.offsets[t]), int(self.offsets[t + 1])
+        return self.arrival_us[a:b], self.L_true[a:b], self.L_pred[a:b], self.slab_tab[a:b]
+
+
+def make_mc_workload(T: int, n: int, seed: int, *, rate_per_s: float, len_mu=math.log(128), len_sigma=0.8,
+                     len_min=8, len_max=2048, beta_ab=(4.0, 2.0), n_buckets=64, variants=256, R=16,
+                     pred_sigma=0.3) -> MCWorkload:
+    """T independent Poisson traces of n requests (vectorised; same recipe as make_trace +
+    slab_table per trace: lognormal lengths, L_pred = L * exp(N(0, 0.3^2)), Beta
+    acceptance, slab bucket = randomised rounding of alpha * n_buckets)."""
+    rng = np.random.default_rng(seed)
+    gaps = rng.exponential(1e6 / rate_per_s, size=(T, n))
+    arr = np.floor(np.cumsum(gaps, axis=1)).astype(np.int64)
+    arr -= arr[:, :1]
+    L = np.clip(np.round(np.exp(rng.normal(len_mu, len_sigma, size=(T, n)))), len_min, len_max).astype(np.int32)
+    Lp = np.maximum(1, np.round(L * np.exp(rng.normal(0, pred_sigma, size=(T, n))))).astype(np.int32)
+    alpha = rng.beta(beta_ab[0], beta_ab[1], size=(T, n))
+    tab = np.empty((T * n, R), np.int32)
+    for t in range(R):
+        x = alpha.reshape(-1) * n_buckets - 0.5
+        b = np.clip(np.floor(x + rng.random(T * n)).astype(np.int64), 0, n_buckets - 1)
+        v = rng.integers(0, variants, size=T * n)
+        tab[:, t] = (b * variants + v).astype(np.int32)
+    return MCWorkload(np.arange(T + 1, dtype=np.int64) * n, arr.reshape(-1), L.reshape(-1), Lp.reshape(-1),
+                      tab, alpha.reshape(-1))
+
+
+def mc_rate_for_load(rho: float, k: int, t_ssm_us: int, t_llm_us: int, len_mu=math.log(128), len_sigma=0.8,
+                     beta_ab=(4.0, 2.0)) -> float:
+    """Arrivals per second giving load rho on one server (batch 1): rho / E[service],
+    E[service] = E[L] / E[tokens per round] * c_round (workload sizing only)."""
+    EL = math.exp(len_mu + len_sigma ** 2 / 2)
+    beta = beta_ab[0] / (beta_ab[0] + beta_ab[1])
+    per_round = float(tokens_per_round(np.array([beta]), k)[0])
+    c_round_s = (k * t_ssm_us + t_llm_us) * 1e-6
+    return rho / (EL / per_round * c_round_s)
+
+
 def tokens_per_round(beta: np.ndarray, k: int) -> np.ndarray:
     """Workload sizing only (arrival rate for a target load): the textbook expected
     tokens per round (1 - b^(k+1)) / (1 - b) of the cited SD papers."""
