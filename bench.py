@@ -65,6 +65,13 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "verify_dram.json"))
+    ap.add_argument("--workload", choices=["c4", "mc"], default="c4",
+                    help="c4 = configs[3] (the headline); mc = configs[4] Monte-Carlo traces")
+    ap.add_argument("--mc-traces", type=int, default=8192, help="configs[4]: traces (whole job)")
+    ap.add_argument("--mc-n", type=int, default=512, help="configs[4]: requests per trace")
+    ap.add_argument("--mc-variants", type=int, default=256, help="configs[4]: slab variants per bucket")
+    ap.add_argument("--mc-policies", default="", help="comma list of policies run to completion "
+                    "for mean JCT (e.g. 0,1,2,3; empty: throughput only)")
     return ap.parse_args()
 
 
@@ -401,6 +408,172 @@ def run_cpu_baseline(args, local, pool, tab, cfg_gpu, budget_s=None, batch=None)
                       f"{el:.1f} s"}
 
 
+
+# --------------------------------------------------------------------------- configs[4]
+MC_METRIC = METRIC
+MC_WORKLOAD = ("configs[4]: Monte-Carlo sweep, 8,192 independent traces x 512 requests, batch 1 per "
+               "trace (P:84), V=32,000, k=4, bf16 p/q, Poisson arrivals at rho=0.8, lognormal(ln 128, "
+               "0.8) lengths, Beta(4,2) acceptance; traces sharded in contiguous blocks over ranks")
+MC_SCHED = dict(K=4, s1_up_us=4 * (4 * 1000 + 10_000), M=2.0, gamma=5, delta=0.05, k=4,
+                t_ssm_us=1000, t_llm_us=10_000, placement=0, pin_rule=0)
+
+
+def build_mc(args, rank, world, dev):
+    c = synth.CONFIGS["c5"]
+    T_local = args.mc_traces // world
+    rate = synth.mc_rate_for_load(c["rho"], c["k"], MC_SCHED["t_ssm_us"], MC_SCHED["t_llm_us"],
+                                  len_mu=c["len_mu"], len_sigma=c["len_sigma"], beta_ab=c["beta_ab"])
+    w = synth.make_mc_workload(T_local, args.mc_n, c["seed"] + rank, rate_per_s=rate, len_mu=c["len_mu"],
+                               len_sigma=c["len_sigma"], len_min=c["len_min"], len_max=c["len_max"],
+                               beta_ab=c["beta_ab"], n_buckets=c["n_buckets"], variants=args.mc_variants,
+                               R=c["R"])
+    pool = synth.make_pool("f2", V=c["V"], k=c["k"], dtype="bf16", n_buckets=c["n_buckets"],
+                           variants=args.mc_variants, seed=c["seed"], device=dev)
+    return w, pool
+
+
+def run_mc(args):
+    import paper_2505_17074_b200 as L
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    c = synth.CONFIGS["c5"]
+    k, V = c["k"], c["V"]
+    w, pool = build_mc(args, rank, world, dev)
+    T = w.T
+    cfg = L.SchedConfig(**MC_SCHED, policy=0, seed=c["seed"])
+    mc = L.MCHandle(cfg, w.offsets, w.arrival_us, w.L_true, w.L_pred, V=V)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(w.slab_tab, device=dev))
+    mc.select(rows)
+    G = max(1, min(args.graph_steps or 20, args.steps))
+    hist = torch.full((G, T), -1, dtype=torch.int32, device=dev)
+    for t in range(args.warmup):
+        mc.step(rows, n_accept=hist[t % G])
+    torch.cuda.synchronize()
+    c0 = L.launch_count()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for t in range(G):
+            mc.step(rows, n_accept=hist[t])
+    launches_per_step = (L.launch_count() - c0) / G
+    reps = max(1, args.steps // G)
+    steps = reps * G
+    st0 = mc.state()[0]["rounds"].astype(np.int64).sum()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    n_acc = hist.cpu().numpy()
+    verified_local = int(mc.state()[0]["rounds"].astype(np.int64).sum() - st0)
+    t = torch.tensor([ms, float(verified_local)], dtype=torch.float64, device=dev)
+    if dist:
+        mx, sm = t.clone(), t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, verified = float(mx[0]), int(sm[1])
+    else:
+        ms_max, verified = ms, verified_local
+    alg_step = algorithmic_bytes(n_acc, V, k) / G
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs") or 6650.0
+    achieved = alg_step / (ms / steps * 1e-3) / 1e9
+    out = {"metric": MC_METRIC, "value": verified * k / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
+           "steps": steps, "warmup": args.warmup, "ms_per_step": ms_max / steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16 rows; fp32 residual + exact Q4.60 "
+           "integer CDF; fp64 scheduler", "data": "synthetic",
+           "config": {"workload": MC_WORKLOAD, "traces_per_gpu": T, "requests_per_trace": args.mc_n,
+                      "V": V, "k": k, "pool": f"F2, {pool.S} slabs x {(2 * k + 1) * V * 2 / 1e6:.2f} MB",
+                      "l2": f"inputs larger than L2 ({pool.S * (2 * k + 1) * V * 2 / 1e9:.1f} GB slab pool)",
+                      "parallelism": f"dp{world}: traces in contiguous blocks, no collective"},
+           "verified_per_step": verified / steps, "gpu_launches": int(round(launches_per_step * steps)),
+           "clocks": clk,
+           "roofline": {"kernel": "whole MC step (verify sub-launches + warp-per-trace update/select)",
+                        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": None,
+                        "algorithmic_bytes_per_step": alg_step,
+                        "timing": f"{steps} steps as replays of a CUDA graph of {G} steps; step-level "
+                                  "bytes / step time (a lower bound for the verify kernel's own rate)"}}
+    if args.mc_policies:
+        out["jct"] = mc_jct(args, L, w, pool, rows, dev, [int(x) for x in args.mc_policies.split(",")])
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = mc_cpu_baseline(args, w, pool, cfg)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def mc_jct(args, L, w, pool, rows, dev, policies):
+    """Run every trace to completion under each policy (same traces, same rows, same
+    seeds: common random numbers) and report the mean JCT (C_i - r_i)."""
+    res = {}
+    c = synth.CONFIGS["c5"]
+    for pol in policies:
+        cfg = L.SchedConfig(**MC_SCHED, policy=pol, seed=c["seed"])
+        mc = L.MCHandle(cfg, w.offsets, w.arrival_us, w.L_true, w.L_pred, V=c["V"])
+        mc.select(rows)
+        G = 64
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(G):
+                act = mc.step(rows)
+        steps, t0 = 0, time.perf_counter()
+        while True:
+            g.replay()
+            steps += G
+            if int(act.item()) == 0 or steps > 2_000_000:
+                break
+        el = time.perf_counter() - t0
+        st = mc.state()[0]
+        jct = (st["C_us"] - w.arrival_us).astype(np.float64)
+        res[["LAPS-SD", "FCFS", "LP-SJF", "LAS"][pol]] = {"mean_jct_ms": float(jct.mean() / 1e3),
+                                                          "steps": steps, "seconds": el,
+                                                          "all_done": bool(st["done"].all())}
+        del mc
+    return res
+
+
+def mc_cpu_baseline(args, w, pool, cfg):
+    """The oracle, single thread, on a bounded sample: whole traces one after another."""
+    import oracle
+
+    P = pool.numpy()
+    ocfg = oracle.SchedConfig(**MC_SCHED, policy=0, seed=cfg.seed)
+    t0 = time.perf_counter()
+    verified = traces = 0
+    while time.perf_counter() - t0 < args.cpu_seconds and traces < w.T:
+        a, lt, lp, tab = w.trace(traces)
+        sim = oracle.Sim(ocfg, a, lt, lp, trace=traces)
+        Pt = dict(P, slab_tab=np.ascontiguousarray(tab), R=tab.shape[1])
+        sel, _ = sim.select(1)
+        while not sim.state()["done"].all() and time.perf_counter() - t0 < args.cpu_seconds:
+            verified += int(sel[0] >= 0)
+            sim.step(Pt, sel)
+        traces += 1
+    el = time.perf_counter() - t0
+    return {"value": verified * MC_SCHED["k"] / el, "unit": UNIT,
+            "cores": 1, "kind": "oracle", "sample": f"{traces} traces (batch 1 each) of the same workload, "
+            f"{verified} verifications, oracle/lapssd_oracle.c single thread, {el:.1f} s"}
+
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args):
     """--impl reference: the CPU oracle, as it stands, timed on this host's cores on the
@@ -455,6 +628,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "mc":
+        run_mc(args)
     else:
         run_ours(args)
 
