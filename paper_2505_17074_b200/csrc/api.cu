@@ -718,6 +718,7 @@ static void carve_mc(Carver &cv, lapssd_mc *h, int32_t T, int64_t n, int32_t gam
     const size_t tt = (size_t)(T > 0 ? T : 1);
     h->mc.g = cv.take<Globals>(tt);
     h->mc.off = cv.take<int64_t>(tt + 1);
+    h->mc.last = cv.take<int32_t>(tt);
     h->desc = cv.take<SlotDesc>(tt);
     h->sel = cv.take<int32_t>(tt);
     h->n_accept = cv.take<int32_t>(tt);
@@ -785,6 +786,7 @@ lapssd_status lapssd_mc_create(const lapssd_config *cfg, int32_t n_traces, const
         e = cudaMemcpyAsync((void *)h->mc.off, trace_offsets, sizeof(int64_t) * (n_traces + 1),
                             cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->sel, 0xFF, sizeof(int32_t) * n_traces, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->mc.last, 0xFF, sizeof(int32_t) * n_traces, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
         delete h;

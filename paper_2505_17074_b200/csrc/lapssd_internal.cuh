@@ -533,6 +533,7 @@ cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &
 struct McDev {
     const int64_t *off;         // [T+1] request offsets of the traces
     Globals *g;                 // [T] per-trace clock, cursor, counts
+    int32_t *last;              // [T] request verified in the previous step (-1: none)
     int32_t T;
 };
 cudaError_t launch_mc_step(const State &st, const Sched &sc, const McDev &mc, const RowsDev &rw,

@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256) mc_step_kernel(const State st, const Sche
     int64_t now = g->now_us;
     if (g->prev_count > 0) now += sc.c_round_us;
     int cursor = g->cursor;
+    const int cursor0 = cursor;
     for (;;) {
         const int j = cursor + lane;
         const bool adm = j < n && st.arrival[off + j] <= now;
@@ -44,15 +45,43 @@ __global__ void __launch_bounds__(256) mc_step_kernel(const State st, const Sche
         cursor += __popc(m);
         if (m != 0xFFFFFFFFu) break;
     }
-    // (a5 + a6) keys (local ids: the trace is its own id space) and the top-1
-    uint64_t best = ~0ull;
-    for (int j = lane; j < n; j += 32) {
-        const int64_t i = off + j;
+    // (a5 + a6) keys (local ids: the trace is its own id space) and the top-1.  Batch 1
+    // changes few keys per step: the request just verified (its update), the one that
+    // ran before it (its running flag is cleared) and the new admissions; every other
+    // key is unchanged (flags, level, estimate and pin move only for the running
+    // request).  So after the first select only those are recomputed, then the warp
+    // takes the minimum of the trace's stored keys (4 KB for 512 requests).
+    auto rekey = [&](int64_t i) {
         const uint32_t fl = st.flags[i];
-        const uint64_t key = build_key(sc, j, cursor, fl, st.L_pred[i], st.acc_tok[i], st.A[i]);
+        const uint64_t key = build_key(sc, (int32_t)(i - off), cursor, fl, st.L_pred[i], st.acc_tok[i], st.A[i]);
         st.key[i] = key;
         if (fl & F_RUNNING) st.flags[i] = fl & ~F_RUNNING;   // they describe the round that ran
-        best = key < best ? key : best;
+        return key;
+    };
+    uint64_t best = ~0ull;
+    if (!n_accept) {                                         // first select: every key
+        for (int j = lane; j < n; j += 32) {
+            const uint64_t key = rekey(off + j);
+            best = key < best ? key : best;
+        }
+    } else {
+        const int32_t ran = desc[t].i, before = mc.last[t];
+        if (lane == 0 && ran >= 0) rekey(ran);
+        if (lane == 1 && before >= 0 && before != ran) rekey(before);
+        for (int j = cursor0 + lane; j < cursor; j += 32) rekey(off + j);   // admitted now
+        __syncwarp();
+        if (lane == 0) mc.last[t] = ran;
+        constexpr int U = 4;                                 // independent loads in flight
+        for (int j0 = 0; j0 < n; j0 += 32 * U) {
+            uint64_t kv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u * 32 + lane;
+                kv[u] = j < n ? st.key[off + j] : ~0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) best = kv[u] < best ? kv[u] : best;
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
