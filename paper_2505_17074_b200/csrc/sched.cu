@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const State st, con
     const int npow2 = next_pow2(sc.n > 0 ? sc.n : 1);
     build_keys(st, sc, cursor, s_buf, npow2);
     const int bp = next_pow2(B);
-    const uint64_t *keys = select_topB(s_buf, sc.n, B, s_buf + npow2, s_buf + npow2 + bp, bp);
+    const uint64_t *keys = select_topB_fast(s_buf, sc.n, B, s_buf + npow2, s_buf + npow2 + bp, bp, s_buf + npow2 + 2 * bp);
     // eligible keys (bit 63 clear) form a prefix of the sorted array
     const int lim = B < bp ? B : bp;
     if (threadIdx.x == 0) s_count = 0;
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kSelThreads) presort_kernel(const State st, co
     }
     __syncthreads();
     const int bp = next_pow2(B);
-    const uint64_t *top = select_topB(s_buf, n, B, s_buf + npow2, s_buf + npow2 + bp, bp);
+    const uint64_t *top = select_topB_fast(s_buf, n, B, s_buf + npow2, s_buf + npow2 + bp, bp, s_buf + npow2 + 2 * bp);
     // records for the fused final select: flags, first-service marker, and the
     // acceptance-test descriptor of the candidate's current round (cached or computed)
     SelRec *rec = pre_recs(out, bp);
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     __syncthreads();
     SSTEP(8);
     const int bp = next_pow2(B);
-    const uint64_t *top = select_topB(s_buf, n, B, s_buf + npow2, s_buf + npow2 + bp, bp);
+    const uint64_t *top = select_topB_fast(s_buf, n, B, s_buf + npow2, s_buf + npow2 + bp, bp, s_buf + npow2 + 2 * bp);
     SSTEP(9);
     SelRec *crec = pre_recs(pre, bp);
     for (int b = threadIdx.x; b < bp; b += T) {
@@ -575,7 +575,7 @@ cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &
     int np = 1, bp = 1;
     while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
     while (bp < B) bp <<= 1;
-    const size_t a = (size_t)(np + 2 * bp) * sizeof(uint64_t);
+    const size_t a = topB_smem_words(np, bp) * sizeof(uint64_t);
     const size_t b = (size_t)4 * bp * sizeof(uint64_t) + 2 * (size_t)((sc.n + 7) & ~7) * sizeof(int16_t) + 64 +
                      (bp <= 1024 ? 2 * (size_t)bp * sizeof(SelRec) : 0);
     select_side_kernel<<<1, kSideThreads, a > b ? a : b, s>>>(st, sc, rw, sel, desc, B, pre, fin, fin_key, snap,
@@ -589,7 +589,7 @@ cudaError_t launch_presort(const State &st, const Sched &sc, const RowsDev &rw, 
     int np = 1, bp = 1;
     while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
     while (bp < B) bp <<= 1;
-    presort_kernel<<<1, kSelThreads, (size_t)(np + 2 * bp) * sizeof(uint64_t), s>>>(st, sc, rw, sel, B, out);
+    presort_kernel<<<1, kSelThreads, topB_smem_words(np, bp) * sizeof(uint64_t), s>>>(st, sc, rw, sel, B, out);
     count_launch();
     return cudaGetLastError();
 }
@@ -609,7 +609,7 @@ cudaError_t launch_select(const State &st, const Sched &sc, const RowsDev &rw, S
     int np = 1, bp = 1;
     while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
     while (bp < B) bp <<= 1;
-    select_kernel<<<1, kSelThreads, (size_t)(np + 2 * bp) * sizeof(uint64_t), s>>>(st, sc, rw, desc, B,
+    select_kernel<<<1, kSelThreads, topB_smem_words(np, bp) * sizeof(uint64_t), s>>>(st, sc, rw, desc, B,
                                                                                     sel_out, count_out);
     count_launch();
     return cudaGetLastError();

@@ -12,6 +12,7 @@ constexpr int kSelThreads = 1024;
 constexpr int kSideThreads = 1024;     // side-stream select (measured: 512 is slower)
 constexpr int kSortCap = 16384;          // keys per CTA (bitonic in place above kMergeCap)
 constexpr int kMergeCap = 8192;          // keys sorted by warp-sort + merge-path (2 buffers)
+constexpr int kFastTopCap = 4096;        // top-B by full sort up to this many keys (else radix select)
 
 // ---------------------------------------------------------------- block sort
 __device__ inline void bitonic_sort(uint64_t *s, int n) {  // n power of two, ascending, in place
@@ -311,6 +312,26 @@ __device__ __forceinline__ int next_pow2(int n) {
     int p = 1;
     while (p < n) p <<= 1;
     return p;
+}
+
+// Same contract as select_topB.  When the caller has npow2 more words of scratch and
+// npow2 <= kMergeCap, a full block sort (warp-register runs + merge-path, ~log2(n/64)
+// barriers) is much shorter than eight radix passes of barriers; keys[0..npow2) must be
+// padded with UINT64_MAX and is clobbered.  topB_smem_words sizes the caller's buffer.  The result is the first bp words of the
+// sorted buffer, with the entries from B on reset to UINT64_MAX (select_topB's padding).
+__device__ inline const uint64_t *select_topB_fast(uint64_t *keys, int n, int B, uint64_t *out, uint64_t *tmp,
+                                                   int bp, uint64_t *scratch) {
+    const int np = next_pow2(n > 0 ? n : 1);
+    if (scratch == nullptr || np < bp || np < 64 || np > kFastTopCap) return select_topB(keys, n, B, out, tmp, bp);
+    uint64_t *s = block_sort(keys, scratch, np);
+    for (int b = B + (int)threadIdx.x; b < bp; b += blockDim.x) s[b] = ~0ull;
+    __syncthreads();
+    return s;
+}
+
+// Shared-memory words for keys[np] + out[bp] + tmp[bp] (+ scratch[np] on the fast path).
+__host__ __device__ inline size_t topB_smem_words(int np, int bp) {
+    return (size_t)np + 2 * (size_t)bp + (np >= bp && np >= 64 && np <= kFastTopCap ? (size_t)np : 0);
 }
 
 __host__ __device__ inline size_t sort_smem_bytes(int n) {

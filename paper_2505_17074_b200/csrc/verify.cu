@@ -575,6 +575,55 @@ __host__ __device__ __forceinline__ int fin_slots(int B, int grid, int f0) {
     return f0 < B ? (B - 1 - f0) / (kGroups * grid) + 1 : 0;
 }
 
+// (slab << 5) | (r + 1) of slot b, 0 = nothing to do: the descriptor checked against
+// sel[] (a stale descriptor or a bad slab index is a contract violation, flagged).
+__device__ __forceinline__ uint32_t slot_word(const VerifyArgs &a, int b) {
+    const int4 *dp = reinterpret_cast<const int4 *>(a.desc + b);
+    const int4 dh = dp[0];  // i, slab, req, round
+    int r = dp[1].x;
+    const int si = a.sel ? a.sel[b] : dh.x;
+    if (r >= 0 && si != dh.x) {
+        if (a.err) atomicOr(a.err, E_STALE_DESC);
+        r = -1;
+    }
+    if (r >= 0 && (uint32_t)dh.y >= (1u << 27)) {
+        if (a.err) atomicOr(a.err, E_BAD_SLOT);
+        r = -1;
+    }
+    return r < 0 ? 0u : ((uint32_t)dh.y << 5) | (uint32_t)(r + 1);
+}
+
+// Producer: item n (slot n / nc, chunk n % nc) into ring stage st -- chunk c of p_r and,
+// when r < k, of q_r, as bulk copies completing on full[st]; nothing for an empty slot.
+template <bool BF16>
+__device__ __forceinline__ void issue_item(const VerifyArgs &a, uint8_t *s_tiles, uint64_t *full_st, int st, int n,
+                                           uint32_t it) {
+    using E = Elt<BF16>;
+    using TC = VerifyCfg<BF16>;
+    if (it == 0) {
+        mbar_arrive(full_st);
+        return;
+    }
+    const int kk = a.rows.k, nc = a.n_chunks;
+    const int64_t V = a.rows.V;
+    const int r = (int)(it & 31u) - 1;
+    const int64_t slab = it >> 5;
+    const int c = n % nc;
+    const int64_t e0 = (int64_t)c * TC::kTileElems;
+    const int64_t ne = V - e0 < TC::kTileElems ? V - e0 : TC::kTileElems;
+    const uint32_t bytes = (uint32_t)(ne * E::kEsz);
+    const char *pr = (const char *)a.rows.p + ((slab * (kk + 1) + r) * V + e0) * E::kEsz;
+    uint8_t *dst = s_tiles + (size_t)st * 2 * kTileBytes;
+    const bool use_q = r < kk;
+    mbar_arrive_tx(full_st, use_q ? 2 * bytes : bytes);
+    CTA_BYTES(use_q ? 2 * bytes : bytes);
+    tma_load_1d(dst, pr, bytes, full_st);
+    if (use_q) {
+        const char *qr = (const char *)a.rows.q + ((slab * kk + r) * V + e0) * E::kEsz;
+        tma_load_1d(dst + kTileBytes, qr, bytes, full_st);
+    }
+}
+
 template <bool BF16>
 __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_constant__ VerifyArgs a,
                                                                     int32_t B) {
@@ -623,26 +672,24 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // ---- the producer issues this CTA's first kStages items (static: blockIdx.x + s grid)
+    // straight from desc[] before the snapshot, so the first bytes are in flight while the
+    // snapshot loads run.  desc[] cannot change before this CTA signals `snap` below.
+    int k_pre = 0;
+    if (tid == 0) {
+        for (; k_pre < kStages; ++k_pre) {
+            const int n = (int)blockIdx.x + k_pre * grid;
+            if (n >= n_items) break;
+            s_stage[k_pre] = n;
+            issue_item<BF16>(a, s_tiles, &full[k_pre], k_pre, n, slot_word(a, n / nc));
+        }
+    }
     // ---- snapshot of everything this CTA reads of desc[] / sel[]: the (slab, r) of every
     // slot (items are claimed dynamically, so any slot may come up) and the descriptors
     // of the finishers' slots.  Once every CTA has signalled, the side-stream select may
     // overwrite desc[] / sel[] with the next batch.
     if (!finisher) {
-        for (int b = tid; b < B; b += (1 + kConsumerWarps) * 32) {
-            const int4 *dp = reinterpret_cast<const int4 *>(a.desc + b);
-            const int4 dh = dp[0];   // i, slab, req, round
-            int r = dp[1].x;
-            const int si = a.sel ? a.sel[b] : dh.x;
-            if (r >= 0 && si != dh.x) {
-                if (a.err) atomicOr(a.err, E_STALE_DESC);
-                r = -1;
-            }
-            if (r >= 0 && (uint32_t)dh.y >= (1u << 27)) {
-                if (a.err) atomicOr(a.err, E_BAD_SLOT);
-                r = -1;
-            }
-            s_slot[b] = r < 0 ? 0u : ((uint32_t)dh.y << 5) | (uint32_t)(r + 1);
-        }
+        for (int b = tid; b < B; b += (1 + kConsumerWarps) * 32) s_slot[b] = slot_word(a, b);
     } else {
         const int f0 = grp * grid + (int)blockIdx.x;
         const int nf = fin_slots(B, grid, f0);
@@ -662,45 +709,22 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
         // Items are claimed dynamically (first item n = blockIdx.x, then grid + ticket), so
         // SMs that stream faster take more of them; one claim is kept in flight ahead.
         if (lane == 0) {
-            const int kk = a.rows.k;
-            const int64_t V = a.rows.V;
-            int n = (int)blockIdx.x;
-            uint32_t nxt = (uint32_t)grid + atomicAdd(work, 1u);
-            for (int k = 0;; ++k) {
+            // after the static items, claims: kStages grid + ticket, one claim kept in flight
+            uint32_t nxt = k_pre == kStages ? (uint32_t)(kStages * grid) + atomicAdd(work, 1u) : (uint32_t)n_items;
+            for (int k = k_pre;; ++k) {
                 const int st = k % kStages;
                 TRACE(1, k & 1023);
                 if (k >= kStages) mbar_wait(&empty[st], ((k / kStages) - 1) & 1);
                 TRACE(2, k & 1023);
-                if (n >= n_items) {  // no more items: tell the consumers
+                const int cur = nxt < (uint32_t)n_items ? (int)nxt : n_items;
+                if (cur >= n_items) {  // no more items: tell the consumers
                     s_stage[st] = -1;
                     mbar_arrive(&full[st]);
                     break;
                 }
-                const int cur = n;
-                n = nxt < (uint32_t)n_items ? (int)nxt : n_items;
-                if (n < n_items) nxt = (uint32_t)grid + atomicAdd(work, 1u);
+                nxt = (uint32_t)(kStages * grid) + atomicAdd(work, 1u);
                 s_stage[st] = cur;
-                const uint32_t it = s_slot[cur / nc];
-                if (it == 0) {
-                    mbar_arrive(&full[st]);
-                } else {
-                    const int r = (int)(it & 31u) - 1;
-                    const int64_t slab = it >> 5;
-                    const int c = cur % nc;
-                    const int64_t e0 = (int64_t)c * TC::kTileElems;
-                    const int64_t ne = V - e0 < TC::kTileElems ? V - e0 : TC::kTileElems;
-                    const uint32_t bytes = (uint32_t)(ne * E::kEsz);
-                    const char *pr = (const char *)a.rows.p + ((slab * (kk + 1) + r) * V + e0) * E::kEsz;
-                    uint8_t *dst = s_tiles + (size_t)st * 2 * kTileBytes;
-                    const bool use_q = r < kk;
-                    mbar_arrive_tx(&full[st], use_q ? 2 * bytes : bytes);
-                    CTA_BYTES(use_q ? 2 * bytes : bytes);
-                    tma_load_1d(dst, pr, bytes, &full[st]);
-                    if (use_q) {
-                        const char *qr = (const char *)a.rows.q + ((slab * kk + r) * V + e0) * E::kEsz;
-                        tma_load_1d(dst + kTileBytes, qr, bytes, &full[st]);
-                    }
-                }
+                issue_item<BF16>(a, s_tiles, &full[st], st, cur, s_slot[cur / nc]);
                 TRACE(8, k & 1023);
                 CTA_TIME(2);
             }
@@ -795,7 +819,10 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
             const int n = s_stage[st];
             if (n < 0) break;
             const uint32_t it = s_slot[n / nc];
-            if (it != 0 && gw < TC::kSegs) {
+            if (it == 0 || gw >= TC::kSegs) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+            } else {
                 const int b = n / nc, c = n % nc;
                 const int r = (int)(it & 31u) - 1;
                 const uint4 qmask = r < a.rows.k ? make_uint4(~0u, ~0u, ~0u, ~0u) : make_uint4(0, 0, 0, 0);
@@ -811,6 +838,10 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                         pv[j] = tp[v];
                         qv[j] = tq[v];
                     }
+                    // the stage is in registers: release it to the producer before the
+                    // arithmetic, so the refill's latency overlaps this item's math
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[st]);
                     uint64_t m = 0;
 #if defined(LAPSSD_DIAG) && (LAPSSD_DIAG & 1)
                     if (pv[0].x == 0x7FFFFFFFu && qv[0].y == 1u) m = 1;  // diagnostic build: no residual math
@@ -830,8 +861,6 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                     if (lane == 0) st_relaxed(&part[((int64_t)b * nc + c) * kPartWords + seg], m | kReady);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
             if (gw == 0 && lane == 0) TRACE(4, k & 1023);
             if (lane == 0) CTA_TIME(3);
         }
