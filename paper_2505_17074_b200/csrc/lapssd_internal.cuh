@@ -161,10 +161,17 @@ uint64_t build_key(const Sched &s, int32_t i, int32_t cursor, uint32_t fl,
 // a3: the state update of local request i after a round with r accepted drafts.
 // P:170 (E_i), P:175 (demotion), P:176 + P:194 (stability, A_i), P:139 + P:198
 // (T~_i), P:148 (placement, AMB-14), P:177 (completion).  One thread per request.
-__device__ __forceinline__ void update_one(const State &st, const Sched &s, int32_t i, int32_t r,
-                                           int64_t now) {
+// Returns the fields the request's new priority key needs.
+struct UpdOut {    // the fields a priority key needs, after the update
+    uint32_t fl;
+    int32_t tok;
+    double A;
+};
+__device__ __forceinline__ UpdOut update_one(const State &st, const Sched &s, int32_t i, int32_t r,
+                                             int64_t now) {
     uint32_t fl = st.flags[i];
-    if (fl & F_DONE) { atomicOr(&st.g->err, E_UPDATE_DONE); return; }
+    double A_new = st.A[i];
+    if (fl & F_DONE) { atomicOr(&st.g->err, E_UPDATE_DONE); return UpdOut{fl, st.acc_tok[i], A_new}; }
     const int32_t Lt = st.L_true[i];
     int32_t tok = st.acc_tok[i];
     const int32_t emitted = r + 1;                  // r drafts + 1 resampled / bonus
@@ -194,6 +201,7 @@ __device__ __forceinline__ void update_one(const State &st, const Sched &s, int3
         if (stable) {
             fl |= F_PERC;
             st.A[i] = mean;
+            A_new = mean;
             const uint64_t T = eq6_us(st.L_pred[i], mean, s);
             const int64_t Ts = T > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)T;
             st.T_total[i] = Ts;
@@ -218,6 +226,7 @@ __device__ __forceinline__ void update_one(const State &st, const Sched &s, int3
     st.rounds[i] = t;
     st.E[i] = E;
     st.flags[i] = fl;
+    return UpdOut{fl, tok, A_new};
 }
 
 // Inputs of update_one for request i, loaded by the whole warp in one round trip
@@ -228,11 +237,6 @@ struct UpdIn {
     int64_t E;
     double A;
     int32_t ring;  // this lane's ring slot
-};
-struct UpdOut {    // the fields a priority key needs, after the update
-    uint32_t fl;
-    int32_t tok;
-    double A;
 };
 __device__ __forceinline__ UpdIn load_update_inputs(const State &st, const Sched &s, int32_t i, int lane) {
     UpdIn u;

@@ -310,12 +310,32 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// The rows are read once per step, so their bulk copies carry an L2 evict-first policy:
+// the 245 MB streamed per step then does not flush the scheduler state, slab table and
+// drafts out of L2, whose dependent loads (the update, the next round's a1, the select)
+// would otherwise queue behind the stream in HBM.
+#ifndef LAPSSD_TMA_EVICT_FIRST
+#define LAPSSD_TMA_EVICT_FIRST 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+#if LAPSSD_TMA_EVICT_FIRST
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first_policy())
+        : "memory");
+#else
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+#endif
 }
 // Published segment sums carry bit 63 as a ready flag (a segment's Q4.60 mass is < 2^61),
 // so each word is self-describing: no fence or counter orders it against other words.
