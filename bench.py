@@ -254,6 +254,12 @@ def run_ours(args):
         launches = int(round(launches_per_step * args.steps))
     st1 = h.state()  # before the instrumented replay, which advances the state further
     clk = clocks.stop()
+    device_error = None
+    try:  # a device-side watchdog expiry or contract violation invalidates the run
+        h.check()
+    except Exception as exc:  # noqa: BLE001 (reported in the JSON line, not swallowed)
+        device_error = str(exc)
+        print(f"bench: device error in the timed region: {device_error}", file=sys.stderr, flush=True)
     prof_ms = None
     if g_prof is not None:
         p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -285,6 +291,8 @@ def run_ours(args):
                       "parallelism": f"dp{world}: requests sharded by id mod {world}"
                       + ("; global top-B via NCCL all-gather of candidate keys" if world > 1 else "")},
            "verified_per_step": verified / args.steps, "gpu_launches": launches, "clocks": clk}
+    if device_error:
+        out["device_error"] = device_error
     if world == 1 and not args.no_profile:
         v_ms, s_ms, p_ms, n_prof = h.profile_read()
         # kernel times: the profiled steps (the last replay of the captured graph, or all

@@ -692,7 +692,8 @@ lapssd_status lapssd_check(lapssd_handle *h, uint32_t *flags_out) {
     if (e == cudaSuccess) e = cudaMemcpy(&g, h->st.g, sizeof g, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_status(e, "lapssd_check");
     if (flags_out) *flags_out = g.err;
-    if (g.err) return fail(LAPSSD_ESTATE, "device contract violation flags 0x%x", g.err);
+    if (g.err) return fail(LAPSSD_ESTATE, "device contract violation flags 0x%x (first watchdog: step %u slot %u)",
+                           g.err, g.err_where >> 16, g.err_where & 0xFFFFu);
     return LAPSSD_OK;
 }
 
@@ -909,7 +910,8 @@ lapssd_status lapssd_mc_check(lapssd_mc *h, uint32_t *flags_out) {
     if (e == cudaSuccess) e = cudaMemcpy(&g, h->st.g, sizeof g, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_status(e, "lapssd_mc_check");
     if (flags_out) *flags_out = g.err;
-    if (g.err) return fail(LAPSSD_ESTATE, "device contract violation flags 0x%x", g.err);
+    if (g.err) return fail(LAPSSD_ESTATE, "device contract violation flags 0x%x (first watchdog: step %u slot %u)",
+                           g.err, g.err_where >> 16, g.err_where & 0xFFFFu);
     return LAPSSD_OK;
 }
 

@@ -35,6 +35,9 @@ enum : uint32_t {
     E_NO_MASS = 2u,        // a row with no probability mass at all
     E_BAD_SLOT = 4u,       // slot refers to an out-of-range request
     E_TIMEOUT = 16u,       // a device-side wait exceeded its watchdog (results invalid)
+    E_TO_FIN = 32u,        // ... the verify finisher's wait for a slot's segment sums
+    E_TO_MERGE = 64u,      // ... the side select's wait for the verified slots' records
+    E_TO_SNAP = 128u,      // ... the side select's wait for the verify CTAs' snapshots
 };
 
 // Watchdog for device-side spin waits: true once `t0` is more than 2 s in the past.
@@ -52,7 +55,8 @@ struct Globals {
     int32_t count;         // size of the batch just selected (this rank)
     uint32_t err;          // sticky contract-violation flags
     uint32_t vstep;        // incremental steps committed: parity of the verify buffers
-    int32_t pad;
+    uint32_t err_where;    // first watchdog expiry: (vstep & 0xFFFF) << 16 | slot
+    uint32_t pad;
 };
 
 // Scheduler constants, passed by value to every kernel.
@@ -239,16 +243,16 @@ struct UpdIn {
     int32_t ring;  // this lane's ring slot
 };
 __device__ __forceinline__ UpdIn load_update_inputs(const State &st, const Sched &s, int32_t i, int lane) {
-    UpdIn u;
-    u.fl = st.flags[i];
+    UpdIn u;   // L1-bypassing loads: the verify kernel reads state an overlapping grid wrote
+    u.fl = __ldcg(st.flags + i);
     u.Lt = st.L_true[i];
     u.Lp = st.L_pred[i];
-    u.tok = st.acc_tok[i];
-    u.acc = st.acc_draft[i];
-    u.t = st.rounds[i];
-    u.E = st.E[i];
-    u.A = st.A[i];
-    u.ring = lane < s.gamma ? st.ring[(int64_t)i * s.gamma + lane] : 0;
+    u.tok = __ldcg(st.acc_tok + i);
+    u.acc = __ldcg(st.acc_draft + i);
+    u.t = __ldcg(st.rounds + i);
+    u.E = __ldcg(st.E + i);
+    u.A = __ldcg(st.A + i);
+    u.ring = lane < s.gamma ? __ldcg(st.ring + (int64_t)i * s.gamma + lane) : 0;
     return u;
 }
 

@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
         __syncthreads();               // everyone has finished with s_m / s_merged
         if (s_merged >= need) break;
         if (waited_too_long(t_start)) {  // watchdog: never hang the GPU
-            if (threadIdx.x == 0) atomicOr(&st.g->err, E_TIMEOUT);
+            if (threadIdx.x == 0) atomicOr(&st.g->err, E_TIMEOUT | E_TO_MERGE);
             break;
         }
         // collect the slots published since the last pass: their keys (stored as ~key,
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
             uint32_t v;
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(snap) : "memory");
             if (v >= snap_target) break;
-            if (waited_too_long(t0)) { atomicOr(&st.g->err, E_TIMEOUT); break; }
+            if (waited_too_long(t0)) { atomicOr(&st.g->err, E_TIMEOUT | E_TO_SNAP); break; }
             __nanosleep(64);
         }
         *snap = 0;
@@ -560,7 +560,15 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
         if (count_out) *count_out = cnt;
         st.g->vstep = st.g->vstep + 1;   // the next verify launch streams into the other set
     }
+    // The next verify launch carries the programmatic-serialization attribute (it overlaps
+    // the current one), and under stream capture that attribute makes every incoming
+    // kernel->kernel edge programmatic -- including the one from this kernel.  So this
+    // kernel triggers its dependents explicitly, and only once the commit (batch,
+    // descriptors, clock, step counter, snapshot counter reset) is performed at GPU scope;
+    // the verify kernel reads these with L2 (.cg) loads.
+    __threadfence();
     __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     ITRACE(100003);
     STRACE(9);
 #ifdef LAPSSD_TRACE

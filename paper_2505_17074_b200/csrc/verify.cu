@@ -273,9 +273,9 @@ constexpr int kMaxSlots = 4096;                            // slots per launch (
 constexpr int kFinCap = 64;                                // slots per finisher warp
 constexpr int kStageBudget = 192 * 1024;                   // shared memory for the ring
 #ifndef LAPSSD_POLL_NS
-#define LAPSSD_POLL_NS 32
+#define LAPSSD_POLL_NS 1024
 #endif
-constexpr int kPollNs = LAPSSD_POLL_NS;                     // finisher back-off between polls
+constexpr int kPollNs = LAPSSD_POLL_NS;  // finisher back-off between polls (measured: 32 ns of polling traffic costs ~2 us/step)
 
 template <bool BF16>
 struct VerifyCfg {
@@ -595,13 +595,26 @@ __host__ __device__ __forceinline__ int fin_slots(int B, int grid, int f0) {
     return f0 < B ? (B - 1 - f0) / (kGroups * grid) + 1 : 0;
 }
 
+// Loads of values another kernel wrote (the batch, the step counter, the clock, the
+// scheduler state) bypass L1 (ld.global.cg): with programmatic dependent launch this
+// grid starts before the previous one has completed, so nothing may be served from a
+// line an earlier grid left in this SM's L1.
+__device__ __forceinline__ SlotDesc ld_desc_cg(const SlotDesc *p) {
+    const int4 *q = reinterpret_cast<const int4 *>(p);
+    const int4 lo = __ldcg(q), hi = __ldcg(q + 1);
+    SlotDesc d;
+    d.i = lo.x; d.slab = lo.y; d.req = (uint32_t)lo.z; d.round = (uint32_t)lo.w;
+    d.r = hi.x; d.trace = (uint32_t)hi.y; d.pad[0] = hi.z; d.pad[1] = hi.w;
+    return d;
+}
+
 // (slab << 5) | (r + 1) of slot b, 0 = nothing to do: the descriptor checked against
 // sel[] (a stale descriptor or a bad slab index is a contract violation, flagged).
 __device__ __forceinline__ uint32_t slot_word(const VerifyArgs &a, int b) {
     const int4 *dp = reinterpret_cast<const int4 *>(a.desc + b);
-    const int4 dh = dp[0];  // i, slab, req, round
-    int r = dp[1].x;
-    const int si = a.sel ? a.sel[b] : dh.x;
+    const int4 dh = __ldcg(dp);  // i, slab, req, round
+    int r = __ldcg(dp + 1).x;
+    const int si = a.sel ? __ldcg(a.sel + b) : dh.x;
     if (r >= 0 && si != dh.x) {
         if (a.err) atomicOr(a.err, E_STALE_DESC);
         r = -1;
@@ -672,7 +685,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
     // the next step's launch may start on SMs as ours retire (programmatic dependent
     // launch): it uses the other (part, work) set, and its finishers wait for this grid
     // before touching outputs.  The set is picked by the committed-step parity.
-    const uint32_t vstep = a.vstep ? *a.vstep : 0u;
+    const uint32_t vstep = a.vstep ? __ldcg(a.vstep) : 0u;
     const int par = (int)(vstep & 1u);
     if (tid == 0) VSTEP_TIME(0, vstep);
 #ifdef LAPSSD_TRACE
@@ -715,8 +728,8 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
         const int nf = fin_slots(B, grid, f0);
         for (int j = lane; j < nf; j += 32) {
             const int b = f0 + j * kGroups * grid;
-            SlotDesc d = a.desc[b];
-            const int si = a.sel ? a.sel[b] : d.i;
+            SlotDesc d = ld_desc_cg(a.desc + b);
+            const int si = a.sel ? __ldcg(a.sel + b) : d.i;
             if (d.r >= 0 && (si != d.i || (uint32_t)d.slab >= (1u << 27))) d.r = -1;
             s_fin[grp][j] = d;
         }
@@ -762,7 +775,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
         if (a.fuse_update) {
             // the state updates first, two slots at a time: each stage of both slots' loads
             // (state + slab table, drafts, gathers) is one round trip
-            const int64_t now = a.st.g->now_us;
+            const int64_t now = __ldcg(&a.st.g->now_us);
             for (int j = 0; j < nf; j += 2) {
                 const SlotDesc d0 = s_fin[grp][j];
                 const bool has1 = j + 1 < nf;
@@ -809,7 +822,10 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                 for (int x = 0; x < kPartWords; ++x) all &= w[x];
                 if (__all_sync(0xFFFFFFFFu, (all & kReady) != 0)) break;
                 if (waited_too_long(t_start)) {
-                    if (lane == 0 && a.err) atomicOr(a.err, E_TIMEOUT);
+                    if (lane == 0 && a.err) {
+                        if (!(atomicOr(a.err, E_TIMEOUT | E_TO_FIN) & E_TIMEOUT) && a.st.g)
+                            a.st.g->err_where = ((vstep & 0xFFFFu) << 16) | ((uint32_t)b & 0xFFFFu);
+                    }
                     break;
                 }
                 __nanosleep(kPollNs);
