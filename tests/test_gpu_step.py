@@ -131,3 +131,47 @@ def test_step_parity_config4_full_size(L):
         _, _, na_o, _ = sim.step(P, sel_o)
         assert (nacc.cpu().numpy() == na_o).all()
         compare_state(h.state(), sim.state(), step)
+
+
+def test_step_parity_graph_replay_config4(L):
+    """The launch configuration bench.py times: laps_step captured in a CUDA graph
+    (consecutive verify launches overlap through programmatic dependent launch, the
+    select runs on the side stream) and replayed; configs[3] sizes.  Every step's
+    accepted counts and tokens, and the whole state after each replay, bit-exact."""
+    c = synth.CONFIGS["c4"]
+    B, G, reps, k = 512, 8, 3, 8
+    tr = synth.make_trace(2048, c["seed"] + 1, arrival="zero", length="uniform", len_min=512,
+                          len_max=4096, beta_ab=(7, 3))
+    pool = synth.make_pool("f2", V=128256, k=k, dtype="bf16", n_buckets=16, variants=4,
+                           seed=c["seed"] + 1, device="cuda")
+    tab = synth.slab_table(tr, 16, 4, R=32, seed=c["seed"] + 1)
+    kw = dict(BASE, k=k, seed=c["seed"] + 1)
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=128256)
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, tab.shape[1]
+    sel_o, _ = sim.select(B)
+    h.laps_select(B)
+    tok = torch.empty(G, B, k + 1, dtype=torch.int32, device="cuda")
+    nacc = torch.empty(G, B, dtype=torch.int32, device="cuda")
+    # one eager step first (as the bench's warm-up), checked like the rest
+    h.laps_step(rows, B, tokens=tok[0], n_accept=nacc[0])
+    _, tok_o, na_o, _ = sim.step(P, sel_o)
+    assert (nacc[0].cpu().numpy() == na_o).all() and (tok[0].cpu().numpy() == tok_o).all()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for t in range(G):
+            h.laps_step(rows, B, tokens=tok[t], n_accept=nacc[t])
+    for rep in range(reps):
+        g.replay()
+        torch.cuda.synchronize()
+        T, NA = tok.cpu().numpy(), nacc.cpu().numpy()
+        for t in range(G):   # (a different batch would show in r / tokens / the state)
+            cnt, tok_o, na_o, _ = sim.step(P, sel_o)   # sel_o becomes the next batch
+            assert (NA[t] == na_o).all(), f"replay {rep} step {t}: r differs"
+            assert (T[t] == tok_o).all(), f"replay {rep} step {t}: tokens differ"
+        compare_state(h.state(), sim.state(), f"replay {rep}")
+        assert (h.sel[:B].cpu().numpy() == sel_o).all(), f"replay {rep}: next batch differs"
+    assert h.check() == 0
