@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-path", action="store_true",
+                    help="N=1 only: time the N>1 step (laps_step_dist) with a one-rank NCCL communicator")
     ap.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "verify_dram.json"))
     ap.add_argument("--workload", choices=["c4", "mc"], default="c4",
                     help="c4 = configs[3] (the headline); mc = configs[4] Monte-Carlo traces")
@@ -180,6 +182,20 @@ def run_ours(args):
         h.laps_candidates(Cn, cand[: Cn + 1])
         dist.all_gather_into_tensor(cand[Cn + 1:], cand[: Cn + 1])
         h.laps_merge(cand[Cn + 1:], Cn, B)
+    elif args.dist_path:
+        # the N>1 step (laps_step_dist: candidates + ncclAllGather + merge) on one rank, to
+        # time its cost on the one GPU available; a one-rank gloo group only carries the
+        # NCCL unique id
+        import torch.distributed as tdist
+        tdist.init_process_group("gloo", rank=0, world_size=1,
+                                 init_method=f"tcp://127.0.0.1:{29500 + os.getpid() % 1000}")
+        comm = L.nccl_comm()
+        tdist.destroy_process_group()
+        cand = torch.zeros(2 * (Cn + 1), dtype=torch.int64, device=dev)
+        h.laps_candidates(Cn, cand[: Cn + 1])
+        cand[Cn + 1:].copy_(cand[: Cn + 1])
+        h.laps_merge(cand[Cn + 1:], Cn, B)
+        args.no_profile = True
     else:
         h.laps_select(B)
     G = min(args.graph_steps, args.steps) if args.graph_steps > 0 else 0
@@ -187,7 +203,7 @@ def run_ours(args):
                       device=dev)
 
     def step(t):
-        if world > 1:
+        if comm is not None:
             h.laps_step_dist(comm, rows, B, Cn, cand)
         else:
             h.laps_step(rows, B, n_accept=hist[t])
@@ -288,7 +304,7 @@ def run_ours(args):
                       "B_per_gpu": B_local, "B_global": B, "V": args.V, "k": args.k,
                       "pool": f"F2 zipf, {pool.S} slabs x {(2 * args.k + 1) * args.V * 2 / 1e6:.2f} MB",
                       "l2": "inputs larger than L2 (4.5 GB slab pool, ~255 MB of rows per step)",
-                      "parallelism": f"dp{world}: requests sharded by id mod {world}"
+                      "parallelism": f"dp{world}: requests sharded by id mod {world}" + ("; laps_step_dist path" if comm is not None and world == 1 else "")
                       + ("; global top-B via NCCL all-gather of candidate keys" if world > 1 else "")},
            "verified_per_step": verified / args.steps, "gpu_launches": launches, "clocks": clk}
     if device_error:

@@ -628,6 +628,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
     VerifyArgs a;
     lapssd_status st = fill_step_verify(h, rows, B_global, sel_inout, nullptr, nullptr, a);
     if (st != LAPSSD_OK) return st;
+    a.count_dev = &h->st.g->count;   // this rank's slots are [0, count) of the B_global
     cudaStream_t s = (cudaStream_t)stream;
     h->last_stream = s;
     st = step_verify(h, a, sel_inout, B_global, s);

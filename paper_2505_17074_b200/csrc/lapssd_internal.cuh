@@ -471,6 +471,10 @@ struct VerifyArgs {
     uint32_t *work1;
     const uint32_t *vstep;
     int32_t fuse_update;
+    // nullable: the number of leading slots that hold work ([0, *count_dev) of the B
+    // slots; the multi-GPU batch keeps this rank's slots first and pads with -1), so the
+    // producers never cycle empty items through the ring
+    const int32_t *count_dev;
     State st;                   // handle mode only
     Sched sc;
     uint32_t *err;              // sticky device flags (nullable in stateless mode)

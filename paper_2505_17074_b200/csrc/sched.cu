@@ -665,22 +665,62 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
     __shared__ int s_tmp[64];
     __shared__ int s_gcount;
     __shared__ unsigned long long s_next;
-    const int total = sc.world * C;
-    const int npow2 = next_pow2(total > 0 ? total : 1);
+    // Every rank's candidate list is sorted (candidates_kernel), so the global order is a
+    // G-way merge: each key's global rank = its index in its own list + the number of
+    // smaller keys in every other list (keys are unique: the global id is in the low
+    // bits).  Each thread ranks a run of kRun consecutive keys of one list: one binary
+    // search per other list for the first key, then a forward scan (the counts are
+    // monotone along the run).  Keys ranked < B land at their rank in top[].
+    const int G = sc.world;
+    const int total = G * C;
+    const int lim = B < total ? B : total;
+    uint64_t *lists = s_buf;            // [G*C]
+    uint64_t *top = s_buf + total;      // [lim] the global top-B, ascending
     if (threadIdx.x == 0) { s_gcount = 0; s_next = ~0ull; }
     __syncthreads();
-    for (int x = threadIdx.x; x < npow2; x += blockDim.x) {
-        uint64_t key = ~0ull;
-        if (x < total) key = all_cand[(int64_t)(x / C) * (C + 1) + (x % C)];
-        s_buf[x] = key;
-    }
-    for (int g = threadIdx.x; g < sc.world; g += blockDim.x)
+    for (int x = threadIdx.x; x < total; x += blockDim.x)
+        lists[x] = all_cand[(int64_t)(x / C) * (C + 1) + (x % C)];
+    for (int x = threadIdx.x; x < lim; x += blockDim.x) top[x] = ~0ull;
+    for (int g = threadIdx.x; g < G; g += blockDim.x)
         atomicMin(&s_next, (unsigned long long)all_cand[(int64_t)g * (C + 1) + C]);
     __syncthreads();
-    const bool two = npow2 >= 64 && npow2 <= kMergeCap;
-    const uint64_t *keys = block_sort(s_buf, two ? s_buf + npow2 : nullptr, npow2);
+    constexpr int kRun = 8;
+    const int runs_per_list = (C + kRun - 1) / kRun;
+    for (int u = threadIdx.x; u < G * runs_per_list; u += blockDim.x) {
+        const int g = u / runs_per_list, c0 = (u % runs_per_list) * kRun;
+        if (c0 >= lim) continue;                       // rank >= own index >= B
+        const uint64_t *Lg = lists + (int64_t)g * C;
+        if (Lg[c0] == ~0ull) continue;                 // padding (ineligible) from here on
+        int rk[kRun];
+#pragma unroll
+        for (int e = 0; e < kRun; ++e) rk[e] = c0 + e;
+        for (int h = 0; h < G; ++h) {
+            if (h == g) continue;
+            const uint64_t *Lh = lists + (int64_t)h * C;
+            int lo = 0, hi = C;                          // lower_bound of the run's first key
+            const uint64_t x0 = Lg[c0];
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (Lh[mid] < x0) lo = mid + 1; else hi = mid;
+            }
+#pragma unroll
+            for (int e = 0; e < kRun; ++e) {
+                if (c0 + e >= C) break;
+                const uint64_t x = Lg[c0 + e];
+                while (lo < C && Lh[lo] < x) ++lo;
+                rk[e] += lo;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < kRun; ++e) {
+            if (c0 + e >= C) break;
+            const uint64_t x = Lg[c0 + e];
+            if (x != ~0ull && rk[e] < lim) top[rk[e]] = x;
+        }
+    }
+    __syncthreads();
+    const uint64_t *keys = top;
     // global batch: first B valid keys; own = id % world == rank
-    const int lim = B < npow2 ? B : npow2;
     const int per = (lim + (int)blockDim.x - 1) / (int)blockDim.x;
     const int lo = (int)threadIdx.x * per;
     int own = 0, valid = 0;
@@ -727,7 +767,8 @@ cudaError_t launch_merge(const State &st, const Sched &sc, const RowsDev &rw, Sl
                          const uint64_t *all_cand, int32_t C, int32_t B, int32_t *sel_out,
                          int32_t *count_out, cudaStream_t s) {
     const int total = sc.world * C;
-    merge_kernel<<<1, kSelThreads, sort_smem_bytes(total > 0 ? total : 1), s>>>(st, sc, rw, desc, all_cand, C,
+    const size_t smem = ((size_t)total + (size_t)(B < total ? B : total)) * sizeof(uint64_t);
+    merge_kernel<<<1, kSelThreads, smem > 0 ? smem : 8, s>>>(st, sc, rw, desc, all_cand, C,
                                                                                 B, sel_out, count_out);
     count_launch();
     return cudaGetLastError();

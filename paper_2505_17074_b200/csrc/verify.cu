@@ -672,7 +672,12 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
     __shared__ uint64_t s_fb[kGroups][kMaxSegs];       // Z = 0 fallback sums
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nc = a.n_chunks;
-    const int n_items = B * nc;
+    int B_work = B;
+    if (a.count_dev) {
+        const int c = __ldcg(a.count_dev);
+        B_work = c < 0 ? 0 : c < B ? c : B;
+    }
+    const int n_items = B_work * nc;
     const int grid = (int)gridDim.x;
     // warp 0 producer; warps 1..16 consumers (gw = segment); warps 17, 18 finishers (grp)
     const int gw = warp >= 1 && warp <= kConsumerWarps ? warp - 1 : -1;

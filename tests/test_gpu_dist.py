@@ -87,3 +87,52 @@ def test_two_handles_candidates_merge_equal_single_rank(L, policy):
         assert (st["C_us"] == ref["C_us"][g::G]).all()
         assert (st["acc_draft"] == ref["acc_draft"][g::G]).all()
         assert hs[g].check() == 0
+
+
+def test_laps_step_dist_one_rank_lockstep(L, monkeypatch):
+    """laps_step_dist end to end (verify + candidates + ncclAllGather + merge) with a
+    one-rank NCCL communicator, step by step against the oracle: batch, r, state."""
+    import torch.distributed as dist
+    monkeypatch.setenv("MASTER_ADDR", "127.0.0.1")
+    monkeypatch.setenv("MASTER_PORT", "29561")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = L.nccl_comm()
+        seed, B, R = 43, 16, 16
+        tr = synth.make_trace(120, seed, arrival="poisson", rate_per_s=60.0, len_mu=np.log(30),
+                              len_sigma=0.6, len_min=4, len_max=200, beta_ab=(4, 2), drift=True)
+        pool = synth.make_pool("f2", V=4096, k=4, dtype="bf16", n_buckets=8, variants=3, seed=seed,
+                               device="cuda")
+        tab = synth.slab_table(tr, 8, 3, R=R, seed=seed)
+        kw = dict(K=4, s1_up_us=56 * MS, gamma=5, delta=0.05, k=4, t_ssm_us=1 * MS, t_llm_us=10 * MS,
+                  seed=17)
+        P = pool.numpy()
+        P["slab_tab"], P["R"] = tab, R
+        sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
+        h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=4096,
+                     rank=0, world=1)
+        rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
+        Cn = B
+        cand = torch.zeros(2 * (Cn + 1), dtype=torch.int64, device="cuda")
+        h.laps_candidates(Cn, cand[: Cn + 1])
+        cand[Cn + 1:].copy_(cand[: Cn + 1])
+        h.laps_merge(cand[Cn + 1:], Cn, B)
+        sel_o, _ = sim.select(B)
+        for step in range(400):
+            sel_g = h.sel[:B].cpu().numpy()
+            assert (sel_g == sel_o).all(), f"step {step}: batch differs"
+            if sim.state()["done"].all():
+                break
+            h.laps_step_dist(comm, rows, B, Cn, cand)
+            sim.step(P, sel_o)
+            if step % 4 == 0:
+                g, o = h.state(), sim.state()
+                for f in ("acc_tok", "acc_draft", "rounds", "E_us", "C_us", "level", "perceptible",
+                          "pinned", "key"):
+                    assert (np.asarray(g[f]) == np.asarray(o[f])).all(), f"step {step}: {f}"
+                assert g["now_us"] == o["now_us"], f"step {step}: clock"
+        assert sim.state()["done"].all()
+        assert h.check() == 0
+        L.nccl_comm_destroy(comm)
+    finally:
+        dist.destroy_process_group()
