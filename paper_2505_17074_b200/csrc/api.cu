@@ -631,18 +631,64 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
     a.count_dev = &h->st.g->count;   // this rank's slots are [0, count) of the B_global
     cudaStream_t s = (cudaStream_t)stream;
     h->last_stream = s;
-    st = step_verify(h, a, sel_inout, B_global, s);
-    if (st != LAPSSD_OK) return st;
     uint64_t *local = cand_scratch;
     uint64_t *all = cand_scratch + (C + 1);
-    st = cuda_status(launch_candidates(h->st, h->sc, C, local, s), "step_dist candidates");
+    int bp = 1;
+    while (bp < B_global) bp <<= 1;
+    static const bool serial = getenv("LAPSSD_DIST_SERIAL") != nullptr;  // A/B switch
+    const bool overlapped = !serial && rows->slab_tab != nullptr && bp <= 4096 && C <= B_global;
+    if (!overlapped) {   // verify, then candidates -> all-gather -> merge on the stream
+        st = step_verify(h, a, sel_inout, B_global, s);
+        if (st != LAPSSD_OK) return st;
+        st = cuda_status(launch_candidates(h->st, h->sc, C, local, s), "step_dist candidates");
+        if (st != LAPSSD_OK) return st;
+        st = nccl_status(allgather(local, all, (size_t)(C + 1), kNcclUint64, nccl_comm, s), "ncclAllGather");
+        if (st != LAPSSD_OK) return st;
+        st = cuda_status(launch_merge(h->st, h->sc, a.rows, h->desc, all, C, B_global, sel_inout, count_out, s),
+                         "step_dist merge");
+        if (st == LAPSSD_OK) h->desc_valid = true;
+        return st;
+    }
+    // Overlapped as laps_step: the verify kernel (finishers run a3 and publish records)
+    // on the stream; on the side stream the select kernel builds this rank's candidates
+    // from the presort + the published records, the all-gather and the global merge +
+    // commit follow, all while the rows stream.  The merge kernel ends with the fenced
+    // trigger the next (programmatic) verify launch needs.
+    if (!h->desc_valid) {
+        st = cuda_status(launch_accept(a.rows, sel_inout, &h->st, &h->sc, nullptr, nullptr, nullptr, h->sc.seed, 0,
+                                       B_global, h->desc, s), "accept");
+        if (st != LAPSSD_OK) return st;
+    }
+    cudaError_t ce = cudaEventRecord(h->ev_fork, s);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_dist fork");
+    h->desc_valid = false;
+    a.fin = h->fin;
+    a.fin_key = h->fin_key;
+    a.snap = h->snap;
+    a.part1 = h->part + (size_t)h->max_batch * h->n_chunks * kPartWords;
+    a.work1 = h->work + 2;
+    a.vstep = &h->st.g->vstep;
+    static const bool no_pdl = getenv("LAPSSD_NO_PDL") != nullptr;
+    st = cuda_status(launch_verify_grid(a, B_global, 1, !no_pdl, s), "laps_step_dist verify");
     if (st != LAPSSD_OK) return st;
-    st = nccl_status(allgather(local, all, (size_t)(C + 1), kNcclUint64, nccl_comm, s), "ncclAllGather");
+    ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_dist fork wait");
+    st = cuda_status(launch_select_side(h->st, h->sc, a.rows, sel_inout, h->desc, B_global, h->pre, h->fin,
+                                        h->fin_key, h->snap, (uint32_t)verify_grid(B_global, a.n_chunks, 1),
+                                        nullptr, h->side, local, C),
+                     "laps_step_dist candidates");
     if (st != LAPSSD_OK) return st;
-    st = cuda_status(launch_merge(h->st, h->sc, a.rows, h->desc, all, C, B_global, sel_inout, count_out, s),
-                     "step_dist merge");
-    if (st == LAPSSD_OK) h->desc_valid = true;
-    return st;
+    st = nccl_status(allgather(local, all, (size_t)(C + 1), kNcclUint64, nccl_comm, h->side), "ncclAllGather");
+    if (st != LAPSSD_OK) return st;
+    st = cuda_status(launch_merge(h->st, h->sc, a.rows, h->desc, all, C, B_global, sel_inout, count_out, h->side),
+                     "laps_step_dist merge");
+    if (st != LAPSSD_OK) return st;
+    ce = cudaEventRecord(h->ev_join, h->side);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_dist join");
+    ce = cudaStreamWaitEvent(s, h->ev_join, 0);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_dist join wait");
+    h->desc_valid = true;
+    return LAPSSD_OK;
 }
 
 // ---------------------------------------------------------------- snapshot / check

@@ -540,7 +540,8 @@ bool verify_fits(int32_t B, int32_t n_chunks, int32_t reserve_sms);      // per-
 int verify_max_batch(int32_t n_chunks, int32_t reserve_sms);
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
                                int32_t B, PreSelect *pre, const SelRec *fin, uint64_t *fin_key, uint32_t *snap,
-                               uint32_t snap_target, int32_t *count_out, cudaStream_t s);
+                               uint32_t snap_target, int32_t *count_out, cudaStream_t s,
+                               uint64_t *cand_out = nullptr, int32_t C = 0);
 // Monte-Carlo replicas (mc.cu): T traces over one concatenated request SoA.
 struct McDev {
     const int64_t *off;         // [T+1] request offsets of the traces

@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
                                                                    int32_t *sel, SlotDesc *desc, int32_t B,
                                                                    PreSelect *pre, const SelRec *fin, uint64_t *fin_key,
                                                                    uint32_t *snap, uint32_t snap_target,
-                                                                   int32_t *count_out) {
+                                                                   int32_t *count_out, uint64_t *cand_out,
+                                                                   int32_t C) {
     extern __shared__ uint64_t s_buf[];
     STRACE(8);
 #ifdef LAPSSD_TRACE
@@ -500,6 +501,26 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
         g_dbg_rec[b][3] = L[b];
     }
 #endif
+    if (cand_out) {
+        // multi-GPU (a8): this rank's C best keys (+ its next arrival) for the all-gather;
+        // merge_kernel commits the global batch.  The verified batch's running flags are
+        // cleared here, as candidates_kernel does after building its keys.
+        for (int c = threadIdx.x; c < C; c += T) {
+            const uint64_t key = c < bp ? L[c] : ~0ull;
+            cand_out[c] = (key >> 63) ? ~0ull : key;
+        }
+        for (int b = threadIdx.x; b < B; b += T) {
+            const int i = sel[b];
+            if (i < 0) continue;
+            st.flags[i] = (rec_smem ? brec[b].flags : fin[b].flags) & ~F_RUNNING;
+        }
+        if (threadIdx.x == 0) {
+            cand_out[C] = s_cursor < n ? (uint64_t)st.arrival[s_cursor] : ~0ull;
+            st.g->now_us = s_now;
+            st.g->cursor = s_cursor;
+        }
+        return;
+    }
     ITRACE(100000);
     SSTEP(3);
     // ---------------- commit
@@ -579,7 +600,8 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
 
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
                                int32_t B, PreSelect *pre, const SelRec *fin, uint64_t *fin_key, uint32_t *snap,
-                               uint32_t snap_target, int32_t *count_out, cudaStream_t s) {
+                               uint32_t snap_target, int32_t *count_out, cudaStream_t s, uint64_t *cand_out,
+                               int32_t C) {
     int np = 1, bp = 1;
     while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
     while (bp < B) bp <<= 1;
@@ -587,7 +609,7 @@ cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &
     const size_t b = (size_t)4 * bp * sizeof(uint64_t) + 2 * (size_t)((sc.n + 7) & ~7) * sizeof(int16_t) + 64 +
                      (bp <= 1024 ? 2 * (size_t)bp * sizeof(SelRec) : 0);
     select_side_kernel<<<1, kSideThreads, a > b ? a : b, s>>>(st, sc, rw, sel, desc, B, pre, fin, fin_key, snap,
-                                                              snap_target, count_out);
+                                                              snap_target, count_out, cand_out, C);
     count_launch();
     return cudaGetLastError();
 }
@@ -760,7 +782,12 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
         st.g->prev_count = g;
         st.g->count = n_own;
         if (count_out) *count_out = n_own;
+        st.g->vstep = st.g->vstep + 1;   // overlapped laps_step_dist: the next verify's buffer set
     }
+    // the next verify launch may be a programmatic dependent (see select_side_kernel)
+    __threadfence();
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 cudaError_t launch_merge(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc,
