@@ -45,6 +45,11 @@ class VerifyOut(C.Structure):
                 ("z_real", C.c_double), ("z_rel_err", C.c_double), ("margin_rel", C.c_double)]
 
 
+class LogitsOut(C.Structure):
+    _fields_ = [("r", C.c_int32), ("y", C.c_int32), ("fallback", C.c_int32), ("pad", C.c_int32),
+                ("Z_lo", C.c_uint64), ("Z_hi", C.c_uint64), ("Sp", C.c_uint64), ("Sq", C.c_uint64)]
+
+
 class OrcConfig(C.Structure):
     _fields_ = [("policy", C.c_int32), ("K", C.c_int32), ("s1_up_us", C.c_int64),
                 ("M", C.c_double), ("gamma", C.c_int32), ("delta", C.c_double),
@@ -79,6 +84,13 @@ def lib():
                                          C.POINTER(VerifyOut)]
         L.orc_verify_request.restype = i32
         L.orc_verify_many.argtypes = [vp, vp, i32, i64, i32, i32, vp, vp, vp, u64, vp, vp]
+        L.orc_exp_hat.argtypes = [C.c_float]
+        L.orc_exp_hat.restype = C.c_float
+        L.orc_verify_logits_request.argtypes = [vp, vp, i32, i64, i32, vp, u32, u32, u64, u32, vp,
+                                                C.POINTER(LogitsOut)]
+        L.orc_verify_logits_request.restype = i32
+        L.orc_verify_logits_many.argtypes = [vp, vp, i32, i64, i32, i32, vp, vp, vp, u64, vp, vp]
+        L.orc_verify_logits_batch.argtypes = [vp, vp, i32, i64, i32, i32, vp, vp, vp, vp, u64, vp, vp, vp]
         L.orc_thresholds.argtypes = [i32, i64, C.c_double, vp]
         L.orc_thresholds.restype = i32
         L.orc_eq6.argtypes = [i64, C.c_double, i32, i64, i64]
@@ -159,6 +171,60 @@ def verify_many(p_rows, q_rows, drafts, req_ids, rounds, seed):
     lib().orc_verify_many(_ptr(p), _ptr(q), _dtype_code(p), V, k, n, _ptr(d), _ptr(ri), _ptr(ro),
                           int(seed) & (2**64 - 1), _ptr(tok), _ptr(r))
     return tok, r
+
+
+def exp_hat(d) -> float:
+    """AMB-30: e^d on [-28, 0] by the fixed fp32 operation sequence."""
+    return float(lib().orc_exp_hat(float(d)))
+
+
+def verify_logits_request(zp_rows, zq_rows, draft, req_id, round_idx, seed, trace=0):
+    """f1: P:57-64 / P:200 with p = softmax(zp), q = softmax(zq), quantised
+    as AMB-30.  zp_rows [k+1,V], zq_rows [k,V] logits (float32 or uint16 bf16 bits)."""
+    p = np.ascontiguousarray(zp_rows)
+    q = np.ascontiguousarray(zq_rows)
+    k = q.shape[0]
+    V = p.shape[1]
+    assert p.shape == (k + 1, V) and q.shape == (k, V) and p.dtype == q.dtype
+    d = _c(draft, np.int32)
+    tok = np.zeros(k + 1, np.int32)
+    out = LogitsOut()
+    lib().orc_verify_logits_request(_ptr(p), _ptr(q), _dtype_code(p), V, k, _ptr(d), int(req_id),
+                                    int(round_idx), int(seed) & (2**64 - 1), int(trace), _ptr(tok),
+                                    C.byref(out))
+    return tok, out
+
+
+def verify_logits_many(zp_rows, zq_rows, drafts, req_ids, rounds, seed):
+    p = np.ascontiguousarray(zp_rows)
+    q = np.ascontiguousarray(zq_rows)
+    k, V = q.shape
+    d = _c(drafts, np.int32)
+    n = d.shape[0]
+    tok = np.zeros((n, k + 1), np.int32)
+    r = np.zeros(n, np.int32)
+    lib().orc_verify_logits_many(_ptr(p), _ptr(q), _dtype_code(p), V, k, n, _ptr(d),
+                                 _ptr(_c(req_ids, np.uint32)), _ptr(_c(rounds, np.uint32)),
+                                 int(seed) & (2**64 - 1), _ptr(tok), _ptr(r))
+    return tok, r
+
+
+def verify_logits_batch(zp, zq, drafts, slab, req_ids, rounds, seed):
+    """B slots; slot b reads slab slab[b] of zp [S,k+1,V], zq [S,k,V], drafts [S,k].
+    Returns (tokens [B,k+1], r [B], Z [B,2] = (lo, hi) of the integer residual mass)."""
+    p = np.ascontiguousarray(zp)
+    q = np.ascontiguousarray(zq)
+    S, k, V = q.shape
+    sl = _c(slab, np.int32)
+    B = sl.shape[0]
+    tok = np.zeros((B, k + 1), np.int32)
+    r = np.zeros(B, np.int32)
+    z = np.zeros((B, 2), np.uint64)
+    lib().orc_verify_logits_batch(_ptr(p), _ptr(q), _dtype_code(p), V, k, B, _ptr(sl),
+                                  _ptr(_c(drafts, np.int32)), _ptr(_c(req_ids, np.uint32)),
+                                  _ptr(_c(rounds, np.uint32)), int(seed) & (2**64 - 1), _ptr(tok),
+                                  _ptr(r), _ptr(z))
+    return tok, r, z
 
 
 def thresholds(K, s1_up_us, M):

@@ -202,6 +202,187 @@ void orc_verify_many(const void *p_rows, const void *q_rows, int32_t dtype, int6
 }
 
 /* ------------------------------------------------------------------------ */
+/* (1b) Verification from LOGITS (DESIGN.md AMB-30).          */
+/* p = softmax of the target head's logits, q = softmax of the draft head's,  */
+/* then exactly the rejection-sampling rule of P:59-64 / P:200.  The softmax  */
+/* is quantised so that every decision is an exact integer comparison:        */
+/*   m_j = max_v z_j[v];  E_j[v] = floor(exphat(fl32(z_j[v] - m_j)) * 2^40);  */
+/*   S_j = sum_v E_j[v];  p^_j(v) = E_j[v] / S_j.                              */
+/* ------------------------------------------------------------------------ */
+
+/* e^d for d in [-28, 0] with a FIXED sequence of IEEE fp32 operations (so any
+ * implementation that performs the same operations gets the same bits):
+ * n = rint(d * log2 e), r = d - n ln2 (two-constant Cody-Waite with fmaf),
+ * e^r by the degree-7 Taylor polynomial in Horner form with fmaf, times 2^n
+ * (exact: n in [-41, 0]).  Below -28, e^d < 2^-40 and E = 0 anyway. */
+float orc_exp_hat(float d)
+{
+    if (!(d >= -28.0f)) return 0.0f;
+    if (d > 0.0f) d = 0.0f;
+    float n = rintf(d * 0x1.715476p+0f);
+    float r = fmaf(-n, 0x1.62e4p-1f, d);
+    r = fmaf(-n, 0x1.7f7d1cp-20f, r);
+    float p = 0x1.a01a02p-13f;                       /* 1/7! */
+    p = fmaf(p, r, 0x1.6c16c2p-10f);                 /* 1/6! */
+    p = fmaf(p, r, 0x1.111112p-7f);                  /* 1/5! */
+    p = fmaf(p, r, 0x1.555556p-5f);                  /* 1/4! */
+    p = fmaf(p, r, 0x1.555556p-3f);                  /* 1/3! */
+    p = fmaf(p, r, 0x1p-1f);                         /* 1/2! */
+    p = fmaf(p, r, 1.0f);
+    p = fmaf(p, r, 1.0f);
+    return ldexpf(p, (int)n);
+}
+
+static float load_logit(const void *rows, int32_t dtype, int64_t idx)
+{
+    return load_prob(rows, dtype, idx);               /* same storage formats */
+}
+
+/* E = floor(exphat(z - m) * 2^40): the 2^40 scaling is exact, the cast truncates. */
+static uint64_t e40(float z, float m)
+{
+    float e = orc_exp_hat(z - m);
+    return (uint64_t)(e * 0x1p40f);
+}
+
+/* Row normaliser: max and the integer mass S = sum_v E[v]. */
+static void row_norm(const void *rows, int32_t dtype, int64_t off, int64_t V, float *m_out, uint64_t *S_out)
+{
+    float m = load_logit(rows, dtype, off);
+    for (int64_t v = 1; v < V; v++) {
+        float z = load_logit(rows, dtype, off + v);
+        if (z > m) m = z;
+    }
+    uint64_t S = 0;
+    for (int64_t v = 0; v < V; v++) S += e40(load_logit(rows, dtype, off + v), m);
+    *m_out = m;
+    *S_out = S;
+}
+
+int32_t orc_verify_logits_request(const void *zp_rows, const void *zq_rows, int32_t dtype,
+                                  int64_t V, int32_t k, const int32_t *draft,
+                                  uint32_t req_id, uint32_t round_idx, uint64_t seed,
+                                  uint32_t trace, int32_t *tokens, orc_logits_out *out)
+{
+    /* Step 1: acceptance, sequentially.  accept iff u < p^/q^, i.e.
+     * u24 / 2^24 < (Ep / Sp) / (Eq / Sq)  <=>  u24 * Eq * Sp < 2^24 * Ep * Sq
+     * (exact in 128-bit integers: <= 2^24 * 2^40 * 2^57). */
+    int32_t r = k;
+    float mp = 0.0f, mq = 0.0f;
+    uint64_t Sp = 0, Sq = 0;
+    for (int32_t j = 0; j < k; j++) {
+        uint32_t u4[4];
+        draw(seed, req_id, round_idx, 0, (uint32_t)(j / 4), trace, u4);
+        uint32_t u24 = u4[j % 4] >> 8;
+        int32_t x = draft[j];
+        row_norm(zp_rows, dtype, (int64_t)j * V, V, &mp, &Sp);
+        row_norm(zq_rows, dtype, (int64_t)j * V, V, &mq, &Sq);
+        uint64_t Ep = e40(load_logit(zp_rows, dtype, (int64_t)j * V + x), mp);
+        uint64_t Eq = e40(load_logit(zq_rows, dtype, (int64_t)j * V + x), mq);
+        int accept = (u128)u24 * Eq * Sp < ((u128)Ep * Sq) << 24;
+        if (!accept) { r = j; break; }
+    }
+
+    /* Step 2: the emitted token's distribution.  r < k: norm(max(0, p^_r - q^_r)),
+     * R_v = max(0, Ep_v Sq - Eq_v Sp) (the residual times Sp Sq, exact).
+     * r = k: the bonus row p^_k, R_v = Ep_v.  AMB-20: no residual mass -> p^_r. */
+    const int64_t off = (int64_t)r * V;
+    if (r == k) {
+        row_norm(zp_rows, dtype, off, V, &mp, &Sp);
+    }
+    int use_q = (r < k);
+    u128 Z = 0;
+    for (int64_t v = 0; v < V; v++) {
+        u128 a = (u128)e40(load_logit(zp_rows, dtype, off + v), mp);
+        if (use_q) {
+            u128 b = (u128)e40(load_logit(zq_rows, dtype, off + v), mq);
+            a = a * Sq;
+            b = b * Sp;
+            Z += a > b ? a - b : 0;
+        } else {
+            Z += a;
+        }
+    }
+    int fallback = 0;
+    if (Z == 0 && use_q) {
+        fallback = 1;
+        use_q = 0;
+        for (int64_t v = 0; v < V; v++) Z += e40(load_logit(zp_rows, dtype, off + v), mp);
+    }
+
+    /* Step 3: inverse-CDF sample: t = floor(U Z / 2^64), U a 64-bit uniform,
+     * computed as U * Z_hi + floor(U * Z_lo / 2^64) (Z < 2^120), then
+     * y = min{ v : sum_{w <= v} R_w > t }. */
+    uint32_t u4[4];
+    draw(seed, req_id, round_idx, 1, 0, trace, u4);
+    uint64_t U = ((uint64_t)u4[0] << 32) | u4[1];
+    uint64_t Zhi = (uint64_t)(Z >> 64), Zlo = (uint64_t)Z;
+    u128 t = (u128)U * Zhi + (((u128)U * Zlo) >> 64);
+    int32_t y = (int32_t)(V - 1);
+    if (Z == 0) {
+        y = (r < k) ? draft[r] : 0;
+    } else {
+        u128 c = 0;
+        for (int64_t v = 0; v < V; v++) {
+            u128 a = (u128)e40(load_logit(zp_rows, dtype, off + v), mp);
+            u128 Rv;
+            if (use_q) {
+                u128 b = (u128)e40(load_logit(zq_rows, dtype, off + v), mq);
+                a = a * Sq;
+                b = b * Sp;
+                Rv = a > b ? a - b : 0;
+            } else {
+                Rv = a;
+            }
+            if (c + Rv > t) { y = (int32_t)v; break; }
+            c += Rv;
+        }
+    }
+    for (int32_t j = 0; j < r; j++) tokens[j] = draft[j];
+    tokens[r] = y;
+    for (int32_t j = r + 1; j <= k; j++) tokens[j] = -1;
+    if (out) {
+        out->r = r;
+        out->y = y;
+        out->fallback = fallback;
+        out->Z_lo = (uint64_t)Z;
+        out->Z_hi = (uint64_t)(Z >> 64);
+        out->Sp = Sp;
+        out->Sq = use_q ? Sq : 0;
+    }
+    return r;
+}
+
+void orc_verify_logits_many(const void *zp_rows, const void *zq_rows, int32_t dtype, int64_t V,
+                            int32_t k, int32_t n_trials, const int32_t *drafts,
+                            const uint32_t *req_ids, const uint32_t *rounds, uint64_t seed,
+                            int32_t *tokens_out, int32_t *r_out)
+{
+    for (int32_t i = 0; i < n_trials; i++)
+        r_out[i] = orc_verify_logits_request(zp_rows, zq_rows, dtype, V, k, drafts + (size_t)i * k,
+                                             req_ids[i], rounds[i], seed, 0,
+                                             tokens_out + (size_t)i * (k + 1), NULL);
+}
+
+/* B independent slots, each with its own rows (slab index per slot): the batch form
+ * of spec_verify_logits for the GPU parity tests. */
+void orc_verify_logits_batch(const void *zp, const void *zq, int32_t dtype, int64_t V, int32_t k,
+                             int32_t B, const int32_t *slab, const int32_t *drafts,
+                             const uint32_t *req_ids, const uint32_t *rounds, uint64_t seed,
+                             int32_t *tokens_out, int32_t *r_out, uint64_t *z_out)
+{
+    const size_t esz = dtype == ORC_BF16 ? 2 : 4;
+    for (int32_t b = 0; b < B; b++) {
+        const char *pr = (const char *)zp + (size_t)slab[b] * (size_t)(k + 1) * (size_t)V * esz;
+        const char *qr = (const char *)zq + (size_t)slab[b] * (size_t)k * (size_t)V * esz;
+        orc_logits_out o;
+        r_out[b] = orc_verify_logits_request(pr, qr, dtype, V, k, drafts + (size_t)slab[b] * k, req_ids[b],
+                                             rounds[b], seed, 0, tokens_out + (size_t)b * (k + 1), &o);
+        if (z_out) { z_out[2 * b] = o.Z_lo; z_out[2 * b + 1] = o.Z_hi; }
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* Scheduler pieces.                                                         */
 /* ------------------------------------------------------------------------ */
 

@@ -63,6 +63,30 @@ void orc_verify_many(const void *p_rows, const void *q_rows, int32_t dtype, int6
                      const uint32_t *req_ids, const uint32_t *rounds, uint64_t seed,
                      int32_t *tokens_out, int32_t *r_out);
 
+/* ---- (1b) verification from logits ---- */
+typedef struct {
+    int32_t  r, y, fallback, pad;
+    uint64_t Z_lo, Z_hi;   /* integer residual mass (times Sp Sq when r < k)        */
+    uint64_t Sp, Sq;       /* integer softmax masses of the rows at position r      */
+} orc_logits_out;
+
+/* e^d on [-28, 0] by a fixed fp32 operation sequence (0 below -28). */
+float orc_exp_hat(float d);
+
+/* zp_rows: (k+1) rows of V logits; zq_rows: k rows; dtype as above.  Returns r. */
+int32_t orc_verify_logits_request(const void *zp_rows, const void *zq_rows, int32_t dtype,
+                                  int64_t V, int32_t k, const int32_t *draft,
+                                  uint32_t req_id, uint32_t round_idx, uint64_t seed,
+                                  uint32_t trace, int32_t *tokens, orc_logits_out *out);
+void orc_verify_logits_many(const void *zp_rows, const void *zq_rows, int32_t dtype, int64_t V,
+                            int32_t k, int32_t n_trials, const int32_t *drafts,
+                            const uint32_t *req_ids, const uint32_t *rounds, uint64_t seed,
+                            int32_t *tokens_out, int32_t *r_out);
+void orc_verify_logits_batch(const void *zp, const void *zq, int32_t dtype, int64_t V, int32_t k,
+                             int32_t B, const int32_t *slab, const int32_t *drafts,
+                             const uint32_t *req_ids, const uint32_t *rounds, uint64_t seed,
+                             int32_t *tokens_out, int32_t *r_out, uint64_t *z_out);
+
 /* ---- scheduler pieces, P:161-202 ---- */
 enum { ORC_POL_LAPSSD = 0, ORC_POL_FCFS = 1, ORC_POL_LPSJF = 2, ORC_POL_LAS = 3 };
 enum { ORC_PLACE_BY_ESTIMATE = 0, ORC_PLACE_STAY = 1 };

@@ -174,6 +174,35 @@ def make_pool(family: str, V: int, k: int, dtype: str, n_buckets: int, variants:
     return Pool(p=p, q=q, draft=draft, family=family, n_buckets=n_buckets, variants=variants)
 
 
+def make_logits_pool(V: int, k: int, dtype: str, n_buckets: int, variants: int, seed: int,
+                     device="cpu", chunk_slabs: int = 16) -> Pool:
+    """F2 as LOGITS (the heads' outputs): zp[S,k+1,V] = Zipf(1.1) +
+    N(0,1.5^2) logits, zq[S,k,V] = zp[:, :k] + eps N(0,1) with eps calibrated per
+    acceptance bucket as in make_pool; drafts sampled from the fp32 softmax of zq (the
+    draft model's sampler, an input to the method).  Returned as Pool(p=zp, q=zq)."""
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    tdt = torch_dtype(dtype)
+    S = n_buckets * variants
+    zp = torch.empty(S, k + 1, V, dtype=tdt, device=device)
+    zq = torch.empty(S, k, V, dtype=tdt, device=device)
+    draft = torch.empty(S, k, dtype=torch.int32, device=device)
+    betas = (torch.arange(n_buckets, dtype=torch.float32) + 0.5) / n_buckets
+    eps_b = calibrate_eps(V, betas.tolist(), gen, device=device)
+    for s0 in range(0, S, chunk_slabs):
+        s1 = min(S, s0 + chunk_slabs)
+        n = s1 - s0
+        eps = eps_b[torch.arange(s0, s1, device=device) // variants]
+        logits = _zipf_logits(n * (k + 1), V, gen, device).view(n, k + 1, V)
+        noise = torch.randn(n, k, V, generator=gen, device=device)
+        zp[s0:s1] = logits.to(tdt)
+        zq[s0:s1] = (logits[:, :k] + eps[:, None, None] * noise).to(tdt)
+        qs = torch.softmax(zq[s0:s1].float(), -1).reshape(n * k, V)
+        draft[s0:s1] = torch.multinomial(qs, 1, generator=gen).view(n, k).to(torch.int32)
+        del logits, noise, qs
+    return Pool(p=zp, q=zq, draft=draft, family="f2-logits", n_buckets=n_buckets, variants=variants)
+
+
 # ---------------------------------------------------------------------------
 # request traces
 @dataclass
