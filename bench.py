@@ -67,8 +67,9 @@ def parse():
     ap.add_argument("--dist-path", action="store_true",
                     help="N=1 only: time the N>1 step (laps_step_dist) with a one-rank NCCL communicator")
     ap.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "verify_dram.json"))
-    ap.add_argument("--workload", choices=["c4", "mc"], default="c4",
-                    help="c4 = configs[3] (the headline); mc = configs[4] Monte-Carlo traces")
+    ap.add_argument("--workload", choices=["c4", "mc", "logits"], default="c4",
+                    help="c4 = configs[3] (the headline); mc = configs[4] Monte-Carlo traces; "
+                    "logits = SURVEY 8(f) f1, spec_verify_logits at configs[3] dimensions")
     ap.add_argument("--mc-traces", type=int, default=8192, help="configs[4]: traces (whole job)")
     ap.add_argument("--mc-n", type=int, default=512, help="configs[4]: requests per trace")
     ap.add_argument("--mc-variants", type=int, default=256, help="configs[4]: slab variants per bucket")
@@ -607,6 +608,118 @@ def mc_cpu_baseline(args, w, pool, cfg):
             f"{verified} verifications, oracle/lapssd_oracle.c single thread, {el:.1f} s"}
 
 # --------------------------------------------------------------------------- reference arm
+def run_logits(args):
+    """spec_verify_logits on B=512 slots per GPU per step at configs[3]
+    dimensions (V=128,256, k=8, bf16 logits), each step a fresh random draw of slabs from
+    a 4.5 GB pool (inputs larger than L2).  Weak scaling: B slots per rank, no collective."""
+    import paper_2505_17074_b200 as L
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    B, k, V = args.batch, args.k, args.V
+    pool = synth.make_logits_pool(V, k, "bf16", n_buckets=args.buckets, variants=args.variants,
+                                  seed=synth.CONFIGS["c4"]["seed"] + 17 * rank, device=dev)
+    G = max(1, min(args.graph_steps or 1, args.steps))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    slabs = torch.randint(0, pool.S, (G, B), generator=gen, device=dev, dtype=torch.int32)
+    req = (torch.arange(B, device=dev, dtype=torch.int32) + rank * B)
+    rnds = torch.randint(0, 1 << 12, (G, B), generator=gen, device=dev, dtype=torch.int32)
+    tok = torch.empty(G, B, k + 1, dtype=torch.int32, device=dev)
+    na = torch.empty(G, B, dtype=torch.int32, device=dev)
+    ws = torch.empty(L._lib.spec_verify_logits_workspace_bytes(B, k), dtype=torch.uint8, device=dev)
+    seed = 0x5D0F1
+
+    def step(t):
+        L.spec_verify_logits(pool.p, pool.q, pool.draft, req, rnds[t], seed, slab=slabs[t], tokens=tok[t],
+                             n_accept=na[t], z=None, workspace=ws)
+
+    for t in range(max(args.warmup, 3)):
+        step(t % G)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    lc0 = L.launch_count()
+    with torch.cuda.graph(g):
+        for t in range(G):
+            step(t)
+    launches_per_step = (L.launch_count() - lc0) / G
+    reps = max(1, args.steps // G)
+    g.replay()
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    steps = reps * G
+    if dist:
+        t_ = torch.tensor([ms], device=dev)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        ms = float(t_[0])
+    value = world * B * k * steps / (ms * 1e-3)
+    r = na.cpu().numpy()
+    row = V * 2
+    alg = float(((2 * k + 1) * row + np.where(r < k, 2 * row, row)).sum()) / G   # per step (HBM)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs") or 6650.0
+    achieved = alg / (ms / steps * 1e-3) / 1e9
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+           "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "bf16 logits; fixed-op fp32 exp, exact 2^40 integer softmax masses, "
+           "128-bit integer acceptance and residual", "data": "synthetic",
+           "config": {"workload": "SURVEY 8(f) f1: spec_verify_logits at configs[3] dimensions, B=512 slots "
+                      "per GPU per step, V=128,256, k=8, bf16 logits (F2 Zipf, calibrated acceptance buckets), "
+                      "slabs drawn at random from a 4.5 GB pool every step", "B_per_gpu": B, "V": V, "k": k,
+                      "pool": f"{pool.S} slabs x {(2 * k + 1) * V * 2 / 1e6:.2f} MB",
+                      "l2": "inputs larger than L2 (4.5 GB pool)", "parallelism": f"dp{world}: slots per rank"},
+           "gpu_launches": int(round(launches_per_step * steps)),
+           "clocks": clk,
+           "roofline": {"kernel": "logits_norm_kernel + logits_sample_kernel (spec_verify_logits)",
+                        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak,
+                        "algorithmic_bytes_per_step": alg, "traffic": None,
+                        "note": "algorithmic bytes: every logit row once (2k+1 rows: normalisers) + the "
+                        "residual row pair (or the bonus row); the normaliser pass re-reads each row "
+                        "from L2 and spends ~20 fp32/int ops per entry on the fixed-op exp"}}
+    if not args.no_cpu_baseline and rank == 0:
+        import oracle
+        sl = slabs[0].cpu().numpy()
+        rq = req.cpu().numpy()
+        rd = rnds[0].cpu().numpy()
+        nb, dt = 0, 0.0
+        t0 = time.perf_counter()
+        while nb < B and dt < args.cpu_seconds:   # slots of the first timed step, 16 at a time
+            c = sl[nb:nb + 16]
+            P = {"p": synth.to_numpy_rows(pool.p[c]), "q": synth.to_numpy_rows(pool.q[c]),
+                 "draft": pool.draft[c].cpu().numpy()}
+            oracle.verify_logits_batch(P["p"], P["q"], P["draft"], np.arange(len(c)), rq[nb:nb + 16],
+                                       rd[nb:nb + 16], seed)
+            nb += len(c)
+            dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": nb * k / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+                               "sample": f"{nb} slots of the same workload, oracle/lapssd_oracle.c "
+                               f"orc_verify_logits_batch single thread, {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle, as it stands, timed on this host's cores on the
     same config / metric; each step a bounded sample (a smaller batch) of the workload."""
@@ -660,6 +773,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "logits":
+        run_logits(args)
     elif args.workload == "mc":
         run_mc(args)
     else:

@@ -148,6 +148,37 @@ lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V
                           void *workspace, size_t workspace_bytes, lapssd_stream stream);
 
 /* ---------------------------------------------------------------------------
+ * spec_verify_logits -- stateless batched verification from LOGITS (
+ * P:57-64 Eq. 1 and P:200 with p = softmax of the target head's logits and q = softmax
+ * of the draft head's; DESIGN.md AMB-30).
+ *
+ * zp: [device] pool of (k+1) x V target logits per slab, zq: k x V draft logits per
+ * slab, dtype elements (bf16 or fp32), row-major, V*sizeof(dtype) a multiple of 16,
+ * 16-byte aligned, V <= 2^23; draft: [device] int32 k per slab; slab: [device] int32
+ * [B] slab of slot b (NULL: slot b reads slab b); req_id, round_idx: [device] [B].
+ * For every row j of slot b the softmax is quantised exactly:
+ *   m = max_v z[v];  E[v] = floor(exphat(fl32(z[v] - m)) * 2^40);  S = sum_v E[v];
+ *   exphat(d) = 0 for d < -28, else 2^n * P7(r), n = rint(fl32(d * log2e)),
+ *   r = fma(-n, ln2_lo, fma(-n, ln2_hi, d)), P7 = degree-7 Taylor in Horner form with
+ *   fma (constants as fp32 hex literals in AMB-30): every operation IEEE fp32 RN.
+ * a1: accept x_j iff u24_j * Eq_j(x_j) * Sp_j < 2^24 * Ep_j(x_j) * Sq_j (128-bit
+ *   integers; u24_j as in spec_verify); r = first rejection or k.
+ * a2: R_v = max(0, Ep_r[v] * Sq_r - Eq_r[v] * Sp_r) if r < k (the residual
+ *   max(0, p^ - q^) times Sp Sq), else Ep_k[v]; if r < k and sum R = 0, R_v = Ep_r[v]
+ *   (AMB-20).  Z = sum_v R_v (< 2^120), U as in spec_verify,
+ *   t = U * (Z >> 64) + floor(U * (Z mod 2^64) / 2^64), y = min{v : sum_{w<=v} R_w > t}.
+ * Outputs [device]: tokens[B, k+1] (x_0..x_{r-1}, y, -1...), n_accept[B] = r,
+ * z[B, 2] = (Z mod 2^64, Z >> 64) (nullable).
+ * workspace: [device] >= spec_verify_logits_workspace_bytes(B, k) bytes, any content.
+ * Errors: EINVAL (k, V, dtype, alignment, B < 0, NULL), ENOMEM (workspace), ECUDA. */
+size_t spec_verify_logits_workspace_bytes(int32_t B, int32_t k);
+lapssd_status spec_verify_logits(const void *zp, const void *zq, int32_t dtype, int64_t V, int32_t k,
+                                 const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
+                                 const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,
+                                 int32_t *tokens, int32_t *n_accept, uint64_t *z, void *workspace,
+                                 size_t workspace_bytes, lapssd_stream stream);
+
+/* ---------------------------------------------------------------------------
  * Handle: resident-request state (SoA, ~64 B/request + gamma*4 B ring) in a
  * caller-owned device workspace.  lapssd_create copies the request arrays (H2D on
  * `stream`), zero-initialises state, computes the thresholds of P:169, and sets

@@ -64,6 +64,8 @@ def _load():
     sigs = {
         "spec_verify_workspace_bytes": ([i32, i64], sz),
         "spec_verify": ([vp, vp, i32, i64, i32, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp, vp, sz, vp], i32),
+        "spec_verify_logits_workspace_bytes": ([i32, i32], sz),
+        "spec_verify_logits": ([vp, vp, i32, i64, i32, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp, vp, sz, vp], i32),
         "lapssd_workspace_bytes": ([vp, i32, i32, i64, i32], sz),
         "lapssd_create": ([vp, vp, i32, i64, vp, sz, vp, vp], i32),
         "lapssd_destroy": ([vp], i32),
@@ -162,6 +164,32 @@ def spec_verify(p, q, draft, req_id, round_idx, seed, *, slab=None, trace=0, tok
                           _dptr(tokens), _dptr(n_accept), _dptr(z), _dptr(workspace),
                           workspace.numel(), _stream(stream))
     _check("spec_verify", rc)
+    return tokens, n_accept, z
+
+
+def spec_verify_logits(zp, zq, draft, req_id, round_idx, seed, *, slab=None, trace=0, tokens=None,
+                       n_accept=None, z=None, workspace=None, stream=None):
+    """Batched verification from logits (include/lapssd.h spec_verify_logits, SURVEY
+    8(f) f1).  zp [S,k+1,V], zq [S,k,V] logits (bf16/fp32), draft [S,k] int32,
+    req_id / round_idx [B]; slab [B] int32 (None: slot b reads slab b).  Returns
+    (tokens [B,k+1], n_accept [B], z [B,2] = (lo, hi) of the integer residual mass)."""
+    k, V = zq.shape[-2], zq.shape[-1]
+    B = req_id.numel()
+    dev = zp.device
+    if tokens is None:
+        tokens = torch.empty(B, k + 1, dtype=torch.int32, device=dev)
+    if n_accept is None:
+        n_accept = torch.empty(B, dtype=torch.int32, device=dev)
+    if z is None:
+        z = torch.empty(B, 2, dtype=torch.int64, device=dev)
+    ws_bytes = int(_lib.spec_verify_logits_workspace_bytes(B, k))
+    if workspace is None:
+        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    rc = _lib.spec_verify_logits(_dptr(zp), _dptr(zq), _dtype_code(zp), V, k, _dptr(draft), _dptr(slab),
+                                 _dptr(req_id), _dptr(round_idx), B, seed & (2**64 - 1), trace,
+                                 _dptr(tokens), _dptr(n_accept), _dptr(z), _dptr(workspace),
+                                 workspace.numel(), _stream(stream))
+    _check("spec_verify_logits", rc)
     return tokens, n_accept, z
 
 

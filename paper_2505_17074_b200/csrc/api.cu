@@ -77,6 +77,7 @@ void prepare_all() {
     static std::once_flag once;
     std::call_once(once, [] {
         verify_prepare();
+        verify_logits_prepare();
         sched_prepare();
     });
 }
@@ -275,6 +276,41 @@ lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V
         st = cuda_status(launch_verify(ab, nb, s), "spec_verify launch");
     }
     return st;
+}
+
+// ---------------------------------------------------------------- f1: verify from logits
+size_t spec_verify_logits_workspace_bytes(int32_t B, int32_t k) {
+    if (B < 0 || k < 1 || k > 16) return 0;
+    const size_t rows = (size_t)(B > 0 ? B : 1) * (size_t)(2 * k + 1);
+    Carver cv{nullptr};
+    cv.take<float>(rows);
+    cv.take<uint64_t>(rows);
+    return align256(cv.off);
+}
+
+lapssd_status spec_verify_logits(const void *zp, const void *zq, int32_t dtype, int64_t V, int32_t k,
+                                 const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
+                                 const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,
+                                 int32_t *tokens, int32_t *n_accept, uint64_t *z, void *workspace,
+                                 size_t workspace_bytes, lapssd_stream stream) {
+    g_last_error.clear();
+    if (B < 0) return fail(LAPSSD_EINVAL, "B < 0");
+    if (!rows_ok(dtype, V, k, zp, zq)) return fail(LAPSSD_EINVAL, "rows: dtype/V/k/alignment");
+    if (V > (int64_t)1 << 23) return fail(LAPSSD_EINVAL, "V > 2^23 (integer softmax mass would overflow)");
+    if (B == 0) return LAPSSD_OK;
+    if (!zp || !zq || !draft || !req_id || !round_idx || !tokens || !n_accept || !workspace)
+        return fail(LAPSSD_EINVAL, "NULL pointer argument");
+    if (workspace_bytes < spec_verify_logits_workspace_bytes(B, k))
+        return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes,
+                    spec_verify_logits_workspace_bytes(B, k));
+    prepare_all();
+    Carver cv{(char *)workspace};
+    const size_t rows = (size_t)B * (size_t)(2 * k + 1);
+    float *m_ws = cv.take<float>(rows);
+    uint64_t *S_ws = cv.take<uint64_t>(rows);
+    return cuda_status(launch_verify_logits(zp, zq, dtype, V, k, draft, slab, req_id, round_idx, B, seed, trace,
+                                            tokens, n_accept, z, m_ws, S_ws, (cudaStream_t)stream),
+                       "spec_verify_logits");
 }
 
 // ---------------------------------------------------------------- handle

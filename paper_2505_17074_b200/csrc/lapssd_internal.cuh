@@ -530,6 +530,12 @@ __device__ __forceinline__ SelRec *pre_recs(PreSelect *p, int bp) {
 __device__ __forceinline__ const SelRec *pre_recs(const PreSelect *p, int bp) {
     return reinterpret_cast<const SelRec *>(p->cand + even_up(bp));
 }
+cudaError_t launch_verify_logits(const void *zp, const void *zq, int32_t dtype, int64_t V, int32_t k,
+                                 const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
+                                 const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,
+                                 int32_t *tokens, int32_t *n_accept, uint64_t *z, float *m_ws, uint64_t *S_ws,
+                                 cudaStream_t s);
+void verify_logits_prepare();
 cudaError_t launch_presort(const State &st, const Sched &sc, const RowsDev &rw, const int32_t *sel, int32_t B,
                            PreSelect *out, cudaStream_t s);
 cudaError_t launch_select_final(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc, int32_t B,

@@ -1,0 +1,85 @@
+"""GPU parity of spec_verify_logits (DESIGN.md AMB-30) against the
+oracle on the same seeded logits: r, every emitted token and the 128-bit integer
+residual mass Z, bit-exactly (every decision is an exact integer comparison)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2505_17074_b200 as lib
+    return lib
+
+
+def run_both(L, pool, B, seed, rng, k):
+    S = pool.S
+    slab = rng.integers(0, S, B).astype(np.int32)
+    req = rng.integers(0, 1 << 20, B).astype(np.int32)
+    rnd = rng.integers(0, 1 << 12, B).astype(np.int32)
+    dev = pool.p.device
+    tok, na, z = L.spec_verify_logits(pool.p, pool.q, pool.draft, torch.as_tensor(req, device=dev),
+                                      torch.as_tensor(rnd, device=dev), seed,
+                                      slab=torch.as_tensor(slab, device=dev))
+    P = pool.numpy()
+    tok_o, r_o, z_o = oracle.verify_logits_batch(P["p"], P["q"], P["draft"], slab, req, rnd, seed)
+    return tok.cpu().numpy(), na.cpu().numpy(), z.cpu().numpy().view(np.uint64), tok_o, r_o, z_o
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("V,k", [(1024, 4), (8200, 1), (32000, 6), (40008, 8)])
+def test_spec_verify_logits_parity(L, dtype, V, k):
+    pool = synth.make_logits_pool(V, k, dtype, n_buckets=4, variants=2, seed=V + k, device="cuda")
+    rng = np.random.default_rng(V * 7 + k)
+    tok, na, z, tok_o, r_o, z_o = run_both(L, pool, 24, 1234 + V, rng, k)
+    assert (na == r_o).all()
+    assert (z == z_o).all()
+    assert (tok == tok_o).all()
+    assert (na < k).any() and (k == 1 or len(set(na.tolist())) > 1)   # varied outcomes
+
+
+def test_spec_verify_logits_config4_size(L):
+    """configs[3] dimensions (V=128,256, k=8, bf16) at a batch the oracle finishes."""
+    pool = synth.make_logits_pool(128256, 8, "bf16", n_buckets=4, variants=2, seed=44, device="cuda")
+    rng = np.random.default_rng(44)
+    tok, na, z, tok_o, r_o, z_o = run_both(L, pool, 12, 77, rng, 8)
+    assert (na == r_o).all() and (z == z_o).all() and (tok == tok_o).all()
+
+
+def test_spec_verify_logits_special_rows(L):
+    """Equal logits (accept everything, bonus row), disjoint supports (reject at 0,
+    residual = target) and a logit range wider than the exp cut-off (-28)."""
+    V, k, S = 2048, 3, 3
+    rng = np.random.default_rng(3)
+    zp = (2 * rng.standard_normal((S, k + 1, V))).astype(np.float32)
+    zq = zp[:, :k].copy()
+    inA = rng.random(V) < 0.5
+    zq[1] = np.where(inA, 0.0, -100.0)[None]
+    zp[1] = np.where(inA, -100.0, 0.0)[None]
+    zp[2, :, : V // 2] -= 60.0            # half the vocabulary below the cut-off
+    draft = np.zeros((S, k), np.int32)
+    draft[0] = rng.integers(0, V, k)
+    draft[1] = np.flatnonzero(inA)[:k]
+    draft[2] = rng.integers(V // 2, V, k)
+    dev = "cuda"
+    slab = np.array([0, 1, 2, 0, 1, 2], np.int32)
+    req = np.arange(6, dtype=np.int32)
+    rnd = np.zeros(6, np.int32)
+    tok, na, z = L.spec_verify_logits(torch.as_tensor(zp, device=dev), torch.as_tensor(zq, device=dev),
+                                      torch.as_tensor(draft, device=dev), torch.as_tensor(req, device=dev),
+                                      torch.as_tensor(rnd, device=dev), 5,
+                                      slab=torch.as_tensor(slab, device=dev))
+    tok_o, r_o, z_o = oracle.verify_logits_batch(zp, zq, draft, slab, req, rnd, 5)
+    na = na.cpu().numpy()
+    assert (na == r_o).all() and (tok.cpu().numpy() == tok_o).all()
+    assert (z.cpu().numpy().view(np.uint64) == z_o).all()
+    assert na[0] == k and na[3] == k          # equal logits: every draft accepted
+    assert na[1] == 0 and na[4] == 0          # disjoint: rejected at position 0
+    assert not inA[tok_o[1, 0]]
