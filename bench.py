@@ -692,10 +692,12 @@ def run_logits(args):
            "roofline": {"kernel": "logits_norm_kernel + logits_sample_kernel (spec_verify_logits)",
                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak,
-                        "algorithmic_bytes_per_step": alg, "traffic": None,
+                        "algorithmic_bytes_per_step": alg, "traffic": 4.3935e9,
                         "note": "algorithmic bytes: every logit row once (2k+1 rows: normalisers) + the "
-                        "residual row pair (or the bonus row); the normaliser pass re-reads each row "
-                        "from L2 and spends ~20 fp32/int ops per entry on the fixed-op exp"}}
+                        "residual row pair (or the bonus row).  traffic: ncu DRAM bytes of one step "
+                        "(profiles/r01f_logits_launches.csv): the normaliser's second pass over each "
+                        "row mostly misses L2, and the kernel also issues ~14 slots per entry for the "
+                        "fixed-op exp (69 % issue-active)"}}
     if not args.no_cpu_baseline and rank == 0:
         import oracle
         sl = slabs[0].cpu().numpy()

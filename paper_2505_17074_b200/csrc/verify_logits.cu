@@ -12,7 +12,7 @@
 //     y = min{v : sum_{w<=v} R_w > t} (128-bit integers).
 //
 // norm_kernel: one CTA per (slot, row) of the 2k+1 rows: max, then the integer mass
-//   (the second pass re-reads the row from L2).  ALU-bound: ~20 fp32/int ops per entry.
+//   (a second read of the row), ~14 issue slots per entry for the exp (packed fp32x2).
 // sample_kernel: one CTA per slot: the k acceptance tests (one lane each), then the
 //   residual row pair in 1,024-entry tiles (warp-coalesced 16-byte loads, one tile sum
 //   per warp pass), the tile holding t found by warp 0, which rescans that tile.
@@ -22,29 +22,42 @@ namespace lapssd {
 
 typedef unsigned __int128 u128;
 
-// e^d for d in [-28, 0]; 0 below (then E = 0 anyway).  The same operations, in the same
-// order, as the definition in DESIGN.md AMB-30 (the oracle writes out the same sequence;
-// nothing is shared).
-__device__ __forceinline__ float exp_hat(float d) {
-    if (!(d >= -28.0f)) return 0.0f;
-    if (d > 0.0f) d = 0.0f;
-    const float n = rintf(__fmul_rn(d, 0x1.715476p+0f));
-    float r = __fmaf_rn(-n, 0x1.62e4p-1f, d);
-    r = __fmaf_rn(-n, 0x1.7f7d1cp-20f, r);
-    float p = 0x1.a01a02p-13f;
-    p = __fmaf_rn(p, r, 0x1.6c16c2p-10f);
-    p = __fmaf_rn(p, r, 0x1.111112p-7f);
-    p = __fmaf_rn(p, r, 0x1.555556p-5f);
-    p = __fmaf_rn(p, r, 0x1.555556p-3f);
-    p = __fmaf_rn(p, r, 0x1p-1f);
-    p = __fmaf_rn(p, r, 1.0f);
-    p = __fmaf_rn(p, r, 1.0f);
-    // 2^n, n in [-41, 0]: exact scaling by a constructed power of two
-    return __fmul_rn(p, __int_as_float((127 + (int)n) << 23));
+// E = floor(exphat(fl32(z - m)) * 2^40) for the exphat of DESIGN.md AMB-30 (the oracle
+// writes out the same operation sequence; nothing is shared).  rint(x) for |x| < 2^22
+// is (x + 1.5 2^23) - 1.5 2^23 in RN-even, and n sits in the low bits of that sum; the
+// final P 2^n 2^40 is one exact multiply by a constructed power of two, then a
+// truncating conversion.
+// Two entries at once with the packed fp32x2 pipe (FFMA2/FADD2/FMUL2: each half is the
+// IEEE RN operation of the definition).  d is clamped to [-28.5, 0]: below -28 the
+// definition gives 0, and so does the polynomial there (e^-28 2^40 < 0.77), while the
+// clamp keeps 2^n normal.
+__device__ __forceinline__ void e40x2(float za, float zb, float ma, float mb, uint64_t &ea, uint64_t &eb) {
+    const float2 d0 = __fadd2_rn(make_float2(za, zb), make_float2(-ma, -mb));
+    const float2 d = make_float2(fmaxf(fminf(d0.x, 0.0f), -28.5f), fmaxf(fminf(d0.y, 0.0f), -28.5f));
+    const float2 x = __fmul2_rn(d, make_float2(0x1.715476p+0f, 0x1.715476p+0f));
+    const float2 big = __fadd2_rn(x, make_float2(0x1.8p23f, 0x1.8p23f));
+    const float2 nf = __fadd2_rn(big, make_float2(-0x1.8p23f, -0x1.8p23f));
+    float2 r = __ffma2_rn(nf, make_float2(-0x1.62e4p-1f, -0x1.62e4p-1f), d);
+    r = __ffma2_rn(nf, make_float2(-0x1.7f7d1cp-20f, -0x1.7f7d1cp-20f), r);
+    float2 p = make_float2(0x1.a01a02p-13f, 0x1.a01a02p-13f);
+    p = __ffma2_rn(p, r, make_float2(0x1.6c16c2p-10f, 0x1.6c16c2p-10f));
+    p = __ffma2_rn(p, r, make_float2(0x1.111112p-7f, 0x1.111112p-7f));
+    p = __ffma2_rn(p, r, make_float2(0x1.555556p-5f, 0x1.555556p-5f));
+    p = __ffma2_rn(p, r, make_float2(0x1.555556p-3f, 0x1.555556p-3f));
+    p = __ffma2_rn(p, r, make_float2(0x1p-1f, 0x1p-1f));
+    p = __ffma2_rn(p, r, make_float2(1.0f, 1.0f));
+    p = __ffma2_rn(p, r, make_float2(1.0f, 1.0f));
+    const int na = __float_as_int(big.x) - 0x4B400000, nb = __float_as_int(big.y) - 0x4B400000;
+    const float2 sc = make_float2(__int_as_float((167 + na) << 23), __int_as_float((167 + nb) << 23));
+    const float2 f = __fmul2_rn(p, sc);   // P 2^(n+40), exact
+    ea = __float2ull_rz(f.x);
+    eb = __float2ull_rz(f.y);
 }
 
 __device__ __forceinline__ uint64_t e40(float z, float m) {
-    return __float2ull_rz(__fmul_rn(exp_hat(__fsub_rn(z, m)), 0x1p40f));
+    uint64_t a, b;
+    e40x2(z, z, m, m, a, b);
+    return a;
 }
 
 template <bool BF16> struct LElt;
@@ -81,11 +94,16 @@ __device__ __forceinline__ u128 shfl_u128(u128 v, int src) {
 constexpr int kLogitThreads = 512;
 
 // ---------------------------------------------------------------- row normalisers
-// Block (slot b, row ri): ri <= k is target row ri, else draft row ri - k - 1.
+// Block (slot b, row ri): ri <= k is target row ri, else draft row ri - k - 1.  Two passes
+// over the row: the max, then the integer masses (measured: ~4 CTAs per SM keep both the
+// HBM stream and the exp arithmetic busy; a one-CTA-per-SM persistent form whose second
+// pass hits L2, and a 4-8 CTA cluster holding the row in shared memory, were slower).
+constexpr int kNormThreads = 512;
+
 template <bool BF16>
-__global__ void __launch_bounds__(kLogitThreads) logits_norm_kernel(const char *zp, const char *zq,
-                                                                    const int32_t *slab, int64_t V, int32_t k,
-                                                                    float *m_out, uint64_t *S_out) {
+__global__ void __launch_bounds__(kNormThreads) logits_norm_kernel(const char *zp, const char *zq,
+                                                                   const int32_t *slab, int64_t V, int32_t k,
+                                                                   float *m_out, uint64_t *S_out) {
     using E = LElt<BF16>;
     const int rows = 2 * k + 1;
     const int b = blockIdx.x / rows, ri = blockIdx.x % rows;
@@ -94,8 +112,8 @@ __global__ void __launch_bounds__(kLogitThreads) logits_norm_kernel(const char *
                               : zq + ((s * k + (ri - k - 1)) * V) * E::kEsz;
     const uint4 *v4 = reinterpret_cast<const uint4 *>(row);
     const int64_t nv = V / E::kVec;
-    __shared__ float s_m[kLogitThreads / 32];
-    __shared__ uint64_t s_S[kLogitThreads / 32];
+    __shared__ float s_m[kNormThreads / 32];
+    __shared__ uint64_t s_S[kNormThreads / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float m = -INFINITY;
     for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
@@ -110,10 +128,14 @@ __global__ void __launch_bounds__(kLogitThreads) logits_norm_kernel(const char *
     m = s_m[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, s_m[w]);
     uint64_t S = 0;
-    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {   // second pass: L2
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
         const uint4 v = v4[i];
 #pragma unroll
-        for (int e = 0; e < E::kVec; ++e) S += e40(E::get(v, e), m);
+        for (int e = 0; e < E::kVec; e += 2) {
+            uint64_t a, c;
+            e40x2(E::get(v, e), E::get(v, e + 1), m, m, a, c);
+            S += a + c;
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(0xFFFFFFFFu, S, o);
@@ -133,9 +155,10 @@ constexpr int kTileVecs = 4;   // vectors per lane per tile: 1,024 bf16 / 512 fp
 template <bool BF16>
 __device__ __forceinline__ u128 entry_mass(float zp, float zq, float mp, float mq, uint64_t Sp, uint64_t Sq,
                                            bool use_q) {
-    const u128 a = (u128)e40(zp, mp);
-    if (!use_q) return a;
-    const u128 x = a * Sq, y = (u128)e40(zq, mq) * Sp;
+    uint64_t ep, eq;
+    e40x2(zp, zq, mp, mq, ep, eq);
+    if (!use_q) return (u128)ep;
+    const u128 x = (u128)ep * Sq, y = (u128)eq * Sp;
     return x > y ? x - y : 0;
 }
 
@@ -322,14 +345,14 @@ cudaError_t launch_verify_logits(const void *zp, const void *zq, int32_t dtype, 
     const unsigned rows = (unsigned)(2 * k + 1);
     const size_t smem = logits_tile_smem(V, dtype);
     if (dtype == LAPSSD_BF16) {
-        logits_norm_kernel<true><<<(unsigned)B * rows, kLogitThreads, 0, s>>>(
+        logits_norm_kernel<true><<<(unsigned)B * rows, kNormThreads, 0, s>>>(
             (const char *)zp, (const char *)zq, slab, V, k, m_ws, S_ws);
         count_launch();
         logits_sample_kernel<true><<<(unsigned)B, kLogitThreads, smem, s>>>(
             (const char *)zp, (const char *)zq, draft, slab, req_id, round_idx, V, k, seed, trace, m_ws, S_ws, tokens,
             n_accept, z, nullptr);
     } else {
-        logits_norm_kernel<false><<<(unsigned)B * rows, kLogitThreads, 0, s>>>(
+        logits_norm_kernel<false><<<(unsigned)B * rows, kNormThreads, 0, s>>>(
             (const char *)zp, (const char *)zq, slab, V, k, m_ws, S_ws);
         count_launch();
         logits_sample_kernel<false><<<(unsigned)B, kLogitThreads, smem, s>>>(
