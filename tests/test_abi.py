@@ -85,6 +85,23 @@ def test_spec_verify_rejects_bad_rows():
     assert rc == -1
 
 
+def test_spec_verify_logits_rejects_bad_arguments():
+    """f1 entry: the same row checks, V <= 2^23 (integer softmax masses), workspace size,
+    NULL pointers -- all EINVAL / ENOMEM before any launch; B == 0 is a no-op."""
+    import paper_2505_17074_b200 as L
+    f = L._lib.spec_verify_logits
+    assert f(16, 16, L.BF16, 12, 4, None, None, None, None, 1, 0, 0, None, None, None, None, 0, None) == -1
+    assert f(16, 16, L.F32, 16, 0, None, None, None, None, 1, 0, 0, None, None, None, None, 0, None) == -1
+    assert f(16, 16, L.F32, 16, 17, None, None, None, None, 1, 0, 0, None, None, None, None, 0, None) == -1
+    assert f(16, 16, L.BF16, (1 << 23) + 8, 4, None, None, None, None, 1, 0, 0, None, None, None, None, 0,
+             None) == -1
+    assert f(16, 16, L.BF16, 16, 4, None, None, None, None, 1, 0, 0, None, None, None, None, 0, None) == -1
+    assert f(16, 16, L.BF16, 16, 4, 16, None, 16, 16, 1, 0, 0, 16, 16, None, 16, 0, None) == -5  # ENOMEM
+    assert f(16, 16, L.BF16, 16, 4, None, None, None, None, 0, 0, 0, None, None, None, None, 0, None) == 0
+    assert L._lib.spec_verify_logits_workspace_bytes(512, 8) >= 512 * 17 * 12
+    assert L._lib.spec_verify_logits_workspace_bytes(1, 0) == 0
+
+
 def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
     """The product path has no fallback: a missing .so is an ImportError."""
     import importlib.util
