@@ -136,3 +136,57 @@ def test_laps_step_dist_one_rank_lockstep(L, monkeypatch):
         L.nccl_comm_destroy(comm)
     finally:
         dist.destroy_process_group()
+
+
+def test_laps_step_dist_one_rank_graph_replay(L, monkeypatch):
+    """The overlapped laps_step_dist captured in a CUDA graph and replayed (as bench.py
+    times it at N > 1): the side stream's candidates -> all-gather -> merge chain and the
+    programmatic edge from the merge kernel to the next verify launch; every step's r and
+    the whole state after each replay against the oracle."""
+    import torch.distributed as dist
+    monkeypatch.setenv("MASTER_ADDR", "127.0.0.1")
+    monkeypatch.setenv("MASTER_PORT", "29563")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = L.nccl_comm()
+        seed, B, R, G, reps = 47, 64, 32, 6, 3
+        tr = synth.make_trace(256, seed, arrival="zero", length="uniform", len_min=200, len_max=900,
+                              beta_ab=(7, 3))
+        pool = synth.make_pool("f2", V=32000, k=8, dtype="bf16", n_buckets=8, variants=4, seed=seed,
+                               device="cuda")
+        tab = synth.slab_table(tr, 8, 4, R=R, seed=seed)
+        kw = dict(K=4, s1_up_us=72 * MS, gamma=5, delta=0.05, k=8, t_ssm_us=1 * MS, t_llm_us=10 * MS,
+                  seed=19)
+        P = pool.numpy()
+        P["slab_tab"], P["R"] = tab, R
+        sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
+        h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=32000,
+                     rank=0, world=1)
+        rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
+        Cn = B
+        cand = torch.zeros(2 * (Cn + 1), dtype=torch.int64, device="cuda")
+        h.laps_candidates(Cn, cand[: Cn + 1])
+        cand[Cn + 1:].copy_(cand[: Cn + 1])
+        h.laps_merge(cand[Cn + 1:], Cn, B)
+        sel_o, _ = sim.select(B)
+        h.laps_step_dist(comm, rows, B, Cn, cand)   # eager warm-up step
+        sim.step(P, sel_o)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(G):
+                h.laps_step_dist(comm, rows, B, Cn, cand)
+        for rep in range(reps):
+            g.replay()
+            torch.cuda.synchronize()
+            for _ in range(G):
+                sim.step(P, sel_o)
+            gs, os_ = h.state(), sim.state()
+            for f in ("acc_tok", "acc_draft", "rounds", "E_us", "level", "perceptible", "pinned", "key"):
+                assert (np.asarray(gs[f]) == np.asarray(os_[f])).all(), f"replay {rep}: {f}"
+            assert gs["now_us"] == os_["now_us"]
+            assert (h.sel[:B].cpu().numpy() == sel_o).all(), f"replay {rep}: next batch"
+        assert h.check() == 0
+        L.nccl_comm_destroy(comm)
+    finally:
+        dist.destroy_process_group()
