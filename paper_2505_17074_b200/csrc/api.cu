@@ -95,6 +95,12 @@ struct lapssd_handle {
     int32_t *n_accept;
     SlotDesc *desc;        // a1 results for the current batch (valid if desc_valid)
     bool desc_valid = false;
+    // laps_step's side-stream select of step t+1 may follow the select of step t directly
+    // (it needs the batch that select committed, not the previous verify's completion):
+    // true after an incremental laps_step on chain_stream; any other call resets it
+    bool side_chained = false;
+    bool chain_captured = false;   // the chained step was recorded into a graph
+    cudaStream_t chain_stream = nullptr;
     lapssd_rows last_rows{};  // rows of the previous laps_step (epoch changes with them)
     uint32_t rows_epoch = 1;
     PreSelect *pre = nullptr;    // presort output (side stream)
@@ -388,6 +394,7 @@ lapssd_status lapssd_destroy(lapssd_handle *h) {
 lapssd_status laps_update(lapssd_handle *h, const int32_t *sel, const int32_t *n_accept, int32_t B,
                           lapssd_stream stream) {
     g_last_error.clear();
+    if (h) h->side_chained = false;
     if (!h || B < 0 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
     if (B > 0 && (!sel || !n_accept)) return fail(LAPSSD_EINVAL, "NULL sel / n_accept");
     h->last_stream = (cudaStream_t)stream;
@@ -398,6 +405,7 @@ lapssd_status laps_update(lapssd_handle *h, const int32_t *sel, const int32_t *n
 lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t *count_out,
                           lapssd_stream stream) {
     g_last_error.clear();
+    if (h) h->side_chained = false;
     if (!h || B < 1 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
     if (!sel_out) return fail(LAPSSD_EINVAL, "sel_out is NULL");
     h->last_stream = (cudaStream_t)stream;
@@ -486,9 +494,25 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
         if (st != LAPSSD_OK) return st;
     }
     // fork: the next selection's side-stream work runs beside the verify kernel (the
-    // verify kernel is launched first so it takes its SMs without waiting)
-    cudaError_t ce = cudaEventRecord(h->ev_fork, s);
-    if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork");
+    // verify kernel is launched first so it takes its SMs without waiting).  After an
+    // incremental step on the same stream the side stream is chained instead: its select
+    // already follows the previous select, which committed everything this one reads, so
+    // it need not also wait for the previous verify grid to drain -- its presort then
+    // runs while that grid's last CTAs sample.  Under capture the side stream must join
+    // the capture through a fork.
+    cudaStreamCaptureStatus cap_s = cudaStreamCaptureStatusNone, cap_side = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap_s);
+    cudaStreamIsCapturing(h->side, &cap_side);
+    static const bool no_chain = getenv("LAPSSD_NO_SIDE_CHAIN") != nullptr;  // A/B switch
+    const bool capturing = cap_s == cudaStreamCaptureStatusActive;
+    const bool fork = no_chain || !incremental || !h->side_chained || h->chain_stream != s || cap_s != cap_side ||
+                      capturing != h->chain_captured || !h->desc_valid;
+    h->side_chained = false;
+    cudaError_t ce = cudaSuccess;
+    if (fork) {
+        ce = cudaEventRecord(h->ev_fork, s);
+        if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork");
+    }
     h->desc_valid = false;
     if (incremental) {
         a.fin = h->fin;
@@ -502,8 +526,10 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
     st = cuda_status(launch_verify_grid(a, B, 1, incremental && !no_pdl, s), "laps_step verify");
     if (st != LAPSSD_OK) return st;
     if (ev) prof_record(ev[1], s);
-    ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
-    if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork wait");
+    if (fork) {
+        ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+        if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork wait");
+    }
     if (incremental) {
         st = cuda_status(launch_select_side(h->st, h->sc, a.rows, sel_inout, h->desc, B, h->pre, h->fin, h->fin_key,
                                             h->snap, (uint32_t)verify_grid(B, a.n_chunks, 1), count_out, h->side),
@@ -519,6 +545,9 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
     if (ce != cudaSuccess) return cuda_status(ce, "laps_step join wait");
     if (incremental) {
         h->desc_valid = true;
+        h->side_chained = true;
+        h->chain_stream = s;
+        h->chain_captured = capturing;
         if (ev) prof_record(ev[2], s);
         return LAPSSD_OK;
     }
@@ -572,6 +601,7 @@ lapssd_status lapssd_profile_read(lapssd_handle *h, double *verify_ms, double *s
 // ---------------------------------------------------------------- a8
 lapssd_status laps_candidates(lapssd_handle *h, int32_t C, uint64_t *cand_out, lapssd_stream stream) {
     g_last_error.clear();
+    if (h) h->side_chained = false;
     if (!h || C < 1 || !cand_out) return fail(LAPSSD_EINVAL, "handle / C / cand_out");
     h->last_stream = (cudaStream_t)stream;
     h->desc_valid = false;
@@ -582,6 +612,7 @@ lapssd_status laps_candidates(lapssd_handle *h, int32_t C, uint64_t *cand_out, l
 lapssd_status laps_merge(lapssd_handle *h, const uint64_t *all_cand, int32_t C, int32_t B, int32_t *sel_out,
                          int32_t *count_out, lapssd_stream stream) {
     g_last_error.clear();
+    if (h) h->side_chained = false;
     if (!h || C < 1 || !all_cand || !sel_out || B < 1 || B > h->max_batch)
         return fail(LAPSSD_EINVAL, "handle / C / B / pointers");
     if ((int64_t)h->sc.world * C > sort_capacity())
@@ -655,6 +686,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
                              int32_t C, int32_t *sel_inout, int32_t *count_out, uint64_t *cand_scratch,
                              lapssd_stream stream) {
     g_last_error.clear();
+    if (h) h->side_chained = false;
     if (!h || !nccl_comm || !cand_scratch || B_global < 1 || B_global > h->max_batch || C < 1)
         return fail(LAPSSD_EINVAL, "handle / comm / scratch / B_global / C");
     if ((int64_t)h->sc.world * C > sort_capacity())
@@ -730,6 +762,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
 // ---------------------------------------------------------------- snapshot / check
 lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *v, lapssd_stream stream) {
     g_last_error.clear();
+    if (h) h->side_chained = false;
     if (!h || !v) return fail(LAPSSD_EINVAL, "handle / view");
     cudaStream_t s = (cudaStream_t)stream;
     const size_t n = (size_t)h->sc.n;

@@ -9,6 +9,8 @@
 // eligible keys become the batch.  The tail of the same kernel runs the acceptance
 // test (a1) of every newly selected slot, so the next verify launch starts streaming
 // after a single descriptor load.
+#include <cstdlib>
+
 #include "select_core.cuh"
 
 namespace lapssd {
@@ -608,8 +610,27 @@ cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &
     const size_t a = topB_smem_words(np, bp) * sizeof(uint64_t);
     const size_t b = (size_t)4 * bp * sizeof(uint64_t) + 2 * (size_t)((sc.n + 7) & ~7) * sizeof(int16_t) + 64 +
                      (bp <= 1024 ? 2 * (size_t)bp * sizeof(SelRec) : 0);
-    select_side_kernel<<<1, kSideThreads, a > b ? a : b, s>>>(st, sc, rw, sel, desc, B, pre, fin, fin_key, snap,
-                                                              snap_target, count_out, cand_out, C);
+    // highest launch priority: when an SM frees up, the block scheduler places this one
+    // CTA before the waiting CTAs of the next (programmatically launched) verify grid
+    static int prio = [] {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        return hi;
+    }();
+    static const bool no_prio = getenv("LAPSSD_SIDE_NO_PRIORITY") != nullptr;  // A/B switch
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(kSideThreads);
+    cfg.dynamicSmemBytes = a > b ? a : b;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = prio;
+    cfg.attrs = attr;
+    cfg.numAttrs = no_prio ? 0 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, select_side_kernel, st, sc, rw, sel, desc, B, pre, fin, fin_key,
+                                             snap, snap_target, count_out, cand_out, C);
+    if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();
 }
