@@ -219,11 +219,20 @@ lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t
                           lapssd_stream stream);
 
 /* laps_step -- one fused step: spec_verify on the current batch sel_inout[B]
- * (from the previous laps_select/laps_step), the laps_update of each verified
- * request by the last CTA that finishes its row, then laps_select into sel_inout.
- * rows: pooled or batch layout (lapssd_rows).  tokens_out [device, B x (k+1)],
- * n_accept_out [device, B] are nullable.  count_out as in laps_select.
- * Errors: EINVAL, ECUDA. */
+ * (from the previous laps_select/laps_step), laps_update of every verified request,
+ * then laps_select into sel_inout -- with the results of that exact sequence.
+ * Execution (DESIGN.md s.6): the state update depends on r only (known from a1 before
+ * any row streams), so the verify kernel's finisher warps run it at kernel start and
+ * publish each request's new key; with pooled rows a select kernel on a library-owned
+ * side stream (forked from / joined back into `stream` with events, highest launch
+ * priority) presorts the other requests, merges the published keys while the rows
+ * stream, and commits the next batch once every verify CTA has snapshotted the current
+ * one; consecutive verify launches overlap (programmatic dependent launch).  Everything
+ * is ordered on `stream` when the call's work completes, and the call may be captured
+ * in a CUDA graph.  rows: pooled or batch layout (lapssd_rows).  tokens_out [device,
+ * B x (k+1)], n_accept_out [device, B] are nullable.  count_out as in laps_select.
+ * Device-side waits carry watchdogs; an expiry sets LAPSSD_ESTATE flags (see
+ * lapssd_check) and the step's results are invalid.  Errors: EINVAL, ECUDA. */
 lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel_inout,
                         int32_t *count_out, int32_t *tokens_out, int32_t *n_accept_out,
                         lapssd_stream stream);
@@ -237,7 +246,9 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
  * laps_merge takes the global top-B keys, keeps the ids with id % world == rank as
  * this rank's batch (sel_out, key order) and advances the clock by the GLOBAL batch.
  * laps_step_dist = verify + update + candidates + ncclAllGather (on `nccl_comm`, a
- * ncclComm_t created by the caller) + merge.  NCCL is resolved at run time with
+ * ncclComm_t created by the caller) + merge, with the results of that sequence; with
+ * pooled rows the candidates / all-gather / merge run on the side stream beside the
+ * verify kernel as in laps_step.  NCCL is resolved at run time with
  * dlopen("libnccl.so.2"); if unavailable the call returns ENCCL. */
 lapssd_status laps_candidates(lapssd_handle *h, int32_t C, uint64_t *cand_out,
                               lapssd_stream stream);
