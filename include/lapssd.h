@@ -285,7 +285,12 @@ lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *host_out,
                                 lapssd_stream stream);
 
 /* Synchronises the handle's last stream; returns LAPSSD_ESTATE if the device flag
- * is set (and the flag bits in *flags_out, nullable), else LAPSSD_OK. */
+ * is set (and the flag bits in *flags_out, nullable), else LAPSSD_OK.  Bits: 1 update
+ * of a completed request, 2 a row with no probability mass, 4 a slot naming a bad
+ * request / slab, 8 a descriptor that does not match the batch, 16 a device-side
+ * watchdog expired (results invalid) with 32 / 64 / 128 naming the wait (verify
+ * finisher / select merge / verify snapshot); lapssd_last_error() then reports the
+ * step and slot of the first expiry. */
 lapssd_status lapssd_check(lapssd_handle *h, uint32_t *flags_out);
 
 /* Per-kernel timing of laps_step for the next max_steps calls: the library records
