@@ -190,6 +190,30 @@ def test_residual_mass_within_1e6_of_exact(dtype):
     assert worst < 1e-6
 
 
+def test_boundary_ambiguity_of_a_float_cdf_design():
+    """PIN-X, second half: how many samples a floating-point CDF would
+    leave within 1e-6 Z of a CDF boundary.  The sampled point t is uniform on [0, Z)
+    given the rows, so the chance that it lies within eps Z of either edge of the
+    emitted token's interval is 2 eps per token with mass, i.e. about 2 eps n_mass in
+    total.  Measured on realistic rows (V = 4,096) it matches that law -- far above the
+    north_star's 1e-5 at full vocabularies -- which is why the kernel's CDF is an exact
+    integer one (identical tokens, zero ambiguous samples; AMB-27)."""
+    pool = synth.make_pool("f2", V=4096, k=4, dtype="bf16", n_buckets=4, variants=2, seed=21)
+    P = pool.numpy()
+    eps, near, n, n_mass = 1e-5, 0, 0, []
+    for s in range(pool.S):
+        for rid in range(400):
+            _, o = oracle.verify_request(P["p"][s], P["q"][s], P["draft"][s], rid, 7, seed=5)
+            near += o.margin_rel < eps
+            n += 1
+        pr = P["p"][s].view(np.uint16).astype(np.uint32) << 16
+        p32 = pr.view(np.float32)
+        n_mass.append(float((p32[0] > 0).sum()))
+    frac = near / n
+    predicted = 2 * eps * float(np.mean(n_mass))   # upper-bound scale: every token with mass
+    assert 0 < frac < 2 * predicted, (frac, predicted)
+
+
 def test_sampling_uses_the_64bit_uniform_against_integer_cdf():
     """With two tokens of residual mass a and b, the emitted token is the first
     whose cumulative mass exceeds t = floor(U Z / 2^64): frequency a/(a+b)."""
