@@ -106,7 +106,10 @@ typedef struct {
  *      same shapes; the request in slot b, local index i, in its round t reads slab
  *      slab_tab[i*R + (t < R ? t : R/2 + (t - R/2) % (R/2))].
  * p: [device] (k+1) x V per slab, q: [device] k x V per slab, row-major, dtype
- * elements; draft: [device] int32 k per slab, drafts x_j sampled from q_j.
+ * elements; draft: [device] int32 k per slab, drafts x_j sampled from q_j.  p, q and
+ * draft may also be pinned host memory (cudaHostAlloc / registered, unified addressing):
+ * the kernels then read in place, over PCIe, only the bytes the step needs.
+ * With the batch layout the acceptance tests always use the rows of the call itself.
  * V*sizeof(dtype) must be a multiple of 16 and p, q 16-byte aligned. */
 typedef struct {
     const void *p;

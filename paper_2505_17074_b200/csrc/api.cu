@@ -461,7 +461,7 @@ static void prof_record(cudaEvent_t e, cudaStream_t s) {
 
 static lapssd_status step_verify(lapssd_handle *h, const VerifyArgs &a, int32_t *sel, int32_t B,
                                  cudaStream_t s) {
-    if (!h->desc_valid) {
+    if (!h->desc_valid || a.rows.slab_tab == nullptr) {   // batch layout: this call's rows
         lapssd_status st = cuda_status(launch_accept(a.rows, sel, &h->st, &h->sc, nullptr, nullptr, nullptr,
                                                      h->sc.seed, 0, B, h->desc, s), "accept");
         if (st != LAPSSD_OK) return st;
@@ -488,7 +488,9 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
     // pooled rows: incremental select on the side stream (presort, then merge the batch
     // slots as the verify finishers publish them); batch layout: presort + final select
     const bool incremental = rows->slab_tab != nullptr && bp <= 4096;
-    if (!h->desc_valid) {  // a1 for the current batch, before the fork: both streams read it
+    // a1 for the current batch, before the fork (both streams read it): always with the
+    // batch layout, whose rows are this call's (the previous select could not know them)
+    if (!h->desc_valid || rows->slab_tab == nullptr) {
         st = cuda_status(launch_accept(a.rows, sel_inout, &h->st, &h->sc, nullptr, nullptr, nullptr, h->sc.seed, 0,
                                        B, h->desc, s), "accept");
         if (st != LAPSSD_OK) return st;

@@ -175,3 +175,43 @@ def test_step_parity_graph_replay_config4(L):
         compare_state(h.state(), sim.state(), f"replay {rep}")
         assert (h.sel[:B].cpu().numpy() == sel_o).all(), f"replay {rep}: next batch differs"
     assert h.check() == 0
+
+
+def _slab_round_index(t, R):
+    h = R // 2
+    return t if t < R else (R - 1 if h == 0 else h + (t - h) % h)
+
+
+def test_step_parity_batch_layout_rows_per_step(L):
+    """Batch layout (no slab table; slot b reads rows b of THIS call): each step the caller
+    gathers the rows of the batch's requests from the pool -- the slab the table assigns
+    to the request's current round -- so the run must equal the pooled oracle run."""
+    tr, pool, tab = workload(80, 4096, 4, "bf16", seed=31, drift=True)
+    kw = dict(BASE, k=4, seed=7)
+    B, R = 8, tab.shape[1]
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=pool.V)
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, R
+    sel_o, _ = sim.select(B)
+    h.laps_select(B)
+    tok = torch.empty(B, 5, dtype=torch.int32, device="cuda")
+    nacc = torch.empty(B, dtype=torch.int32, device="cuda")
+    for step in range(3000):
+        sel_g = h.sel[:B].cpu().numpy()
+        assert (sel_g == sel_o).all(), f"step {step}: batch differs"
+        if sim.state()["done"].all():
+            break
+        rounds = h.state()["rounds"]
+        slabs = [int(tab[i, _slab_round_index(int(rounds[i]), R)]) if i >= 0 else 0 for i in sel_g]
+        idx = torch.as_tensor(slabs, device="cuda")
+        rows = L.Rows(pool.p[idx].contiguous(), pool.q[idx].contiguous(), pool.draft[idx].contiguous(), None)
+        h.laps_step(rows, B, tokens=tok, n_accept=nacc)
+        _, tok_o, na_o, _ = sim.step(P, sel_o)
+        live = sel_g >= 0
+        assert (nacc.cpu().numpy()[live] == na_o[live]).all(), f"step {step}: r differs"
+        assert (tok.cpu().numpy()[live] == tok_o[live]).all(), f"step {step}: tokens differ"
+        if step % 5 == 0:
+            compare_state(h.state(), sim.state(), step)
+    assert sim.state()["done"].all()
+    assert h.check() == 0
