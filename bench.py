@@ -559,6 +559,26 @@ def run_mc(args):
         dist.destroy_process_group()
 
 
+def estimator_accuracy(st, w, sched):
+    """SURVEY 8(f) f3 (the paper's Fig. 7 analogue): for every request
+    that became perceptible and completed, the Eq. (6) estimate fixed at stabilisation
+    (T~_i, from the engine's state) against the service it actually received (E_i =
+    rounds x round cost).  Reported twice: as the engine computed it (with the predicted
+    length L_pred, lognormal error sigma 0.3) and with the true length (the error of the
+    acceptance-rate part alone, T~ rescaled by L_true / L_pred)."""
+    m = st["perceptible"].astype(bool) & st["done"].astype(bool)
+    est = st["T_total_us"][m].astype(np.float64)
+    real = st["E_us"][m].astype(np.float64)
+    lp = np.asarray(w.L_pred)[m].astype(np.float64)
+    lt = np.asarray(w.L_true)[m].astype(np.float64)
+    err = np.abs(est - real) / real
+    err_true = np.abs(est * lt / lp - real) / real
+    return {"requests": int(m.sum()), "perceptible_frac": float(m.mean()),
+            "mape_with_L_pred": float(err.mean()), "mape_with_L_true": float(err_true.mean()),
+            "signed_mean_with_L_true": float(((est * lt / lp - real) / real).mean()),
+            "paper_context": "6.84 % overall on an L20 with a learned length predictor (P:315)"}
+
+
 def mc_jct(args, L, w, pool, rows, dev, policies):
     """Run every trace to completion under each policy (same traces, same rows, same
     seeds: common random numbers) and report the mean JCT (C_i - r_i)."""
@@ -582,9 +602,11 @@ def mc_jct(args, L, w, pool, rows, dev, policies):
         el = time.perf_counter() - t0
         st = mc.state()[0]
         jct = (st["C_us"] - w.arrival_us).astype(np.float64)
-        res[["LAPS-SD", "FCFS", "LP-SJF", "LAS"][pol]] = {"mean_jct_ms": float(jct.mean() / 1e3),
-                                                          "steps": steps, "seconds": el,
-                                                          "all_done": bool(st["done"].all())}
+        r = {"mean_jct_ms": float(jct.mean() / 1e3), "steps": steps, "seconds": el,
+             "all_done": bool(st["done"].all())}
+        if pol == 0:
+            r["estimator"] = estimator_accuracy(st, w, MC_SCHED)
+        res[["LAPS-SD", "FCFS", "LP-SJF", "LAS"][pol]] = r
         del mc
     return res
 
