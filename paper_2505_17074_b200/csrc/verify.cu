@@ -275,6 +275,13 @@ constexpr int kStageBudget = 192 * 1024;                   // shared memory for 
 #ifndef LAPSSD_POLL_NS
 #define LAPSSD_POLL_NS 1024
 #endif
+#ifndef LAPSSD_POLL_NEAR
+#define LAPSSD_POLL_NEAR 2
+#endif
+#ifndef LAPSSD_POLL_NEAR_NS
+#define LAPSSD_POLL_NEAR_NS 128
+#endif
+constexpr int kPollNearNs = LAPSSD_POLL_NEAR_NS;  // back-off when <= LAPSSD_POLL_NEAR chunks are pending
 constexpr int kPollNs = LAPSSD_POLL_NS;  // finisher back-off between polls (measured: 32 ns of polling traffic costs ~2 us/step)
 
 template <bool BF16>
@@ -825,7 +832,8 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                 uint64_t all = kReady;
 #pragma unroll
                 for (int x = 0; x < kPartWords; ++x) all &= w[x];
-                if (__all_sync(0xFFFFFFFFu, (all & kReady) != 0)) break;
+                const unsigned pending = __ballot_sync(0xFFFFFFFFu, (all & kReady) == 0);
+                if (pending == 0) break;
                 if (waited_too_long(t_start)) {
                     if (lane == 0 && a.err) {
                         if (!(atomicOr(a.err, E_TIMEOUT | E_TO_FIN) & E_TIMEOUT) && a.st.g)
@@ -833,7 +841,8 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                     }
                     break;
                 }
-                __nanosleep(kPollNs);
+                // long back-off while many chunks are outstanding, short once a few are left
+                __nanosleep(__popc(pending) <= LAPSSD_POLL_NEAR ? kPollNearNs : kPollNs);
             }
             if (lane == 0) TRACE(6, b);
             if (lane == 0) CTA_TIME(4);
