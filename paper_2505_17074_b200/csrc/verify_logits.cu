@@ -91,7 +91,13 @@ __device__ __forceinline__ u128 shfl_u128(u128 v, int src) {
     return ((u128)hi << 64) | lo;
 }
 
-constexpr int kLogitThreads = 512;
+#ifndef LAPSSD_SAMPLE_THREADS
+#define LAPSSD_SAMPLE_THREADS 512
+#endif
+#ifndef LAPSSD_SAMPLE_MINB
+#define LAPSSD_SAMPLE_MINB 2
+#endif
+constexpr int kLogitThreads = LAPSSD_SAMPLE_THREADS;   // sample kernel: one slot per CTA
 
 // ---------------------------------------------------------------- row normalisers
 // Block (slot b, row ri): ri <= k is target row ri, else draft row ri - k - 1.  Two passes
@@ -163,7 +169,7 @@ __device__ __forceinline__ u128 entry_mass(float zp, float zq, float mp, float m
 }
 
 template <bool BF16>
-__global__ void __launch_bounds__(kLogitThreads) logits_sample_kernel(
+__global__ void __launch_bounds__(kLogitThreads, LAPSSD_SAMPLE_MINB) logits_sample_kernel(
     const char *zp, const char *zq, const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
     const uint32_t *round_idx, int64_t V, int32_t k, uint64_t seed, uint32_t trace, const float *m_in,
     const uint64_t *S_in, int32_t *tokens, int32_t *n_accept, uint64_t *z_out, uint32_t *err) {
