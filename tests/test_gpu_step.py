@@ -215,3 +215,30 @@ def test_step_parity_batch_layout_rows_per_step(L):
             compare_state(h.state(), sim.state(), step)
     assert sim.state()["done"].all()
     assert h.check() == 0
+
+
+def test_step_parity_max_batch_4096(L):
+    """The largest batch the incremental step takes (B = 4,096 slots: the verify
+    kernel's per-CTA snapshot capacity; the side select then works on 8,192 keys with
+    the radix top-B path), a few steps bit-exact against the oracle."""
+    n, B = 8192, 4096
+    tr = synth.make_trace(n, 0x5D0009, arrival="zero", length="uniform", len_min=64, len_max=512,
+                          beta_ab=(7, 3))
+    pool = synth.make_pool("f2", V=1024, k=4, dtype="bf16", n_buckets=8, variants=4, seed=9, device="cuda")
+    tab = synth.slab_table(tr, 8, 4, R=16, seed=9)
+    kw = dict(BASE, k=4, seed=13)
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=1024)
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, 16
+    sel_o, _ = sim.select(B)
+    h.laps_select(B)
+    nacc = torch.empty(B, dtype=torch.int32, device="cuda")
+    for step in range(6):
+        assert (h.sel[:B].cpu().numpy() == sel_o).all(), f"step {step}: batch differs"
+        h.laps_step(rows, B, n_accept=nacc)
+        _, _, na_o, _ = sim.step(P, sel_o)
+        assert (nacc.cpu().numpy() == na_o).all(), f"step {step}: r differs"
+        compare_state(h.state(), sim.state(), step)
+    assert h.check() == 0
