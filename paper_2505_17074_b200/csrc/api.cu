@@ -825,8 +825,10 @@ struct lapssd_mc {
     McDev mc{};
     SlotDesc *desc = nullptr;   // [T] a1 of each trace's selected request
     int32_t *sel = nullptr, *n_accept = nullptr, *tokens = nullptr, *active = nullptr;
-    uint64_t *part = nullptr;   // verify scratch for one sub-launch
-    uint32_t *work = nullptr;
+    uint64_t *part = nullptr;   // verify scratch: two sets (consecutive sub-launches overlap)
+    uint32_t *work = nullptr;   // [4]: two (claim, retired) counter pairs
+    uint32_t *par = nullptr;    // [2] = {0, 1}: the set a sub-launch uses (its "step parity")
+    size_t part_set = 0;        // words per set
     int32_t T = 0, bmax = 0;
     int64_t n = 0, V = 0;
     cudaStream_t last_stream = nullptr;
@@ -846,8 +848,10 @@ static void carve_mc(Carver &cv, lapssd_mc *h, int32_t T, int64_t n, int32_t gam
     const int32_t nc = n_chunks_max(V);
     const int32_t bmax = verify_max_batch(nc, 0);
     const int32_t nb = T < bmax ? (T > 0 ? T : 1) : bmax;
-    h->part = cv.take<uint64_t>((size_t)nb * nc * kPartWords);
-    h->work = cv.take<uint32_t>(2);
+    h->part_set = (size_t)nb * nc * kPartWords;
+    h->part = cv.take<uint64_t>(2 * h->part_set);
+    h->work = cv.take<uint32_t>(4);
+    h->par = cv.take<uint32_t>(2);
 }
 
 extern "C" {
@@ -906,6 +910,7 @@ lapssd_status lapssd_mc_create(const lapssd_config *cfg, int32_t n_traces, const
                             cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->sel, 0xFF, sizeof(int32_t) * n_traces, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->mc.last, 0xFF, sizeof(int32_t) * n_traces, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->par + 1, 0x01, 1, s);   // par = {0, 1}
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
         delete h;
@@ -956,14 +961,22 @@ lapssd_status laps_mc_step(lapssd_mc *h, const lapssd_rows *rows, int32_t *token
     a.work = h->work;
     a.fuse_update = 0;
     a.err = &h->st.g->err;
+    a.part1 = h->part + h->part_set;
+    a.work1 = h->work + 2;
     lapssd_status st = LAPSSD_OK;
-    for (int32_t b0 = 0; b0 < h->T && st == LAPSSD_OK; b0 += h->bmax) {
+    static const bool no_pdl = getenv("LAPSSD_NO_PDL") != nullptr;
+    int j = 0;
+    for (int32_t b0 = 0; b0 < h->T && st == LAPSSD_OK; b0 += h->bmax, ++j) {
         VerifyArgs ab = a;
         const int32_t nb = h->T - b0 < h->bmax ? h->T - b0 : h->bmax;
         ab.desc = h->desc + b0;
         ab.tokens = tok + (int64_t)b0 * (rows->k + 1);
         ab.n_accept = na + b0;
-        st = cuda_status(launch_verify(ab, nb, s), "laps_mc_step verify");
+        ab.vstep = h->par + (j & 1);   // alternate scratch sets
+        // the second sub-launch overlaps the first's tail (programmatic dependent launch:
+        // its CTAs take SMs as the first's retire; it reads nothing the first writes).  A
+        // third one would share the first's set, so only j == 1 overlaps.
+        st = cuda_status(launch_verify_grid(ab, nb, 0, j == 1 && !no_pdl, s), "laps_mc_step verify");
     }
     if (st != LAPSSD_OK) return st;
     if (active_out) {
