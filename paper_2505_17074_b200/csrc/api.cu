@@ -963,6 +963,10 @@ lapssd_status laps_mc_step(lapssd_mc *h, const lapssd_rows *rows, int32_t *token
     a.err = &h->st.g->err;
     a.part1 = h->part + h->part_set;
     a.work1 = h->work + 2;
+    if (active_out) {   // before the verify launches: the select follows the last one directly
+        const cudaError_t e = cudaMemsetAsync(active_out, 0, sizeof(int32_t), s);
+        if (e != cudaSuccess) return cuda_status(e, "laps_mc_step");
+    }
     lapssd_status st = LAPSSD_OK;
     static const bool no_pdl = getenv("LAPSSD_NO_PDL") != nullptr;
     int j = 0;
@@ -979,10 +983,6 @@ lapssd_status laps_mc_step(lapssd_mc *h, const lapssd_rows *rows, int32_t *token
         st = cuda_status(launch_verify_grid(ab, nb, 0, j == 1 && !no_pdl, s), "laps_mc_step verify");
     }
     if (st != LAPSSD_OK) return st;
-    if (active_out) {
-        const cudaError_t e = cudaMemsetAsync(active_out, 0, sizeof(int32_t), s);
-        if (e != cudaSuccess) return cuda_status(e, "laps_mc_step");
-    }
     // a3 + a4-a7 + a1, one warp per trace
     return cuda_status(launch_mc_step(h->st, h->sc, h->mc, rw, na, h->desc, h->sel, active_out, s),
                        "laps_mc_step update/select");

@@ -13,6 +13,8 @@
 //   (a1) the acceptance test of the selected request's round for the next verify.
 // The per-trace result is exactly the single-trace handle's (and the oracle's) with
 // B = 1; traces share nothing but the slab pool.
+#include <cstdlib>
+
 #include "select_core.cuh"
 
 namespace lapssd {
@@ -28,8 +30,11 @@ __global__ void __launch_bounds__(256) mc_step_kernel(const State st, const Sche
     Globals *g = mc.g + t;
     // (a3) the round this trace just verified
     if (n_accept && lane == 0) {
+        // r of the round that ran is the descriptor's (a1 before the rows streamed; the
+        // verify kernel only copies it to n_accept), so this kernel reads nothing the
+        // verify kernel writes and may overlap its tail
         const SlotDesc d = desc[t];
-        const int r = n_accept[t];
+        const int r = d.r;
         if (d.i >= 0 && r >= 0) update_one(st, sc, d.i, r, g->now_us);
     }
     __syncwarp();
@@ -127,9 +132,21 @@ cudaError_t launch_mc_step(const State &st, const Sched &sc, const McDev &mc, co
     if (mc.T <= 0) return cudaSuccess;
     const int warps_per_block = 8;
     const int blocks = (mc.T + warps_per_block - 1) / warps_per_block;
-    mc_step_kernel<<<blocks, 32 * warps_per_block, 0, s>>>(st, sc, mc, rw, n_accept, desc, sel_out, active);
+    // a programmatic dependent of the last verify sub-launch: its warps start on SMs as
+    // that grid's CTAs retire (the verify CTAs trigger after snapshotting desc[])
+    static const bool no_pdl = getenv("LAPSSD_NO_PDL") != nullptr;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(32 * warps_per_block);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (no_pdl || !n_accept) ? 0 : 1;   // only right after laps_mc_step's verify
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, mc_step_kernel, st, sc, mc, rw, n_accept, desc, sel_out, active);
     count_launch();
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace lapssd

@@ -710,7 +710,6 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
     uint64_t *const part = par ? a.part1 : a.part;
     uint32_t *const work = par ? a.work1 : a.work;
     if (tid == 0) {
-        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumerWarps);
@@ -748,6 +747,9 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
     }
     __syncthreads();
     if (tid == 0 && a.snap) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.snap) : "memory");
+    // dependents may launch once every CTA has taken its snapshot of desc[] / sel[]: the
+    // next verify (laps_step) and the Monte-Carlo select, which rewrites desc[]
+    if (tid == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
