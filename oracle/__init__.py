@@ -24,6 +24,7 @@ _SRC = os.path.join(_HERE, "lapssd_oracle.c")
 
 F32, BF16 = 0, 1
 POL_LAPSSD, POL_FCFS, POL_LPSJF, POL_LAS = 0, 1, 2, 3
+COST_EQ6, COST_FIG1 = 0, 1
 POLICIES = {"laps-sd": POL_LAPSSD, "fcfs": POL_FCFS, "lp-sjf": POL_LPSJF, "las": POL_LAS}
 
 
@@ -54,7 +55,9 @@ class OrcConfig(C.Structure):
     _fields_ = [("policy", C.c_int32), ("K", C.c_int32), ("s1_up_us", C.c_int64),
                 ("M", C.c_double), ("gamma", C.c_int32), ("delta", C.c_double),
                 ("k", C.c_int32), ("t_ssm_us", C.c_int64), ("t_llm_us", C.c_int64),
-                ("placement", C.c_int32), ("pin_rule", C.c_int32), ("seed", C.c_uint64)]
+                ("placement", C.c_int32), ("pin_rule", C.c_int32), ("seed", C.c_uint64),
+                ("cost_model", C.c_int32), ("t_tok_us", C.c_int64), ("switch_c0_us", C.c_int64),
+                ("switch_c1_us", C.c_int64)]
 
 
 class StateView(C.Structure):
@@ -67,7 +70,9 @@ class StateView(C.Structure):
                 ("perceptible", C.POINTER(C.c_uint8)), ("pinned", C.POINTER(C.c_uint8)),
                 ("level", C.POINTER(C.c_uint8)), ("running", C.POINTER(C.c_uint8)),
                 ("A", C.POINTER(C.c_double)), ("key", C.POINTER(C.c_uint64)),
-                ("ring", C.POINTER(C.c_int32))]
+                ("ring", C.POINTER(C.c_int32)), ("switch_us", C.POINTER(C.c_int64)),
+                ("in_batch", C.POINTER(C.c_uint8)), ("step_cost_us", C.c_int64),
+                ("switch_total_us", C.c_int64)]
 
 
 _lib = None
@@ -76,7 +81,9 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
+        # LAPSSD_ORACLE_LIB: a mutated build of the same source (tests/test_oracle_mutants.py
+        # checks that the pins reject it); default: the oracle itself
+        _lib = C.CDLL(os.environ.get("LAPSSD_ORACLE_LIB") or build())
         L = _lib
         vp, i32, i64, u32, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
@@ -95,14 +102,18 @@ def lib():
         L.orc_thresholds.restype = i32
         L.orc_eq6.argtypes = [i64, C.c_double, i32, i64, i64]
         L.orc_eq6.restype = u64
-        L.orc_sim_create.argtypes = [C.POINTER(OrcConfig), i32, vp, vp, vp, i32, i32]
+        L.orc_fig1_est.argtypes = [i64, C.c_double, i64]
+        L.orc_fig1_est.restype = u64
+        L.orc_sim_make_perceptible.argtypes = [vp, i32, C.c_double]
+        L.orc_sim_make_perceptible.restype = i32
+        L.orc_sim_create.argtypes = [C.POINTER(OrcConfig), i32, vp, vp, vp, vp, i32, i32]
         L.orc_sim_create.restype = vp
         L.orc_sim_destroy.argtypes = [vp]
         L.orc_sim_set_trace.argtypes = [vp, u32]
         L.orc_sim_select.argtypes = [vp, i32, vp]
         L.orc_sim_select.restype = i32
-        L.orc_sim_candidates.argtypes = [vp, i32, vp, vp]
-        L.orc_sim_merge.argtypes = [vp, vp, i32, vp, i32, vp, vp]
+        L.orc_sim_candidates.argtypes = [vp, i32, vp, vp, vp]
+        L.orc_sim_merge.argtypes = [vp, vp, vp, i32, vp, i32, vp, vp]
         L.orc_sim_merge.restype = i32
         L.orc_sim_update.argtypes = [vp, vp, vp, i32]
         L.orc_sim_step.argtypes = [vp, vp, vp, vp, i32, i64, vp, i32, i32, vp, vp, vp, vp]
@@ -239,6 +250,11 @@ def eq6(L, A, k, t_ssm_us, t_llm_us) -> int:
     return int(lib().orc_eq6(int(L), float(A), int(k), int(t_ssm_us), int(t_llm_us)))
 
 
+def fig1_est(L, A, t_tok_us) -> int:
+    """Fig. 1 model: floor(L t_tok / A) us."""
+    return int(lib().orc_fig1_est(int(L), float(A), int(t_tok_us)))
+
+
 def jobs_schedule(policy, arrival_us, service_us, L_pred=None, est_us=None):
     """Non-preemptive job-level schedule (Fig. 1 semantics).  policy: 0 SJF-by-est,
     1 FCFS, 2 LP-SJF.  Returns (sum of C_i - r_i, order, C)."""
@@ -279,25 +295,33 @@ class SchedConfig:
     placement: int = 0
     pin_rule: int = 0
     seed: int = 0
+    cost_model: int = COST_EQ6
+    t_tok_us: int = 0
+    switch_c0_us: int = 0
+    switch_c1_us: int = 0
 
     def c(self) -> OrcConfig:
         return OrcConfig(self.policy, self.K, self.s1_up_us, self.M, self.gamma, self.delta,
                          self.k, self.t_ssm_us, self.t_llm_us, self.placement, self.pin_rule,
-                         self.seed & (2**64 - 1))
+                         self.seed & (2**64 - 1), self.cost_model, self.t_tok_us,
+                         self.switch_c0_us, self.switch_c1_us)
 
 
 class Sim:
     """The resident-request simulation: admit / select / verify / update / clock."""
 
-    def __init__(self, cfg: SchedConfig, arrival_us, L_true, L_pred, rank=0, world=1, trace=0):
+    def __init__(self, cfg: SchedConfig, arrival_us, L_true, L_pred, rank=0, world=1, trace=0,
+                 prompt=None):
         self.cfg = cfg
         self._a = _c(arrival_us, np.int64)
         self._lt = _c(L_true, np.int32)
         self._lp = _c(L_pred, np.int32)
+        self._pr = _c(prompt, np.int32) if prompt is not None else None
         self.n = len(self._a)
         self._cc = cfg.c()
         self.h = lib().orc_sim_create(C.byref(self._cc), self.n, _ptr(self._a), _ptr(self._lt),
-                                      _ptr(self._lp), rank, world)
+                                      _ptr(self._lp), _ptr(self._pr) if self._pr is not None else None,
+                                      rank, world)
         if not self.h:
             raise ValueError("orc_sim_create rejected the configuration")
         if trace:
@@ -315,18 +339,29 @@ class Sim:
         cnt = lib().orc_sim_select(self.h, B, _ptr(sel))
         return sel, cnt
 
-    def candidates(self, Cn):
+    def make_perceptible(self, i, A):
+        """Test hook (Fig. 1(c) clairvoyant case): request i perceptible with rate A."""
+        rc = lib().orc_sim_make_perceptible(self.h, int(i), float(A))
+        if rc != 0:
+            raise ValueError("make_perceptible rejected")
+
+    def candidates(self, Cn, with_switch=False):
         keys = np.zeros(Cn, np.uint64)
+        sw = np.zeros(Cn, np.int64)
         nxt = np.zeros(1, np.int64)
-        lib().orc_sim_candidates(self.h, Cn, _ptr(keys), _ptr(nxt))
+        lib().orc_sim_candidates(self.h, Cn, _ptr(keys), _ptr(sw), _ptr(nxt))
+        if with_switch:
+            return keys, sw, int(nxt[0])
         return keys, int(nxt[0])
 
-    def merge(self, all_keys, Cn, all_next, B):
+    def merge(self, all_keys, Cn, all_next, B, all_switch=None):
         k = _c(all_keys, np.uint64)
         nx = _c(all_next, np.int64)
+        sw = _c(all_switch, np.int64) if all_switch is not None else None
         sel = np.full(B, -1, np.int32)
         g = np.zeros(1, np.int32)
-        own = lib().orc_sim_merge(self.h, _ptr(k), Cn, _ptr(nx), B, _ptr(sel), _ptr(g))
+        own = lib().orc_sim_merge(self.h, _ptr(k), _ptr(sw) if sw is not None else None, Cn,
+                                  _ptr(nx), B, _ptr(sel), _ptr(g))
         return sel, own, int(g[0])
 
     def update(self, sel, n_accept):
@@ -361,4 +396,6 @@ class Sim:
                     x_us=arr(v.x_us), admitted=arr(v.admitted), done=arr(v.done),
                     perceptible=arr(v.perceptible), pinned=arr(v.pinned), level=arr(v.level),
                     running=arr(v.running), A=arr(v.A), key=arr(v.key),
-                    ring=arr(v.ring, n * g).reshape(n, g) if n else np.zeros((0, g)))
+                    ring=arr(v.ring, n * g).reshape(n, g) if n else np.zeros((0, g)),
+                    switch_us=arr(v.switch_us), in_batch=arr(v.in_batch),
+                    step_cost_us=v.step_cost_us, switch_total_us=v.switch_total_us)

@@ -422,46 +422,70 @@ uint64_t orc_eq6(int64_t L, double A, int32_t k, int64_t t_ssm_us, int64_t t_llm
     return (uint64_t)T;                              /* floor, T >= 0 */
 }
 
+/* The Fig. 1 cost model: a request of output length L at acceptance rate A
+ * needs L / A candidate tokens, each verified in t_tok ("10 ms per token", SSM time
+ * omitted), so T~ = floor((L * t_tok) / A) in fp64, in this order (AMB-3, AMB-31);
+ * A = 0 gives no finite estimate and saturates. */
+uint64_t orc_fig1_est(int64_t L, double A, int64_t t_tok_us)
+{
+    double num = (double)L * (double)t_tok_us;
+    double T = num / A;
+    if (!(T > 0.0)) return (L > 0 && t_tok_us > 0) ? UINT64_MAX : 0;   /* A = 0: unbounded */
+    if (T >= 1.8e19) return UINT64_MAX;
+    return (uint64_t)T;
+}
+
 struct orc_sim {
     orc_config cfg;
     int32_t n, rank, world;
     uint32_t trace;
     int64_t *arrival;
-    int32_t *L_true, *L_pred;
+    int32_t *L_true, *L_pred, *prompt;
     int64_t S_up[16];
-    int64_t c_round;
+    int64_t c_round;       /* service of one round: k T_SSM + T_LLM (EQ6) or k t_tok (FIG1) */
     /* state, one entry per local request */
     int32_t *acc_tok, *acc_draft, *rounds, *ring;
     int64_t *E, *T_total, *C, *x;
     uint8_t *admitted, *done, *perceptible, *pinned, *level, *running;
     double *A;
     uint64_t *key;
+    uint8_t *in_batch;     /* member of the batch that ran last (switch-in test, AMB-24) */
+    int64_t *switch_us;    /* switching time charged on this request's entries */
     int64_t now;
+    int64_t step_cost;     /* duration of the step that ran last: c_round + switch-ins */
+    int64_t switch_total;  /* system time spent switching (AMB-24) */
     int32_t cursor, prev_count;
     /* scratch */
     int32_t *order;
 };
 
 orc_sim *orc_sim_create(const orc_config *cfg, int32_t n_local, const int64_t *arrival_us,
-                        const int32_t *L_true, const int32_t *L_pred,
+                        const int32_t *L_true, const int32_t *L_pred, const int32_t *prompt,
                         int32_t rank, int32_t world)
 {
     if (cfg->K < 1 || cfg->K > 16 || cfg->gamma < 2 || !(cfg->delta >= 0.0) ||
-        cfg->k < 1 || cfg->k > 16 || n_local < 0 || world < 1 || rank < 0 || rank >= world)
+        cfg->k < 1 || cfg->k > 16 || n_local < 0 || world < 1 || rank < 0 || rank >= world ||
+        (cfg->cost_model != ORC_COST_EQ6 && cfg->cost_model != ORC_COST_FIG1) ||
+        cfg->t_tok_us < 0 || cfg->switch_c0_us < 0 || cfg->switch_c1_us < 0)
         return NULL;
     orc_sim *s = (orc_sim *)calloc(1, sizeof *s);
     s->cfg = *cfg;
     s->n = n_local; s->rank = rank; s->world = world;
     if (orc_thresholds(cfg->K, cfg->s1_up_us, cfg->M, s->S_up) != 0) { free(s); return NULL; }
-    s->c_round = (int64_t)cfg->k * cfg->t_ssm_us + cfg->t_llm_us;
+    /* one round's service (E_i increment): Eq. 6's k T_SSM + T_LLM, or in
+     * the Fig. 1 model the k candidates verified at t_tok each (AMB-3) */
+    s->c_round = cfg->cost_model == ORC_COST_FIG1 ? (int64_t)cfg->k * cfg->t_tok_us
+                                                  : (int64_t)cfg->k * cfg->t_ssm_us + cfg->t_llm_us;
     size_t n = (size_t)(n_local > 0 ? n_local : 1);
     s->arrival = (int64_t *)malloc(n * sizeof(int64_t));
     s->L_true = (int32_t *)malloc(n * sizeof(int32_t));
     s->L_pred = (int32_t *)malloc(n * sizeof(int32_t));
+    s->prompt = (int32_t *)calloc(n, sizeof(int32_t));
     if (n_local > 0) {
         memcpy(s->arrival, arrival_us, (size_t)n_local * sizeof(int64_t));
         memcpy(s->L_true, L_true, (size_t)n_local * sizeof(int32_t));
         memcpy(s->L_pred, L_pred, (size_t)n_local * sizeof(int32_t));
+        if (prompt) memcpy(s->prompt, prompt, (size_t)n_local * sizeof(int32_t));
     }
     s->acc_tok = (int32_t *)calloc(n, sizeof(int32_t));
     s->acc_draft = (int32_t *)calloc(n, sizeof(int32_t));
@@ -481,7 +505,10 @@ orc_sim *orc_sim_create(const orc_config *cfg, int32_t n_local, const int64_t *a
     s->A = (double *)calloc(n, sizeof(double));
     s->key = (uint64_t *)calloc(n, sizeof(uint64_t));
     s->order = (int32_t *)malloc(n * sizeof(int32_t));
+    s->in_batch = (uint8_t *)calloc(n, 1);
+    s->switch_us = (int64_t *)calloc(n, sizeof(int64_t));
     s->now = 0; s->cursor = 0; s->prev_count = 0; s->trace = 0;
+    s->step_cost = s->c_round; s->switch_total = 0;
     return s;
 }
 
@@ -490,7 +517,8 @@ void orc_sim_set_trace(orc_sim *s, uint32_t trace) { s->trace = trace; }
 void orc_sim_destroy(orc_sim *s)
 {
     if (!s) return;
-    free(s->arrival); free(s->L_true); free(s->L_pred);
+    free(s->arrival); free(s->L_true); free(s->L_pred); free(s->prompt);
+    free(s->in_batch); free(s->switch_us);
     free(s->acc_tok); free(s->acc_draft); free(s->rounds); free(s->ring);
     free(s->E); free(s->T_total); free(s->C); free(s->x);
     free(s->admitted); free(s->done); free(s->perceptible); free(s->pinned);
@@ -512,6 +540,14 @@ typedef struct {
 } prio;
 
 static uint64_t sat32(uint64_t v) { return v > 0xFFFFFFFFull ? 0xFFFFFFFFull : v; }
+
+/* T~ for L tokens at rate A under the configured cost model: Eq. (6) or the
+ * Fig. 1 model. */
+static uint64_t estimate(const orc_sim *s, int64_t L, double A)
+{
+    if (s->cfg.cost_model == ORC_COST_FIG1) return orc_fig1_est(L, A, s->cfg.t_tok_us);
+    return orc_eq6(L, A, s->cfg.k, s->cfg.t_ssm_us, s->cfg.t_llm_us);
+}
 
 static prio prio_of(const orc_sim *s, int32_t i)
 {
@@ -540,8 +576,7 @@ static prio prio_of(const orc_sim *s, int32_t i)
         if (s->perceptible[i]) {
             int64_t L_rem = (int64_t)s->L_pred[i] - s->acc_tok[i];   /* AMB-12 */
             if (L_rem < 0) L_rem = 0;
-            f.secondary = sat32(orc_eq6(L_rem, s->A[i], s->cfg.k, s->cfg.t_ssm_us,
-                                        s->cfg.t_llm_us));
+            f.secondary = sat32(estimate(s, L_rem, s->A[i]));
             f.notrun = 0;
         } else {
             f.notrun = !s->running[i];
@@ -575,11 +610,12 @@ static int cmp_idx(const void *pa, const void *pb)
     return prio_cmp(&a, &b);
 }
 
-/* a7 + a4: the clock advances by the cost of the step that just ran, then
- * every request with r_i <= now is admitted (Eq. (3) x_i >= r_i). */
+/* a7 + a4: the clock advances by the duration of the step that just ran (one round,
+ * AMB-17, plus the switch-ins it paid, AMB-24), then every request with r_i <= now is
+ * admitted (Eq. (3) x_i >= r_i). */
 static void advance_and_admit(orc_sim *s)
 {
-    if (s->prev_count > 0) s->now += s->c_round;                /* AMB-17 */
+    if (s->prev_count > 0) s->now += s->step_cost;
     while (s->cursor < s->n && s->arrival[s->cursor] <= s->now) {
         s->admitted[s->cursor] = 1;
         s->cursor++;
@@ -600,12 +636,35 @@ static int32_t sort_eligible(orc_sim *s)
     return m;
 }
 
-static void commit_selection(orc_sim *s, const int32_t *sel, int32_t B, int32_t global_count,
-                             int64_t next_arrival)
+/* Switching cost of request i if it enters the batch now (AMB-24): a
+ * request that did not run in the previous step has its KV cache (prompt + generated
+ * tokens) switched in, c0 + c1 (prompt + tokens).  0 if it ran in the previous step. */
+static int64_t switch_in_cost(const orc_sim *s, int32_t i)
 {
+    if (s->in_batch[i]) return 0;
+    return s->cfg.switch_c0_us + s->cfg.switch_c1_us * ((int64_t)s->prompt[i] + s->acc_tok[i]);
+}
+
+/* Commit this rank's part of the batch.  switch_sum: the switching time of the GLOBAL
+ * batch (< 0: single rank, computed here from its own entries).  The step then lasts
+ * c_round + switch_sum (system time, not attained service: AMB-24). */
+static void commit_selection(orc_sim *s, const int32_t *sel, int32_t B, int32_t global_count,
+                             int64_t next_arrival, int64_t switch_sum)
+{
+    int64_t own_switch = 0;
     for (int32_t b = 0; b < B; b++) {
         int32_t i = sel[b];
         if (i < 0) continue;
+        int64_t c = switch_in_cost(s, i);
+        s->switch_us[i] += c;
+        own_switch += c;
+    }
+    if (switch_sum < 0) switch_sum = own_switch;
+    for (int32_t i = 0; i < s->n; i++) s->in_batch[i] = 0;
+    for (int32_t b = 0; b < B; b++) {
+        int32_t i = sel[b];
+        if (i < 0) continue;
+        s->in_batch[i] = 1;
         if (s->x[i] < 0) s->x[i] = s->now;                   /* x_i */
         switch (s->cfg.policy) {
         case ORC_POL_FCFS: case ORC_POL_LPSJF: s->pinned[i] = 1; break;
@@ -619,6 +678,8 @@ static void commit_selection(orc_sim *s, const int32_t *sel, int32_t B, int32_t 
     if (global_count == 0 && next_arrival != INT64_MAX && next_arrival > s->now)
         s->now = next_arrival;                                  /* idle: jump */
     s->prev_count = global_count;
+    s->step_cost = s->c_round + (global_count > 0 ? switch_sum : 0);
+    if (global_count > 0) s->switch_total += switch_sum;
 }
 
 int32_t orc_sim_select(orc_sim *s, int32_t B, int32_t *sel_out)
@@ -628,16 +689,19 @@ int32_t orc_sim_select(orc_sim *s, int32_t B, int32_t *sel_out)
     int32_t count = m < B ? m : B;
     for (int32_t b = 0; b < B; b++) sel_out[b] = b < count ? s->order[b] : -1;
     int64_t next = s->cursor < s->n ? s->arrival[s->cursor] : INT64_MAX;
-    commit_selection(s, sel_out, B, count, next);
+    commit_selection(s, sel_out, B, count, next, -1);
     return count;
 }
 
-void orc_sim_candidates(orc_sim *s, int32_t C, uint64_t *keys_out, int64_t *next_arrival_out)
+void orc_sim_candidates(orc_sim *s, int32_t C, uint64_t *keys_out, int64_t *switch_out,
+                        int64_t *next_arrival_out)
 {
     advance_and_admit(s);
     int32_t m = sort_eligible(s);
-    for (int32_t c = 0; c < C; c++)
+    for (int32_t c = 0; c < C; c++) {
         keys_out[c] = c < m ? s->key[s->order[c]] : UINT64_MAX;
+        if (switch_out) switch_out[c] = c < m ? switch_in_cost(s, s->order[c]) : 0;
+    }
     *next_arrival_out = s->cursor < s->n ? s->arrival[s->cursor] : INT64_MAX;
 }
 
@@ -647,7 +711,7 @@ static int cmp_u64(const void *a, const void *b)
     return x < y ? -1 : x > y ? 1 : 0;
 }
 
-int32_t orc_sim_merge(orc_sim *s, const uint64_t *all_keys, int32_t C,
+int32_t orc_sim_merge(orc_sim *s, const uint64_t *all_keys, const int64_t *all_switch, int32_t C,
                       const int64_t *all_next_arrival, int32_t B, int32_t *sel_out,
                       int32_t *global_count_out)
 {
@@ -656,11 +720,15 @@ int32_t orc_sim_merge(orc_sim *s, const uint64_t *all_keys, int32_t C,
     memcpy(tmp, all_keys, (size_t)total * sizeof(uint64_t));
     qsort(tmp, (size_t)total, sizeof(uint64_t), cmp_u64);
     int32_t gcount = 0, own = 0;
+    int64_t sw = 0;
     for (int32_t c = 0; c < total && gcount < B; c++) {
         if (tmp[c] == UINT64_MAX || (tmp[c] >> 63)) break;
         uint32_t id = (uint32_t)(tmp[c] & 0xFFFFFFu);
         if ((int32_t)(id % (uint32_t)s->world) == s->rank)
             sel_out[own++] = (int32_t)(id / (uint32_t)s->world);
+        if (all_switch)                              /* the selected key's switch-in cost */
+            for (int32_t x = 0; x < total; x++)
+                if (all_keys[x] == tmp[c]) { sw += all_switch[x]; break; }
         gcount++;
     }
     for (int32_t b = own; b < B; b++) sel_out[b] = -1;
@@ -668,9 +736,36 @@ int32_t orc_sim_merge(orc_sim *s, const uint64_t *all_keys, int32_t C,
     int64_t next = INT64_MAX;
     for (int32_t g = 0; g < s->world; g++)
         if (all_next_arrival[g] < next) next = all_next_arrival[g];
-    commit_selection(s, sel_out, B, gcount, next);
+    commit_selection(s, sel_out, B, gcount, next, sw);
     if (global_count_out) *global_count_out = gcount;
     return own;
+}
+
+/* The Stabilized event: request i becomes perceptible with predicted
+ * acceptance rate A, its execution time is estimated (Eq. 6 at the predicted length,
+ * P:198) and it is "moved to the corresponding queue": the queue whose interval
+ * contains T~ (AMB-14), or it stays (placement STAY).  PIN_ON_STABLE pins it now
+ * (AMB-15).  Shared by the update (A = the window mean) and the clairvoyance hook. */
+static void stabilise(orc_sim *s, int32_t i, double A)
+{
+    s->perceptible[i] = 1;
+    s->A[i] = A;                                                        /* P:194, AMB-8 */
+    uint64_t T = estimate(s, s->L_pred[i], A);                          /* P:139, Eq. 6 */
+    s->T_total[i] = T > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)T;
+    if (s->cfg.placement == ORC_PLACE_BY_ESTIMATE)                      /* P:148, AMB-14 */
+        s->level[i] = (uint8_t)level_of(s->S_up, s->cfg.K, s->T_total[i]);
+    if (s->cfg.pin_rule == ORC_PIN_ON_STABLE) s->pinned[i] = 1;
+}
+
+/* Test hook: the clairvoyant case of Fig. 1(c) ("if we have information about
+ * both the request length and the acceptance rate"): request i is perceptible with
+ * rate A from now on, through the same Stabilized event as the update.  Returns -1 if
+ * i is out of range, not LAPS-SD, or already perceptible. */
+int32_t orc_sim_make_perceptible(orc_sim *s, int32_t i, double A)
+{
+    if (i < 0 || i >= s->n || s->cfg.policy != ORC_POL_LAPSSD || s->perceptible[i]) return -1;
+    stabilise(s, i, A);
+    return 0;
 }
 
 /* a3: the LAPS-SD state update after one round. */
@@ -709,14 +804,7 @@ void orc_sim_update(orc_sim *s, const int32_t *sel, const int32_t *n_accept, int
                 if (mx - mn < s->cfg.delta) { stable = 1; mean = sum / (double)gamma; }
             }
             if (stable) {
-                s->perceptible[i] = 1;                                  /* P:137 */
-                s->A[i] = mean;                                         /* P:194, AMB-8 */
-                uint64_t T = orc_eq6(s->L_pred[i], mean, k, s->cfg.t_ssm_us,
-                                     s->cfg.t_llm_us);                  /* P:139, Eq. 6 */
-                s->T_total[i] = T > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)T;
-                if (s->cfg.placement == ORC_PLACE_BY_ESTIMATE)          /* P:148, AMB-14 */
-                    s->level[i] = (uint8_t)level_of(s->S_up, K, s->T_total[i]);
-                if (s->cfg.pin_rule == ORC_PIN_ON_STABLE) s->pinned[i] = 1;
+                stabilise(s, i, mean);
             } else {
                 int32_t lev = level_of(s->S_up, K, s->E[i]);            /* P:175 */
                 if (lev > s->level[i]) { s->level[i] = (uint8_t)lev; demoted = 1; }
@@ -727,7 +815,7 @@ void orc_sim_update(orc_sim *s, const int32_t *sel, const int32_t *n_accept, int
         }
         if (s->acc_tok[i] >= s->L_true[i]) {                            /* P:177 */
             s->done[i] = 1;
-            s->C[i] = s->now + s->c_round;                              /* C_i, P:86 */
+            s->C[i] = s->now + s->step_cost;        /* C_i, P:86: the end of this step */
         }
         s->running[i] = (uint8_t)(!s->done[i] && !demoted);
     }
@@ -779,6 +867,8 @@ void orc_sim_view(orc_sim *s, orc_state_view *v)
     v->admitted = s->admitted; v->done = s->done; v->perceptible = s->perceptible;
     v->pinned = s->pinned; v->level = s->level; v->running = s->running;
     v->A = s->A; v->key = s->key; v->ring = s->ring;
+    v->switch_us = s->switch_us; v->in_batch = s->in_batch;
+    v->step_cost_us = s->step_cost; v->switch_total_us = s->switch_total;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -16,7 +16,11 @@
  *                            special cases p=q / disjoint / one-hot / mixture family
  *   orc_thresholds ......... P:169 formula hand values
  *   orc_eq6 ................ P:196-200 hand values
- *   orc_sim_* .............. Fig. 1 token-level expectations (renewal DP),
+ *   orc_sim_* .............. Fig. 1 clairvoyant run (R3,R1,R2 / 450 ms) and FCFS /
+ *                            LP-SJF (583 / 683 ms) through the token-level simulation,
+ *                            perceptible-first + SJF on T~_rem, placement,
+ *                            switching-cost hand values,
+ *                            Fig. 1 token-level expectations (renewal DP),
  *                            stability deadline (P:194 + 1/t bound), degeneracies,
  *                            invariants
  *   orc_jobs_schedule ...... Fig. 1 printed averages 583 / 683 ms,
@@ -91,6 +95,7 @@ void orc_verify_logits_batch(const void *zp, const void *zq, int32_t dtype, int6
 enum { ORC_POL_LAPSSD = 0, ORC_POL_FCFS = 1, ORC_POL_LPSJF = 2, ORC_POL_LAS = 3 };
 enum { ORC_PLACE_BY_ESTIMATE = 0, ORC_PLACE_STAY = 1 };
 enum { ORC_PIN_ON_SELECT = 0, ORC_PIN_ON_STABLE = 1 };
+enum { ORC_COST_EQ6 = 0, ORC_COST_FIG1 = 1 };
 
 typedef struct {
     int32_t  policy;
@@ -105,32 +110,46 @@ typedef struct {
     int32_t  placement;    /* ORC_PLACE_*                                           */
     int32_t  pin_rule;     /* ORC_PIN_*                                             */
     uint64_t seed;
+    int32_t  cost_model;   /* ORC_COST_EQ6: round = k T_SSM + T_LLM, T~ = Eq. 6;
+                              ORC_COST_FIG1: round = k t_tok, T~ = L t_tok / A */
+    int64_t  t_tok_us;     /* Fig. 1 verification time per candidate token          */
+    int64_t  switch_c0_us; /* switch-in cost c0 + c1 (prompt + tokens) (AMB-24)      */
+    int64_t  switch_c1_us;
 } orc_config;
 
 /* S_up[j] = floor(s1_up * M^j), j = 0..K-2, iterative fp64 multiply. */
 int32_t  orc_thresholds(int32_t K, int64_t s1_up_us, double M, int64_t *S_up_out);
 /* Eq. (6): floor(L (k T_SSM + T_LLM) / (k A + 1)) in microseconds. */
 uint64_t orc_eq6(int64_t L, double A, int32_t k, int64_t t_ssm_us, int64_t t_llm_us);
+/* Fig. 1 model: floor(L t_tok / A) microseconds (UINT64_MAX if A = 0). */
+uint64_t orc_fig1_est(int64_t L, double A, int64_t t_tok_us);
 
 /* ---- the resident-request simulation (a3-a8) ---- */
 typedef struct orc_sim orc_sim;
 
+/* prompt: prompt lengths (switching cost, AMB-24), nullable = 0. */
 orc_sim *orc_sim_create(const orc_config *cfg, int32_t n_local, const int64_t *arrival_us,
-                        const int32_t *L_true, const int32_t *L_pred,
+                        const int32_t *L_true, const int32_t *L_pred, const int32_t *prompt,
                         int32_t rank, int32_t world);
 void     orc_sim_destroy(orc_sim *s);
 /* Monte-Carlo traces: Philox counter word c3 (AMB-21). */
 void     orc_sim_set_trace(orc_sim *s, uint32_t trace);
+/* TEST HOOK (Fig. 1(c) clairvoyant case): request i becomes perceptible with rate A
+ * through the update's own Stabilized event (estimate, placement, pin rule). */
+int32_t  orc_sim_make_perceptible(orc_sim *s, int32_t i, double A);
 
 /* Single-rank select: advance clock, admit, build keys, take top-B.  Returns count;
  * sel_out[B] holds local indices in key order, -1 padded. */
 int32_t  orc_sim_select(orc_sim *s, int32_t B, int32_t *sel_out);
 /* Multi-rank select, phase 1: advance clock, admit, build keys, write this rank's
- * C smallest eligible keys (ascending, UINT64_MAX padded) and its next arrival. */
-void     orc_sim_candidates(orc_sim *s, int32_t C, uint64_t *keys_out, int64_t *next_arrival_out);
+ * C smallest eligible keys (ascending, UINT64_MAX padded), each one's switch-in cost
+ * if it is selected (switch_out, nullable) and its next arrival. */
+void     orc_sim_candidates(orc_sim *s, int32_t C, uint64_t *keys_out, int64_t *switch_out,
+                            int64_t *next_arrival_out);
 /* Multi-rank select, phase 2: given the gathered candidates of all ranks
- * (world*C keys, world next arrivals), take the global top-B and keep own ids. */
-int32_t  orc_sim_merge(orc_sim *s, const uint64_t *all_keys, int32_t C,
+ * (world*C keys, their switch-in costs (nullable), world next arrivals), take the
+ * global top-B, keep own ids, advance the clock by the global batch's step. */
+int32_t  orc_sim_merge(orc_sim *s, const uint64_t *all_keys, const int64_t *all_switch, int32_t C,
                        const int64_t *all_next_arrival, int32_t B, int32_t *sel_out,
                        int32_t *global_count_out);
 
@@ -156,6 +175,10 @@ typedef struct {
     double  *A;
     uint64_t *key;
     int32_t *ring;         /* n_local * gamma */
+    int64_t *switch_us;    /* switching time charged on each request's entries (AMB-24) */
+    uint8_t *in_batch;     /* in the batch that ran last */
+    int64_t step_cost_us;  /* duration of the step that ran last */
+    int64_t switch_total_us;
 } orc_state_view;
 void     orc_sim_view(orc_sim *s, orc_state_view *v);
 /* keys exactly as the last select built them (ineligible ones included) */
