@@ -143,6 +143,19 @@ def build_workload(args, rank, world, device, pool_slabs=None):
     return tr, local, pool, tab
 
 
+def build_digest() -> str:
+    """sha256 of liblapssd.so's sources, header and nvcc flags: identifies the build an
+    ncu capture under profiles/ belongs to."""
+    import hashlib
+    sys.path.insert(0, os.path.join(ROOT, "paper_2505_17074_b200"))
+    import build as lb
+    h = hashlib.sha256(" ".join(lb.FLAGS).encode())
+    for f in sorted(lb.sources() + [os.path.join(lb.CSRC, x) for x in ("lapssd_internal.cuh", "select_core.cuh")]
+                    + [os.path.join(ROOT, "include", "lapssd.h")]):
+        h.update(open(f, "rb").read())
+    return h.hexdigest()[:16]
+
+
 def algorithmic_bytes(n_acc: np.ndarray, V: int, k: int, s: int = 2) -> float:
     """SURVEY s.8(d): per verified slot (r<k ? 2 : 1) V s row bytes + 2 s min(r+1,k)
     gathered scalars + 4k draft bytes.  n_acc holds r per slot (-1 = empty)."""
@@ -171,18 +184,21 @@ def run_ours(args):
     B = B_local * world                        # global batch (weak scaling)
     tr, local, pool, tab = build_workload(args, rank, world, dev)
     cfg = L.SchedConfig(**SCHED, seed=synth.CONFIGS["c4"]["seed"])
+    # the slab pool is static, so consecutive verify launches may overlap (lapssd.h:
+    # lapssd_set_step_overlap)
     h = L.Handle(cfg, local.arrival_us, local.L_true, local.L_pred, max_batch=B, V=args.V,
-                 rank=rank, world=world)
+                 rank=rank, world=world, overlap=True)
     tab_d = torch.as_tensor(tab, device=dev)
     rows = L.Rows(pool.p, pool.q, pool.draft, tab_d)
     comm = cand = None
     Cn = min(B, args.n_per_gpu)
+    W = 2 * Cn + 1                             # candidate block: keys, switch costs, next arrival
     if world > 1:
         comm = L.nccl_comm()
-        cand = torch.zeros((world + 1) * (Cn + 1), dtype=torch.int64, device=dev)
-        h.laps_candidates(Cn, cand[: Cn + 1])
-        dist.all_gather_into_tensor(cand[Cn + 1:], cand[: Cn + 1])
-        h.laps_merge(cand[Cn + 1:], Cn, B)
+        cand = torch.zeros((world + 1) * W, dtype=torch.int64, device=dev)
+        h.laps_candidates(Cn, cand[:W])
+        dist.all_gather_into_tensor(cand[W:], cand[:W])
+        h.laps_merge(cand[W:], Cn, B)
     elif args.dist_path:
         # the N>1 step (laps_step_dist: candidates + ncclAllGather + merge) on one rank, to
         # time its cost on the one GPU available; a one-rank gloo group only carries the
@@ -192,16 +208,18 @@ def run_ours(args):
                                  init_method=f"tcp://127.0.0.1:{29500 + os.getpid() % 1000}")
         comm = L.nccl_comm()
         tdist.destroy_process_group()
-        cand = torch.zeros(2 * (Cn + 1), dtype=torch.int64, device=dev)
-        h.laps_candidates(Cn, cand[: Cn + 1])
-        cand[Cn + 1:].copy_(cand[: Cn + 1])
-        h.laps_merge(cand[Cn + 1:], Cn, B)
+        cand = torch.zeros(2 * W, dtype=torch.int64, device=dev)
+        h.laps_candidates(Cn, cand[:W])
+        cand[W:].copy_(cand[:W])
+        h.laps_merge(cand[W:], Cn, B)
         args.no_profile = True
     else:
         h.laps_select(B)
     G = min(args.graph_steps, args.steps) if args.graph_steps > 0 else 0
-    hist = torch.full((max(args.warmup, G, 1) + 1 + (0 if G else args.steps), B), -1, dtype=torch.int32,
-                      device=dev)
+    # r of every step: rows [0, warmup) warm-up, [warmup, warmup + steps) the timed steps,
+    # the last row scratch (the instrumented replay)
+    hist = torch.full((args.warmup + args.steps + 1, B), -1, dtype=torch.int32, device=dev)
+    scratch_row = args.warmup + args.steps
 
     def step(t):
         if comm is not None:
@@ -218,24 +236,20 @@ def run_ours(args):
     launches_per_step = None
     g_prof = None
     if G:
-        # timed steps: replays of an UNINSTRUMENTED captured graph of G steps (the host
-        # enqueue cost is removed; the presort/merge side stream's fork/join is in the graph)
+        # timed steps: replays of UNINSTRUMENTED captured graphs of G steps each (the host
+        # enqueue cost is removed; the side stream's fork/join is in the graph), each graph
+        # writing its steps' r to their own rows of hist (the roofline's bytes are those of
+        # exactly the timed steps)
         if world == 1:
             h.profile(0)
         c0 = L.launch_count()
-        g1 = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g1):
-            for t in range(G):
-                step(max(args.warmup, G))  # n_accept of timed steps goes to a scratch row
-        launches_per_step = (L.launch_count() - c0) / G
-        graphs = [g1] * (args.steps // G)
-        rem = args.steps % G
-        if rem:
-            g2 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g2):
-                for t in range(rem):
-                    step(max(args.warmup, G))
-            graphs.append(g2)
+        for g0 in range(0, args.steps, G):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                for t in range(g0, min(g0 + G, args.steps)):
+                    step(args.warmup + t)
+            graphs.append(gr)
+        launches_per_step = (L.launch_count() - c0) / args.steps
         if world == 1 and not args.no_profile:
             # a second graph of G steps with the library's per-kernel CUDA events,
             # replayed right after the timed region (events add graph nodes, so they are
@@ -244,7 +258,7 @@ def run_ours(args):
             g_prof = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g_prof):
                 for t in range(G):
-                    step(t)
+                    step(scratch_row)
         torch.cuda.synchronize()
     elif world == 1 and not args.no_profile:
         h.profile(args.steps)
@@ -312,9 +326,8 @@ def run_ours(args):
         out["device_error"] = device_error
     if world == 1 and not args.no_profile:
         v_ms, s_ms, p_ms, n_prof = h.profile_read()
-        # kernel times: the profiled steps (the last replay of the captured graph, or all
-        # timed steps when not using graphs); algorithmic bytes from the same steps' r_b
-        n_acc = (hist[:G] if G else hist[args.warmup:args.warmup + args.steps]).cpu().numpy()
+        # algorithmic bytes of exactly the timed steps (their r_b rows of hist)
+        n_acc = hist[args.warmup:args.warmup + args.steps].cpu().numpy()
         alg = algorithmic_bytes(n_acc, args.V, args.k)
         per_launch = alg / n_acc.shape[0]
         avg_v = v_ms / n_prof
@@ -330,10 +343,16 @@ def run_ours(args):
         # events serialise consecutive launches, so they are reported beside it.
         interval_ms = ms_max / args.steps
         achieved = per_launch / (interval_ms * 1e-3) / 1e9
-        traffic = None
+        # ncu DRAM bytes of one verify launch, only if captured for THIS build (the
+        # digest of the library's sources and flags), else null
+        traffic, traffic_note = None, "no ncu capture on file"
         if os.path.exists(args.traffic_file):
             try:
-                traffic = json.load(open(args.traffic_file)).get("dram_bytes_per_launch")
+                tf = json.load(open(args.traffic_file))
+                if tf.get("build_digest") == build_digest():
+                    traffic, traffic_note = tf.get("dram_bytes_per_launch"), tf.get("source")
+                else:
+                    traffic_note = "ncu capture on file is for another build: not reported"
             except (OSError, ValueError):
                 traffic = None
         out["roofline"] = {"kernel": "verify_kernel<bf16> (laps_step)", "bound": "hbm",
@@ -341,6 +360,7 @@ def run_ours(args):
                            "frac": achieved / peak, "peak_source": peak_src,
                            "frac_of_8TBs": achieved / 8000.0,
                            "algorithmic_bytes_per_launch": per_launch, "traffic": traffic,
+                           "traffic_source": traffic_note,
                            "verify_interval_ms": interval_ms,
                            "verify_ms_avg_instrumented": avg_v, "select_ms_avg": s_ms / n_prof,
                            "presort_end_ms_avg": p_ms / n_prof,

@@ -68,7 +68,18 @@ typedef enum {
 
 /* Scheduler parameters.  Validation (EINVAL):
  * 1 <= K <= 16, s1_up_us > 0, M > 1, 2 <= gamma <= 32, delta >= 0, 1 <= k <= 16,
- * t_ssm_us >= 0, t_llm_us >= 0.  delta == 0 disables stabilisation. */
+ * t_ssm_us >= 0, t_llm_us >= 0, cost_model in {0, 1}, t_tok_us >= 0, switch_c0_us >= 0,
+ * switch_c1_us >= 0.  delta == 0 disables stabilisation.
+ *
+ * Cost model (DESIGN.md AMB-3, AMB-31): LAPSSD_COST_EQ6 -- one round is k*T_SSM + T_LLM of
+ * service and T~(L, A) = floor(L (k T_SSM + T_LLM) / (k A + 1)) (Eq. 6);
+ * LAPSSD_COST_FIG1 -- the Fig. 1 model: a round verifies k candidates at t_tok
+ * each (k*t_tok of service) and T~(L, A) = floor(L t_tok / A) (A = 0: unbounded).
+ *
+ * Switching cost (DESIGN.md AMB-24): a request that enters the
+ * batch without having been in the batch that ran last pays c0 + c1 (prompt + generated
+ * tokens) of SYSTEM time: the step lasts one round plus the switch-ins of its batch
+ * (the clock and C_i advance by it), while attained service E_i is not charged. */
 typedef struct {
     int32_t policy;        /* lapssd_policy                                            */
     int32_t K;             /* number of priority queues Q_1..Q_K                       */
@@ -83,13 +94,20 @@ typedef struct {
     int32_t pin_rule;      /* 0 = pin perceptible requests when selected, 1 = when
                               stable (AMB-15)                                          */
     uint64_t seed;         /* Philox key for every draw of the method (AMB-21)         */
+    int32_t cost_model;    /* LAPSSD_COST_EQ6 (default) or LAPSSD_COST_FIG1            */
+    int64_t t_tok_us;      /* FIG1: verification time per candidate token              */
+    int64_t switch_c0_us;  /* switch-in cost c0 + c1 (prompt + tokens), default 0      */
+    int64_t switch_c1_us;
 } lapssd_config;
+
+enum { LAPSSD_COST_EQ6 = 0, LAPSSD_COST_FIG1 = 1 };
 
 /* The resident requests of this rank.  [host] arrays of n entries, copied at
  * create.  Local request l has global id l*world + rank; arrival_us must be
  * non-decreasing in l (ids encode arrival order, AMB-19).  L_true >= 1 is the
  * output length that ends the request, L_pred >= 1 the predicted length L_i
- * used by Eq. 6 and LP-SJF.  Global ids must be < 2^24 - 1 (the all-ones key
+ * used by Eq. 6 and LP-SJF.  prompt >= 0 is the prompt length the switching
+ * cost charges (nullable: all 0).  Global ids must be < 2^24 - 1 (the all-ones key
  * stays unused). */
 typedef struct {
     const int64_t *arrival_us;
@@ -97,6 +115,7 @@ typedef struct {
     const int32_t *L_pred;
     int32_t n;
     int32_t rank, world;
+    const int32_t *prompt;
 } lapssd_requests;
 
 /* Where a step's probability rows live.  Two layouts:
@@ -197,26 +216,29 @@ lapssd_status lapssd_destroy(lapssd_handle *h);
 
 /* laps_update -- (a3) state update of the B verified slots:
  * tokens += min(r+1, L_true - tokens) (AMB-18); accepted drafts += r; rounds += 1;
- * E_i += k*T_SSM + T_LLM; ring of cumulative accepted drafts; if the request
- * is non-perceptible and the cumulative acceptance rates a_s/(k s) of the last gamma
- * rounds span < delta: A_i = their mean, perceptible, T~_i = Eq. 6 at
- * L_pred, placement (AMB-14); otherwise demotion to the queue of E_i;
- * completion when tokens >= L_true with C_i = now + round cost.
+ * E_i += one round's service (cost model above); ring of cumulative accepted
+ * drafts; if the request is non-perceptible and the cumulative acceptance rates
+ * a_s/(k s) of the last gamma rounds span < delta: A_i = their mean,
+ * perceptible, T~_i = the estimate at L_pred (Eq. 6 or Fig. 1 model), placement
+ * (AMB-14); otherwise demotion to the queue of E_i; completion when
+ * tokens >= L_true with C_i = now + the step's duration (round + switch-ins).
  * sel: [device] int32 [B] local indices (-1 = empty slot); n_accept: [device] [B].
  * Errors: EINVAL, ECUDA; updating a complete request sets the ESTATE flag. */
 lapssd_status laps_update(lapssd_handle *h, const int32_t *sel, const int32_t *n_accept,
                           int32_t B, lapssd_stream stream);
 
-/* laps_select -- (a4-a7): if the previous batch was non-empty, now += k*T_SSM +
- * T_LLM; admit every request with arrival <= now; build every resident
- * request's 64-bit priority key (smaller = sooner; AMB-15/16/19):
+/* laps_select -- (a4-a7): if the previous batch was non-empty, now += its step's
+ * duration (one round + the switch-ins it paid, AMB-17, AMB-24); admit every request
+ * with arrival <= now; build every resident request's 64-bit priority key
+ * (smaller = sooner; AMB-15/16/19):
  *   [63] ineligible | [62] not pinned | [61:58] queue level | [57] non-perceptible |
  *   [56] not running (non-perceptible) | [55:24] T~_rem us saturated (perceptible) or
  *   policy secondary | [23:0] global id
  * and write the B smallest eligible keys' local indices in ascending key order to
  * sel_out [device int32 B] (-1 padded), their count to count_out [device int32,
  * nullable].  Selected requests get x_i = now on first selection and are pinned per
- * pin_rule.  If nothing is eligible, now jumps to the next arrival.
+ * pin_rule; those not in the previous batch pay their switch-in cost (AMB-24).  If
+ * nothing is eligible, now jumps to the next arrival.
  * Errors: EINVAL (B > max_batch), ECUDA. */
 lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t *count_out,
                           lapssd_stream stream);
@@ -230,24 +252,36 @@ lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t
  * side stream (forked from / joined back into `stream` with events, highest launch
  * priority) presorts the other requests, merges the published keys while the rows
  * stream, and commits the next batch once every verify CTA has snapshotted the current
- * one; consecutive verify launches overlap (programmatic dependent launch).  Everything
- * is ordered on `stream` when the call's work completes, and the call may be captured
- * in a CUDA graph.  rows: pooled or batch layout (lapssd_rows).  tokens_out [device,
+ * one.  Everything is ordered on `stream` when the call's work completes, and the call
+ * may be captured in a CUDA graph.  By default the verify kernel starts after all prior
+ * work on `stream` (plain stream order).  After lapssd_set_step_overlap(h, 1) a pooled-
+ * rows laps_step's verify launch is a programmatic dependent of what precedes it on the
+ * stream (the previous laps_step's select): it may start -- and read rows, drafts and
+ * the slab table -- before that work completes.  The caller then guarantees that no
+ * work it enqueues between consecutive laps_step calls on the stream writes anything the
+ * step reads (e.g. a static slab pool); rows produced by a kernel on the same stream need
+ * the default.  rows: pooled or batch layout (lapssd_rows).  tokens_out [device,
  * B x (k+1)], n_accept_out [device, B] are nullable.  count_out as in laps_select.
  * Device-side waits carry watchdogs; an expiry sets LAPSSD_ESTATE flags (see
  * lapssd_check) and the step's results are invalid.  Errors: EINVAL, ECUDA. */
 lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel_inout,
                         int32_t *count_out, int32_t *tokens_out, int32_t *n_accept_out,
                         lapssd_stream stream);
+/* Opt in (enable = 1) or out (0, the default) of overlapping consecutive laps_step /
+ * laps_step_dist verify launches (programmatic dependent launch; contract above).
+ * Errors: EINVAL (NULL handle). */
+lapssd_status lapssd_set_step_overlap(lapssd_handle *h, int32_t enable);
 
 /* ---------------------------------------------------------------------------
  * Multi-GPU (a8): requests are sharded by global id mod world; every rank keeps the
  * same global clock.  laps_candidates does laps_select's clock/admission/keys and
- * writes this rank's C smallest eligible keys (ascending, UINT64_MAX padded) into
- * cand_out[device u64, C+1]; cand_out[C] = this rank's next arrival time (as u64,
- * UINT64_MAX if none).  After an all-gather of the world*(C+1) words,
- * laps_merge takes the global top-B keys, keeps the ids with id % world == rank as
- * this rank's batch (sel_out, key order) and advances the clock by the GLOBAL batch.
+ * writes this rank's candidate block of 2C+1 words into cand_out [device u64]:
+ * [0, C) its C smallest eligible keys (ascending, UINT64_MAX padded), [C, 2C) each
+ * key's switch-in cost in us if it is selected (0 for padding; AMB-24), [2C] this
+ * rank's next arrival time (as u64, UINT64_MAX if none).  After an all-gather of the
+ * world*(2C+1) words, laps_merge takes the global top-B keys, keeps the ids with
+ * id % world == rank as this rank's batch (sel_out, key order) and advances the clock by
+ * the GLOBAL batch (one round plus the selected keys' switch-in costs).
  * laps_step_dist = verify + update + candidates + ncclAllGather (on `nccl_comm`, a
  * ncclComm_t created by the caller) + merge, with the results of that sequence; with
  * pooled rows the candidates / all-gather / merge run on the side stream beside the
@@ -259,7 +293,7 @@ lapssd_status laps_merge(lapssd_handle *h, const uint64_t *all_cand, int32_t C, 
                          int32_t *sel_out, int32_t *count_out, lapssd_stream stream);
 lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_rows *rows,
                              int32_t B_global, int32_t C, int32_t *sel_inout, int32_t *count_out,
-                             uint64_t *cand_scratch /* [device] (world+1)*(C+1) words */,
+                             uint64_t *cand_scratch /* [device] (world+1)*(2C+1) words */,
                              lapssd_stream stream);
 /* C must be the same on every rank and world*C <= 16384: the caller passes
  * C = min(B_global, max over ranks of n_local).  sel_inout has B_global slots.
@@ -283,6 +317,9 @@ typedef struct {
     double *A;                                    /* n                 */
     uint64_t *key;                                /* n: last select's keys */
     int32_t *ring;                                /* n * gamma         */
+    int64_t *switch_us;                           /* n: switching time charged on its entries */
+    int64_t step_cost_us;     /* out: duration of the step selected last (round + switch-ins) */
+    int64_t switch_total_us;  /* out: system time spent switching so far (AMB-24)           */
 } lapssd_state_view;
 lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *host_out,
                                 lapssd_stream stream);
@@ -338,7 +375,7 @@ typedef struct lapssd_mc lapssd_mc;
 size_t lapssd_mc_workspace_bytes(const lapssd_config *cfg, int32_t n_traces, int64_t n_total, int64_t V);
 lapssd_status lapssd_mc_create(const lapssd_config *cfg, int32_t n_traces, const int64_t *trace_offsets,
                                const int64_t *arrival_us, const int32_t *L_true, const int32_t *L_pred,
-                               int64_t V, void *workspace, size_t workspace_bytes, lapssd_stream stream,
+                               const int32_t *prompt /* [host] nullable: all 0 */, int64_t V, void *workspace, size_t workspace_bytes, lapssd_stream stream,
                                lapssd_mc **out);
 lapssd_status lapssd_mc_destroy(lapssd_mc *h);
 lapssd_status laps_mc_select(lapssd_mc *h, const lapssd_rows *rows, lapssd_stream stream);

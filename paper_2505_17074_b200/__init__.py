@@ -21,6 +21,7 @@ _SO = os.environ.get("LAPSSD_LIBRARY") or os.path.join(_HERE, "liblapssd.so")  #
 
 F32, BF16 = 0, 1
 POL_LAPSSD, POL_FCFS, POL_LPSJF, POL_LAS = 0, 1, 2, 3
+COST_EQ6, COST_FIG1 = 0, 1
 STATUS = {0: "OK", -1: "EINVAL", -2: "ECUDA", -3: "ENCCL", -4: "ESTATE", -5: "ENOMEM"}
 
 
@@ -34,12 +35,14 @@ class _Config(C.Structure):
     _fields_ = [("policy", C.c_int32), ("K", C.c_int32), ("s1_up_us", C.c_int64),
                 ("M", C.c_double), ("gamma", C.c_int32), ("delta", C.c_double),
                 ("k", C.c_int32), ("t_ssm_us", C.c_int64), ("t_llm_us", C.c_int64),
-                ("placement", C.c_int32), ("pin_rule", C.c_int32), ("seed", C.c_uint64)]
+                ("placement", C.c_int32), ("pin_rule", C.c_int32), ("seed", C.c_uint64),
+                ("cost_model", C.c_int32), ("t_tok_us", C.c_int64), ("switch_c0_us", C.c_int64),
+                ("switch_c1_us", C.c_int64)]
 
 
 class _Requests(C.Structure):
     _fields_ = [("arrival_us", C.c_void_p), ("L_true", C.c_void_p), ("L_pred", C.c_void_p),
-                ("n", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32)]
+                ("n", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("prompt", C.c_void_p)]
 
 
 class _Rows(C.Structure):
@@ -52,7 +55,10 @@ class _StateView(C.Structure):
     _fields_ = [("now_us", C.c_int64), ("cursor", C.c_int32), ("prev_count", C.c_int32)] + [
         (n, C.c_void_p) for n in ("acc_tok", "acc_draft", "rounds", "E_us", "T_total_us", "C_us",
                                   "x_us", "admitted", "done", "perceptible", "pinned", "level",
-                                  "running", "A", "key", "ring")]
+                                  "running", "A", "key", "ring", "switch_us")] + [
+        ("step_cost_us", C.c_int64), ("switch_total_us", C.c_int64)]
+
+_VIEW_ARRAYS = [f for f, t in _StateView._fields_[3:] if t is C.c_void_p]
 
 
 def _load():
@@ -72,6 +78,7 @@ def _load():
         "laps_update": ([vp, vp, vp, i32, vp], i32),
         "laps_select": ([vp, i32, vp, vp, vp], i32),
         "laps_step": ([vp, vp, i32, vp, vp, vp, vp, vp], i32),
+        "lapssd_set_step_overlap": ([vp, i32], i32),
         "laps_candidates": ([vp, i32, vp, vp], i32),
         "laps_merge": ([vp, vp, i32, i32, vp, vp, vp], i32),
         "laps_step_dist": ([vp, vp, vp, i32, i32, vp, vp, vp, vp], i32),
@@ -83,7 +90,7 @@ def _load():
         "lapssd_profile": ([vp, i32], i32),
         "lapssd_profile_read": ([vp, vp, vp, vp, vp], i32),
         "lapssd_mc_workspace_bytes": ([vp, i32, i64, i64], sz),
-        "lapssd_mc_create": ([vp, i32, vp, vp, vp, vp, i64, vp, sz, vp, vp], i32),
+        "lapssd_mc_create": ([vp, i32, vp, vp, vp, vp, vp, i64, vp, sz, vp, vp], i32),
         "lapssd_mc_destroy": ([vp], i32),
         "laps_mc_select": ([vp, vp, vp], i32),
         "laps_mc_step": ([vp, vp, vp, vp, vp, vp], i32),
@@ -209,11 +216,16 @@ class SchedConfig:
     placement: int = 0
     pin_rule: int = 0
     seed: int = 0
+    cost_model: int = COST_EQ6
+    t_tok_us: int = 0
+    switch_c0_us: int = 0
+    switch_c1_us: int = 0
 
     def c(self):
         return _Config(self.policy, self.K, self.s1_up_us, self.M, self.gamma, self.delta,
                        self.k, self.t_ssm_us, self.t_llm_us, self.placement, self.pin_rule,
-                       self.seed & (2**64 - 1))
+                       self.seed & (2**64 - 1), self.cost_model, self.t_tok_us,
+                       self.switch_c0_us, self.switch_c1_us)
 
 
 class Rows:
@@ -231,15 +243,18 @@ class Handle:
     """A LAPS-SD resident-request state on one GPU (lapssd_create)."""
 
     def __init__(self, cfg: SchedConfig, arrival_us, L_true, L_pred, *, max_batch: int, V: int,
-                 rank: int = 0, world: int = 1, device="cuda", stream=None):
+                 rank: int = 0, world: int = 1, prompt=None, overlap: bool = False, device="cuda",
+                 stream=None):
         self.cfg = cfg
         self._cc = cfg.c()
         a = np.ascontiguousarray(arrival_us, np.int64)
         lt = np.ascontiguousarray(L_true, np.int32)
         lp = np.ascontiguousarray(L_pred, np.int32)
+        pr = np.ascontiguousarray(prompt, np.int32) if prompt is not None else None
         self.n = len(a)
         self.max_batch, self.V, self.rank, self.world = max_batch, V, rank, world
-        req = _Requests(a.ctypes.data, lt.ctypes.data, lp.ctypes.data, self.n, rank, world)
+        req = _Requests(a.ctypes.data, lt.ctypes.data, lp.ctypes.data, self.n, rank, world,
+                        pr.ctypes.data if pr is not None else None)
         nbytes = int(_lib.lapssd_workspace_bytes(C.byref(self._cc), self.n, max_batch, V, world))
         if nbytes == 0:
             raise LapssdError("lapssd_workspace_bytes", -1, "invalid sizes")
@@ -251,6 +266,13 @@ class Handle:
         self.h = h
         self.sel = torch.full((max_batch,), -1, dtype=torch.int32, device=device)
         self.count = torch.zeros(1, dtype=torch.int32, device=device)
+        if overlap:
+            self.set_step_overlap(True)
+
+    def set_step_overlap(self, enable: bool):
+        """lapssd_set_step_overlap: consecutive verify launches overlap (the caller does not
+        write the step's rows between laps_step calls on the stream)."""
+        _check("lapssd_set_step_overlap", _lib.lapssd_set_step_overlap(self.h, 1 if enable else 0))
 
     def close(self):
         if getattr(self, "h", None):
@@ -300,9 +322,10 @@ class Handle:
     # -- snapshot -----------------------------------------------------------------
     def state(self, stream=None) -> dict:
         arrs = _state_arrays(self.n, self.cfg.gamma)
-        v = _StateView(0, 0, 0, *[arrs[f].ctypes.data for f, _ in _StateView._fields_[3:]])
+        v = _StateView(0, 0, 0, *[arrs[f].ctypes.data for f in _VIEW_ARRAYS], 0, 0)
         _check("lapssd_read_state", _lib.lapssd_read_state(self.h, C.byref(v), _stream(stream)))
-        arrs.update(now_us=v.now_us, cursor=v.cursor, prev_count=v.prev_count)
+        arrs.update(now_us=v.now_us, cursor=v.cursor, prev_count=v.prev_count,
+                    step_cost_us=v.step_cost_us, switch_total_us=v.switch_total_us)
         return arrs
 
     def profile(self, max_steps: int):
@@ -331,7 +354,8 @@ def _state_arrays(n, gamma):
                 done=np.zeros(n, np.uint8), perceptible=np.zeros(n, np.uint8),
                 pinned=np.zeros(n, np.uint8), level=np.zeros(n, np.uint8),
                 running=np.zeros(n, np.uint8), A=np.zeros(n, np.float64),
-                key=np.zeros(n, np.uint64), ring=np.zeros((n, gamma), np.int32))
+                key=np.zeros(n, np.uint64), ring=np.zeros((n, gamma), np.int32),
+                switch_us=np.zeros(n, np.int64))
 
 
 # --------------------------------------------------------------------------- Monte-Carlo replicas
@@ -339,14 +363,15 @@ class MCHandle:
     """T independent traces, batch 1 each (lapssd_mc_create): configs[4]'s engine.
     Requests are concatenated trace by trace; offsets[t]..offsets[t+1] belong to trace t."""
 
-    def __init__(self, cfg: SchedConfig, offsets, arrival_us, L_true, L_pred, *, V: int, device="cuda",
-                 stream=None):
+    def __init__(self, cfg: SchedConfig, offsets, arrival_us, L_true, L_pred, *, V: int, prompt=None,
+                 device="cuda", stream=None):
         self.cfg = cfg
         self._cc = cfg.c()
         off = np.ascontiguousarray(offsets, np.int64)
         a = np.ascontiguousarray(arrival_us, np.int64)
         lt = np.ascontiguousarray(L_true, np.int32)
         lp = np.ascontiguousarray(L_pred, np.int32)
+        pr = np.ascontiguousarray(prompt, np.int32) if prompt is not None else None
         self.T, self.n, self.V = len(off) - 1, int(off[-1]), V
         self.offsets = off
         nbytes = int(_lib.lapssd_mc_workspace_bytes(C.byref(self._cc), self.T, self.n, V))
@@ -355,7 +380,8 @@ class MCHandle:
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
         h = C.c_void_p()
         rc = _lib.lapssd_mc_create(C.byref(self._cc), self.T, off.ctypes.data, a.ctypes.data, lt.ctypes.data,
-                                   lp.ctypes.data, V, _dptr(self.workspace), nbytes, _stream(stream), C.byref(h))
+                                   lp.ctypes.data, pr.ctypes.data if pr is not None else None, V,
+                                   _dptr(self.workspace), nbytes, _stream(stream), C.byref(h))
         _check("lapssd_mc_create", rc)
         self.h = h
         self.active = torch.zeros(1, dtype=torch.int32, device=device)
@@ -379,12 +405,13 @@ class MCHandle:
     def state(self, stream=None):
         """(per-request state dict over all traces, now_us[T], cursor[T], sel[T])."""
         arrs = _state_arrays(self.n, self.cfg.gamma)
-        v = _StateView(0, 0, 0, *[arrs[f].ctypes.data for f, _ in _StateView._fields_[3:]])
+        v = _StateView(0, 0, 0, *[arrs[f].ctypes.data for f in _VIEW_ARRAYS], 0, 0)
         now = np.zeros(self.T, np.int64)
         cur = np.zeros(self.T, np.int32)
         sel = np.zeros(self.T, np.int32)
         _check("lapssd_mc_read", _lib.lapssd_mc_read(self.h, C.byref(v), now.ctypes.data, cur.ctypes.data,
                                                       sel.ctypes.data, _stream(stream)))
+        arrs["switch_total_us"] = v.switch_total_us
         return arrs, now, cur, sel
 
     def check(self):

@@ -28,7 +28,7 @@ def stale() -> bool:
     if not os.path.exists(SO):
         return True
     t = os.path.getmtime(SO)
-    deps = sources() + [os.path.join(CSRC, "lapssd_internal.cuh"),
+    deps = sources() + [os.path.join(CSRC, "lapssd_internal.cuh"), os.path.join(CSRC, "select_core.cuh"),
                         os.path.join(HERE, "..", "include", "lapssd.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 

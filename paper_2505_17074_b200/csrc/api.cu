@@ -100,6 +100,10 @@ struct lapssd_handle {
     // true after an incremental laps_step on chain_stream; any other call resets it
     bool side_chained = false;
     bool chain_captured = false;   // the chained step was recorded into a graph
+    // lapssd_set_step_overlap: consecutive verify launches may overlap (programmatic
+    // dependent launch).  Off by default: the verify kernel then follows all prior work on
+    // the caller's stream (a rows-producing kernel of the caller, say).
+    bool overlap = false;
     cudaStream_t chain_stream = nullptr;
     lapssd_rows last_rows{};  // rows of the previous laps_step (epoch changes with them)
     uint32_t rows_epoch = 1;
@@ -127,6 +131,8 @@ static void carve_state(Carver &cv, State &st, int64_t n, int32_t gamma) {
     st.arrival = cv.take<int64_t>(nn);
     st.L_true = cv.take<int32_t>(nn);
     st.L_pred = cv.take<int32_t>(nn);
+    st.prompt = cv.take<int32_t>(nn);
+    st.switch_us = cv.take<int64_t>(nn);
     st.acc_tok = cv.take<int32_t>(nn);
     st.acc_draft = cv.take<int32_t>(nn);
     st.rounds = cv.take<int32_t>(nn);
@@ -136,7 +142,8 @@ static void carve_state(Carver &cv, State &st, int64_t n, int32_t gamma) {
     st.A = cv.take<double>(nn);
     st.flags = cv.take<uint32_t>(nn);
     st.key = cv.take<uint64_t>(nn);
-    st.C = cv.take<int64_t>(nn);   // C, x, next_tag are initialised to all-ones (contiguous)
+    st.last_sel = cv.take<int32_t>(nn);   // last_sel, C, x, next_tag: all-ones at create (contiguous)
+    st.C = cv.take<int64_t>(nn);
     st.x = cv.take<int64_t>(nn);
     st.next_tag = cv.take<uint64_t>(nn);
     st.next_sr = cv.take<int2>(nn);
@@ -170,6 +177,10 @@ static lapssd_status check_config(const lapssd_config *c) {
     if (c->t_ssm_us < 0 || c->t_llm_us < 0) return fail(LAPSSD_EINVAL, "negative round cost");
     if (c->placement < 0 || c->placement > 1 || c->pin_rule < 0 || c->pin_rule > 1)
         return fail(LAPSSD_EINVAL, "placement / pin_rule");
+    if (c->cost_model != LAPSSD_COST_EQ6 && c->cost_model != LAPSSD_COST_FIG1)
+        return fail(LAPSSD_EINVAL, "cost_model %d", c->cost_model);
+    if (c->t_tok_us < 0) return fail(LAPSSD_EINVAL, "negative t_tok_us");
+    if (c->switch_c0_us < 0 || c->switch_c1_us < 0) return fail(LAPSSD_EINVAL, "negative switching cost");
     return LAPSSD_OK;
 }
 
@@ -179,8 +190,14 @@ static void fill_sched(Sched &sc, const lapssd_config *cfg, int32_t n, int32_t r
     sc.placement = cfg->placement; sc.pin_rule = cfg->pin_rule;
     sc.n = n; sc.rank = rank; sc.world = world;
     sc.delta = cfg->delta;
-    sc.t_ssm_us = cfg->t_ssm_us; sc.t_llm_us = cfg->t_llm_us;
-    sc.c_round_us = (int64_t)cfg->k * cfg->t_ssm_us + cfg->t_llm_us;   // S:194, Eq. 6 denominators
+    sc.t_ssm_us = cfg->t_ssm_us; sc.t_llm_us = cfg->t_llm_us; sc.t_tok_us = cfg->t_tok_us;
+    sc.cost_model = cfg->cost_model;
+    // one round's service: k T_SSM + T_LLM (Eq. 6's numerator), or in the
+    // Fig. 1 model the k candidates verified at t_tok each (AMB-3)
+    sc.c_round_us = cfg->cost_model == LAPSSD_COST_FIG1 ? (int64_t)cfg->k * cfg->t_tok_us
+                                                        : (int64_t)cfg->k * cfg->t_ssm_us + cfg->t_llm_us;
+    sc.sw_c0_us = cfg->switch_c0_us; sc.sw_c1_us = cfg->switch_c1_us;   // AMB-24
+    sc.sw_on = cfg->switch_c0_us > 0 || cfg->switch_c1_us > 0;
     sc.seed = cfg->seed;
     // S_j^up = M^(j-1) S_1^up; zero-based S_up[j] = floor(s1_up * M^j), M^j by
     // iterative fp64 multiplication (AMB-11).
@@ -196,12 +213,16 @@ static void fill_sched(Sched &sc, const lapssd_config *cfg, int32_t n, int32_t r
     }
 }
 
-// Zero-fill a state workspace, all-ones for C / x / next_tag, copy the request arrays.
+// Zero-fill a state workspace, all-ones for last_sel / C / x / next_tag, copy the request
+// arrays (prompt nullable: zeros).
 static cudaError_t init_state(void *workspace, size_t bytes, const State &st, int64_t n, const int64_t *arrival,
-                              const int32_t *L_true, const int32_t *L_pred, cudaStream_t s) {
+                              const int32_t *L_true, const int32_t *L_pred, const int32_t *prompt, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(workspace, 0, bytes, s);
     if (e == cudaSuccess)
-        e = cudaMemsetAsync(st.C, 0xFF, (size_t)((char *)(st.next_tag + (n > 0 ? n : 1)) - (char *)st.C), s);
+        e = cudaMemsetAsync(st.last_sel, 0xFF,
+                            (size_t)((char *)(st.next_tag + (n > 0 ? n : 1)) - (char *)st.last_sel), s);
+    if (e == cudaSuccess && n > 0 && prompt)
+        e = cudaMemcpyAsync((void *)st.prompt, prompt, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && n > 0) {
         e = cudaMemcpyAsync((void *)st.arrival, arrival, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s);
         if (e == cudaSuccess)
@@ -352,6 +373,7 @@ lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req
     if (V < 1 || V > (int64_t)kMaxSegs * kSegElems) return fail(LAPSSD_EINVAL, "V out of range");
     for (int32_t i = 0; i < req->n; ++i) {
         if (req->L_true[i] < 1 || req->L_pred[i] < 1) return fail(LAPSSD_EINVAL, "L < 1 at %d", i);
+        if (req->prompt && req->prompt[i] < 0) return fail(LAPSSD_EINVAL, "prompt < 0 at %d", i);
         if (i > 0 && req->arrival_us[i] < req->arrival_us[i - 1])
             return fail(LAPSSD_EINVAL, "arrivals not sorted at %d", i);
     }
@@ -372,7 +394,8 @@ lapssd_status lapssd_create(const lapssd_config *cfg, const lapssd_requests *req
     fill_sched(h->sc, cfg, req->n, req->rank, req->world);
     cudaStream_t s = (cudaStream_t)stream;
     h->last_stream = s;
-    cudaError_t e = init_state(workspace, need, h->st, req->n, req->arrival_us, req->L_true, req->L_pred, s);
+    cudaError_t e = init_state(workspace, need, h->st, req->n, req->arrival_us, req->L_true, req->L_pred,
+                               req->prompt, s);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
@@ -525,7 +548,7 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
         a.vstep = &h->st.g->vstep;
     }
     static const bool no_pdl = getenv("LAPSSD_NO_PDL") != nullptr;  // A/B switch for measurements
-    st = cuda_status(launch_verify_grid(a, B, 1, incremental && !no_pdl, s), "laps_step verify");
+    st = cuda_status(launch_verify_grid(a, B, 1, incremental && h->overlap && !no_pdl, s), "laps_step verify");
     if (st != LAPSSD_OK) return st;
     if (ev) prof_record(ev[1], s);
     if (fork) {
@@ -558,6 +581,13 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
     if (st == LAPSSD_OK) h->desc_valid = true;
     if (ev) prof_record(ev[2], s);
     return st;
+}
+
+lapssd_status lapssd_set_step_overlap(lapssd_handle *h, int32_t enable) {
+    g_last_error.clear();
+    if (!h) return fail(LAPSSD_EINVAL, "handle is NULL");
+    h->overlap = enable != 0;
+    return LAPSSD_OK;
 }
 
 lapssd_status lapssd_profile(lapssd_handle *h, int32_t max_steps) {
@@ -701,8 +731,8 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
     a.count_dev = &h->st.g->count;   // this rank's slots are [0, count) of the B_global
     cudaStream_t s = (cudaStream_t)stream;
     h->last_stream = s;
-    uint64_t *local = cand_scratch;
-    uint64_t *all = cand_scratch + (C + 1);
+    uint64_t *local = cand_scratch;                 // this rank's block: 2C+1 words
+    uint64_t *all = cand_scratch + (2 * (size_t)C + 1);
     int bp = 1;
     while (bp < B_global) bp <<= 1;
     static const bool serial = getenv("LAPSSD_DIST_SERIAL") != nullptr;  // A/B switch
@@ -712,7 +742,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
         if (st != LAPSSD_OK) return st;
         st = cuda_status(launch_candidates(h->st, h->sc, C, local, s), "step_dist candidates");
         if (st != LAPSSD_OK) return st;
-        st = nccl_status(allgather(local, all, (size_t)(C + 1), kNcclUint64, nccl_comm, s), "ncclAllGather");
+        st = nccl_status(allgather(local, all, 2 * (size_t)C + 1, kNcclUint64, nccl_comm, s), "ncclAllGather");
         if (st != LAPSSD_OK) return st;
         st = cuda_status(launch_merge(h->st, h->sc, a.rows, h->desc, all, C, B_global, sel_inout, count_out, s),
                          "step_dist merge");
@@ -739,7 +769,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
     a.work1 = h->work + 2;
     a.vstep = &h->st.g->vstep;
     static const bool no_pdl = getenv("LAPSSD_NO_PDL") != nullptr;
-    st = cuda_status(launch_verify_grid(a, B_global, 1, !no_pdl, s), "laps_step_dist verify");
+    st = cuda_status(launch_verify_grid(a, B_global, 1, h->overlap && !no_pdl, s), "laps_step_dist verify");
     if (st != LAPSSD_OK) return st;
     ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
     if (ce != cudaSuccess) return cuda_status(ce, "laps_step_dist fork wait");
@@ -748,7 +778,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
                                         nullptr, h->side, local, C),
                      "laps_step_dist candidates");
     if (st != LAPSSD_OK) return st;
-    st = nccl_status(allgather(local, all, (size_t)(C + 1), kNcclUint64, nccl_comm, h->side), "ncclAllGather");
+    st = nccl_status(allgather(local, all, 2 * (size_t)C + 1, kNcclUint64, nccl_comm, h->side), "ncclAllGather");
     if (st != LAPSSD_OK) return st;
     st = cuda_status(launch_merge(h->st, h->sc, a.rows, h->desc, all, C, B_global, sel_inout, count_out, h->side),
                      "laps_step_dist merge");
@@ -783,6 +813,7 @@ lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *v, lapssd_s
     CP(v->A, h->st.A, n)
     CP(v->key, h->st.key, n)
     CP(v->ring, h->st.ring, n * h->sc.gamma)
+    CP(v->switch_us, h->st.switch_us, n)
 #undef CP
     if (e == cudaSuccess && n) e = cudaMemcpyAsync(flags.data(), h->st.flags, 4 * n, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -790,6 +821,8 @@ lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *v, lapssd_s
     v->now_us = g.now_us;
     v->cursor = g.cursor;
     v->prev_count = g.prev_count;
+    v->step_cost_us = h->sc.c_round_us + g.step_sw;
+    v->switch_total_us = g.switch_total;
     for (size_t i = 0; i < n; ++i) {
         const uint32_t f = flags[i];
         if (v->admitted) v->admitted[i] = (int32_t)i < g.cursor;
@@ -866,7 +899,8 @@ size_t lapssd_mc_workspace_bytes(const lapssd_config *cfg, int32_t n_traces, int
 }
 
 lapssd_status lapssd_mc_create(const lapssd_config *cfg, int32_t n_traces, const int64_t *trace_offsets,
-                               const int64_t *arrival_us, const int32_t *L_true, const int32_t *L_pred, int64_t V,
+                               const int64_t *arrival_us, const int32_t *L_true, const int32_t *L_pred,
+                               const int32_t *prompt, int64_t V,
                                void *workspace, size_t workspace_bytes, lapssd_stream stream, lapssd_mc **out) {
     g_last_error.clear();
     if (!out) return fail(LAPSSD_EINVAL, "out is NULL");
@@ -885,6 +919,7 @@ lapssd_status lapssd_mc_create(const lapssd_config *cfg, int32_t n_traces, const
         if (b - a > (1 << 24) - 2) return fail(LAPSSD_EINVAL, "trace %d: local ids must be < 2^24 - 1", t);
         for (int64_t i = a; i < b; ++i) {
             if (L_true[i] < 1 || L_pred[i] < 1) return fail(LAPSSD_EINVAL, "L < 1 at %lld", (long long)i);
+            if (prompt && prompt[i] < 0) return fail(LAPSSD_EINVAL, "prompt < 0 at %lld", (long long)i);
             if (i > a && arrival_us[i] < arrival_us[i - 1])
                 return fail(LAPSSD_EINVAL, "trace %d: arrivals not sorted at %lld", t, (long long)i);
         }
@@ -904,7 +939,7 @@ lapssd_status lapssd_mc_create(const lapssd_config *cfg, int32_t n_traces, const
     fill_sched(h->sc, cfg, 0, 0, 1);   // every trace is its own id space (world 1, local ids)
     cudaStream_t s = (cudaStream_t)stream;
     h->last_stream = s;
-    cudaError_t e = init_state(workspace, need, h->st, n, arrival_us, L_true, L_pred, s);
+    cudaError_t e = init_state(workspace, need, h->st, n, arrival_us, L_true, L_pred, prompt, s);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync((void *)h->mc.off, trace_offsets, sizeof(int64_t) * (n_traces + 1),
                             cudaMemcpyHostToDevice, s);
@@ -1012,10 +1047,16 @@ lapssd_status lapssd_mc_read(lapssd_mc *h, lapssd_state_view *v, int64_t *now_us
     CP(v->A, h->st.A, n)
     CP(v->key, h->st.key, n)
     CP(v->ring, h->st.ring, n * h->sc.gamma)
+    CP(v->switch_us, h->st.switch_us, n)
 #undef CP
     if (e == cudaSuccess && n) e = cudaMemcpyAsync(flags.data(), h->st.flags, 4 * n, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_status(e, "lapssd_mc_read");
+    if (v) {   // per-trace scalars have no place in the view: the totals over the traces
+        v->step_cost_us = 0;
+        v->switch_total_us = 0;
+        for (size_t t = 0; t < T; ++t) v->switch_total_us += g[t].switch_total;
+    }
     for (size_t t = 0; t < T; ++t) {
         if (now_us) now_us[t] = g[t].now_us;
         if (cursor) cursor[t] = g[t].cursor;

@@ -56,7 +56,9 @@ struct Globals {
     uint32_t err;          // sticky contract-violation flags
     uint32_t vstep;        // incremental steps committed: parity of the verify buffers
     uint32_t err_where;    // first watchdog expiry: (vstep & 0xFFFF) << 16 | slot
-    uint32_t pad;
+    uint32_t sel_seq;      // selections committed (a request in the batch that ran last has last_sel == sel_seq)
+    int64_t step_sw;       // switch-in time of the batch selected last: its step lasts c_round + step_sw (AMB-24)
+    int64_t switch_total;  // system time spent switching (AMB-24)
 };
 
 // Scheduler constants, passed by value to every kernel.
@@ -64,8 +66,11 @@ struct Sched {
     int32_t policy, K, gamma, k;
     int32_t placement, pin_rule;
     int32_t n, rank, world;
+    int32_t cost_model;    // LAPSSD_COST_EQ6 / LAPSSD_COST_FIG1
+    int32_t sw_on;         // switching cost configured (c0 or c1 > 0)
     double delta;
-    int64_t t_ssm_us, t_llm_us, c_round_us;
+    int64_t t_ssm_us, t_llm_us, t_tok_us, c_round_us;
+    int64_t sw_c0_us, sw_c1_us;
     int64_t S_up[16];
     uint64_t seed;
 };
@@ -73,7 +78,9 @@ struct Sched {
 // Resident-request SoA in the caller's workspace.
 struct State {
     const int64_t *arrival;
-    const int32_t *L_true, *L_pred;
+    const int32_t *L_true, *L_pred, *prompt;
+    int32_t *last_sel;     // sel_seq of the request's last selection (-1: never)
+    int64_t *switch_us;    // switching time charged on the request's entries
     int32_t *acc_tok, *acc_draft, *rounds, *ring;
     int64_t *E, *T_total, *C, *x;
     double *A;
@@ -110,6 +117,36 @@ __device__ __forceinline__ uint64_t eq6_us(int64_t L, double A, const Sched &s) 
     if (!(T > 0.0)) return 0;
     if (T >= 1.8e19) return ~0ull;
     return (uint64_t)T;
+}
+
+// The Fig. 1 model: L tokens at acceptance rate A need L / A candidates, each
+// verified in t_tok: floor((L * t_tok) / A) in fp64, in this order (AMB-31).  A = 0 has
+// no finite estimate (saturates) unless nothing is left to generate.
+__device__ __forceinline__ uint64_t fig1_us(int64_t L, double A, const Sched &s) {
+    const double num = __dmul_rn((double)L, (double)s.t_tok_us);
+    const double T = __ddiv_rn(num, A);
+    if (!(T > 0.0)) return (L > 0 && s.t_tok_us > 0) ? ~0ull : 0;
+    if (T >= 1.8e19) return ~0ull;
+    return (uint64_t)T;
+}
+
+// T~ of L tokens at rate A under the configured cost model (P:139, P:198 / P:25-26).
+__device__ __forceinline__ uint64_t estimate_us(int64_t L, double A, const Sched &s) {
+    return s.cost_model == LAPSSD_COST_FIG1 ? fig1_us(L, A, s) : eq6_us(L, A, s);
+}
+
+// Switching cost of local request i entering the batch now (AMB-24): 0 if
+// it was in the batch that ran last (its last selection is the latest, seq), else
+// c0 + c1 (prompt + generated tokens).
+__device__ __forceinline__ int64_t switch_in_cost(const State &st, const Sched &s, int32_t i, uint32_t seq) {
+    if (!s.sw_on || st.last_sel[i] == (int32_t)seq) return 0;
+    return s.sw_c0_us + s.sw_c1_us * ((int64_t)st.prompt[i] + st.acc_tok[i]);
+}
+// Charge a committed selection (selection number seq + 1) to request i.
+__device__ __forceinline__ void charge_switch(const State &st, const Sched &s, int32_t i, uint32_t seq, int64_t c) {
+    if (!s.sw_on) return;
+    st.last_sel[i] = (int32_t)(seq + 1);
+    if (c) st.switch_us[i] += c;
 }
 
 // Queue index of attained service / estimate x (AMB-11).
@@ -153,7 +190,7 @@ uint64_t build_key(const Sched &s, int32_t i, int32_t cursor, uint32_t fl,
         if (perc) {
             int64_t L_rem = (int64_t)L_pred - acc_tok;                  // AMB-12
             if (L_rem < 0) L_rem = 0;
-            sec = sat32(eq6_us(L_rem, A, s));
+            sec = sat32(estimate_us(L_rem, A, s));
         } else {
             notrun = !running;
         }
@@ -171,8 +208,9 @@ struct UpdOut {    // the fields a priority key needs, after the update
     int32_t tok;
     double A;
 };
+// t_end: the end of the step that ran (now + c_round + its switch-ins): C_i if it completes.
 __device__ __forceinline__ UpdOut update_one(const State &st, const Sched &s, int32_t i, int32_t r,
-                                             int64_t now) {
+                                             int64_t t_end) {
     uint32_t fl = st.flags[i];
     double A_new = st.A[i];
     if (fl & F_DONE) { atomicOr(&st.g->err, E_UPDATE_DONE); return UpdOut{fl, st.acc_tok[i], A_new}; }
@@ -206,7 +244,7 @@ __device__ __forceinline__ UpdOut update_one(const State &st, const Sched &s, in
             fl |= F_PERC;
             st.A[i] = mean;
             A_new = mean;
-            const uint64_t T = eq6_us(st.L_pred[i], mean, s);
+            const uint64_t T = estimate_us(st.L_pred[i], mean, s);
             const int64_t Ts = T > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)T;
             st.T_total[i] = Ts;
             if (s.placement == 0) level = level_of(Ts, s);
@@ -221,7 +259,7 @@ __device__ __forceinline__ UpdOut update_one(const State &st, const Sched &s, in
     }
     if (tok >= Lt) {
         fl |= F_DONE;
-        st.C[i] = now + s.c_round_us;
+        st.C[i] = t_end;
     }
     fl = (fl & ~(F_LEVEL_MASK | F_RUNNING)) | ((uint32_t)level << F_LEVEL_SHIFT);
     if (!(fl & F_DONE) && !demoted) fl |= F_RUNNING;
@@ -258,7 +296,7 @@ __device__ __forceinline__ UpdIn load_update_inputs(const State &st, const Sched
 
 // update_one with preloaded inputs, executed by a full warp (uniform control flow,
 // lane 0 stores).  Same arithmetic, same order as update_one.
-__device__ __forceinline__ UpdOut update_warp(const State &st, const Sched &s, int32_t i, int32_t r, int64_t now,
+__device__ __forceinline__ UpdOut update_warp(const State &st, const Sched &s, int32_t i, int32_t r, int64_t t_end,
                                               const UpdIn &u, int lane) {
     uint32_t fl = u.fl;
     UpdOut out{fl, u.tok, u.A};
@@ -294,7 +332,7 @@ __device__ __forceinline__ UpdOut update_warp(const State &st, const Sched &s, i
         if (stable) {
             fl |= F_PERC;
             out.A = mean;
-            const uint64_t T = eq6_us(u.Lp, mean, s);
+            const uint64_t T = estimate_us(u.Lp, mean, s);
             const int64_t Ts = T > (uint64_t)INT64_MAX ? INT64_MAX : (int64_t)T;
             if (lane == 0) { st.A[i] = mean; st.T_total[i] = Ts; }
             if (s.placement == 0) level = level_of(Ts, s);
@@ -309,7 +347,7 @@ __device__ __forceinline__ UpdOut update_warp(const State &st, const Sched &s, i
     }
     if (tok >= u.Lt) {
         fl |= F_DONE;
-        if (lane == 0) st.C[i] = now + s.c_round_us;
+        if (lane == 0) st.C[i] = t_end;
     }
     fl = (fl & ~(F_LEVEL_MASK | F_RUNNING)) | ((uint32_t)level << F_LEVEL_SHIFT);
     if (!(fl & F_DONE) && !demoted) fl |= F_RUNNING;

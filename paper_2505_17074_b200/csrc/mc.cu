@@ -35,12 +35,12 @@ __global__ void __launch_bounds__(256) mc_step_kernel(const State st, const Sche
         // verify kernel writes and may overlap its tail
         const SlotDesc d = desc[t];
         const int r = d.r;
-        if (d.i >= 0 && r >= 0) update_one(st, sc, d.i, r, g->now_us);
+        if (d.i >= 0 && r >= 0) update_one(st, sc, d.i, r, g->now_us + sc.c_round_us + g->step_sw);
     }
     __syncwarp();
     // (a7 + a4) clock and admission over the trace's sorted arrivals
     int64_t now = g->now_us;
-    if (g->prev_count > 0) now += sc.c_round_us;
+    if (g->prev_count > 0) now += sc.c_round_us + g->step_sw;   // AMB-17, AMB-24
     int cursor = g->cursor;
     const int cursor0 = cursor;
     for (;;) {
@@ -100,9 +100,11 @@ __global__ void __launch_bounds__(256) mc_step_kernel(const State st, const Sche
         d.i = -1; d.slab = 0; d.req = 0; d.round = 0; d.r = -1;
         d.trace = (uint32_t)t; d.pad[0] = d.pad[1] = 0;
         int64_t nnow = now;
+        const uint32_t seq = g->sel_seq;
+        int64_t sw = 0;
         if (have) {
             const int64_t i = off + jsel;
-            commit_one(st, sc, (int32_t)i, now);
+            sw = commit_one(st, sc, (int32_t)i, now, seq);   // switch-in unless it just ran (AMB-24)
             // (a1) for the next verify: x_j ~ q_j of the slab of this round, Philox c3 = t
             const int32_t rnd = st.rounds[i];
             const int64_t slab = rw.slab_tab[i * rw.R + slab_round_index(rnd, rw.R)];
@@ -123,7 +125,14 @@ __global__ void __launch_bounds__(256) mc_step_kernel(const State st, const Sche
         g->cursor = cursor;
         g->prev_count = have ? 1 : 0;
         g->count = have ? 1 : 0;
+        g->step_sw = sw;
+        g->switch_total += sw;
+        g->sel_seq = seq + 1;
     }
+    // this grid is a programmatic dependent of the last verify sub-launch: it completes
+    // only after that grid has (so whatever follows it on the stream -- the next step's
+    // verify, a read of n_accept -- is ordered after the verify's writes)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 cudaError_t launch_mc_step(const State &st, const Sched &sc, const McDev &mc, const RowsDev &rw,

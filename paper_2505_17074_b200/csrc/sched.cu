@@ -82,7 +82,7 @@ __global__ void update_kernel(const State st, const Sched sc, const int32_t *sel
     const int32_t i = sel[b];
     if (i < 0) return;
     if (i >= sc.n) { atomicOr(&st.g->err, E_BAD_SLOT); return; }
-    update_one(st, sc, i, n_accept[b], st.g->now_us);
+    update_one(st, sc, i, n_accept[b], st.g->now_us + sc.c_round_us + st.g->step_sw);
 }
 
 cudaError_t launch_update(const State &st, const Sched &sc, const int32_t *sel,
@@ -100,9 +100,11 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const State st, con
     extern __shared__ uint64_t s_buf[];
     __shared__ int64_t s_now;
     __shared__ int s_cursor, s_count;
+    __shared__ unsigned long long s_sw;
     advance_and_admit(st, sc, &s_now, &s_cursor);
     const int64_t now = s_now;
     const int cursor = s_cursor;
+    const uint32_t seq = st.g->sel_seq;
     const int npow2 = next_pow2(sc.n > 0 ? sc.n : 1);
     build_keys(st, sc, cursor, s_buf, npow2);
     const int bp = next_pow2(B);
@@ -116,16 +118,18 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const State st, con
     if (valid) atomicAdd(&s_count, valid);
     __syncthreads();
     const int cnt = s_count;
+    int64_t sw = 0;
     for (int b = threadIdx.x; b < B; b += blockDim.x) {
         int32_t i = -1;
         if (b < cnt) {
             const uint32_t id = (uint32_t)(keys[b] & 0xFFFFFFull);
             i = (int32_t)(id / (uint32_t)sc.world);
-            commit_one(st, sc, i, now);
+            sw += commit_one(st, sc, i, now, seq);
         }
         sel_out[b] = i;
         if (rw.valid) desc[b] = make_desc(rw, st, sc, b, i);    // a1 for the next verify
     }
+    commit_switch(st, sc, sw, cnt, &s_sw);
     if (threadIdx.x == 0) {
         int64_t nnow = now;
         if (cnt == 0 && cursor < sc.n) {                             // idle: jump
@@ -219,10 +223,12 @@ __global__ void __launch_bounds__(kSelThreads) select_final_kernel(const State s
                                                                     int32_t *count_out, const PreSelect *pre) {
     extern __shared__ uint64_t s_buf[];
     __shared__ int s_count;
+    __shared__ unsigned long long s_sw;
     STRACE(0);
     const int bp = next_pow2(B);
     const int64_t now = pre->now_us;
     const int cursor = pre->cursor;
+    const uint32_t seq = st.g->sel_seq;
     // keys of the verified batch, after their update
     for (int b = threadIdx.x; b < bp; b += blockDim.x) {
         uint64_t key = ~0ull;
@@ -264,16 +270,18 @@ __global__ void __launch_bounds__(kSelThreads) select_final_kernel(const State s
     __syncthreads();
     const int cnt = s_count;
     STRACE(4);
+    int64_t sw = 0;
     for (int b = threadIdx.x; b < B; b += blockDim.x) {
         int32_t i = -1;
         if (b < cnt) {
             const uint32_t id = (uint32_t)(merged[b] & 0xFFFFFFull);
             i = (int32_t)(id / (uint32_t)sc.world);
-            commit_one(st, sc, i, now);
+            sw += commit_one(st, sc, i, now, seq);
         }
         sel[b] = i;
         if (rw.valid) desc[b] = make_desc(rw, st, sc, b, i);
     }
+    commit_switch(st, sc, sw, cnt, &s_sw);
     if (threadIdx.x == 0) {
         int64_t nnow = now;
         if (cnt == 0 && cursor < sc.n) {
@@ -321,6 +329,7 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     __shared__ uint32_t s_member[kSortCap / 32];
     __shared__ uint32_t s_pend[4096 / 32];    // expected slots not yet merged (B <= 4096 here)
     __shared__ int s_snap_ok;
+    __shared__ unsigned long long s_sw_side;
     const int n = sc.n;
     const int T = blockDim.x;
     // ---------------- phase 1: presort of every request outside the batch
@@ -507,9 +516,14 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
         // multi-GPU (a8): this rank's C best keys (+ its next arrival) for the all-gather;
         // merge_kernel commits the global batch.  The verified batch's running flags are
         // cleared here, as candidates_kernel does after building its keys.
+        const uint32_t seq = st.g->sel_seq;
         for (int c = threadIdx.x; c < C; c += T) {
             const uint64_t key = c < bp ? L[c] : ~0ull;
-            cand_out[c] = (key >> 63) ? ~0ull : key;
+            const bool ok = (key >> 63) == 0;
+            cand_out[c] = ok ? key : ~0ull;
+            cand_out[C + c] = ok ? (uint64_t)switch_in_cost(st, sc, (int32_t)((uint32_t)(key & 0xFFFFFFull) /
+                                                                              (uint32_t)sc.world), seq)
+                                 : 0ull;
         }
         for (int b = threadIdx.x; b < B; b += T) {
             const int i = sel[b];
@@ -517,7 +531,7 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
             st.flags[i] = (rec_smem ? brec[b].flags : fin[b].flags) & ~F_RUNNING;
         }
         if (threadIdx.x == 0) {
-            cand_out[C] = s_cursor < n ? (uint64_t)st.arrival[s_cursor] : ~0ull;
+            cand_out[2 * C] = s_cursor < n ? (uint64_t)st.arrival[s_cursor] : ~0ull;
             st.g->now_us = s_now;
             st.g->cursor = s_cursor;
         }
@@ -533,6 +547,8 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     const int cnt = s_count;
     ITRACE(100001);
     const int64_t now = s_now;
+    const uint32_t seq = st.g->sel_seq;
+    int64_t sw = 0;
     uint8_t *mark = reinterpret_cast<uint8_t *>(L2);     // [bp] 1 reselected, 2 +pin
     int32_t *old_i = reinterpret_cast<int32_t *>(nk);    // [bp] the verified batch
     for (int b = threadIdx.x; b < bp; b += T) { mark[b] = 0; old_i[b] = b < B ? sel[b] : -1; }
@@ -557,10 +573,14 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
                 if (pin && !(rec.flags & F_PINNED)) st.flags[i] = rec.flags | F_PINNED;
                 if (rec.x_unset) st.x[i] = now;      // x_i
             }
+            const int64_t c = sl >= 0 ? 0 : switch_in_cost(st, sc, i, seq);   // the verified batch ran last
+            charge_switch(st, sc, i, seq, c);
+            sw += c;
         }
         sel[b] = d.i;
         desc[b] = d;
     }
+    commit_switch(st, sc, sw, cnt, &s_sw_side);
     __syncthreads();
     ITRACE(100002);
     for (int b = threadIdx.x; b < B; b += T) {   // the verified batch: running flags cleared
@@ -668,7 +688,8 @@ cudaError_t launch_select(const State &st, const Sched &sc, const RowsDev &rw, S
 
 // ---------------------------------------------------------------- a8 candidates
 // cand_out[0..C) = this rank's C smallest eligible keys (UINT64_MAX padded),
-// cand_out[C] = its next arrival time (UINT64_MAX if none).
+// cand_out[C..2C) = their switch-in costs if selected (AMB-24), cand_out[2C] = its next
+// arrival time (UINT64_MAX if none).
 __global__ void __launch_bounds__(kSelThreads) candidates_kernel(const State st, const Sched sc, int32_t C,
                                                                   uint64_t *cand_out) {
     extern __shared__ uint64_t s_buf[];
@@ -679,12 +700,17 @@ __global__ void __launch_bounds__(kSelThreads) candidates_kernel(const State st,
     build_keys(st, sc, s_cursor, s_buf, npow2);
     const bool two = npow2 >= 64 && npow2 <= kMergeCap;
     const uint64_t *keys = block_sort(s_buf, two ? s_buf + npow2 : nullptr, npow2);
+    const uint32_t seq = st.g->sel_seq;
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
         const uint64_t key = c < npow2 ? keys[c] : ~0ull;
-        cand_out[c] = (key >> 63) ? ~0ull : key;
+        const bool ok = (key >> 63) == 0;
+        cand_out[c] = ok ? key : ~0ull;
+        cand_out[C + c] = ok ? (uint64_t)switch_in_cost(st, sc, (int32_t)((uint32_t)(key & 0xFFFFFFull) /
+                                                                          (uint32_t)sc.world), seq)
+                             : 0ull;
     }
     if (threadIdx.x == 0) {
-        cand_out[C] = s_cursor < sc.n ? (uint64_t)st.arrival[s_cursor] : ~0ull;
+        cand_out[2 * C] = s_cursor < sc.n ? (uint64_t)st.arrival[s_cursor] : ~0ull;
         st.g->now_us = s_now;
         st.g->cursor = s_cursor;
     }
@@ -698,8 +724,9 @@ cudaError_t launch_candidates(const State &st, const Sched &sc, int32_t C, uint6
 }
 
 // ---------------------------------------------------------------- a8 merge
-// all_cand: world blocks of (C keys, 1 next-arrival word).  Global top-B by key;
-// this rank keeps the ids with id % world == rank, in key order.
+// all_cand: world blocks of (C keys, C switch-in costs, 1 next-arrival word).  Global
+// top-B by key; this rank keeps the ids with id % world == rank, in key order; the step
+// lasts one round plus the switch-ins of the whole global batch (AMB-24).
 __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, const Sched sc, const RowsDev rw,
                                                              SlotDesc *desc, const uint64_t *all_cand,
                                                              int32_t C, int32_t B, int32_t *sel_out,
@@ -707,7 +734,7 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
     extern __shared__ uint64_t s_buf[];
     __shared__ int s_tmp[64];
     __shared__ int s_gcount;
-    __shared__ unsigned long long s_next;
+    __shared__ unsigned long long s_next, s_sw;
     // Every rank's candidate list is sorted (candidates_kernel), so the global order is a
     // G-way merge: each key's global rank = its index in its own list + the number of
     // smaller keys in every other list (keys are unique: the global id is in the low
@@ -717,15 +744,17 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
     const int G = sc.world;
     const int total = G * C;
     const int lim = B < total ? B : total;
+    const int64_t blk = 2 * (int64_t)C + 1;   // words per rank
     uint64_t *lists = s_buf;            // [G*C]
     uint64_t *top = s_buf + total;      // [lim] the global top-B, ascending
+    uint64_t *top_sw = top + lim;       // [lim] their switch-in costs
     if (threadIdx.x == 0) { s_gcount = 0; s_next = ~0ull; }
     __syncthreads();
     for (int x = threadIdx.x; x < total; x += blockDim.x)
-        lists[x] = all_cand[(int64_t)(x / C) * (C + 1) + (x % C)];
-    for (int x = threadIdx.x; x < lim; x += blockDim.x) top[x] = ~0ull;
+        lists[x] = all_cand[(int64_t)(x / C) * blk + (x % C)];
+    for (int x = threadIdx.x; x < lim; x += blockDim.x) { top[x] = ~0ull; top_sw[x] = 0; }
     for (int g = threadIdx.x; g < G; g += blockDim.x)
-        atomicMin(&s_next, (unsigned long long)all_cand[(int64_t)g * (C + 1) + C]);
+        atomicMin(&s_next, (unsigned long long)all_cand[(int64_t)g * blk + 2 * C]);
     __syncthreads();
     constexpr int kRun = 8;
     const int runs_per_list = (C + kRun - 1) / kRun;
@@ -758,7 +787,10 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
         for (int e = 0; e < kRun; ++e) {
             if (c0 + e >= C) break;
             const uint64_t x = Lg[c0 + e];
-            if (x != ~0ull && rk[e] < lim) top[rk[e]] = x;
+            if (x != ~0ull && rk[e] < lim) {
+                top[rk[e]] = x;
+                top_sw[rk[e]] = all_cand[(int64_t)g * blk + C + c0 + e];
+            }
         }
     }
     __syncthreads();
@@ -767,10 +799,12 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
     const int per = (lim + (int)blockDim.x - 1) / (int)blockDim.x;
     const int lo = (int)threadIdx.x * per;
     int own = 0, valid = 0;
+    int64_t sw = 0;   // switch-ins of the GLOBAL batch
     for (int x = lo; x < lo + per && x < lim; ++x) {
         const uint64_t key = keys[x];
         if (key >> 63) continue;
         ++valid;
+        sw += (int64_t)top_sw[x];
         const uint32_t id = (uint32_t)(key & 0xFFFFFFull);
         own += (int)(id % (uint32_t)sc.world) == sc.rank;
     }
@@ -778,6 +812,7 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
     int n_own = 0;
     int pos = block_excl_scan(own, s_tmp, &n_own);
     const int64_t now = st.g->now_us;
+    const uint32_t seq = st.g->sel_seq;
     for (int x = lo; x < lo + per && x < lim; ++x) {
         const uint64_t key = keys[x];
         if (key >> 63) continue;
@@ -785,7 +820,7 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
         if ((int)(id % (uint32_t)sc.world) == sc.rank) {
             const int32_t i = (int32_t)(id / (uint32_t)sc.world);
             sel_out[pos] = i;
-            commit_one(st, sc, i, now);
+            (void)commit_one(st, sc, i, now, seq);   // its cost is the candidate's, summed above
             if (rw.valid) desc[pos] = make_desc(rw, st, sc, pos, i);
             ++pos;
         }
@@ -795,6 +830,7 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(const State st, cons
         if (rw.valid) desc[b] = make_desc(rw, st, sc, b, -1);
     }
     __syncthreads();
+    commit_switch(st, sc, sw, s_gcount, &s_sw);
     if (threadIdx.x == 0) {
         const int g = s_gcount;
         int64_t nnow = now;
@@ -815,7 +851,7 @@ cudaError_t launch_merge(const State &st, const Sched &sc, const RowsDev &rw, Sl
                          const uint64_t *all_cand, int32_t C, int32_t B, int32_t *sel_out,
                          int32_t *count_out, cudaStream_t s) {
     const int total = sc.world * C;
-    const size_t smem = ((size_t)total + (size_t)(B < total ? B : total)) * sizeof(uint64_t);
+    const size_t smem = ((size_t)total + 2 * (size_t)(B < total ? B : total)) * sizeof(uint64_t);
     merge_kernel<<<1, kSelThreads, smem > 0 ? smem : 8, s>>>(st, sc, rw, desc, all_cand, C,
                                                                                 B, sel_out, count_out);
     count_launch();

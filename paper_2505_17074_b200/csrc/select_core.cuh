@@ -367,12 +367,13 @@ __device__ inline int block_excl_scan(int v, int *s_tmp, int *total) {
     return before + x - v;
 }
 
-// a7 (first half) + a4: advance the clock by the round that ran, admit arrivals.
+// a7 (first half) + a4: advance the clock by the step that ran (its round plus the
+// switch-ins it paid), admit arrivals.
 // Arrivals are sorted, so the admitted set is the prefix [0, cursor).
 __device__ inline void advance_and_admit(const State &st, const Sched &sc, int64_t *s_now, int *s_cursor) {
     if (threadIdx.x == 0) {
         int64_t now = st.g->now_us;
-        if (st.g->prev_count > 0) now += sc.c_round_us;         // AMB-17
+        if (st.g->prev_count > 0) now += sc.c_round_us + st.g->step_sw;   // AMB-17, AMB-24
         *s_now = now;
         *s_cursor = st.g->cursor;
     }
@@ -408,14 +409,38 @@ __device__ inline void build_keys(const State &st, const Sched &sc, int cursor, 
     __syncthreads();
 }
 
-// Commit one selected request: first-service time and pinning (AMB-15, AMB-25).
-__device__ __forceinline__ void commit_one(const State &st, const Sched &sc, int32_t i, int64_t now) {
+// Commit one selected request: first-service time and pinning (AMB-15, AMB-25), and its
+// switch-in cost for selection number seq + 1 (AMB-24), which it returns.
+__device__ __forceinline__ int64_t commit_one(const State &st, const Sched &sc, int32_t i, int64_t now,
+                                              uint32_t seq) {
     if (st.x[i] < 0) st.x[i] = now;                                // x_i
     const uint32_t fl = st.flags[i];
     bool pin = false;
     if (sc.policy == LAPSSD_POL_FCFS || sc.policy == LAPSSD_POL_LPSJF) pin = true;
     else if (sc.policy == LAPSSD_POL_LAPSSD && sc.pin_rule == 0 && (fl & F_PERC)) pin = true;
     if (pin && !(fl & F_PINNED)) st.flags[i] = fl | F_PINNED;
+    const int64_t c = switch_in_cost(st, sc, i, seq);
+    charge_switch(st, sc, i, seq, c);
+    return c;
+}
+
+// Block-wide sum of the committed switch-in costs and the commit's globals: the step of
+// the batch just selected lasts c_round + sw (nothing when the batch is empty), the
+// selection counter advances.  Every thread passes its partial sum; thread 0 writes.
+__device__ inline void commit_switch(const State &st, const Sched &sc, int64_t part, int global_count,
+                                     unsigned long long *s_sum) {
+    if (sc.sw_on) {
+        if (threadIdx.x == 0) *s_sum = 0;
+        __syncthreads();
+        if (part) atomicAdd(s_sum, (unsigned long long)part);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int64_t sw = sc.sw_on && global_count > 0 ? (int64_t)*s_sum : 0;
+        st.g->step_sw = sw;
+        st.g->switch_total += sw;
+        st.g->sel_seq = st.g->sel_seq + 1;
+    }
 }
 
 

@@ -789,7 +789,8 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
         if (a.fuse_update) {
             // the state updates first, two slots at a time: each stage of both slots' loads
             // (state + slab table, drafts, gathers) is one round trip
-            const int64_t now = __ldcg(&a.st.g->now_us);
+            // the end of the step being verified: C_i of a request it completes
+            const int64_t now = __ldcg(&a.st.g->now_us) + a.sc.c_round_us + __ldcg(&a.st.g->step_sw);
             for (int j = 0; j < nf; j += 2) {
                 const SlotDesc d0 = s_fin[grp][j];
                 const bool has1 = j + 1 < nf;

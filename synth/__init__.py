@@ -259,6 +259,13 @@ def make_trace(n: int, seed: int, *, arrival="poisson", rate_per_s=35.0,
     return Trace(arr, L, Lp, a_s, amp, dec, per)
 
 
+def prompt_lengths(n: int, seed: int, median=150.0, sigma=0.7, lo=4, hi=2048) -> np.ndarray:
+    """Prompt lengths for the switching-cost workloads (f2, DESIGN.md AMB-24): lognormal
+    around `median` tokens, clipped to [lo, hi], int32."""
+    rng = np.random.default_rng(seed ^ 0x9E37)
+    return np.clip(np.round(np.exp(rng.normal(math.log(median), sigma, n))), lo, hi).astype(np.int32)
+
+
 def slab_table(trace: Trace, n_buckets: int, variants: int, R: int, seed: int) -> np.ndarray:
     """tab[i, t] = slab seen by request i in round t (t < R; later rounds reuse the
     stable half).  Bucket = randomised rounding of alpha_i(t)*n_buckets

@@ -23,8 +23,8 @@ def L():
     return lib
 
 
-@pytest.mark.parametrize("policy", [0, 2])
-def test_two_handles_candidates_merge_equal_single_rank(L, policy):
+@pytest.mark.parametrize("policy,switch", [(0, False), (2, False), (0, True), (3, True)])
+def test_two_handles_candidates_merge_equal_single_rank(L, policy, switch):
     seed, B, G, R = 41, 6, 2, 16
     tr = synth.make_trace(40, seed, arrival="poisson", rate_per_s=50.0, len_mu=np.log(30), len_sigma=0.6,
                           len_min=4, len_max=200, beta_ab=(3, 2), drift=True)
@@ -32,10 +32,14 @@ def test_two_handles_candidates_merge_equal_single_rank(L, policy):
     tab = synth.slab_table(tr, 8, 3, R=R, seed=seed)
     kw = dict(policy=policy, K=4, s1_up_us=30 * MS, gamma=3, delta=0.05, k=4, t_ssm_us=1 * MS,
               t_llm_us=10 * MS, seed=12)
+    pr = None
+    if switch:   # AMB-24: the step lasts one round plus the GLOBAL batch's switch-ins
+        kw.update(switch_c0_us=2 * MS, switch_c1_us=12)
+        pr = synth.prompt_lengths(tr.n, seed)
     # reference: one rank, oracle
     P = pool.numpy()
     P["slab_tab"], P["R"] = tab, R
-    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, prompt=pr)
     sel_o, _ = sim.select(B)
     ref_steps = [sel_o.copy()]
     while not sim.state()["done"].all():
@@ -47,9 +51,9 @@ def test_two_handles_candidates_merge_equal_single_rank(L, policy):
     for g in range(G):
         sh = tr.shard(g, G)
         hs.append(L.Handle(L.SchedConfig(**kw), sh.arrival_us, sh.L_true, sh.L_pred, max_batch=B, V=2048,
-                           rank=g, world=G))
+                           rank=g, world=G, prompt=pr[g::G] if pr is not None else None))
     Cn = B
-    cand = [torch.zeros(Cn + 1, dtype=torch.int64, device="cuda") for _ in range(G)]
+    cand = [torch.zeros(2 * Cn + 1, dtype=torch.int64, device="cuda") for _ in range(G)]
     sels = [torch.full((B,), -1, dtype=torch.int32, device="cuda") for _ in range(G)]
 
     def exchange():
@@ -86,15 +90,19 @@ def test_two_handles_candidates_merge_equal_single_rank(L, policy):
         st = hs[g].state()
         assert (st["C_us"] == ref["C_us"][g::G]).all()
         assert (st["acc_draft"] == ref["acc_draft"][g::G]).all()
+        assert (st["switch_us"] == ref["switch_us"][g::G]).all()
+        assert st["switch_total_us"] == ref["switch_total_us"]
         assert hs[g].check() == 0
+    assert (ref["switch_total_us"] > 0) == switch
 
 
-def test_laps_step_dist_one_rank_lockstep(L, monkeypatch):
+@pytest.mark.parametrize("switch", [False, True])
+def test_laps_step_dist_one_rank_lockstep(L, monkeypatch, switch):
     """laps_step_dist end to end (verify + candidates + ncclAllGather + merge) with a
     one-rank NCCL communicator, step by step against the oracle: batch, r, state."""
     import torch.distributed as dist
     monkeypatch.setenv("MASTER_ADDR", "127.0.0.1")
-    monkeypatch.setenv("MASTER_PORT", "29561")
+    monkeypatch.setenv("MASTER_PORT", "29565" if switch else "29561")
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
         comm = L.nccl_comm()
@@ -106,17 +114,22 @@ def test_laps_step_dist_one_rank_lockstep(L, monkeypatch):
         tab = synth.slab_table(tr, 8, 3, R=R, seed=seed)
         kw = dict(K=4, s1_up_us=56 * MS, gamma=5, delta=0.05, k=4, t_ssm_us=1 * MS, t_llm_us=10 * MS,
                   seed=17)
+        pr = None
+        if switch:
+            kw.update(switch_c0_us=2 * MS, switch_c1_us=12)
+            pr = synth.prompt_lengths(tr.n, seed)
         P = pool.numpy()
         P["slab_tab"], P["R"] = tab, R
-        sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
+        sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, prompt=pr)
         h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=4096,
-                     rank=0, world=1)
+                     rank=0, world=1, prompt=pr, overlap=switch)
         rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
         Cn = B
-        cand = torch.zeros(2 * (Cn + 1), dtype=torch.int64, device="cuda")
-        h.laps_candidates(Cn, cand[: Cn + 1])
-        cand[Cn + 1:].copy_(cand[: Cn + 1])
-        h.laps_merge(cand[Cn + 1:], Cn, B)
+        W = 2 * Cn + 1
+        cand = torch.zeros(2 * W, dtype=torch.int64, device="cuda")
+        h.laps_candidates(Cn, cand[:W])
+        cand[W:].copy_(cand[:W])
+        h.laps_merge(cand[W:], Cn, B)
         sel_o, _ = sim.select(B)
         for step in range(400):
             sel_g = h.sel[:B].cpu().numpy()
@@ -128,9 +141,10 @@ def test_laps_step_dist_one_rank_lockstep(L, monkeypatch):
             if step % 4 == 0:
                 g, o = h.state(), sim.state()
                 for f in ("acc_tok", "acc_draft", "rounds", "E_us", "C_us", "level", "perceptible",
-                          "pinned", "key"):
+                          "pinned", "key", "switch_us"):
                     assert (np.asarray(g[f]) == np.asarray(o[f])).all(), f"step {step}: {f}"
                 assert g["now_us"] == o["now_us"], f"step {step}: clock"
+                assert g["switch_total_us"] == o["switch_total_us"], f"step {step}: switching"
         assert sim.state()["done"].all()
         assert h.check() == 0
         L.nccl_comm_destroy(comm)
@@ -161,13 +175,14 @@ def test_laps_step_dist_one_rank_graph_replay(L, monkeypatch):
         P["slab_tab"], P["R"] = tab, R
         sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
         h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=32000,
-                     rank=0, world=1)
+                     rank=0, world=1, overlap=True)
         rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
         Cn = B
-        cand = torch.zeros(2 * (Cn + 1), dtype=torch.int64, device="cuda")
-        h.laps_candidates(Cn, cand[: Cn + 1])
-        cand[Cn + 1:].copy_(cand[: Cn + 1])
-        h.laps_merge(cand[Cn + 1:], Cn, B)
+        W = 2 * Cn + 1
+        cand = torch.zeros(2 * W, dtype=torch.int64, device="cuda")
+        h.laps_candidates(Cn, cand[:W])
+        cand[W:].copy_(cand[:W])
+        h.laps_merge(cand[W:], Cn, B)
         sel_o, _ = sim.select(B)
         h.laps_step_dist(comm, rows, B, Cn, cand)   # eager warm-up step
         sim.step(P, sel_o)

@@ -22,25 +22,27 @@ def L():
 
 
 FIELDS = ["acc_tok", "acc_draft", "rounds", "E_us", "T_total_us", "C_us", "x_us", "admitted", "done",
-          "perceptible", "pinned", "level", "running", "key"]
+          "perceptible", "pinned", "level", "running", "key", "switch_us"]
 
 
-def run_mc_lockstep(L, kw, T, n, V, k, dtype, seed, R=8, max_steps=4000):
+def run_mc_lockstep(L, kw, T, n, V, k, dtype, seed, R=8, max_steps=4000, prompt=False):
     rate = synth.mc_rate_for_load(0.8, k, kw["t_ssm_us"], kw["t_llm_us"], len_mu=np.log(30))
     w = synth.make_mc_workload(T, n, seed, rate_per_s=rate, len_mu=np.log(30), len_sigma=0.6, len_min=4,
                                len_max=200, n_buckets=8, variants=3, R=R)
     pool = synth.make_pool("f2", V=V, k=k, dtype=dtype, n_buckets=8, variants=3, seed=seed, device="cuda")
     P = pool.numpy()
     cfg = dict(kw, k=k)
+    pr = synth.prompt_lengths(T * n, seed) if prompt else None
     sims, sels, Ps = [], [], []
     for t in range(T):
         a, lt, lp, tab = w.trace(t)
-        sim = oracle.Sim(oracle.SchedConfig(**cfg), a, lt, lp, trace=t)
+        sim = oracle.Sim(oracle.SchedConfig(**cfg), a, lt, lp, trace=t,
+                         prompt=pr[t * n:(t + 1) * n] if prompt else None)
         sel, _ = sim.select(1)
         Pt = dict(P)
         Pt["slab_tab"], Pt["R"] = np.ascontiguousarray(tab), R
         sims.append(sim), sels.append(sel), Ps.append(Pt)
-    mc = L.MCHandle(L.SchedConfig(**cfg), w.offsets, w.arrival_us, w.L_true, w.L_pred, V=V)
+    mc = L.MCHandle(L.SchedConfig(**cfg), w.offsets, w.arrival_us, w.L_true, w.L_pred, V=V, prompt=pr)
     rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(w.slab_tab, device="cuda"))
     mc.select(rows)
     tokens = torch.full((T, k + 1), -9, dtype=torch.int32, device="cuda")
@@ -74,6 +76,7 @@ def run_mc_lockstep(L, kw, T, n, V, k, dtype, seed, R=8, max_steps=4000):
         assert (st["A"][a:b].view(np.uint64) == o["A"].view(np.uint64)).all(), f"trace {t}: A differs"
         assert (st["ring"][a:b] == o["ring"]).all(), f"trace {t}: ring differs"
         assert now[t] == o["now_us"] and cur[t] == o["cursor"], f"trace {t}: clock differs"
+    assert st["switch_total_us"] == sum(s.state()["switch_total_us"] for s in sims)
     assert mc.check() == 0
     return steps
 
@@ -122,3 +125,40 @@ def test_mc_sub_launch_split(L):
             if ran:
                 assert na[t] == na_o[0]
     assert mc.check() == 0
+
+
+@pytest.mark.parametrize("policy", [0, 3])
+def test_mc_switching_cost(L, policy):
+    """f2 (AMB-24) on the Monte-Carlo engine: batch 1 per trace, a request
+    that did not run in the trace's previous step pays c0 + c1 (prompt + tokens)."""
+    kw = dict(BASE, policy=policy, switch_c0_us=3 * MS, switch_c1_us=20)
+    run_mc_lockstep(L, kw, T=8, n=20, V=2048, k=4, dtype="bf16", seed=70 + policy, prompt=True)
+
+
+def test_mc_multi_step_no_sync(L):
+    """Several laps_mc_step calls back to back without host synchronisation (T fits one
+    verify sub-launch, so consecutive steps share its scratch set): mc_step_kernel waits
+    for the verify grid it overlaps before it completes, so the results equal
+    those of a synchronised run."""
+    kw = dict(BASE, policy=0)
+    T, n, V, k, R = 64, 16, 4096, 4, 8
+    rate = synth.mc_rate_for_load(0.8, k, kw["t_ssm_us"], kw["t_llm_us"], len_mu=np.log(30))
+    w = synth.make_mc_workload(T, n, 81, rate_per_s=rate, len_mu=np.log(30), len_sigma=0.6, len_min=4,
+                               len_max=200, n_buckets=8, variants=3, R=R)
+    pool = synth.make_pool("f2", V=V, k=k, dtype="bf16", n_buckets=8, variants=3, seed=81, device="cuda")
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(w.slab_tab, device="cuda"))
+    outs = []
+    for sync in (True, False):
+        mc = L.MCHandle(L.SchedConfig(**dict(kw, k=k)), w.offsets, w.arrival_us, w.L_true, w.L_pred, V=V)
+        mc.select(rows)
+        nacc = torch.empty(40, T, dtype=torch.int32, device="cuda")
+        for s in range(40):
+            mc.step(rows, n_accept=nacc[s])
+            if sync:
+                torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        st, now, _, _ = mc.state()
+        outs.append((nacc.cpu().numpy(), st["acc_tok"], now))
+        assert mc.check() == 0
+    assert (outs[0][0] == outs[1][0]).all()
+    assert (outs[0][1] == outs[1][1]).all() and (outs[0][2] == outs[1][2]).all()

@@ -12,7 +12,7 @@ import synth
 pytestmark = pytest.mark.gpu
 
 FIELDS = ["acc_tok", "acc_draft", "rounds", "E_us", "T_total_us", "C_us", "x_us", "admitted",
-          "done", "perceptible", "pinned", "level", "running", "key", "ring"]
+          "done", "perceptible", "pinned", "level", "running", "key", "ring", "switch_us"]
 
 
 @pytest.fixture(scope="module")
@@ -38,15 +38,16 @@ def compare_state(g, o, step):
         a, b = np.asarray(g[f]), np.asarray(o[f])
         assert a.shape == b.shape and (a == b).all(), f"step {step}: field {f} differs"
     assert (g["A"].view(np.uint64) == o["A"].view(np.uint64)).all(), f"step {step}: A differs"
-    for f in ("now_us", "cursor", "prev_count"):
+    for f in ("now_us", "cursor", "prev_count", "step_cost_us", "switch_total_us"):
         assert g[f] == o[f], f"step {step}: {f} {g[f]} != {o[f]}"
 
 
-def run_lockstep(L, cfg_kw, tr, pool, tab, B, max_steps=5000, check_every=1):
+def run_lockstep(L, cfg_kw, tr, pool, tab, B, max_steps=5000, check_every=1, prompt=None, overlap=False):
     gcfg = L.SchedConfig(**cfg_kw)
     ocfg = oracle.SchedConfig(**cfg_kw)
-    h = L.Handle(gcfg, tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=pool.V)
-    sim = oracle.Sim(ocfg, tr.arrival_us, tr.L_true, tr.L_pred)
+    h = L.Handle(gcfg, tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=pool.V, prompt=prompt,
+                 overlap=overlap)
+    sim = oracle.Sim(ocfg, tr.arrival_us, tr.L_true, tr.L_pred, prompt=prompt)
     rows = L.Rows(pool.p, pool.q, pool.draft,
                   torch.as_tensor(tab, dtype=torch.int32, device="cuda"))
     P = pool.numpy()
@@ -146,7 +147,8 @@ def test_step_parity_graph_replay_config4(L):
                            seed=c["seed"] + 1, device="cuda")
     tab = synth.slab_table(tr, 16, 4, R=32, seed=c["seed"] + 1)
     kw = dict(BASE, k=k, seed=c["seed"] + 1)
-    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=128256)
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=128256,
+                 overlap=True)
     sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred)
     rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
     P = pool.numpy()
@@ -241,4 +243,97 @@ def test_step_parity_max_batch_4096(L):
         _, _, na_o, _ = sim.step(P, sel_o)
         assert (nacc.cpu().numpy() == na_o).all(), f"step {step}: r differs"
         compare_state(h.state(), sim.state(), step)
+    assert h.check() == 0
+
+
+# ---------------------------------------------------------------- f2: switching cost, Fig. 1 model
+SWITCH = dict(switch_c0_us=2_000, switch_c1_us=15)   # 2 ms + 15 us per (prompt + generated) token
+
+
+@pytest.mark.parametrize("policy", [0, 1, 3])
+def test_step_parity_switching_cost(L, policy):
+    """AMB-24: requests entering the batch pay c0 + c1 (prompt + tokens) of
+    system time; clock, C_i, per-request switching time and the total, bit-exact."""
+    tr, pool, tab = workload(120, 4096, 4, "bf16", seed=0x5F00 + policy, drift=True)
+    pr = synth.prompt_lengths(tr.n, 0x5F00 + policy)
+    run_lockstep(L, dict(BASE, policy=policy, k=4, seed=21, **SWITCH), tr, pool, tab, B=8, prompt=pr)
+
+
+def test_step_parity_switching_cost_overlap_batch1(L):
+    """Batch 1 (preemption at every round boundary makes switching frequent), the
+    overlapped launch configuration."""
+    tr, pool, tab = workload(40, 2048, 4, "bf16", seed=0x5F10, drift=True, rate=20.0)
+    pr = synth.prompt_lengths(tr.n, 0x5F10)
+    run_lockstep(L, dict(BASE, k=4, seed=22, **SWITCH), tr, pool, tab, B=1, prompt=pr, overlap=True)
+
+
+def test_step_parity_switching_cost_batch_layout(L):
+    """Batch layout (presort + final select path) with switching cost."""
+    tr, pool, tab = workload(60, 2048, 4, "bf16", seed=0x5F20, drift=True)
+    pr = synth.prompt_lengths(tr.n, 0x5F20)
+    kw = dict(BASE, k=4, seed=23, **SWITCH)
+    B, R = 6, tab.shape[1]
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=pool.V, prompt=pr)
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, prompt=pr)
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, R
+    sel_o, _ = sim.select(B)
+    h.laps_select(B)
+    for step in range(3000):
+        sel_g = h.sel[:B].cpu().numpy()
+        assert (sel_g == sel_o).all(), f"step {step}: batch differs"
+        if sim.state()["done"].all():
+            break
+        rounds = h.state()["rounds"]
+        slabs = [int(tab[i, _slab_round_index(int(rounds[i]), R)]) if i >= 0 else 0 for i in sel_g]
+        idx = torch.as_tensor(slabs, device="cuda")
+        rows = L.Rows(pool.p[idx].contiguous(), pool.q[idx].contiguous(), pool.draft[idx].contiguous(), None)
+        h.laps_step(rows, B)
+        sim.step(P, sel_o)
+        if step % 7 == 0:
+            compare_state(h.state(), sim.state(), step)
+    compare_state(h.state(), sim.state(), "end")
+    assert sim.state()["switch_total_us"] > 0
+    assert h.check() == 0
+
+
+def test_step_parity_fig1_cost_model(L):
+    """cost_model FIG1: a round is k candidates at t_tok, T~ = L t_tok / A."""
+    tr, pool, tab = workload(80, 2048, 4, "bf16", seed=0x5F30, drift=True)
+    kw = dict(BASE, k=4, seed=24, cost_model=1, t_tok_us=10_000, s1_up_us=160_000, t_ssm_us=0, t_llm_us=0)
+    run_lockstep(L, kw, tr, pool, tab, B=4)
+
+
+def test_update_select_standalone_switching_cost(L):
+    """laps_update + laps_select as separate calls (stateless spec_verify between them)."""
+    tr, pool, tab = workload(50, 2048, 4, "bf16", seed=0x5F40, drift=True)
+    pr = synth.prompt_lengths(tr.n, 0x5F40)
+    kw = dict(BASE, k=4, seed=25, **SWITCH)
+    B, R = 5, tab.shape[1]
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=pool.V, prompt=pr)
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, prompt=pr)
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, R
+    sel_o, _ = sim.select(B)
+    h.laps_select(B)
+    for step in range(3000):
+        sel_g = h.sel[:B].cpu().numpy()
+        assert (sel_g == sel_o).all(), f"step {step}: batch differs"
+        if sim.state()["done"].all():
+            break
+        st = h.state()
+        live = sel_g >= 0
+        rounds = np.where(live, st["rounds"][np.maximum(sel_g, 0)], 0).astype(np.int32)
+        slab = np.array([tab[i, _slab_round_index(int(rounds[b]), R)] if i >= 0 else 0
+                         for b, i in enumerate(sel_g)], np.int32)
+        req = np.where(live, sel_g, 0).astype(np.int32)
+        _, na, _ = L.spec_verify(pool.p, pool.q, pool.draft, torch.as_tensor(req, device="cuda"),
+                                 torch.as_tensor(rounds, device="cuda"), kw["seed"],
+                                 slab=torch.as_tensor(slab, device="cuda"))
+        h.laps_update(h.sel[:B], na)
+        h.laps_select(B)
+        sim.step(P, sel_o)
+        if step % 5 == 0:
+            compare_state(h.state(), sim.state(), step)
+    compare_state(h.state(), sim.state(), "end")
     assert h.check() == 0
