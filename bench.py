@@ -440,9 +440,29 @@ def run_e2e(args, L, local, pool, cfg, dev):
                     "accepted counts and tokens read back to pinned host memory every step"}
 
 
+def host_info():
+    """The host the CPU oracle ran on: logical CPUs and the lscpu model name."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": os.cpu_count(), "lscpu_model": model}
+
+
+def omp_threads():
+    return int(os.environ.get("OMP_NUM_THREADS") or os.cpu_count() or 1)
+
+
 def run_cpu_baseline(args, local, pool, tab, cfg_gpu, budget_s=None, batch=None):
-    """The oracle as it stands (single thread, plain C) on a bounded sample of the same
-    workload: the first steps of the same request set, same rows, same config."""
+    """The oracle as it stands on a bounded sample of the same workload (the first steps of
+    the same request set, same rows, same config): the -fopenmp build of the same source on
+    all host cores (a step's requests verified in parallel), and the plain single-thread
+    build beside it."""
     import oracle
 
     budget_s = budget_s or args.cpu_seconds
@@ -450,19 +470,26 @@ def run_cpu_baseline(args, local, pool, tab, cfg_gpu, budget_s=None, batch=None)
     P["slab_tab"], P["R"] = tab, tab.shape[1]
     ocfg = oracle.SchedConfig(**SCHED, seed=cfg_gpu.seed)
     B = batch or args.batch
-    sim = oracle.Sim(ocfg, local.arrival_us, local.L_true, local.L_pred)
-    sel, _ = sim.select(B)
-    t0 = time.perf_counter()
-    steps = verified = 0
-    while time.perf_counter() - t0 < budget_s:
-        verified += int((sel >= 0).sum())
-        sim.step(P, sel)
-        steps += 1
-    el = time.perf_counter() - t0
-    return {"value": verified * args.k / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {steps} steps of the bench workload ({B} verifications per step, "
-                      f"V={args.V}, k={args.k}, bf16), oracle/lapssd_oracle.c single thread, "
-                      f"{el:.1f} s"}
+    res = {}
+    for parallel, share in ((True, 0.6), (False, 0.4)):
+        sim = oracle.Sim(ocfg, local.arrival_us, local.L_true, local.L_pred, parallel=parallel)
+        sel, _ = sim.select(B)
+        t0 = time.perf_counter()
+        steps = verified = 0
+        while time.perf_counter() - t0 < budget_s * share:
+            verified += int((sel >= 0).sum())
+            sim.step(P, sel)
+            steps += 1
+        el = time.perf_counter() - t0
+        res[parallel] = (verified * args.k / el, steps, el)
+    (v_all, n_all, el_all), (v_one, n_one, el_one) = res[True], res[False]
+    return {"value": v_all, "unit": UNIT, "cores": omp_threads(), "kind": "oracle",
+            "sample": f"first {n_all} steps of the bench workload ({B} verifications per step, "
+                      f"V={args.V}, k={args.k}, bf16), oracle/lapssd_oracle.c built with -fopenmp "
+                      f"(per-request verify loop on {omp_threads()} threads), {el_all:.1f} s",
+            "single_thread": {"value": v_one, "cores": 1, "sample": f"first {n_one} steps, plain build, "
+                              f"{el_one:.1f} s"},
+            "host": host_info()}
 
 
 
@@ -782,17 +809,18 @@ def run_reference(args):
     tr, local, pool, tab = build_workload(args, 0, 1, dev, pool_slabs=128)
     # each step is a bounded sample: pick the batch so the whole run takes ~2 minutes
     probe = oracle.Sim(oracle.SchedConfig(**SCHED, seed=1), local.arrival_us, local.L_true,
-                       local.L_pred)
+                       local.L_pred, parallel=True)
     P = pool.numpy()
     P["slab_tab"], P["R"] = tab, tab.shape[1]
-    sel, _ = probe.select(8)
+    nb = 4 * omp_threads()
+    sel, _ = probe.select(nb)
     t0 = time.perf_counter()
     probe.step(P, sel)
-    per_verify = (time.perf_counter() - t0) / 8
+    per_verify = (time.perf_counter() - t0) / nb
     total_steps = args.warmup + args.steps
     b_ref = int(max(1, min(args.batch, 100.0 / (total_steps * per_verify))))
     sim = oracle.Sim(oracle.SchedConfig(**SCHED, seed=synth.CONFIGS["c4"]["seed"]),
-                     local.arrival_us, local.L_true, local.L_pred)
+                     local.arrival_us, local.L_true, local.L_pred, parallel=True)
     sel, _ = sim.select(b_ref)
     for _ in range(args.warmup):
         sim.step(P, sel)
@@ -803,7 +831,8 @@ def run_reference(args):
         sim.step(P, sel)
     el = time.perf_counter() - t0
     value = verified * args.k / el
-    sample = (f"oracle/lapssd_oracle.c single thread; each step verifies a batch of {b_ref} "
+    sample = (f"oracle/lapssd_oracle.c built with -fopenmp ({omp_threads()} threads: a step's requests "
+              f"verified in parallel); each step verifies a batch of {b_ref} "
               f"(of {args.batch}) requests of the same workload, V={args.V}, k={args.k}, bf16")
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
@@ -811,8 +840,8 @@ def run_reference(args):
            "data": "synthetic", "impl": "reference",
            "config": {"workload": WORKLOAD, "N_resident_per_gpu": args.n_per_gpu,
                       "B_per_step": b_ref, "V": args.V, "k": args.k},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": omp_threads(), "kind": "oracle",
+                            "sample": sample, "host": host_info()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

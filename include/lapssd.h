@@ -295,6 +295,14 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
                              int32_t B_global, int32_t C, int32_t *sel_inout, int32_t *count_out,
                              uint64_t *cand_scratch /* [device] (world+1)*(2C+1) words */,
                              lapssd_stream stream);
+/* laps_step_candidates -- laps_step_dist without the collective: verify + update of this
+ * rank's slots of sel_inout, then this rank's candidate block (2C+1 words, layout as
+ * laps_candidates) into cand_out [device], ordered on `stream`.  The caller exchanges the
+ * world blocks with a collective of its choice (NCCL, gloo, MPI: world*(2C+1) words in
+ * rank order) and calls laps_merge(h, all, C, B_global, sel_inout, ...); the two calls
+ * together have the results of laps_step_dist.  Errors: EINVAL, ECUDA. */
+lapssd_status laps_step_candidates(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t C,
+                                   int32_t *sel_inout, uint64_t *cand_out, lapssd_stream stream);
 /* C must be the same on every rank and world*C <= 16384: the caller passes
  * C = min(B_global, max over ranks of n_local).  sel_inout has B_global slots.
  * NCCL plumbing without torch internals: rank 0 calls lapssd_nccl_unique_id, the

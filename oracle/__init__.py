@@ -28,15 +28,20 @@ COST_EQ6, COST_FIG1 = 0, 1
 POLICIES = {"laps-sd": POL_LAPSSD, "fcfs": POL_FCFS, "lp-sjf": POL_LPSJF, "las": POL_LAS}
 
 
+_SO_OMP = os.path.join(_HERE, "liblapssd_oracle_omp.so")
+
+
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (no fast-math, no FP contraction)."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
-        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "lapssd_oracle.h"))
-    ):
-        subprocess.check_call(
-            ["gcc", "-O2", "-std=c11", "-Wall", "-ffp-contract=off", "-fPIC", "-shared",
-             "-o", _SO, _SRC, "-lm"]
-        )
+    """Compile the oracle with gcc (no fast-math, no FP contraction), and the same source
+    with -fopenmp (the all-cores CPU baseline: only the per-request verify loop of a step
+    runs in parallel)."""
+    deps = max(os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "lapssd_oracle.h")))
+    for so, extra in ((_SO, []), (_SO_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(so) or os.path.getmtime(so) < deps:
+            subprocess.check_call(
+                ["gcc", "-O2", "-std=c11", "-Wall", "-Wno-unknown-pragmas", "-ffp-contract=off", "-fPIC", "-shared", *extra,
+                 "-o", so, _SRC, "-lm"]
+            )
     return _SO
 
 
@@ -75,16 +80,17 @@ class StateView(C.Structure):
                 ("switch_total_us", C.c_int64)]
 
 
-_lib = None
+_libs = {}
 
 
-def lib():
-    global _lib
-    if _lib is None:
+def lib(parallel: bool = False):
+    """The oracle library; parallel=True: the -fopenmp build of the same source."""
+    if parallel not in _libs:
         # LAPSSD_ORACLE_LIB: a mutated build of the same source (tests/test_oracle_mutants.py
         # checks that the pins reject it); default: the oracle itself
-        _lib = C.CDLL(os.environ.get("LAPSSD_ORACLE_LIB") or build())
-        L = _lib
+        build()
+        path = _SO_OMP if parallel else (os.environ.get("LAPSSD_ORACLE_LIB") or _SO)
+        _libs[parallel] = L = C.CDLL(path)
         vp, i32, i64, u32, u64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         L.orc_verify_request.argtypes = [vp, vp, i32, i64, i32, vp, u32, u32, u64, u32, vp,
@@ -123,7 +129,7 @@ def lib():
         L.orc_jobs_schedule.restype = i64
         L.orc_brute_force.argtypes = [i32, vp, vp, vp]
         L.orc_brute_force.restype = i64
-    return _lib
+    return _libs[parallel]
 
 
 def _ptr(a: np.ndarray):
@@ -311,37 +317,39 @@ class Sim:
     """The resident-request simulation: admit / select / verify / update / clock."""
 
     def __init__(self, cfg: SchedConfig, arrival_us, L_true, L_pred, rank=0, world=1, trace=0,
-                 prompt=None):
+                 prompt=None, parallel=False):
+        """parallel: the -fopenmp build (the all-cores CPU baseline; same source)."""
         self.cfg = cfg
+        self._L = lib(parallel)
         self._a = _c(arrival_us, np.int64)
         self._lt = _c(L_true, np.int32)
         self._lp = _c(L_pred, np.int32)
         self._pr = _c(prompt, np.int32) if prompt is not None else None
         self.n = len(self._a)
         self._cc = cfg.c()
-        self.h = lib().orc_sim_create(C.byref(self._cc), self.n, _ptr(self._a), _ptr(self._lt),
+        self.h = self._L.orc_sim_create(C.byref(self._cc), self.n, _ptr(self._a), _ptr(self._lt),
                                       _ptr(self._lp), _ptr(self._pr) if self._pr is not None else None,
                                       rank, world)
         if not self.h:
             raise ValueError("orc_sim_create rejected the configuration")
         if trace:
-            lib().orc_sim_set_trace(self.h, trace)
+            self._L.orc_sim_set_trace(self.h, trace)
         self.rank, self.world = rank, world
 
     def __del__(self):
         h = getattr(self, "h", None)
         if h:
-            lib().orc_sim_destroy(h)
+            self._L.orc_sim_destroy(h)
             self.h = None
 
     def select(self, B):
         sel = np.full(B, -1, np.int32)
-        cnt = lib().orc_sim_select(self.h, B, _ptr(sel))
+        cnt = self._L.orc_sim_select(self.h, B, _ptr(sel))
         return sel, cnt
 
     def make_perceptible(self, i, A):
         """Test hook (Fig. 1(c) clairvoyant case): request i perceptible with rate A."""
-        rc = lib().orc_sim_make_perceptible(self.h, int(i), float(A))
+        rc = self._L.orc_sim_make_perceptible(self.h, int(i), float(A))
         if rc != 0:
             raise ValueError("make_perceptible rejected")
 
@@ -349,7 +357,7 @@ class Sim:
         keys = np.zeros(Cn, np.uint64)
         sw = np.zeros(Cn, np.int64)
         nxt = np.zeros(1, np.int64)
-        lib().orc_sim_candidates(self.h, Cn, _ptr(keys), _ptr(sw), _ptr(nxt))
+        self._L.orc_sim_candidates(self.h, Cn, _ptr(keys), _ptr(sw), _ptr(nxt))
         if with_switch:
             return keys, sw, int(nxt[0])
         return keys, int(nxt[0])
@@ -360,14 +368,14 @@ class Sim:
         sw = _c(all_switch, np.int64) if all_switch is not None else None
         sel = np.full(B, -1, np.int32)
         g = np.zeros(1, np.int32)
-        own = lib().orc_sim_merge(self.h, _ptr(k), _ptr(sw) if sw is not None else None, Cn,
+        own = self._L.orc_sim_merge(self.h, _ptr(k), _ptr(sw) if sw is not None else None, Cn,
                                   _ptr(nx), B, _ptr(sel), _ptr(g))
         return sel, own, int(g[0])
 
     def update(self, sel, n_accept):
         s = _c(sel, np.int32)
         na = _c(n_accept, np.int32)
-        lib().orc_sim_update(self.h, _ptr(s), _ptr(na), len(s))
+        self._L.orc_sim_update(self.h, _ptr(s), _ptr(na), len(s))
 
     def step(self, pools, sel):
         """pools: dict(p, q, draft, slab_tab, R) from synth.  sel is updated in place."""
@@ -378,13 +386,13 @@ class Sim:
         tok = np.zeros((B, k + 1), np.int32)
         na = np.zeros(B, np.int32)
         z = np.zeros(B, np.uint64)
-        cnt = lib().orc_sim_step(self.h, _ptr(p), _ptr(q), _ptr(d), _dtype_code(p), V, _ptr(tab),
+        cnt = self._L.orc_sim_step(self.h, _ptr(p), _ptr(q), _ptr(d), _dtype_code(p), V, _ptr(tab),
                                  int(pools["R"]), B, _ptr(sel), _ptr(tok), _ptr(na), _ptr(z))
         return cnt, tok, na, z
 
     def state(self) -> dict:
         v = StateView()
-        lib().orc_sim_view(self.h, C.byref(v))
+        self._L.orc_sim_view(self.h, C.byref(v))
         n, g = self.n, self.cfg.gamma
 
         def arr(ptr, m=n):

@@ -837,6 +837,10 @@ int32_t orc_sim_step(orc_sim *s, const void *p_pool, const void *q_pool,
     const size_t es = dtype == ORC_BF16 ? 2 : 4;
     int32_t *nacc = (int32_t *)malloc((size_t)(B > 0 ? B : 1) * sizeof(int32_t));
     int32_t *tok = (int32_t *)malloc((size_t)(B > 0 ? B : 1) * (size_t)(k + 1) * sizeof(int32_t));
+    /* The batch's requests are verified independently (per request: each writes
+     * only its own slot).  Built with -fopenmp (the all-cores CPU baseline, bench.py) they
+     * run on the host's cores; otherwise the pragma is ignored. */
+#pragma omp parallel for schedule(dynamic, 1)
     for (int32_t b = 0; b < B; b++) {
         int32_t i = sel_inout[b];
         nacc[b] = -1;

@@ -82,6 +82,7 @@ def _load():
         "laps_candidates": ([vp, i32, vp, vp], i32),
         "laps_merge": ([vp, vp, i32, i32, vp, vp, vp], i32),
         "laps_step_dist": ([vp, vp, vp, i32, i32, vp, vp, vp, vp], i32),
+        "laps_step_candidates": ([vp, vp, i32, i32, vp, vp, vp], i32),
         "lapssd_nccl_unique_id": ([vp], i32),
         "lapssd_nccl_comm_init": ([vp, i32, vp, i32], i32),
         "lapssd_nccl_comm_destroy": ([vp], i32),
@@ -318,6 +319,14 @@ class Handle:
                                                      _dptr(sel), _dptr(count), _dptr(cand_scratch),
                                                      _stream(stream)))
         return sel, count
+
+    def laps_step_candidates(self, rows: Rows, B_global, Cn, cand_out, sel=None, stream=None):
+        """verify + update of this rank's slots, then its candidate block (2 Cn + 1 words)
+        into cand_out; the caller all-gathers the blocks and calls laps_merge."""
+        sel = self.sel if sel is None else sel
+        _check("laps_step_candidates", _lib.laps_step_candidates(self.h, C.byref(rows.c), B_global, Cn,
+                                                                 _dptr(sel), _dptr(cand_out), _stream(stream)))
+        return sel
 
     # -- snapshot -----------------------------------------------------------------
     def state(self, stream=None) -> dict:

@@ -714,22 +714,16 @@ lapssd_status lapssd_nccl_comm_destroy(void *comm) {
     return nccl_status(f(comm), "ncclCommDestroy");
 }
 
-lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_rows *rows, int32_t B_global,
-                             int32_t C, int32_t *sel_inout, int32_t *count_out, uint64_t *cand_scratch,
-                             lapssd_stream stream) {
-    g_last_error.clear();
-    if (h) h->side_chained = false;
-    if (!h || !nccl_comm || !cand_scratch || B_global < 1 || B_global > h->max_batch || C < 1)
-        return fail(LAPSSD_EINVAL, "handle / comm / scratch / B_global / C");
-    if ((int64_t)h->sc.world * C > sort_capacity())
-        return fail(LAPSSD_EINVAL, "world*C exceeds %d", sort_capacity());
-    auto allgather = nccl_sym<nccl_allgather_t>("ncclAllGather");
-    if (!allgather) return fail(LAPSSD_ENCCL, "ncclAllGather not found");
+// The multi-GPU step.  allgather == nullptr (laps_step_candidates): stop once this rank's
+// candidate block is in cand_scratch[0, 2C+1) and joined into `stream`; the caller
+// exchanges the blocks with any collective and calls laps_merge.
+static lapssd_status step_dist(lapssd_handle *h, void *nccl_comm, nccl_allgather_t allgather, const lapssd_rows *rows,
+                               int32_t B_global, int32_t C, int32_t *sel_inout, int32_t *count_out,
+                               uint64_t *cand_scratch, cudaStream_t s, const char *who) {
     VerifyArgs a;
     lapssd_status st = fill_step_verify(h, rows, B_global, sel_inout, nullptr, nullptr, a);
     if (st != LAPSSD_OK) return st;
     a.count_dev = &h->st.g->count;   // this rank's slots are [0, count) of the B_global
-    cudaStream_t s = (cudaStream_t)stream;
     h->last_stream = s;
     uint64_t *local = cand_scratch;                 // this rank's block: 2C+1 words
     uint64_t *all = cand_scratch + (2 * (size_t)C + 1);
@@ -740,12 +734,12 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
     if (!overlapped) {   // verify, then candidates -> all-gather -> merge on the stream
         st = step_verify(h, a, sel_inout, B_global, s);
         if (st != LAPSSD_OK) return st;
-        st = cuda_status(launch_candidates(h->st, h->sc, C, local, s), "step_dist candidates");
-        if (st != LAPSSD_OK) return st;
+        st = cuda_status(launch_candidates(h->st, h->sc, C, local, s), who);
+        if (st != LAPSSD_OK || !allgather) return st;
         st = nccl_status(allgather(local, all, 2 * (size_t)C + 1, kNcclUint64, nccl_comm, s), "ncclAllGather");
         if (st != LAPSSD_OK) return st;
         st = cuda_status(launch_merge(h->st, h->sc, a.rows, h->desc, all, C, B_global, sel_inout, count_out, s),
-                         "step_dist merge");
+                         who);
         if (st == LAPSSD_OK) h->desc_valid = true;
         return st;
     }
@@ -760,7 +754,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
         if (st != LAPSSD_OK) return st;
     }
     cudaError_t ce = cudaEventRecord(h->ev_fork, s);
-    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_dist fork");
+    if (ce != cudaSuccess) return cuda_status(ce, "step fork");
     h->desc_valid = false;
     a.fin = h->fin;
     a.fin_key = h->fin_key;
@@ -769,26 +763,57 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
     a.work1 = h->work + 2;
     a.vstep = &h->st.g->vstep;
     static const bool no_pdl = getenv("LAPSSD_NO_PDL") != nullptr;
-    st = cuda_status(launch_verify_grid(a, B_global, 1, h->overlap && !no_pdl, s), "laps_step_dist verify");
+    // the split form's merge runs on the caller's stream after a collective of the
+    // caller's choosing: the next verify then follows it in plain stream order
+    st = cuda_status(launch_verify_grid(a, B_global, 1, allgather && h->overlap && !no_pdl, s), who);
     if (st != LAPSSD_OK) return st;
     ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
-    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_dist fork wait");
+    if (ce != cudaSuccess) return cuda_status(ce, "step fork wait");
     st = cuda_status(launch_select_side(h->st, h->sc, a.rows, sel_inout, h->desc, B_global, h->pre, h->fin,
                                         h->fin_key, h->snap, (uint32_t)verify_grid(B_global, a.n_chunks, 1),
                                         nullptr, h->side, local, C),
-                     "laps_step_dist candidates");
+                     who);
     if (st != LAPSSD_OK) return st;
-    st = nccl_status(allgather(local, all, 2 * (size_t)C + 1, kNcclUint64, nccl_comm, h->side), "ncclAllGather");
-    if (st != LAPSSD_OK) return st;
-    st = cuda_status(launch_merge(h->st, h->sc, a.rows, h->desc, all, C, B_global, sel_inout, count_out, h->side),
-                     "laps_step_dist merge");
-    if (st != LAPSSD_OK) return st;
+    if (allgather) {
+        st = nccl_status(allgather(local, all, 2 * (size_t)C + 1, kNcclUint64, nccl_comm, h->side), "ncclAllGather");
+        if (st != LAPSSD_OK) return st;
+        st = cuda_status(launch_merge(h->st, h->sc, a.rows, h->desc, all, C, B_global, sel_inout, count_out, h->side),
+                         who);
+        if (st != LAPSSD_OK) return st;
+    }
     ce = cudaEventRecord(h->ev_join, h->side);
-    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_dist join");
+    if (ce != cudaSuccess) return cuda_status(ce, "step join");
     ce = cudaStreamWaitEvent(s, h->ev_join, 0);
-    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_dist join wait");
-    h->desc_valid = true;
+    if (ce != cudaSuccess) return cuda_status(ce, "step join wait");
+    h->desc_valid = allgather != nullptr;   // laps_merge (no rows) leaves the next a1 to the next call
     return LAPSSD_OK;
+}
+
+lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_rows *rows, int32_t B_global,
+                             int32_t C, int32_t *sel_inout, int32_t *count_out, uint64_t *cand_scratch,
+                             lapssd_stream stream) {
+    g_last_error.clear();
+    if (h) h->side_chained = false;
+    if (!h || !nccl_comm || !cand_scratch || B_global < 1 || B_global > h->max_batch || C < 1)
+        return fail(LAPSSD_EINVAL, "handle / comm / scratch / B_global / C");
+    if ((int64_t)h->sc.world * C > sort_capacity())
+        return fail(LAPSSD_EINVAL, "world*C exceeds %d", sort_capacity());
+    auto allgather = nccl_sym<nccl_allgather_t>("ncclAllGather");
+    if (!allgather) return fail(LAPSSD_ENCCL, "ncclAllGather not found");
+    return step_dist(h, nccl_comm, allgather, rows, B_global, C, sel_inout, count_out, cand_scratch,
+                     (cudaStream_t)stream, "laps_step_dist");
+}
+
+lapssd_status laps_step_candidates(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t C,
+                                   int32_t *sel_inout, uint64_t *cand_out, lapssd_stream stream) {
+    g_last_error.clear();
+    if (h) h->side_chained = false;
+    if (!h || !cand_out || B_global < 1 || B_global > h->max_batch || C < 1)
+        return fail(LAPSSD_EINVAL, "handle / cand_out / B_global / C");
+    if ((int64_t)h->sc.world * C > sort_capacity())
+        return fail(LAPSSD_EINVAL, "world*C exceeds %d", sort_capacity());
+    return step_dist(h, nullptr, nullptr, rows, B_global, C, sel_inout, nullptr, cand_out, (cudaStream_t)stream,
+                     "laps_step_candidates");
 }
 
 // ---------------------------------------------------------------- snapshot / check

@@ -387,3 +387,27 @@ def test_sharded_global_topB_equals_single_rank(policy):
         st = s.state()
         assert (st["C_us"] == st_ref["C_us"][g::G]).all()
         assert (st["acc_draft"] == st_ref["acc_draft"][g::G]).all()
+
+
+def test_openmp_build_equals_plain_oracle():
+    """The all-cores CPU baseline (the same source built with -fopenmp: a step's requests
+    verified in parallel) computes exactly what the plain single-thread oracle computes."""
+    import synth
+    tr = synth.make_trace(60, 5, arrival="poisson", rate_per_s=80.0, len_mu=np.log(20), len_sigma=0.5,
+                          len_min=4, len_max=80, drift=True)
+    pool = synth.make_pool("f2", V=512, k=4, dtype="bf16", n_buckets=4, variants=2, seed=5, device="cpu")
+    tab = synth.slab_table(tr, 4, 2, R=8, seed=5)
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, 8
+    out = []
+    for parallel in (False, True):
+        sim = oracle.Sim(oracle.SchedConfig(k=4, seed=3), tr.arrival_us, tr.L_true, tr.L_pred, parallel=parallel)
+        sel, _ = sim.select(12)
+        toks = []
+        while not sim.state()["done"].all():
+            _, tok, na, _ = sim.step(P, sel)
+            toks.append(tok.copy())
+        out.append((np.concatenate(toks), sim.state()))
+    assert (out[0][0] == out[1][0]).all()
+    for f in ("C_us", "acc_draft", "E_us", "key"):
+        assert (out[0][1][f] == out[1][1][f]).all()
