@@ -143,6 +143,23 @@ def build_workload(args, rank, world, device, pool_slabs=None):
     return tr, local, pool, tab
 
 
+def upload_graphs(graphs):
+    """cuGraphUpload every captured graph before the timed region, so the first replay
+    does not pay the upload of its executable graph to the device."""
+    import ctypes
+    try:
+        cu = ctypes.CDLL("libcuda.so.1")
+    except OSError:
+        return False
+    s = torch.cuda.current_stream().cuda_stream
+    ok = True
+    for g in graphs:
+        rc = cu.cuGraphUpload(ctypes.c_void_p(g.raw_cuda_graph_exec()), ctypes.c_void_p(s))
+        ok &= rc == 0
+    torch.cuda.synchronize()
+    return ok
+
+
 def build_digest() -> str:
     """sha256 of liblapssd.so's sources, header and nvcc flags: identifies the build an
     ncu capture under profiles/ belongs to."""
@@ -260,6 +277,7 @@ def run_ours(args):
                 for t in range(G):
                     step(scratch_row)
         torch.cuda.synchronize()
+        upload_graphs(graphs + ([g_prof] if g_prof is not None else []))
     elif world == 1 and not args.no_profile:
         h.profile(args.steps)
     st0 = h.state()
