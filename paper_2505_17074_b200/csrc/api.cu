@@ -111,6 +111,7 @@ struct lapssd_handle {
     SelRec *fin = nullptr;       // finisher records, one per slot (fused select)
     uint32_t *snap = nullptr;    // verify CTAs that have read sel/desc (incremental select)
     uint64_t *fin_key = nullptr; // per-slot published keys (~key, 0 = none) of fin[] (incremental select)
+    WaitList wl{};               // the side select's persistent waiting list (wl.valid: host-tracked)
     cudaStream_t side = nullptr; // side stream for the presort, fork/join events
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t last_stream;
@@ -163,6 +164,13 @@ static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma,
     h->fin = cv.take<SelRec>((size_t)max_batch);
     h->snap = cv.take<uint32_t>(1);
     h->fin_key = cv.take<uint64_t>((size_t)max_batch);
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    h->wl.keys[0] = cv.take<uint64_t>(nn);
+    h->wl.keys[1] = cv.take<uint64_t>(nn);
+    h->wl.fresh_i = cv.take<int32_t>((size_t)max_batch);
+    h->wl.fresh_key = cv.take<uint64_t>((size_t)max_batch);
+    h->wl.meta = cv.take<int32_t>(4);
+    h->wl.valid = 0;
 }
 
 static lapssd_status check_config(const lapssd_config *c) {
@@ -417,7 +425,7 @@ lapssd_status lapssd_destroy(lapssd_handle *h) {
 lapssd_status laps_update(lapssd_handle *h, const int32_t *sel, const int32_t *n_accept, int32_t B,
                           lapssd_stream stream) {
     g_last_error.clear();
-    if (h) h->side_chained = false;
+    if (h) { h->side_chained = false; h->wl.valid = 0; }
     if (!h || B < 0 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
     if (B > 0 && (!sel || !n_accept)) return fail(LAPSSD_EINVAL, "NULL sel / n_accept");
     h->last_stream = (cudaStream_t)stream;
@@ -428,7 +436,7 @@ lapssd_status laps_update(lapssd_handle *h, const int32_t *sel, const int32_t *n
 lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t *count_out,
                           lapssd_stream stream) {
     g_last_error.clear();
-    if (h) h->side_chained = false;
+    if (h) { h->side_chained = false; h->wl.valid = 0; }
     if (!h || B < 1 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
     if (!sel_out) return fail(LAPSSD_EINVAL, "sel_out is NULL");
     h->last_stream = (cudaStream_t)stream;
@@ -556,10 +564,15 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
         if (ce != cudaSuccess) return cuda_status(ce, "laps_step fork wait");
     }
     if (incremental) {
+        static const bool no_wl = getenv("LAPSSD_NO_WAITLIST") != nullptr;   // A/B switch
+        const WaitList *wl = no_wl ? nullptr : &h->wl;
         st = cuda_status(launch_select_side(h->st, h->sc, a.rows, sel_inout, h->desc, B, h->pre, h->fin, h->fin_key,
-                                            h->snap, (uint32_t)verify_grid(B, a.n_chunks, 1), count_out, h->side),
+                                            h->snap, (uint32_t)verify_grid(B, a.n_chunks, 1), count_out, h->side,
+                                            nullptr, 0, wl),
                          "laps_step select");
+        h->wl.valid = wl != nullptr && bp <= 1024;   // the commit leaves the next list
     } else {
+        h->wl.valid = 0;
         st = cuda_status(launch_presort(h->st, h->sc, a.rows, sel_inout, B, h->pre, h->side), "laps_step presort");
     }
     if (st != LAPSSD_OK) return st;
@@ -633,7 +646,7 @@ lapssd_status lapssd_profile_read(lapssd_handle *h, double *verify_ms, double *s
 // ---------------------------------------------------------------- a8
 lapssd_status laps_candidates(lapssd_handle *h, int32_t C, uint64_t *cand_out, lapssd_stream stream) {
     g_last_error.clear();
-    if (h) h->side_chained = false;
+    if (h) { h->side_chained = false; h->wl.valid = 0; }
     if (!h || C < 1 || !cand_out) return fail(LAPSSD_EINVAL, "handle / C / cand_out");
     h->last_stream = (cudaStream_t)stream;
     h->desc_valid = false;
@@ -644,7 +657,7 @@ lapssd_status laps_candidates(lapssd_handle *h, int32_t C, uint64_t *cand_out, l
 lapssd_status laps_merge(lapssd_handle *h, const uint64_t *all_cand, int32_t C, int32_t B, int32_t *sel_out,
                          int32_t *count_out, lapssd_stream stream) {
     g_last_error.clear();
-    if (h) h->side_chained = false;
+    if (h) { h->side_chained = false; h->wl.valid = 0; }
     if (!h || C < 1 || !all_cand || !sel_out || B < 1 || B > h->max_batch)
         return fail(LAPSSD_EINVAL, "handle / C / B / pointers");
     if ((int64_t)h->sc.world * C > sort_capacity())
@@ -793,7 +806,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
                              int32_t C, int32_t *sel_inout, int32_t *count_out, uint64_t *cand_scratch,
                              lapssd_stream stream) {
     g_last_error.clear();
-    if (h) h->side_chained = false;
+    if (h) { h->side_chained = false; h->wl.valid = 0; }
     if (!h || !nccl_comm || !cand_scratch || B_global < 1 || B_global > h->max_batch || C < 1)
         return fail(LAPSSD_EINVAL, "handle / comm / scratch / B_global / C");
     if ((int64_t)h->sc.world * C > sort_capacity())
@@ -807,7 +820,7 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
 lapssd_status laps_step_candidates(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t C,
                                    int32_t *sel_inout, uint64_t *cand_out, lapssd_stream stream) {
     g_last_error.clear();
-    if (h) h->side_chained = false;
+    if (h) { h->side_chained = false; h->wl.valid = 0; }
     if (!h || !cand_out || B_global < 1 || B_global > h->max_batch || C < 1)
         return fail(LAPSSD_EINVAL, "handle / cand_out / B_global / C");
     if ((int64_t)h->sc.world * C > sort_capacity())
@@ -819,7 +832,7 @@ lapssd_status laps_step_candidates(lapssd_handle *h, const lapssd_rows *rows, in
 // ---------------------------------------------------------------- snapshot / check
 lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *v, lapssd_stream stream) {
     g_last_error.clear();
-    if (h) h->side_chained = false;
+    if (h) h->side_chained = false;   // (reads only: the waiting list stays valid)
     if (!h || !v) return fail(LAPSSD_EINVAL, "handle / view");
     cudaStream_t s = (cudaStream_t)stream;
     const size_t n = (size_t)h->sc.n;

@@ -582,10 +582,22 @@ cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_s
 int verify_grid(int32_t B, int32_t n_chunks, int32_t reserve_sms);       // CTAs of that launch
 bool verify_fits(int32_t B, int32_t n_chunks, int32_t reserve_sms);      // per-CTA snapshot capacity
 int verify_max_batch(int32_t n_chunks, int32_t reserve_sms);
+// The persistent waiting list of laps_step's side select: the sorted keys of every
+// eligible request outside the current batch.  A waiting request's state -- hence its key
+// -- does not change, so a step merges the few keys that changed (the verified batch,
+// admissions) instead of sorting all N (select_side_kernel).
+constexpr int kAdmCap = 1024;   // admissions merged per step (more: the list is rebuilt)
+struct WaitList {
+    uint64_t *keys[2];     // [n] double buffer, sorted ascending; keys[meta[1]] is current
+    int32_t *fresh_i;      // [max_batch] the last commit's verified, not reselected requests
+    uint64_t *fresh_key;   // [max_batch] their waiting keys (st.key rewritten at the next select)
+    int32_t *meta;         // [4] length, current buffer, fresh count, pad (nullptr: no list)
+    int32_t valid;         // the list describes the state (else the side select rebuilds it)
+};
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
                                int32_t B, PreSelect *pre, const SelRec *fin, uint64_t *fin_key, uint32_t *snap,
                                uint32_t snap_target, int32_t *count_out, cudaStream_t s,
-                               uint64_t *cand_out = nullptr, int32_t C = 0);
+                               uint64_t *cand_out = nullptr, int32_t C = 0, const WaitList *wl = nullptr);
 // Monte-Carlo replicas (mc.cu): T traces over one concatenated request SoA.
 struct McDev {
     const int64_t *off;         // [T+1] request offsets of the traces

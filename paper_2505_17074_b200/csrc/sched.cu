@@ -299,6 +299,25 @@ __global__ void __launch_bounds__(kSelThreads) select_final_kernel(const State s
     STRACE(5);
 }
 
+// Shared-memory words of the side select before the waiting-list regions: the larger of
+// the phase-1 buffers (top-B, or the full sort that rebuilds the waiting list) and the
+// phase-2 / commit buffers (4 lists of bp keys, slot / candidate maps, records).
+__host__ __device__ inline size_t side_r0_words(int n, int bp) {
+    int np = 1;
+    while (np < (n > 0 ? n : 1)) np <<= 1;
+    const size_t a = topB_smem_words(np, bp);
+    const size_t a2 = (np >= 64 && np <= kMergeCap) ? 2 * (size_t)np : (size_t)np;
+    const size_t b = 4 * (size_t)bp + (2 * (size_t)((n + 7) & ~7) * sizeof(int16_t) + 64 +
+                                       (bp <= 1024 ? 2 * (size_t)bp * sizeof(SelRec) : 0) + 7) / 8;
+    size_t r = a > a2 ? a : a2;
+    r = r > b ? r : b;
+    return (r + 1) & ~(size_t)1;
+}
+// admissions [kAdmCap], Kw [bp], S [bp + kAdmCap], rank histogram [bp + kAdmCap + 1] ints
+__host__ __device__ inline size_t side_wl_words(int bp) {
+    return 2 * (size_t)kAdmCap + 2 * (size_t)bp + ((size_t)bp + kAdmCap + 2) / 2;
+}
+
 // ---------------------------------------------------------------- incremental select
 // One CTA on the side stream, concurrent with the verify kernel (which leaves it one
 // SM).  Phase 1 = the presort above.  Phase 2: the verify finishers publish each
@@ -312,7 +331,7 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
                                                                    PreSelect *pre, const SelRec *fin, uint64_t *fin_key,
                                                                    uint32_t *snap, uint32_t snap_target,
                                                                    int32_t *count_out, uint64_t *cand_out,
-                                                                   int32_t C) {
+                                                                   int32_t C, const WaitList wl) {
     extern __shared__ uint64_t s_buf[];
     STRACE(8);
 #ifdef LAPSSD_TRACE
@@ -330,8 +349,19 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     __shared__ uint32_t s_pend[4096 / 32];    // expected slots not yet merged (B <= 4096 here)
     __shared__ int s_snap_ok;
     __shared__ unsigned long long s_sw_side;
+    __shared__ int s_cursor0, s_na, s_wlen, s_rebuild, s_par, s_xw, s_xa, s_nkw;
     const int n = sc.n;
     const int T = blockDim.x;
+    const int bp = next_pow2(B);
+    const int npow2 = next_pow2(n > 0 ? n : 1);
+    // the persistent waiting list (WaitList): its regions follow the phase-1/2 buffers
+    const bool use_wl = wl.meta != nullptr;
+    uint64_t *s_adm = s_buf + side_r0_words(n, bp);      // [kAdmCap] this step's admissions, sorted
+    // (with no list these regions are not allocated and not touched)
+    uint64_t *s_kw = s_adm + kAdmCap;                     // [bp] verified, not reselected: waiting keys
+    uint64_t *s_S = s_kw + bp;                            // [bp + kAdmCap] merge(A suffix, Kw)
+    int *s_hist = reinterpret_cast<int *>(s_S + bp + kAdmCap);   // [bp + kAdmCap + 1] rank histogram
+    if (threadIdx.x == 0) s_cursor0 = st.g->cursor;
     // ---------------- phase 1: presort of every request outside the batch
     for (int w = threadIdx.x; w < (n + 31) / 32; w += T) s_member[w] = 0;
     for (int w = threadIdx.x; w < 4096 / 32; w += T) s_pend[w] = 0;
@@ -351,30 +381,113 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     if (expected) atomicAdd(&s_expected, expected);
     __syncthreads();
     SSTEP(7);
-    const int npow2 = next_pow2(n > 0 ? n : 1);
     const int cursor = s_cursor;
-    for (int i = threadIdx.x; i < npow2; i += T) {
-        uint64_t key = ~0ull;
-        if (i < n && !((s_member[i >> 5] >> (i & 31)) & 1u)) {
-            const uint32_t fl = st.flags[i];
-            const int32_t lp = st.L_pred[i], tok = st.acc_tok[i];
-            const double A = st.A[i];
-            const int32_t rnd = st.rounds[i];
-            const uint64_t tag = st.next_tag[i];
-            key = build_key(sc, i, cursor, fl, lp, tok, A);
-            st.key[i] = key;
-            if (key >> 63) key = ~0ull;   // ineligible: never selected
-            // a1 of a waiting request's current round, memoised once (make_desc stores it):
-            // the records below then never wait on row gathers under the verify stream
-            else if (rw.valid && rw.slab_tab && tag != (((uint64_t)rw.epoch << 32) | (uint32_t)rnd))
-                (void)make_desc(rw, st, sc, 0, i);
-        }
-        s_buf[i] = key;
+    const uint64_t *top;
+    // rebuild the waiting list from every request's state: no valid list, or a burst of
+    // admissions larger than the admission buffer
+    if (threadIdx.x == 0) {
+        s_na = cursor - s_cursor0;
+        s_rebuild = !use_wl || !wl.valid || s_na > kAdmCap;
+        s_wlen = use_wl ? wl.meta[0] : 0;
+        s_par = use_wl ? (wl.meta[1] & 1) : 0;
     }
     __syncthreads();
-    SSTEP(8);
-    const int bp = next_pow2(B);
-    const uint64_t *top = select_topB_fast(s_buf, n, B, s_buf + npow2, s_buf + npow2 + bp, bp, s_buf + npow2 + 2 * bp);
+    if (s_rebuild) {
+        // ---- every key of the requests outside the batch (the old presort)
+        for (int i = threadIdx.x; i < npow2; i += T) {
+            uint64_t key = ~0ull;
+            if (i < n && !((s_member[i >> 5] >> (i & 31)) & 1u)) {
+                const uint32_t fl = st.flags[i];
+                const int32_t lp = st.L_pred[i], tok = st.acc_tok[i];
+                const double A = st.A[i];
+                const int32_t rnd = st.rounds[i];
+                const uint64_t tag = st.next_tag[i];
+                key = build_key(sc, i, cursor, fl, lp, tok, A);
+                st.key[i] = key;
+                if (key >> 63) key = ~0ull;   // ineligible: never selected
+                // a1 of a waiting request's current round, memoised once (make_desc stores it):
+                // the records below then never wait on row gathers under the verify stream
+                else if (rw.valid && rw.slab_tab && tag != (((uint64_t)rw.epoch << 32) | (uint32_t)rnd))
+                    (void)make_desc(rw, st, sc, 0, i);
+            }
+            s_buf[i] = key;
+        }
+        __syncthreads();
+        SSTEP(8);
+        if (use_wl) {
+            // the whole list sorted: the waiting list (eligible keys form a prefix), written
+            // to the current buffer; no admissions pending (they are in it)
+            const uint64_t *srt = block_sort(s_buf, npow2 >= 64 && npow2 <= kMergeCap ? s_buf + npow2 : nullptr,
+                                             npow2);
+            int m = 0;
+            for (int i = threadIdx.x; i < n; i += T) m += srt[i] != ~0ull;
+            __shared__ int s_m_el;
+            if (threadIdx.x == 0) s_m_el = 0;
+            __syncthreads();
+            if (m) atomicAdd(&s_m_el, m);
+            __syncthreads();
+            uint64_t *wl_cur = wl.keys[s_par];
+            for (int i = threadIdx.x; i < s_m_el; i += T) wl_cur[i] = srt[i];
+            if (threadIdx.x == 0) { s_wlen = s_m_el; s_na = 0; }
+            // candidates: the first bp (padding beyond the list)
+            uint64_t *cand = s_buf + (srt == s_buf ? npow2 : 0);
+            if (npow2 < bp || npow2 > kMergeCap) cand = s_S;   // no second buffer: the S region
+            __syncthreads();
+            for (int b = threadIdx.x; b < bp; b += T) cand[b] = b < s_m_el ? srt[b] : ~0ull;
+            __syncthreads();
+            top = cand;
+        } else {
+            top = select_topB_fast(s_buf, n, B, s_buf + npow2, s_buf + npow2 + bp, bp, s_buf + npow2 + 2 * bp);
+        }
+    } else {
+        // ---- persistent list: the keys that changed since the last commit are the
+        // verified batch's (published in phase 2), the last commit's verified-but-not-
+        // reselected requests (their key drops the running bit now: rewritten) and the
+        // admissions; every other waiting key is unchanged (a waiting request's
+        // state does not change)
+        const int nf = wl.meta[2];
+        for (int f = threadIdx.x; f < nf; f += T) st.key[wl.fresh_i[f]] = wl.fresh_key[f];
+        const int na = s_na;
+        const int nap = next_pow2(na > 0 ? na : 1);
+        uint64_t *tmp = s_S;             // sort scratch (free until the commit)
+        for (int x = threadIdx.x; x < nap; x += T) {
+            uint64_t key = ~0ull;
+            if (x < na) {
+                const int i = s_cursor0 + x;
+                key = build_key(sc, i, cursor, st.flags[i], st.L_pred[i], st.acc_tok[i], st.A[i]);
+                st.key[i] = key;
+                if (key >> 63) key = ~0ull;
+            }
+            s_adm[x] = key;
+        }
+        __syncthreads();
+        if (na > 1) {
+            const uint64_t *srt = block_sort(s_adm, nap >= 64 && nap <= kMergeCap ? tmp : nullptr, nap);
+            if (srt != s_adm) {
+                for (int x = threadIdx.x; x < nap; x += T) s_adm[x] = srt[x];
+                __syncthreads();
+            }
+        }
+        // candidates: the first bp of merge(waiting list, admissions)
+        const uint64_t *W = wl.keys[s_par];
+        const int wlen = s_wlen;
+        uint64_t *cand = s_buf;
+        uint64_t *wtop = s_buf + bp;
+        for (int b = threadIdx.x; b < bp; b += T) wtop[b] = b < wlen ? __ldcg(W + b) : ~0ull;
+        __syncthreads();
+        for (int o = threadIdx.x; o < bp; o += T) {   // merge path over (wtop[bp], s_adm[na])
+            int lo = o - na > 0 ? o - na : 0, hi = o < bp ? o : bp;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (wtop[mid] <= s_adm[o - 1 - mid]) lo = mid + 1; else hi = mid;
+            }
+            const int i = lo, j = o - lo;
+            const bool takeA = j >= na || (i < bp && wtop[i] <= s_adm[j]);
+            cand[o] = takeA ? wtop[i] : s_adm[j];
+        }
+        __syncthreads();
+        top = cand;
+    }
     SSTEP(9);
     SelRec *crec = pre_recs(pre, bp);
     for (int b = threadIdx.x; b < bp; b += T) {
@@ -614,6 +727,100 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     ITRACE(100003);
     STRACE(9);
+    if (use_wl) {
+        // ---- the next waiting list, off the critical path (only the next side select reads
+        // it): W' = merge(W[x_W:], A[x_A:], Kw) where x_W / x_A are the selected prefixes
+        // of the list and of the admissions (the top-B of a union of sorted lists takes a
+        // prefix of each) and Kw the verified requests that were not reselected, with the
+        // running bit dropped (AMB-16: it describes the round that just ran)
+        if (threadIdx.x == 0) { s_xw = 0; s_xa = 0; s_nkw = 0; }
+        __syncthreads();
+        int xw = 0, xa = 0;
+        for (int b = threadIdx.x; b < cnt; b += T) {
+            const int i = (int)((uint32_t)(L[b] & 0xFFFFFFull) / (uint32_t)sc.world);
+            if (slot_of[i] >= 0) continue;
+            if (i >= s_cursor0 && i < s_cursor0 + s_na) ++xa; else ++xw;
+        }
+        if (xw) atomicAdd(&s_xw, xw);
+        if (xa) atomicAdd(&s_xa, xa);
+        const bool notrun_bit = sc.policy == LAPSSD_POL_LAS || sc.policy == LAPSSD_POL_LAPSSD;
+        for (int b = threadIdx.x; b < B; b += T) {
+            const int i = old_i[b];
+            if (i < 0 || mark[b]) continue;
+            const SelRec &rec = rec_smem ? brec[b] : fin[b];
+            if (rec.key >> 63) continue;                            // completed
+            const uint64_t key = rec.key | ((notrun_bit && (sc.policy == LAPSSD_POL_LAS || !(rec.flags & F_PERC)))
+                                                ? (1ull << 56) : 0ull);
+            s_kw[atomicAdd(&s_nkw, 1)] = key;
+        }
+        __syncthreads();
+        const int nkw = s_nkw;
+        for (int x = nkw + (int)threadIdx.x; x < bp; x += T) s_kw[x] = ~0ull;
+        __syncthreads();
+        const uint64_t *kw = block_sort(s_kw, bp >= 64 && bp <= kMergeCap ? ntmp : nullptr, bp);
+        for (int f = threadIdx.x; f < nkw; f += T) {
+            wl.fresh_key[f] = kw[f];
+            wl.fresh_i[f] = (int32_t)((uint32_t)(kw[f] & 0xFFFFFFull) / (uint32_t)sc.world);
+        }
+        // S = merge(A[x_A:na), Kw[0:nkw))
+        const int xa0 = s_xa, na = s_na, nA = na - xa0, nS = nA + nkw;
+        const uint64_t *Aw = s_adm + xa0;
+        for (int o = threadIdx.x; o < nS; o += T) {
+            int lo = o - nkw > 0 ? o - nkw : 0, hi = o < nA ? o : nA;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (Aw[mid] <= kw[o - 1 - mid]) lo = mid + 1; else hi = mid;
+            }
+            const int i = lo, j = o - lo;
+            const bool takeA = j >= nkw || (i < nA && Aw[i] <= kw[j]);
+            s_S[o] = takeA ? Aw[i] : kw[j];
+        }
+        __syncthreads();
+        // W' = merge(W[x_W:wlen), S) by ranks: W[j] goes to (j - x_W) + r_j with r_j = #{S < W[j]}
+        // (a binary search in shared memory; coalesced loads and stores), and S[c] to
+        // c + #{j : r_j <= c} (a histogram of the r_j and its prefix sum)
+        const uint64_t *W = wl.keys[s_par];
+        uint64_t *Wn = wl.keys[s_par ^ 1];
+        const int x0 = s_xw, wlen = s_wlen, m = wlen - x0;
+        for (int c = threadIdx.x; c <= nS; c += T) s_hist[c] = 0;
+        __syncthreads();
+        for (int j = x0 + (int)threadIdx.x; j < wlen; j += T) {
+            const uint64_t w = __ldcg(W + j);
+            int lo = 0, hi = nS;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (s_S[mid] < w) lo = mid + 1; else hi = mid;
+            }
+            Wn[(j - x0) + lo] = w;
+            if (nS) atomicAdd(&s_hist[lo], 1);
+        }
+        __syncthreads();
+        if (nS) {
+            // inclusive prefix sum of s_hist[0..nS) (<= bp + kAdmCap entries), warp 0
+            if (threadIdx.x < 32) {
+                const int lane = threadIdx.x;
+                int carry = 0;
+                for (int c0 = 0; c0 < nS; c0 += 32) {
+                    int v = c0 + lane < nS ? s_hist[c0 + lane] : 0;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int u = __shfl_up_sync(0xFFFFFFFFu, v, o);
+                        if (lane >= o) v += u;
+                    }
+                    if (c0 + lane < nS) s_hist[c0 + lane] = v + carry;
+                    carry += __shfl_sync(0xFFFFFFFFu, v, 31);
+                }
+            }
+            __syncthreads();
+            for (int c = threadIdx.x; c < nS; c += T) Wn[c + s_hist[c]] = s_S[c];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            wl.meta[0] = m + nS;
+            wl.meta[1] = s_par ^ 1;
+            wl.meta[2] = nkw;
+        }
+    }
 #ifdef LAPSSD_TRACE
     if (threadIdx.x == 0) g_sstep_t[vstep0 & 63][4] = gtimer();
     if (threadIdx.x == 0) { unsigned c = atomicAdd(&g_scount, 1u); if (c < 64) g_send[c] = gtimer(); }
@@ -623,13 +830,12 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
                                int32_t B, PreSelect *pre, const SelRec *fin, uint64_t *fin_key, uint32_t *snap,
                                uint32_t snap_target, int32_t *count_out, cudaStream_t s, uint64_t *cand_out,
-                               int32_t C) {
-    int np = 1, bp = 1;
-    while (np < (sc.n > 0 ? sc.n : 1)) np <<= 1;
+                               int32_t C, const WaitList *wl) {
+    int bp = 1;
     while (bp < B) bp <<= 1;
-    const size_t a = topB_smem_words(np, bp) * sizeof(uint64_t);
-    const size_t b = (size_t)4 * bp * sizeof(uint64_t) + 2 * (size_t)((sc.n + 7) & ~7) * sizeof(int16_t) + 64 +
-                     (bp <= 1024 ? 2 * (size_t)bp * sizeof(SelRec) : 0);
+    WaitList w{};
+    if (wl && wl->meta && !cand_out && bp <= 1024) w = *wl;   // else: the per-step presort
+    const size_t smem = (side_r0_words(sc.n, bp) + (w.meta ? side_wl_words(bp) : 0)) * sizeof(uint64_t);
     // highest launch priority: when an SM frees up, the block scheduler places this one
     // CTA before the waiting CTAs of the next (programmatically launched) verify grid
     static int prio = [] {
@@ -641,7 +847,7 @@ cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(1);
     cfg.blockDim = dim3(kSideThreads);
-    cfg.dynamicSmemBytes = a > b ? a : b;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributePriority;
@@ -649,7 +855,7 @@ cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &
     cfg.attrs = attr;
     cfg.numAttrs = no_prio ? 0 : 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, select_side_kernel, st, sc, rw, sel, desc, B, pre, fin, fin_key,
-                                             snap, snap_target, count_out, cand_out, C);
+                                             snap, snap_target, count_out, cand_out, C, w);
     if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();
@@ -868,6 +1074,8 @@ void sched_prepare() {
     set_smem_attr((const void *)presort_kernel);
     set_smem_attr((const void *)select_final_kernel);
     set_smem_attr((const void *)select_side_kernel);
+    cudaFuncSetAttribute((const void *)select_side_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    (void)cudaGetLastError();   // an attribute error must not surface as a later launch error
 }
 
 }  // namespace lapssd

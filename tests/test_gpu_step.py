@@ -337,3 +337,46 @@ def test_update_select_standalone_switching_cost(L):
             compare_state(h.state(), sim.state(), step)
     compare_state(h.state(), sim.state(), "end")
     assert h.check() == 0
+
+
+# ---------------------------------------------------------------- the side select's waiting list
+def test_step_parity_n16384_resident(L):
+    """configs[3]'s literal 16,384 concurrent requests resident on ONE GPU (B=512, V=128256,
+    k=8): the side select merges the changed keys into its persistent waiting list instead
+    of sorting all N every step.  Every step's batch, r and the whole state bit-exact."""
+    c = synth.CONFIGS["c4"]
+    n, B = 16384, 512
+    tr = synth.make_trace(n, c["seed"] + 2, arrival="zero", length="uniform", len_min=512, len_max=4096,
+                          beta_ab=(7, 3))
+    pool = synth.make_pool("f2", V=128256, k=8, dtype="bf16", n_buckets=16, variants=2, seed=c["seed"],
+                           device="cuda")
+    tab = synth.slab_table(tr, 16, 2, R=16, seed=c["seed"] + 2)
+    kw = dict(BASE, k=8, seed=c["seed"] + 2)
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=128256, overlap=True)
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, parallel=True)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, 16
+    sel_o, _ = sim.select(B)
+    h.laps_select(B)
+    nacc = torch.empty(B, dtype=torch.int32, device="cuda")
+    for step in range(8):
+        assert (h.sel.cpu().numpy() == sel_o).all(), f"step {step}: batch differs"
+        h.laps_step(rows, B, n_accept=nacc)
+        _, _, na_o, _ = sim.step(P, sel_o)
+        assert (nacc.cpu().numpy() == na_o).all(), f"step {step}: r differs"
+        compare_state(h.state(), sim.state(), step)
+    assert h.check() == 0
+
+
+@pytest.mark.parametrize("burst", [300, 1500])
+def test_step_parity_admission_burst(L, burst):
+    """Admissions after an idle period: a burst within the waiting list's per-step
+    admission buffer (merged) and one beyond it (the list is rebuilt that step)."""
+    n0 = 60
+    tr = synth.make_trace(n0 + burst, 0xAB + burst, arrival="zero", length="uniform", len_min=6, len_max=40,
+                          beta_ab=(4, 2), drift=True)
+    tr.arrival_us[n0:] = 900_000          # all at 0.9 s: after the first requests have finished
+    pool = synth.make_pool("f2", V=2048, k=4, dtype="bf16", n_buckets=8, variants=3, seed=burst, device="cuda")
+    tab = synth.slab_table(tr, 8, 3, R=16, seed=burst)
+    run_lockstep(L, dict(BASE, k=4, seed=33), tr, pool, tab, B=32, check_every=2, overlap=True)

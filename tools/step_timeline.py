@@ -14,11 +14,12 @@ import paper_2505_17074_b200 as L  # noqa: E402
 import synth  # noqa: E402
 
 lib = C.CDLL(os.environ["LAPSSD_LIBRARY"])
-tr = synth.make_trace(2048, 7, arrival="zero", length="uniform", len_min=512, len_max=4096, beta_ab=(7, 3))
+N = int(os.environ.get("N", 2048))
+tr = synth.make_trace(N, 7, arrival="zero", length="uniform", len_min=512, len_max=4096, beta_ab=(7, 3))
 pool = synth.make_pool("f2", V=128256, k=8, dtype="bf16", n_buckets=64, variants=16, seed=7, device="cuda")
 tab = synth.slab_table(tr, 64, 16, R=64, seed=7)
 h = L.Handle(L.SchedConfig(K=4, s1_up_us=72000, k=8, seed=9), tr.arrival_us, tr.L_true, tr.L_pred,
-             max_batch=512, V=128256)
+             max_batch=512, V=128256, overlap=True)
 rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
 h.laps_select(512)
 for _ in range(3):
