@@ -56,6 +56,12 @@ class LogitsOut(C.Structure):
                 ("Z_lo", C.c_uint64), ("Z_hi", C.c_uint64), ("Sp", C.c_uint64), ("Sq", C.c_uint64)]
 
 
+class TreeOut(C.Structure):
+    _fields_ = [("n_accept", C.c_int32), ("y", C.c_int32), ("final_node", C.c_int32),
+                ("n_rejected", C.c_int32), ("fallback", C.c_int32), ("invalid", C.c_int32),
+                ("Z", C.c_uint64)]
+
+
 class OrcConfig(C.Structure):
     _fields_ = [("policy", C.c_int32), ("K", C.c_int32), ("s1_up_us", C.c_int64),
                 ("M", C.c_double), ("gamma", C.c_int32), ("delta", C.c_double),
@@ -104,6 +110,11 @@ def lib(parallel: bool = False):
         L.orc_verify_logits_request.restype = i32
         L.orc_verify_logits_many.argtypes = [vp, vp, i32, i64, i32, i32, vp, vp, vp, u64, vp, vp]
         L.orc_verify_logits_batch.argtypes = [vp, vp, i32, i64, i32, i32, vp, vp, vp, vp, u64, vp, vp, vp]
+        L.orc_draft_sample.argtypes = [vp, i32, i64, u32, u32, u32, u64, u32, vp, vp]
+        L.orc_draft_sample.restype = i32
+        L.orc_verify_tree.argtypes = [vp, vp, i32, i64, i32, vp, vp, u32, u32, u64, u32, vp, vp,
+                                      C.POINTER(TreeOut)]
+        L.orc_verify_tree.restype = i32
         L.orc_thresholds.argtypes = [i32, i64, C.c_double, vp]
         L.orc_thresholds.restype = i32
         L.orc_eq6.argtypes = [i64, C.c_double, i32, i64, i64]
@@ -242,6 +253,35 @@ def verify_logits_batch(zp, zq, drafts, slab, req_ids, rounds, seed):
                                   _ptr(_c(rounds, np.uint32)), int(seed) & (2**64 - 1), _ptr(tok),
                                   _ptr(r), _ptr(z))
     return tok, r, z
+
+
+def draft_sample(q_row, req_id, round_idx, pos, seed, trace=0):
+    """one draft token from the row q_row by the exact integer inverse CDF
+    (lapssd_oracle.h orc_draft_sample).  Returns (x, Z, invalid)."""
+    q = np.ascontiguousarray(q_row)
+    Z = np.zeros(1, np.uint64)
+    inv = np.zeros(1, np.int32)
+    x = lib().orc_draft_sample(_ptr(q), _dtype_code(q), q.shape[-1], int(req_id), int(round_idx), int(pos),
+                               seed & (2**64 - 1), trace, _ptr(Z), _ptr(inv))
+    return int(x), int(Z[0]), bool(inv[0])
+
+
+def verify_tree(p_rows, q_rows, parent, token, req_id, round_idx, seed, trace=0):
+    """token-tree verification (lapssd_oracle.h orc_verify_tree).
+    p_rows / q_rows [n_nodes, V]; parent / token [n_nodes].  Returns (n_accept, tokens,
+    path, TreeOut)."""
+    p = np.ascontiguousarray(p_rows)
+    q = np.ascontiguousarray(q_rows)
+    par = _c(parent, np.int32)
+    tok = _c(token, np.int32)
+    n = len(par)
+    toks = np.zeros(n, np.int32)
+    path = np.zeros(n, np.int32)
+    o = TreeOut()
+    na = lib().orc_verify_tree(_ptr(p), _ptr(q), _dtype_code(p), p.shape[-1], n, _ptr(par), _ptr(tok),
+                               int(req_id), int(round_idx), seed & (2**64 - 1), trace, _ptr(toks),
+                               _ptr(path), C.byref(o))
+    return int(na), toks, path, o
 
 
 def thresholds(K, s1_up_us, M):

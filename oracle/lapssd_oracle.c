@@ -188,6 +188,169 @@ int32_t orc_verify_request(const void *p_rows, const void *q_rows, int32_t dtype
     return r;
 }
 
+/* ------------------------------------------------------------------------ */
+/* (1c) SURVEY 8(f) f4: drafting-side sampling and token-tree verification. */
+/* ------------------------------------------------------------------------ */
+/* Inverse CDF over the integer masses of one row given by mass(v): the smallest v with
+ * sum_{w<=v} R_w > t.  Plain sequential loop. */
+typedef uint64_t (*mass_fn)(const void *ctx, int64_t v);
+
+static int32_t inverse_cdf(mass_fn mass, const void *ctx, int64_t V, uint64_t t)
+{
+    u128 c = 0;
+    for (int64_t v = 0; v < V; v++) {
+        uint64_t R = mass(ctx, v);
+        if (c + R > t) return (int32_t)v;
+        c += R;
+    }
+    return (int32_t)(V - 1);
+}
+
+static u128 total_mass(mass_fn mass, const void *ctx, int64_t V)
+{
+    u128 Z = 0;
+    for (int64_t v = 0; v < V; v++) Z += mass(ctx, v);
+    return Z;
+}
+
+typedef struct { const void *rows; int32_t dtype; int64_t off; } row_ctx;
+
+static uint64_t row_q460(const void *ctx, int64_t v)      /* floor(row[v] 2^60) */
+{
+    const row_ctx *c = (const row_ctx *)ctx;
+    return q460(load_prob(c->rows, c->dtype, c->off + v), 0.0f);
+}
+
+int32_t orc_draft_sample(const void *q_row, int32_t dtype, int64_t V, uint32_t req_id,
+                         uint32_t round_idx, uint32_t pos, uint64_t seed, uint32_t trace,
+                         uint64_t *Z_out, int32_t *invalid)
+{
+    row_ctx c = { q_row, dtype, 0 };
+    u128 Z = total_mass(row_q460, &c, V);
+    if (Z_out) *Z_out = (uint64_t)Z;
+    if (invalid) *invalid = Z == 0;
+    if (Z == 0) return 0;
+    uint32_t u4[4];
+    draw(seed, req_id, round_idx, 2u << 8, pos, trace, u4);      /* c2 = (2 << 16) | pos */
+    uint64_t U = ((uint64_t)u4[0] << 32) | u4[1];
+    uint64_t t = (uint64_t)(((u128)U * Z) >> 64);
+    return inverse_cdf(row_q460, &c, V, t);
+}
+
+/* The residual of stage i at node u (AMB-35): D_1 = floor(max(0, fl32(p - q)) 2^60) and
+ * D_{s+1} = max(0, floor(D_s 2^60 / Z_s) - floor(q 2^60)), with the totals Z_1..Z_{i-1}. */
+typedef struct { const void *p, *q; int32_t dtype; int64_t off; int32_t stage; const uint64_t *Zs; } tree_ctx;
+
+static uint64_t tree_mass(const void *ctx, int64_t v)
+{
+    const tree_ctx *c = (const tree_ctx *)ctx;
+    float p = load_prob(c->p, c->dtype, c->off + v);
+    float q = load_prob(c->q, c->dtype, c->off + v);
+    uint64_t D = q460(p, q);
+    uint64_t Q = q460(q, 0.0f);
+    for (int32_t s = 1; s < c->stage; s++) {
+        uint64_t n = (uint64_t)(((u128)D << 60) / c->Zs[s]);      /* renormalise to 2^60 */
+        D = n > Q ? n - Q : 0;
+    }
+    return D;
+}
+
+/* u24 q(x) Z < D(x) 2^24 exactly, q(x) = m 2^e the stored float (AMB-35). */
+static int tree_accept(uint32_t u24, float qx, uint64_t Dx, uint64_t Z)
+{
+    if (Dx == 0) return 0;
+    if (!(qx > 0.0f)) return 1;                                     /* q(x) = 0 < D(x) / Z */
+    int e;
+    double fr = frexp((double)qx, &e);                              /* qx = fr 2^e, fr in [1/2, 1) */
+    uint64_t m = (uint64_t)ldexp(fr, 24);                           /* exact: <= 24 significant bits */
+    int sh = 24 - (e - 24);                                         /* compare u24 m Z < D 2^sh */
+    u128 lhs = (u128)u24 * m * Z;                                   /* < 2^24 2^24 2^62 */
+    int bits = 64 - __builtin_clzll(Dx);
+    if (bits + sh > 127) return 1;                                  /* D 2^sh >= 2^127 > lhs */
+    return lhs < ((u128)Dx << sh);
+}
+
+int32_t orc_verify_tree(const void *p_rows, const void *q_rows, int32_t dtype, int64_t V,
+                        int32_t n_nodes, const int32_t *parent, const int32_t *token,
+                        uint32_t req_id, uint32_t round_idx, uint64_t seed, uint32_t trace,
+                        int32_t *tokens, int32_t *path, orc_tree_out *out)
+{
+    for (int32_t j = 0; j < n_nodes; j++) { tokens[j] = -1; if (path) path[j] = -1; }
+    int32_t depth[64];
+    if (n_nodes < 1 || n_nodes > 64) return -1;
+    depth[0] = 0;
+    for (int32_t c = 1; c < n_nodes; c++) {
+        if (parent[c] < 0) { depth[c] = -1; continue; }
+        if (parent[c] >= c || depth[parent[c]] < 0 || token[c] < 0 || token[c] >= V) return -1;
+        depth[c] = depth[parent[c]] + 1;
+    }
+    int32_t u = 0, n_acc = 0, n_rej = 0, fallback = 0;
+    uint64_t Zfinal = 0;
+    int32_t y = -1;
+    for (;;) {
+        int32_t ch[64], w = 0;
+        for (int32_t c = u + 1; c < n_nodes; c++)
+            if (parent[c] == u) ch[w++] = c;
+        const int64_t off = (int64_t)u * V;
+        int32_t next = -1;
+        uint64_t Zs[65];
+        int32_t stage = 0;                /* the residual to draw from if no child is accepted */
+        for (int32_t i = 0; i < w && next < 0; i++) {
+            int32_t x = token[ch[i]];
+            float qx = load_prob(q_rows, dtype, off + x);
+            int accept;
+            if (i == 0) {                 /* stage 0: the linear verification's rule */
+                uint32_t u4[4];
+                draw(seed, req_id, round_idx, 0, (uint32_t)(depth[u] / 4), trace, u4);
+                uint32_t u24 = u4[depth[u] % 4] >> 8;
+                float px = load_prob(p_rows, dtype, off + x);
+                accept = (double)u24 * (double)qx < (double)px * 16777216.0;
+            } else {                      /* stage i: against the normalised residual D_i */
+                uint32_t u4[4];
+                draw(seed, req_id, round_idx, (3u << 8) | (uint32_t)u, (uint32_t)((i - 1) / 4), trace, u4);
+                uint32_t u24 = u4[(i - 1) % 4] >> 8;
+                tree_ctx c = { p_rows, q_rows, dtype, off, i, Zs };
+                accept = tree_accept(u24, qx, tree_mass(&c, x), Zs[i]);
+            }
+            if (accept) { next = ch[i]; break; }
+            n_rej++;
+            tree_ctx c = { p_rows, q_rows, dtype, off, i + 1, Zs };   /* D_{i+1} after rejecting c_{i+1} */
+            u128 Z = total_mass(tree_mass, &c, V);
+            Zs[i + 1] = (uint64_t)Z;
+            stage = i + 1;
+            if (Z == 0) { fallback = 1; break; }                      /* AMB-20 */
+        }
+        if (next >= 0) {
+            tokens[n_acc] = token[next];
+            if (path) path[n_acc] = next;
+            n_acc++;
+            u = next;
+            continue;
+        }
+        /* the emitted token: from D_stage (all w children rejected), else the row p_u
+         * (a leaf's bonus token, or the AMB-20 fallback) */
+        uint32_t u4[4];
+        draw(seed, req_id, round_idx, 1, 0, trace, u4);
+        uint64_t U = ((uint64_t)u4[0] << 32) | u4[1];
+        if (stage > 0 && !fallback) {
+            tree_ctx c = { p_rows, q_rows, dtype, off, stage, Zs };
+            Zfinal = Zs[stage];
+            y = inverse_cdf(tree_mass, &c, V, (uint64_t)(((u128)U * Zfinal) >> 64));
+        } else {
+            row_ctx c = { p_rows, dtype, off };
+            u128 Z = total_mass(row_q460, &c, V);
+            Zfinal = (uint64_t)Z;
+            y = Z == 0 ? 0 : inverse_cdf(row_q460, &c, V, (uint64_t)(((u128)U * Z) >> 64));
+        }
+        tokens[n_acc] = y;
+        if (out) {
+            out->n_accept = n_acc; out->y = y; out->final_node = u; out->n_rejected = n_rej;
+            out->fallback = fallback; out->invalid = Zfinal == 0; out->Z = Zfinal;
+        }
+        return n_acc;
+    }
+}
+
 /* Many independent trials of the same rows (statistical pins): trial i uses
  * drafts[i*k..], request id req_ids[i] and round rounds[i]. */
 void orc_verify_many(const void *p_rows, const void *q_rows, int32_t dtype, int64_t V,

@@ -91,6 +91,43 @@ void orc_verify_logits_batch(const void *zp, const void *zq, int32_t dtype, int6
                              const uint32_t *req_ids, const uint32_t *rounds, uint64_t seed,
                              int32_t *tokens_out, int32_t *r_out, uint64_t *z_out);
 
+/* ---- (1c) SURVEY 8(f) f4: the steps on either side of verification (AMB-34, AMB-35) ---- */
+/* Drafting-side sampling ("the draft model autoregressively generates the
+ * subsequent L tokens"): one token from the stored row q (V values, `dtype`) by the exact
+ * integer inverse CDF R_v = floor(q[v] 2^60), Z = sum R, U = Philox(req, round,
+ * (2 << 16) | pos, trace) lanes 0-1, t = floor(U Z / 2^64), x = min{v : sum_{w<=v} R_w > t}.
+ * Returns x (0 if Z = 0, *invalid set); *Z_out = Z. */
+int32_t orc_draft_sample(const void *q_row, int32_t dtype, int64_t V, uint32_t req_id,
+                         uint32_t round_idx, uint32_t pos, uint64_t seed, uint32_t trace,
+                         uint64_t *Z_out, int32_t *invalid);
+
+/* Token-tree verification by multi-step speculative sampling (SpecInfer, cited at P:322;
+ * P:59-64 per step).  Node 0 is the root; parent[c] < c for every used node c >= 1
+ * (parent[c] < 0: unused); token[c] the draft token of node c; children of u are the used
+ * nodes with parent u, in index order.  p_rows / q_rows hold n_nodes rows of V: p_u the
+ * target distribution after the prefix ending at u, q_u the draft distribution its
+ * children were drawn from.  At node u (depth d) with children c_1..c_w:
+ *   stage 0: accept c_1 iff u24 q_u(x) < p_u(x) 2^24 (fp64, exact), u24 from Philox
+ *            (req, round, d / 4, trace) lane d % 4 -- the linear verification's rule;
+ *   rejecting c_i gives the residual D_i: D_1 = floor(max(0, fl32(p_u - q_u)) 2^60),
+ *            D_{i+1} = max(0, floor(D_i 2^60 / Z_i) - floor(q_u 2^60)), Z_i = sum D_i;
+ *   stage i >= 1: accept c_{i+1} iff u24 q_u(x) Z_i < D_i(x) 2^24 (exact integers), u24
+ *            from Philox(req, round, (3 << 16) | (u << 8) | ((i-1) / 4), trace) lane (i-1) % 4;
+ *   accepted child: emit its token, continue at it; all rejected: emit y ~ D_w; a leaf:
+ *   emit the bonus y ~ floor(p_u 2^60); Z_i = 0 after a rejection: y ~ floor(p_u 2^60)
+ *   (*fallback, AMB-20).  y by the inverse CDF with U = Philox(req, round, 1 << 8, trace).
+ * A chain (one child per node) is exactly orc_verify_request.  tokens[n_nodes]: accepted
+ * tokens, y, then -1; path[n_nodes]: accepted nodes then -1.  Returns the accepted count,
+ * -1 for a malformed tree (parent >= child, a token outside [0, V)). */
+typedef struct {
+    int32_t  n_accept, y, final_node, n_rejected, fallback, invalid;
+    uint64_t Z;            /* mass of the final draw's row                          */
+} orc_tree_out;
+int32_t orc_verify_tree(const void *p_rows, const void *q_rows, int32_t dtype, int64_t V,
+                        int32_t n_nodes, const int32_t *parent, const int32_t *token,
+                        uint32_t req_id, uint32_t round_idx, uint64_t seed, uint32_t trace,
+                        int32_t *tokens, int32_t *path, orc_tree_out *out);
+
 /* ---- scheduler pieces, P:161-202 ---- */
 enum { ORC_POL_LAPSSD = 0, ORC_POL_FCFS = 1, ORC_POL_LPSJF = 2, ORC_POL_LAS = 3 };
 enum { ORC_PLACE_BY_ESTIMATE = 0, ORC_PLACE_STAY = 1 };

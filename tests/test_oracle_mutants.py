@@ -15,6 +15,10 @@ switching-cost pin files; at least one pin must fail for every mutant:
   switch_in_E       switching time added to attained service E_i (AMB-24)
   no_semi           every request scheduled as non-perceptible with no estimate (the
                     round-1 advisor's mutation: nonperc = 1, secondary = 0)
+  tree_no_renorm    f4 tree: the residual D_i not renormalised before q is subtracted
+  tree_stage_p      f4 tree: later children tested against p instead of the residual
+  tree_draw_p       f4 tree: after every child is rejected, the token drawn from p_u
+  draft_same_u      f4 draft sampler: one uniform for every position (the counter drops pos)
 """
 import os
 import subprocess
@@ -38,9 +42,16 @@ MUTANTS = {
     "switch_in_E": ("s->switch_us[i] += c;", "s->switch_us[i] += c; s->E[i] += c;"),
     "no_semi": [("f.nonperc = !s->perceptible[i];", "f.nonperc = 1;"),
                 ("f.secondary = sat32(estimate(s, L_rem, s->A[i]));", "f.secondary = 0;")],
+    "tree_no_renorm": ("uint64_t n = (uint64_t)(((u128)D << 60) / c->Zs[s]);", "uint64_t n = D;"),
+    "tree_stage_p": ("accept = tree_accept(u24, qx, tree_mass(&c, x), Zs[i]);",
+                     "accept = (double)u24 * (double)qx < (double)load_prob(p_rows, dtype, off + x) * 16777216.0;"),
+    "tree_draw_p": ("if (stage > 0 && !fallback) {", "if (0) {"),
+    "draft_same_u": ("draw(seed, req_id, round_idx, 2u << 8, pos, trace, u4);",
+                     "draw(seed, req_id, round_idx, 2u << 8, 0, trace, u4);"),
 }
 
 PIN_FILES = ["tests/test_oracle_semiclairvoyant.py", "tests/test_oracle_switch.py"]
+F4_FILES = ["tests/test_oracle_f4.py"]
 
 
 @pytest.mark.parametrize("name", sorted(MUTANTS))
@@ -57,7 +68,8 @@ def test_pins_reject_mutant(name, tmp_path):
     subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
                            "-I", os.path.join(ROOT, "oracle"), "-o", str(so), str(mut), "-lm"])
     env = dict(os.environ, LAPSSD_ORACLE_LIB=str(so))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", *PIN_FILES],
+    files = F4_FILES if name.startswith(("tree_", "draft_")) else PIN_FILES
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", *files],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode != 0, f"mutant {name} passed every pin:\n{r.stdout[-2000:]}"
     assert "failed" in r.stdout, r.stdout[-2000:]
