@@ -201,6 +201,54 @@ lapssd_status spec_verify_logits(const void *zp, const void *zq, int32_t dtype, 
                                  size_t workspace_bytes, lapssd_stream stream);
 
 /* ---------------------------------------------------------------------------
+ * spec_draft_sample -- drafting-side sampling ("the draft model
+ * autoregressively generates the subsequent L tokens"; DESIGN.md AMB-34).  For each of
+ * R rows (row r = q + (row ? row[r] : r) * V elements, dtype bf16 / fp32, 16-byte aligned,
+ * V*sizeof(dtype) a multiple of 16, V <= 524288):
+ *   R_v = floor(q[v] 2^60) (exact), Z = sum_v R_v (uint64), U = Philox4x32-10(key = seed,
+ *   ctr = (req_id[r], round_idx[r], (2 << 16) | pos[r], trace)) lanes 0-1 as a 64-bit word,
+ *   t = floor(U Z / 2^64), draft_out[r] = min{v : sum_{w<=v} R_w > t}  (0 if Z = 0).
+ * pos[r] < 65536 is the draft position (one call per autoregressive step with pos = j,
+ * or all positions at once).  Outputs [device]: draft_out[R], z_out[R] (nullable).
+ * HBM: one read of each row.  Errors: EINVAL (dtype, V, alignment, R < 0, NULL), ECUDA. */
+lapssd_status spec_draft_sample(const void *q, int32_t dtype, int64_t V, const int32_t *row,
+                                const uint32_t *req_id, const uint32_t *round_idx, const uint32_t *pos,
+                                int32_t R, uint64_t seed, uint32_t trace, int32_t *draft_out,
+                                uint64_t *z_out, lapssd_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * spec_verify_tree -- token-tree verification by multi-step speculative sampling
+ * (SpecInfer, cited at P:322; each step the rule of P:59-64; DESIGN.md
+ * AMB-35).  Request b owns a tree of n_nodes (1..64) nodes: node 0 is the root, node
+ * c >= 1 is used iff parent[b, c] >= 0, with parent[b, c] < c and token[b, c] in [0, V)
+ * its draft token; the children of a node are its used children in index order.
+ * p, q: [device] [B, n_nodes, V] rows: p[b, u] the target distribution after the prefix
+ * ending at node u, q[b, u] the draft distribution u's children were drawn from.
+ * At node u (depth d) with children c_1..c_w:
+ *   c_1 is accepted iff u24 q_u(x) < p_u(x) 2^24 (fp64, exact), u24 = Philox(req, round,
+ *     d / 4, trace)[d % 4] >> 8 -- exactly spec_verify's test at position d;
+ *   rejecting c_i leaves the residual D_i: D_1 = floor(max(0, fl32(p_u - q_u)) 2^60),
+ *     D_{i+1} = max(0, floor(D_i 2^60 / Z_i) - floor(q_u 2^60)), Z_i = sum_v D_i;
+ *   c_{i+1} (i >= 1) is accepted iff u24 q_u(x) Z_i < D_i(x) 2^24 (exact integers),
+ *     u24 = Philox(req, round, (3 << 16) | (u << 8) | ((i-1) / 4), trace)[(i-1) % 4] >> 8;
+ *   the first accepted child's token is emitted and its subtree continues; if every child
+ *   is rejected the token is drawn from D_w, at a leaf the bonus token from floor(p_u 2^60),
+ *   and if some Z_i = 0 from floor(p_u 2^60) (AMB-20); draws: U = Philox(req, round,
+ *   1 << 8, trace), t = floor(U Z / 2^64), y = min{v : sum_{w<=v} mass_w > t}.
+ * A chain (one child per node) gives exactly spec_verify's result.
+ * Outputs [device]: tokens[B, n_nodes] (accepted tokens, the drawn token, then -1),
+ * path[B, n_nodes] (accepted node indices then -1, nullable), n_accept[B] (-1: malformed
+ * tree, nothing else written), z_out[B] (mass of the final draw's row, nullable).
+ * HBM per request: the gathered scalars, one pass over (p_u, q_u) per rejected child,
+ * one over p_u at a leaf.  Errors: EINVAL (dtype, V, n_nodes, alignment, B < 0, NULL),
+ * ECUDA. */
+lapssd_status spec_verify_tree(const void *p, const void *q, int32_t dtype, int64_t V, int32_t n_nodes,
+                               const int32_t *parent, const int32_t *token, const uint32_t *req_id,
+                               const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,
+                               int32_t *tokens, int32_t *path, int32_t *n_accept, uint64_t *z_out,
+                               lapssd_stream stream);
+
+/* ---------------------------------------------------------------------------
  * Handle: resident-request state (SoA, ~64 B/request + gamma*4 B ring) in a
  * caller-owned device workspace.  lapssd_create copies the request arrays (H2D on
  * `stream`), zero-initialises state, computes the thresholds of P:169, and sets

@@ -72,6 +72,8 @@ def _load():
         "spec_verify": ([vp, vp, i32, i64, i32, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp, vp, sz, vp], i32),
         "spec_verify_logits_workspace_bytes": ([i32, i32], sz),
         "spec_verify_logits": ([vp, vp, i32, i64, i32, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp, vp, sz, vp], i32),
+        "spec_draft_sample": ([vp, i32, i64, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp], i32),
+        "spec_verify_tree": ([vp, vp, i32, i64, i32, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp, vp, vp], i32),
         "lapssd_workspace_bytes": ([vp, i32, i32, i64, i32], sz),
         "lapssd_create": ([vp, vp, i32, i64, vp, sz, vp, vp], i32),
         "lapssd_destroy": ([vp], i32),
@@ -199,6 +201,41 @@ def spec_verify_logits(zp, zq, draft, req_id, round_idx, seed, *, slab=None, tra
                                  workspace.numel(), _stream(stream))
     _check("spec_verify_logits", rc)
     return tokens, n_accept, z
+
+
+def spec_draft_sample(q, req_id, round_idx, pos, seed, *, row=None, trace=0, out=None, z=None, stream=None):
+    """Drafting-side sampling (include/lapssd.h spec_draft_sample): one
+    token per row.  q [..., V] rows (bf16 / fp32; row r = q.view(-1, V)[row[r] if row is
+    given else r]); req_id / round_idx / pos [R] int32.  Returns (draft [R], z [R])."""
+    V = q.shape[-1]
+    R = req_id.numel()
+    dev = q.device
+    if out is None:
+        out = torch.empty(R, dtype=torch.int32, device=dev)
+    if z is None:
+        z = torch.empty(R, dtype=torch.int64, device=dev)
+    rc = _lib.spec_draft_sample(_dptr(q), _dtype_code(q), V, _dptr(row), _dptr(req_id), _dptr(round_idx),
+                                _dptr(pos), R, seed & (2**64 - 1), trace, _dptr(out), _dptr(z), _stream(stream))
+    _check("spec_draft_sample", rc)
+    return out, z
+
+
+def spec_verify_tree(p, q, parent, token, req_id, round_idx, seed, *, trace=0, tokens=None, path=None,
+                     n_accept=None, z=None, stream=None):
+    """Token-tree verification (include/lapssd.h spec_verify_tree).  p, q
+    [B, n_nodes, V]; parent / token [B, n_nodes] int32; req_id / round_idx [B].  Returns
+    (tokens [B, n_nodes], path [B, n_nodes], n_accept [B], z [B])."""
+    B, n, V = p.shape
+    dev = p.device
+    tokens = torch.empty(B, n, dtype=torch.int32, device=dev) if tokens is None else tokens
+    path = torch.empty(B, n, dtype=torch.int32, device=dev) if path is None else path
+    n_accept = torch.empty(B, dtype=torch.int32, device=dev) if n_accept is None else n_accept
+    z = torch.empty(B, dtype=torch.int64, device=dev) if z is None else z
+    rc = _lib.spec_verify_tree(_dptr(p), _dptr(q), _dtype_code(p), V, n, _dptr(parent), _dptr(token),
+                               _dptr(req_id), _dptr(round_idx), B, seed & (2**64 - 1), trace, _dptr(tokens),
+                               _dptr(path), _dptr(n_accept), _dptr(z), _stream(stream))
+    _check("spec_verify_tree", rc)
+    return tokens, path, n_accept, z
 
 
 # --------------------------------------------------------------------------- handle

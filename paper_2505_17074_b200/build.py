@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "liblapssd.so")
-SOURCES = ["api.cu", "verify.cu", "verify_logits.cu", "sched.cu", "mc.cu"]
+SOURCES = ["api.cu", "verify.cu", "verify_logits.cu", "sched.cu", "mc.cu", "draft_tree.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -348,6 +348,39 @@ lapssd_status spec_verify_logits(const void *zp, const void *zq, int32_t dtype, 
                        "spec_verify_logits");
 }
 
+// ---------------------------------------------------------------- f4: draft sampling, tree verification
+lapssd_status spec_draft_sample(const void *q, int32_t dtype, int64_t V, const int32_t *row, const uint32_t *req_id,
+                                const uint32_t *round_idx, const uint32_t *pos, int32_t R, uint64_t seed,
+                                uint32_t trace, int32_t *draft_out, uint64_t *z_out, lapssd_stream stream) {
+    g_last_error.clear();
+    if (R < 0) return fail(LAPSSD_EINVAL, "R < 0");
+    if (!rows_ok(dtype, V, 1, q, q)) return fail(LAPSSD_EINVAL, "rows: dtype/V/alignment");
+    if (R == 0) return LAPSSD_OK;
+    if (!q || !req_id || !round_idx || !pos || !draft_out) return fail(LAPSSD_EINVAL, "NULL pointer argument");
+    prepare_all();
+    return cuda_status(launch_draft_sample(q, dtype, V, row, req_id, round_idx, pos, R, seed, trace, draft_out,
+                                           z_out, (cudaStream_t)stream),
+                       "spec_draft_sample");
+}
+
+lapssd_status spec_verify_tree(const void *p, const void *q, int32_t dtype, int64_t V, int32_t n_nodes,
+                               const int32_t *parent, const int32_t *token, const uint32_t *req_id,
+                               const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,
+                               int32_t *tokens, int32_t *path, int32_t *n_accept, uint64_t *z_out,
+                               lapssd_stream stream) {
+    g_last_error.clear();
+    if (B < 0) return fail(LAPSSD_EINVAL, "B < 0");
+    if (n_nodes < 1 || n_nodes > 64) return fail(LAPSSD_EINVAL, "n_nodes=%d outside 1..64", n_nodes);
+    if (!rows_ok(dtype, V, 1, p, q)) return fail(LAPSSD_EINVAL, "rows: dtype/V/alignment");
+    if (B == 0) return LAPSSD_OK;
+    if (!p || !q || !parent || !token || !req_id || !round_idx || !tokens || !n_accept)
+        return fail(LAPSSD_EINVAL, "NULL pointer argument");
+    prepare_all();
+    return cuda_status(launch_verify_tree(p, q, dtype, V, n_nodes, parent, token, req_id, round_idx, B, seed, trace,
+                                          tokens, path, n_accept, z_out, (cudaStream_t)stream),
+                       "spec_verify_tree");
+}
+
 // ---------------------------------------------------------------- handle
 size_t lapssd_workspace_bytes(const lapssd_config *cfg, int32_t n_local, int32_t max_batch, int64_t V,
                               int32_t world) {

@@ -574,6 +574,14 @@ cudaError_t launch_verify_logits(const void *zp, const void *zq, int32_t dtype, 
                                  int32_t *tokens, int32_t *n_accept, uint64_t *z, float *m_ws, uint64_t *S_ws,
                                  cudaStream_t s);
 void verify_logits_prepare();
+// f4 (draft_tree.cu)
+cudaError_t launch_draft_sample(const void *q, int32_t dtype, int64_t V, const int32_t *row_idx,
+                                const uint32_t *req, const uint32_t *rnd, const uint32_t *pos, int32_t R,
+                                uint64_t seed, uint32_t trace, int32_t *out, uint64_t *z_out, cudaStream_t s);
+cudaError_t launch_verify_tree(const void *p, const void *q, int32_t dtype, int64_t V, int32_t n_nodes,
+                               const int32_t *parent, const int32_t *token, const uint32_t *req,
+                               const uint32_t *rnd, int32_t B, uint64_t seed, uint32_t trace, int32_t *tokens,
+                               int32_t *path, int32_t *n_accept, uint64_t *z_out, cudaStream_t s);
 cudaError_t launch_presort(const State &st, const Sched &sc, const RowsDev &rw, const int32_t *sel, int32_t B,
                            PreSelect *out, cudaStream_t s);
 cudaError_t launch_select_final(const State &st, const Sched &sc, const RowsDev &rw, SlotDesc *desc, int32_t B,
