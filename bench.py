@@ -67,9 +67,12 @@ def parse():
     ap.add_argument("--dist-path", action="store_true",
                     help="N=1 only: time the N>1 step (laps_step_dist) with a one-rank NCCL communicator")
     ap.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "verify_dram.json"))
-    ap.add_argument("--workload", choices=["c4", "mc", "logits"], default="c4",
+    ap.add_argument("--workload", choices=["c4", "mc", "logits", "draft", "tree"], default="c4",
                     help="c4 = configs[3] (the headline); mc = configs[4] Monte-Carlo traces; "
-                    "logits = SURVEY 8(f) f1, spec_verify_logits at configs[3] dimensions")
+                    "logits = SURVEY 8(f) f1, spec_verify_logits at configs[3] dimensions; "
+                    "draft / tree = SURVEY 8(f) f4, spec_draft_sample / spec_verify_tree")
+    ap.add_argument("--tree-nodes", type=int, default=16, help="f4 tree: nodes per request")
+    ap.add_argument("--tree-width", type=int, default=3, help="f4 tree: max children per node")
     ap.add_argument("--mc-traces", type=int, default=8192, help="configs[4]: traces (whole job)")
     ap.add_argument("--mc-n", type=int, default=512, help="configs[4]: requests per trace")
     ap.add_argument("--mc-variants", type=int, default=256, help="configs[4]: slab variants per bucket")
@@ -813,6 +816,197 @@ def run_logits(args):
         dist.destroy_process_group()
 
 
+def timed_graph(args, step, G, local_rank, dist=None):
+    """Warm-up, capture G steps in a CUDA graph, upload it, replay it over the timed
+    region (CUDA events, NVML clocks, max over ranks).  Returns (ms_total, steps, clocks,
+    launches_per_step)."""
+    import paper_2505_17074_b200 as L
+    for t in range(max(args.warmup, 3)):
+        step(t % G)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    lc0 = L.launch_count()
+    with torch.cuda.graph(g):
+        for t in range(G):
+            step(t)
+    launches = (L.launch_count() - lc0) / G
+    upload_graphs([g])
+    reps = max(1, args.steps // G)
+    clocks = Clocks(int(os.environ.get("LOCAL_RANK", local_rank)))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t_ = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        ms = float(t_[0])
+    return ms, reps * G, clk, launches
+
+
+def hbm_peak():
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    return peaks.get("hbm_gbs") or 6650.0
+
+
+def run_f4(args):
+    """SURVEY 8(f) f4 at configs[3] dimensions (V=128,256, bf16, 512 requests per GPU per
+    step).  draft: spec_draft_sample of the k=8 draft rows of every request (4,096 rows of
+    256 KB per step, drawn at random from a 2.1 GB pool of F2 draft rows).  tree:
+    spec_verify_tree of 512 token trees of --tree-nodes nodes (at most --tree-width children
+    per node, tokens drawn from the parent's draft row), two input sets alternating
+    (2 x 4.2 GB).  Weak scaling: requests per rank, no collective."""
+    import paper_2505_17074_b200 as L
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    B, k, V = args.batch, args.k, args.V
+    pool = synth.make_pool("f2", V=V, k=k, dtype="bf16", n_buckets=args.buckets, variants=args.variants,
+                           seed=synth.CONFIGS["c4"]["seed"] + 31 * rank, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4000 + rank)
+    G = max(1, min(args.graph_steps or 1, args.steps))
+    peak = hbm_peak()
+    seed = 0x5D0F4
+    if args.workload == "draft":
+        R = B * k
+        qrows = pool.q.view(-1, V)
+        rows = torch.randint(0, qrows.shape[0], (G, R), generator=gen, device=dev, dtype=torch.int32)
+        req = (torch.arange(B, device=dev, dtype=torch.int32) + rank * B).repeat_interleave(k)
+        pos = torch.arange(k, device=dev, dtype=torch.int32).repeat(B)
+        rnds = torch.randint(0, 1 << 12, (G, R), generator=gen, device=dev, dtype=torch.int32)
+        out = torch.empty(G, R, dtype=torch.int32, device=dev)
+        zbuf = torch.empty(G, R, dtype=torch.int64, device=dev)
+
+        def step(t):
+            L.spec_draft_sample(qrows, req, rnds[t], pos, seed, row=rows[t], out=out[t], z=zbuf[t])
+
+        ms, steps, clk, lps = timed_graph(args, step, G, local_rank, dist)
+        alg = float(R * V * 2)
+        unit, value = "drafted tokens/s", world * R * steps / (ms * 1e-3)
+        kernel = "draft_sample_kernel<bf16> (spec_draft_sample)"
+        cfg = {"workload": f"SURVEY 8(f) f4 drafting: spec_draft_sample of B={B} requests x k={k} draft rows per "
+                           f"GPU per step, V={V}, bf16 F2 draft rows drawn at random from a "
+                           f"{qrows.shape[0] * V * 2 / 1e9:.1f} GB pool", "rows_per_step": R, "V": V,
+               "l2": "inputs larger than L2", "parallelism": f"dp{world}: requests per rank"}
+        cpu = None
+        if not args.no_cpu_baseline and rank == 0:
+            import oracle
+            Q = synth.to_numpy_rows(qrows[rows[0][:64].long()])
+            t0, n_ = time.perf_counter(), 0
+            while n_ < 64 and time.perf_counter() - t0 < args.cpu_seconds:
+                oracle.draft_sample(Q[n_], int(req[n_]), int(rnds[0][n_]), int(pos[n_]), seed)
+                n_ += 1
+            dt = time.perf_counter() - t0
+            cpu = {"value": n_ / dt, "unit": unit, "cores": 1, "kind": "oracle",
+                   "sample": f"{n_} rows of the first timed step, orc_draft_sample single thread, {dt:.1f} s"}
+    else:
+        n, wmax = args.tree_nodes, args.tree_width
+        sets = []
+        for si in range(2):
+            idx = torch.randint(0, pool.S, (B,), generator=gen, device=dev)
+            # node u's rows: target row u % (k+1) and draft row u % k of the request's slab
+            ui = torch.arange(n, device=dev)
+            p = pool.p[idx][:, ui % (k + 1)].contiguous()
+            q = pool.q[idx][:, ui % k].contiguous()
+            rng = np.random.default_rng(100 * rank + si)
+            par = np.full((B, n), -1, np.int32)
+            kids = np.zeros((B, n), np.int32)
+            tok = np.zeros((B, n), np.int32)
+            for c in range(1, n):
+                for b in range(B):
+                    cands = [u for u in range(c) if (u == 0 or par[b, u] >= 0) and kids[b, u] < wmax]
+                    u = int(rng.choice(cands))
+                    par[b, c] = u
+                    kids[b, u] += 1
+            # tokens: drawn from the parent's draft row on the GPU (the f4 sampler itself)
+            qv = q.view(-1, V)
+            rows_ = torch.as_tensor((np.arange(B)[:, None] * n + np.maximum(par, 0)).reshape(-1), device=dev,
+                                    dtype=torch.int32)
+            rq = torch.arange(B * n, device=dev, dtype=torch.int32)
+            tk, _ = L.spec_draft_sample(qv, rq, rq * 0 + si, rq * 0, 77, row=rows_)
+            tok = tk.view(B, n).contiguous()
+            tok[:, 0] = 0
+            sets.append((p, q, torch.as_tensor(par, device=dev), tok, par))
+        req = torch.arange(B, device=dev, dtype=torch.int32) + rank * B
+        rnds = torch.randint(0, 1 << 12, (G, B), generator=gen, device=dev, dtype=torch.int32)
+        outs = [(torch.empty(B, n, dtype=torch.int32, device=dev), torch.empty(B, n, dtype=torch.int32, device=dev),
+                 torch.empty(B, dtype=torch.int32, device=dev), torch.empty(B, dtype=torch.int64, device=dev))
+                for _ in range(G)]
+
+        def step(t):
+            p, q, par_d, tok, _ = sets[t % 2]
+            L.spec_verify_tree(p, q, par_d, tok, req, rnds[t], seed, tokens=outs[t][0], path=outs[t][1],
+                               n_accept=outs[t][2], z=outs[t][3])
+
+        ms, steps, clk, lps = timed_graph(args, step, G, local_rank, dist)
+        # algorithmic bytes from the outcomes: per request, the final node's passes --
+        # one over (p_u, q_u) per rejected child (all of its w children), or one over p_u
+        # at a leaf -- plus two gathered scalars per tested child
+        emitted = alg = 0.0
+        for t in range(G):
+            par = sets[t % 2][4]
+            path = outs[t][1].cpu().numpy()
+            na = outs[t][2].cpu().numpy()
+            for b in range(B):
+                u = 0 if na[b] == 0 else int(path[b, na[b] - 1])
+                w = int((par[b] == u).sum())
+                alg += (w * 2 if w else 1) * V * 2 + 4 * (na[b] + w)
+                emitted += na[b] + 1
+        alg /= G
+        unit = "emitted tokens/s"
+        value = world * emitted / G * steps / (ms * 1e-3)
+        kernel = "tree_verify_kernel<bf16> (spec_verify_tree)"
+        cfg = {"workload": f"SURVEY 8(f) f4 tree verification: spec_verify_tree of B={B} token trees per GPU "
+                           f"per step, {n} nodes (<= {wmax} children per node, draft tokens sampled from the "
+                           f"parent's draft row), V={V}, bf16 F2 rows, two input sets of "
+                           f"{2 * B * n * V * 2 / 1e9:.1f} GB alternating", "trees_per_step": B, "nodes": n,
+               "max_children": wmax, "V": V, "mean_accepted": emitted / G / B - 1,
+               "l2": "inputs larger than L2", "parallelism": f"dp{world}: trees per rank"}
+        cpu = None
+        if not args.no_cpu_baseline and rank == 0:
+            import oracle
+            p, q, _, tok, par = sets[0]
+            t0, n_ = time.perf_counter(), 0
+            tk = tok.cpu().numpy()
+            while n_ < B and time.perf_counter() - t0 < args.cpu_seconds:
+                oracle.verify_tree(synth.to_numpy_rows(p[n_]), synth.to_numpy_rows(q[n_]), par[n_], tk[n_],
+                                   int(req[n_]), int(rnds[0][n_]), seed)
+                n_ += 1
+            dt = time.perf_counter() - t0
+            cpu = {"value": n_ * (emitted / G / B) / dt, "unit": unit, "cores": 1, "kind": "oracle",
+                   "sample": f"{n_} trees of the first input set, orc_verify_tree single thread, {dt:.1f} s"}
+    achieved = alg / (ms / steps * 1e-3) / 1e9
+    res = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": steps,
+           "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "bf16 rows; exact Q4.60 integer masses, 128-bit residual tests",
+           "data": "synthetic", "config": cfg, "gpu_launches": int(round(lps * steps)), "clocks": clk,
+           "roofline": {"kernel": kernel, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "algorithmic_bytes_per_step": alg, "traffic": None,
+                        "timing": f"{steps} steps as replays of a CUDA graph of {G} steps"}}
+    if cpu:
+        res["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle, as it stands, timed on this host's cores on the
     same config / metric; each step a bounded sample (a smaller batch) of the workload."""
@@ -870,6 +1064,8 @@ def main():
         run_reference(args)
     elif args.workload == "logits":
         run_logits(args)
+    elif args.workload in ("draft", "tree"):
+        run_f4(args)
     elif args.workload == "mc":
         run_mc(args)
     else:

@@ -228,7 +228,9 @@ lapssd_status spec_draft_sample(const void *q, int32_t dtype, int64_t V, const i
  *   c_1 is accepted iff u24 q_u(x) < p_u(x) 2^24 (fp64, exact), u24 = Philox(req, round,
  *     d / 4, trace)[d % 4] >> 8 -- exactly spec_verify's test at position d;
  *   rejecting c_i leaves the residual D_i: D_1 = floor(max(0, fl32(p_u - q_u)) 2^60),
- *     D_{i+1} = max(0, floor(D_i 2^60 / Z_i) - floor(q_u 2^60)), Z_i = sum_v D_i;
+ *     D_{i+1} = floor(max(0, D_i 2^60 - Z_i floor(q_u 2^60)) / 2^b(Z_i)), Z_i = sum_v D_i,
+ *     b(Z) the bit length of Z (the residual of the normalised D_i, scaled, in exact
+ *     128-bit integers: every entry stays below 2^60);
  *   c_{i+1} (i >= 1) is accepted iff u24 q_u(x) Z_i < D_i(x) 2^24 (exact integers),
  *     u24 = Philox(req, round, (3 << 16) | (u << 8) | ((i-1) / 4), trace)[(i-1) % 4] >> 8;
  *   the first accepted child's token is emitted and its subtree continues; if every child

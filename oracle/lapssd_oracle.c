@@ -238,7 +238,11 @@ int32_t orc_draft_sample(const void *q_row, int32_t dtype, int64_t V, uint32_t r
 }
 
 /* The residual of stage i at node u (AMB-35): D_1 = floor(max(0, fl32(p - q)) 2^60) and
- * D_{s+1} = max(0, floor(D_s 2^60 / Z_s) - floor(q 2^60)), with the totals Z_1..Z_{i-1}. */
+ * D_{s+1} = floor(max(0, D_s 2^60 - Z_s floor(q 2^60)) / 2^b(Z_s)), b(Z) the bit length of
+ * Z: the residual max(0, D_s / Z_s - q) of the normalised D_s, scaled by Z_s 2^60 (exact
+ * 128-bit integers), then by 2^-b(Z_s) so that every entry stays below 2^60. */
+static int bitlen(uint64_t x) { int b = 0; while (x) { b++; x >>= 1; } return b; }
+
 typedef struct { const void *p, *q; int32_t dtype; int64_t off; int32_t stage; const uint64_t *Zs; } tree_ctx;
 
 static uint64_t tree_mass(const void *ctx, int64_t v)
@@ -249,8 +253,8 @@ static uint64_t tree_mass(const void *ctx, int64_t v)
     uint64_t D = q460(p, q);
     uint64_t Q = q460(q, 0.0f);
     for (int32_t s = 1; s < c->stage; s++) {
-        uint64_t n = (uint64_t)(((u128)D << 60) / c->Zs[s]);      /* renormalise to 2^60 */
-        D = n > Q ? n - Q : 0;
+        u128 a = (u128)D << 60, b = (u128)c->Zs[s] * Q;            /* D_s / Z_s - q, times Z_s 2^60 */
+        D = a > b ? (uint64_t)((a - b) >> bitlen(c->Zs[s])) : 0;
     }
     return D;
 }

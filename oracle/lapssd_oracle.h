@@ -110,7 +110,8 @@ int32_t orc_draft_sample(const void *q_row, int32_t dtype, int64_t V, uint32_t r
  *   stage 0: accept c_1 iff u24 q_u(x) < p_u(x) 2^24 (fp64, exact), u24 from Philox
  *            (req, round, d / 4, trace) lane d % 4 -- the linear verification's rule;
  *   rejecting c_i gives the residual D_i: D_1 = floor(max(0, fl32(p_u - q_u)) 2^60),
- *            D_{i+1} = max(0, floor(D_i 2^60 / Z_i) - floor(q_u 2^60)), Z_i = sum D_i;
+ *            D_{i+1} = floor(max(0, D_i 2^60 - Z_i floor(q_u 2^60)) / 2^b(Z_i)), Z_i = sum D_i,
+ *            b(Z) the bit length of Z (the normalised residual, scaled; exact integers);
  *   stage i >= 1: accept c_{i+1} iff u24 q_u(x) Z_i < D_i(x) 2^24 (exact integers), u24
  *            from Philox(req, round, (3 << 16) | (u << 8) | ((i-1) / 4), trace) lane (i-1) % 4;
  *   accepted child: emit its token, continue at it; all rejected: emit y ~ D_w; a leaf:

@@ -7,8 +7,9 @@
 // spec_verify_tree (SpecInfer's multi-step speculative sampling, cited at P:322; each
 //   step the rule of P:59-64; AMB-35): per request a token tree; at a node the children
 //   are tested in index order, the first with the linear verification's exact rule, the
-//   later ones against the renormalised residual D_{i+1} = max(0, floor(D_i 2^60 / Z_i) -
-//   floor(q 2^60)) (exact 128-bit comparison); the first accepted child is emitted and
+//   later ones against the residual of the normalised D_i, D_{i+1} = floor(max(0, D_i 2^60 -
+//   Z_i floor(q 2^60)) / 2^b(Z_i)) (exact 128-bit integers; b = bit length), by an exact
+//   128-bit comparison; the first accepted child is emitted and
 //   its subtree continues; if all are rejected the token comes from the last residual, at
 //   a leaf the bonus token from p.  A chain is exactly spec_verify.
 //
@@ -22,10 +23,12 @@ namespace lapssd {
 namespace {
 
 typedef unsigned __int128 u128;
-typedef __int128 i128;
 
-constexpr int kRowThreads = 512;
-constexpr int kRowWarps = kRowThreads / 32;
+constexpr int kRowThreads = 512;        // draft sampling: one row per CTA, 4 CTAs per SM
+#ifndef LAPSSD_TREE_THREADS
+#define LAPSSD_TREE_THREADS 512
+#endif
+constexpr int kTreeThreads = LAPSSD_TREE_THREADS;   // tree verification: one tree per SM (measured: 256 / 128 slower)
 constexpr int kTreeMax = 64;            // nodes per tree
 
 __device__ __forceinline__ uint4 ld_nc(const void *ptr) {
@@ -71,35 +74,43 @@ __device__ __forceinline__ uint64_t wscan(uint64_t v, int lane) {
     return v;
 }
 
-// floor(D 2^60 / Z) exactly, for D <= Z < 2^63: an fp64 estimate (error < 2^10), one fp64
-// correction of the 128-bit remainder, then at most a step or two.
-__device__ __forceinline__ uint64_t divfloor60(uint64_t D, uint64_t Z, double inv) {
-    uint64_t qh = (uint64_t)__dmul_rn((double)D, inv);
-    const u128 num = (u128)D << 60;
-    i128 rem = (i128)num - (i128)((u128)qh * Z);
-    const double rd = (double)(int64_t)(rem >> 64) * 0x1p64 + (double)(uint64_t)rem;
-    const int64_t c = (int64_t)floor(rd / (double)Z);
-    qh += (uint64_t)c;
-    rem -= (i128)c * (i128)Z;
-    while (rem < 0) { --qh; rem += (i128)Z; }
-    while (rem >= (i128)Z) { ++qh; rem -= (i128)Z; }
-    return qh;
-}
-
-// Stage mass of one entry (AMB-35): D_1 = mass460(p, q); D_{s+1} = max(0, floor(D_s 2^60 /
-// Z_s) - floor(q 2^60)).  stage 0: the row p alone (bonus / fallback / draft sampling).
+// Stage mass of one entry (AMB-35): D_1 = mass460(p, q); D_{s+1} = floor(max(0, D_s 2^60 -
+// Z_s floor(q 2^60)) / 2^b(Z_s)).  stage 0: the row p alone (bonus / fallback / draft).
 struct StageMass {
     int stage;
     const uint64_t *Zs;      // shared: Z_1..Z_{stage-1}
-    const double *inv;       // shared: 2^60 / Z_s
+    const int *zb;           // shared: their bit lengths
     __device__ __forceinline__ uint64_t operator()(float p, float q) const {
         if (stage == 0) return mass460(p, 0.0f);
         uint64_t D = mass460(p, q);
         if (stage == 1) return D;
         const uint64_t Q = mass460(q, 0.0f);
         for (int s = 1; s < stage; ++s) {
-            const uint64_t n = divfloor60(D, Zs[s], inv[s]);
-            D = n > Q ? n - Q : 0;
+            const u128 a = (u128)D << 60, b = (u128)Zs[s] * Q;
+            D = a > b ? (uint64_t)((a - b) >> zb[s]) : 0;
+        }
+        return D;
+    }
+};
+
+// The same stage mass with the stage a compile-time constant S (1..4) and Z_s / b(Z_s) in
+// registers: the chain unrolls without branches or shared-memory loads per entry.
+template <int S>
+struct StageMassT {
+    uint64_t z[S];
+    int zb[S];
+    __device__ __forceinline__ StageMassT(const uint64_t *Zs, const int *b) {
+#pragma unroll
+        for (int s = 1; s < S; ++s) { z[s] = Zs[s]; zb[s] = b[s]; }
+    }
+    __device__ __forceinline__ uint64_t operator()(float p, float q) const {
+        uint64_t D = mass460(p, q);
+        if (S == 1) return D;
+        const uint64_t Q = mass460(q, 0.0f);
+#pragma unroll
+        for (int s = 1; s < S; ++s) {
+            const u128 a = (u128)D << 60, b = (u128)z[s] * Q;
+            D = a > b ? (uint64_t)((a - b) >> zb[s]) : 0;
         }
         return D;
     }
@@ -114,7 +125,8 @@ __device__ uint64_t row_pass(const char *prow, const char *qrow, int64_t V, cons
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nseg = (int)((V + kSegElems - 1) / kSegElems);
     uint64_t mine = 0;
-    for (int s = warp; s < nseg; s += kRowWarps) {
+    const int nwarps = (int)(blockDim.x >> 5);
+    for (int s = warp; s < nseg; s += nwarps) {
         const int64_t base = (int64_t)s * kSegElems;
         uint4 pv[J], qv[J];
 #pragma unroll
@@ -141,6 +153,14 @@ __device__ uint64_t row_pass(const char *prow, const char *qrow, int64_t V, cons
     __syncthreads();
     return Z;
 }
+
+// row_pass / row_search for a runtime stage: compile-time chains for stages 0..4.
+template <bool BF16>
+__device__ uint64_t stage_pass(const char *prow, const char *qrow, int64_t V, int stage, const uint64_t *Zs,
+                               const int *zb, uint64_t *seg, uint64_t *s_tot);
+template <bool BF16>
+__device__ int stage_search(const char *prow, const char *qrow, int64_t V, int stage, const uint64_t *Zs,
+                            const int *zb, const uint64_t *seg, uint64_t t);
 
 // Warp 0: y = min{v : sum_{w<=v} mass_w > t} for t < Z, from the segment sums and one rescan.
 template <bool BF16, class MassF>
@@ -198,6 +218,31 @@ __device__ int row_search(const char *prow, const char *qrow, int64_t V, const M
     return (int)(V - 1);   // unreachable for t < Z
 }
 
+template <bool BF16>
+__device__ uint64_t stage_pass(const char *prow, const char *qrow, int64_t V, int stage, const uint64_t *Zs,
+                               const int *zb, uint64_t *seg, uint64_t *s_tot) {
+    switch (stage) {
+    case 0: return row_pass<BF16>(prow, nullptr, V, StageMass{0, nullptr, nullptr}, seg, s_tot);
+    case 1: return row_pass<BF16>(prow, qrow, V, StageMassT<1>(Zs, zb), seg, s_tot);
+    case 2: return row_pass<BF16>(prow, qrow, V, StageMassT<2>(Zs, zb), seg, s_tot);
+    case 3: return row_pass<BF16>(prow, qrow, V, StageMassT<3>(Zs, zb), seg, s_tot);
+    case 4: return row_pass<BF16>(prow, qrow, V, StageMassT<4>(Zs, zb), seg, s_tot);
+    default: return row_pass<BF16>(prow, qrow, V, StageMass{stage, Zs, zb}, seg, s_tot);
+    }
+}
+template <bool BF16>
+__device__ int stage_search(const char *prow, const char *qrow, int64_t V, int stage, const uint64_t *Zs,
+                            const int *zb, const uint64_t *seg, uint64_t t) {
+    switch (stage) {
+    case 0: return row_search<BF16>(prow, nullptr, V, StageMass{0, nullptr, nullptr}, seg, t);
+    case 1: return row_search<BF16>(prow, qrow, V, StageMassT<1>(Zs, zb), seg, t);
+    case 2: return row_search<BF16>(prow, qrow, V, StageMassT<2>(Zs, zb), seg, t);
+    case 3: return row_search<BF16>(prow, qrow, V, StageMassT<3>(Zs, zb), seg, t);
+    case 4: return row_search<BF16>(prow, qrow, V, StageMassT<4>(Zs, zb), seg, t);
+    default: return row_search<BF16>(prow, qrow, V, StageMass{stage, Zs, zb}, seg, t);
+    }
+}
+
 __device__ __forceinline__ uint64_t philox_u64(uint32_t req, uint32_t rnd, uint32_t c2, uint32_t trace,
                                                uint64_t seed) {
     const uint4 u = philox4x32_10(make_uint4(req, rnd, c2, trace), (uint32_t)seed, (uint32_t)(seed >> 32));
@@ -216,7 +261,7 @@ __global__ void __launch_bounds__(kRowThreads) draft_sample_kernel(const char *q
     const int64_t row = row_idx ? row_idx[r] : r;
     const char *qrow = q + row * V * RowElt<BF16>::kEsz;
     const StageMass m{0, nullptr, nullptr};
-    const uint64_t Z = row_pass<BF16>(qrow, nullptr, V, m, seg, &s_tot);
+    const uint64_t Z = row_pass<BF16>(qrow, nullptr, V, m, seg, &s_tot);   // (draft: stage 0 = the row)
     if (threadIdx.x >= 32) return;
     int x = 0;
     if (Z) {
@@ -246,7 +291,7 @@ __device__ __forceinline__ bool tree_accept(uint32_t u24, float qx, uint64_t Dx,
 }
 
 template <bool BF16>
-__global__ void __launch_bounds__(kRowThreads) tree_verify_kernel(const char *p, const char *q, int64_t V,
+__global__ void __launch_bounds__(kTreeThreads, 512 / kTreeThreads) tree_verify_kernel(const char *p, const char *q, int64_t V,
                                                                   int32_t n_nodes, const int32_t *parent,
                                                                   const int32_t *token, const uint32_t *req_id,
                                                                   const uint32_t *round_idx, uint64_t seed,
@@ -256,7 +301,7 @@ __global__ void __launch_bounds__(kRowThreads) tree_verify_kernel(const char *p,
     __shared__ uint64_t seg[kMaxSegs];
     __shared__ uint64_t s_tot;
     __shared__ uint64_t s_Zs[kTreeMax + 1];
-    __shared__ double s_inv[kTreeMax + 1];
+    __shared__ int s_zb[kTreeMax + 1];
     __shared__ int s_par[kTreeMax], s_tok[kTreeMax], s_dep[kTreeMax], s_ch[kTreeMax];
     __shared__ int s_ok, s_w, s_acc;
     const int b = blockIdx.x, n = n_nodes;
@@ -322,7 +367,7 @@ __global__ void __launch_bounds__(kRowThreads) tree_verify_kernel(const char *p,
                                                    (uint32_t)(seed >> 32));
                     const int l = (i - 1) & 3;
                     const uint32_t wv = l == 0 ? r4.x : l == 1 ? r4.y : l == 2 ? r4.z : r4.w;
-                    const StageMass m{i, s_Zs, s_inv};
+                    const StageMass m{i, s_Zs, s_zb};
                     acc = tree_accept(wv >> 8, qx, m(px, qx), s_Zs[i]);
                 }
                 s_acc = acc;
@@ -330,12 +375,11 @@ __global__ void __launch_bounds__(kRowThreads) tree_verify_kernel(const char *p,
             __syncthreads();
             if (s_acc) { next = s_ch[i]; break; }
             // D_{i+1} and its total (the segment sums stay for a final draw from it)
-            const StageMass m{i + 1, s_Zs, s_inv};
-            const uint64_t Z = row_pass<BF16>(prow, qrow, V, m, seg, &s_tot);
+            const uint64_t Z = stage_pass<BF16>(prow, qrow, V, i + 1, s_Zs, s_zb, seg, &s_tot);
             stage = i + 1;
             if (threadIdx.x == 0) {
                 s_Zs[stage] = Z;
-                s_inv[stage] = Z ? __ddiv_rn(0x1p60, (double)Z) : 0.0;
+                s_zb[stage] = 64 - __clzll((long long)Z);
             }
             __syncthreads();
             if (Z == 0) { fallback = true; break; }   // AMB-20: no residual mass
@@ -353,18 +397,18 @@ __global__ void __launch_bounds__(kRowThreads) tree_verify_kernel(const char *p,
         // the emitted token: from D_stage (every child rejected), else from the row p_u
         // (a leaf's bonus token or the AMB-20 fallback)
         uint64_t Z;
-        StageMass m{stage, s_Zs, s_inv};
+        int st_draw = stage;
         if (stage > 0 && !fallback) {
             Z = s_Zs[stage];
         } else {
-            m.stage = 0;
-            Z = row_pass<BF16>(prow, nullptr, V, m, seg, &s_tot);
+            st_draw = 0;
+            Z = stage_pass<BF16>(prow, nullptr, V, 0, s_Zs, s_zb, seg, &s_tot);
         }
         if (threadIdx.x < 32) {
             int y = 0;
             if (Z) {
                 const uint64_t U = philox_u64(req, rnd, 1u << 8, trace, seed);
-                y = row_search<BF16>(prow, m.stage ? qrow : nullptr, V, m, seg, __umul64hi(U, Z));
+                y = stage_search<BF16>(prow, qrow, V, st_draw, s_Zs, s_zb, seg, __umul64hi(U, Z));
             }
             if (threadIdx.x == 0) {
                 tok_o[nacc] = y;
@@ -398,11 +442,11 @@ cudaError_t launch_verify_tree(const void *p, const void *q, int32_t dtype, int6
                                int32_t *path, int32_t *n_accept, uint64_t *z_out, cudaStream_t s) {
     if (B <= 0) return cudaSuccess;
     if (dtype == LAPSSD_BF16)
-        tree_verify_kernel<true><<<B, kRowThreads, 0, s>>>((const char *)p, (const char *)q, V, n_nodes, parent,
+        tree_verify_kernel<true><<<B, kTreeThreads, 0, s>>>((const char *)p, (const char *)q, V, n_nodes, parent,
                                                            token, req, rnd, seed, trace, tokens, path, n_accept,
                                                            z_out);
     else
-        tree_verify_kernel<false><<<B, kRowThreads, 0, s>>>((const char *)p, (const char *)q, V, n_nodes, parent,
+        tree_verify_kernel<false><<<B, kTreeThreads, 0, s>>>((const char *)p, (const char *)q, V, n_nodes, parent,
                                                             token, req, rnd, seed, trace, tokens, path, n_accept,
                                                             z_out);
     count_launch();

@@ -42,7 +42,7 @@ MUTANTS = {
     "switch_in_E": ("s->switch_us[i] += c;", "s->switch_us[i] += c; s->E[i] += c;"),
     "no_semi": [("f.nonperc = !s->perceptible[i];", "f.nonperc = 1;"),
                 ("f.secondary = sat32(estimate(s, L_rem, s->A[i]));", "f.secondary = 0;")],
-    "tree_no_renorm": ("uint64_t n = (uint64_t)(((u128)D << 60) / c->Zs[s]);", "uint64_t n = D;"),
+    "tree_no_renorm": ("u128 a = (u128)D << 60, b = (u128)c->Zs[s] * Q;", "u128 a = (u128)D << 60, b = (u128)Q << 60;"),
     "tree_stage_p": ("accept = tree_accept(u24, qx, tree_mass(&c, x), Zs[i]);",
                      "accept = (double)u24 * (double)qx < (double)load_prob(p_rows, dtype, off + x) * 16777216.0;"),
     "tree_draw_p": ("if (stage > 0 && !fallback) {", "if (0) {"),
