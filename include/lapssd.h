@@ -34,7 +34,9 @@
  *    that lapssd_check() reports as LAPSSD_ESTATE.
  *  - A handle is bound to one stream at a time and is not thread-safe.
  *  - Times are integer microseconds (int64).  Probabilities are float32 or bf16
- *    in [0, 1]; each stored row of p is expected to sum to about 1.
+ *    in [0, 1]; each stored row of p is expected to sum to about 1 (a verified row pair
+ *    whose residual mass exceeds 2 sets device flag 256, see lapssd_check; full
+ *    validation: lapssd_set_row_check).
  */
 #ifndef LAPSSD_H
 #define LAPSSD_H
@@ -321,6 +323,14 @@ lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, in
  * laps_step_dist verify launches (programmatic dependent launch; contract above).
  * Errors: EINVAL (NULL handle). */
 lapssd_status lapssd_set_step_overlap(lapssd_handle *h, int32_t enable);
+/* Row validation (default off): with enable = 1 the verify kernel of laps_step /
+ * laps_step_dist also checks every streamed row pair's residual mass and sets device flag
+ * 256 (lapssd_check) for rows that are not probabilities (a vector of 8 entries or a lane
+ * of 32 with mass >= 2, five lanes of a 1,024-entry segment with >= 0.25 each, or a segment
+ * >= 4): such masses never wrap silently into the integer sums.  Costs ~4 % of the step
+ * (measured).  Independently of it, a row pair whose total residual mass exceeds 2 always
+ * sets flag 256.  Errors: EINVAL (NULL handle). */
+lapssd_status lapssd_set_row_check(lapssd_handle *h, int32_t enable);
 
 /* ---------------------------------------------------------------------------
  * Multi-GPU (a8): requests are sharded by global id mod world; every rank keeps the
@@ -387,8 +397,9 @@ lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *host_out,
  * of a completed request, 2 a row with no probability mass, 4 a slot naming a bad
  * request / slab, 8 a descriptor that does not match the batch, 16 a device-side
  * watchdog expired (results invalid) with 32 / 64 / 128 naming the wait (verify
- * finisher / select merge / verify snapshot); lapssd_last_error() then reports the
- * step and slot of the first expiry. */
+ * finisher / select merge / verify snapshot), 256 a row pair whose residual mass exceeds 2
+ * (rows that are not probabilities: the integer sums are invalid, never silently wrapped);
+ * lapssd_last_error() then reports the step and slot of the first expiry. */
 lapssd_status lapssd_check(lapssd_handle *h, uint32_t *flags_out);
 
 /* Per-kernel timing of laps_step for the next max_steps calls: the library records

@@ -81,6 +81,7 @@ def _load():
         "laps_select": ([vp, i32, vp, vp, vp], i32),
         "laps_step": ([vp, vp, i32, vp, vp, vp, vp, vp], i32),
         "lapssd_set_step_overlap": ([vp, i32], i32),
+        "lapssd_set_row_check": ([vp, i32], i32),
         "laps_candidates": ([vp, i32, vp, vp], i32),
         "laps_merge": ([vp, vp, i32, i32, vp, vp, vp], i32),
         "laps_step_dist": ([vp, vp, vp, i32, i32, vp, vp, vp, vp], i32),
@@ -306,6 +307,10 @@ class Handle:
         self.count = torch.zeros(1, dtype=torch.int32, device=device)
         if overlap:
             self.set_step_overlap(True)
+
+    def set_row_check(self, enable: bool):
+        """lapssd_set_row_check: validate the streamed rows' masses (device flag 256)."""
+        _check("lapssd_set_row_check", _lib.lapssd_set_row_check(self.h, 1 if enable else 0))
 
     def set_step_overlap(self, enable: bool):
         """lapssd_set_step_overlap: consecutive verify launches overlap (the caller does not

@@ -104,6 +104,7 @@ struct lapssd_handle {
     // dependent launch).  Off by default: the verify kernel then follows all prior work on
     // the caller's stream (a rows-producing kernel of the caller, say).
     bool overlap = false;
+    bool check_rows = false;   // lapssd_set_row_check
     cudaStream_t chain_stream = nullptr;
     lapssd_rows last_rows{};  // rows of the previous laps_step (epoch changes with them)
     uint32_t rows_epoch = 1;
@@ -505,6 +506,7 @@ static lapssd_status fill_step_verify(lapssd_handle *h, const lapssd_rows *rows,
     a.z = nullptr;
     a.part = h->part; a.work = h->work;
     a.fuse_update = 1;
+    a.check_rows = h->check_rows;
     a.st = h->st; a.sc = h->sc;
     a.err = &h->st.g->err;
     (void)B;
@@ -633,6 +635,13 @@ lapssd_status lapssd_set_step_overlap(lapssd_handle *h, int32_t enable) {
     g_last_error.clear();
     if (!h) return fail(LAPSSD_EINVAL, "handle is NULL");
     h->overlap = enable != 0;
+    return LAPSSD_OK;
+}
+
+lapssd_status lapssd_set_row_check(lapssd_handle *h, int32_t enable) {
+    g_last_error.clear();
+    if (!h) return fail(LAPSSD_EINVAL, "handle is NULL");
+    h->check_rows = enable != 0;
     return LAPSSD_OK;
 }
 

@@ -38,6 +38,7 @@ enum : uint32_t {
     E_TO_FIN = 32u,        // ... the verify finisher's wait for a slot's segment sums
     E_TO_MERGE = 64u,      // ... the side select's wait for the verified slots' records
     E_TO_SNAP = 128u,      // ... the side select's wait for the verify CTAs' snapshots
+    E_MASS = 256u,         // a row pair with residual mass > 2 (not probability rows): sums invalid
 };
 
 // Watchdog for device-side spin waits: true once `t0` is more than 2 s in the past.
@@ -523,6 +524,7 @@ struct VerifyArgs {
     // +1 per CTA (release) once it has read all it needs of desc[] / sel[]; the side
     // select overwrites those only after every CTA has signalled (nullable)
     uint32_t *snap;
+    int32_t check_rows;         // validate the rows' masses in the consumers (E_MASS)
 };
 
 enum : uint32_t { E_STALE_DESC = 8u };

@@ -487,11 +487,15 @@ __device__ __forceinline__ void sample_slot_warp(const VerifyArgs &a, uint64_t *
     // chunk sums: cs0 for chunk lane, cs1 for chunk lane + 32 (fp32 tiling only)
     uint64_t cs0 = 0, cs1 = 0;
 #pragma unroll
+    uint64_t za = 0;   // Z / 16, which cannot wrap: the row mass check (E_MASS)
+#pragma unroll
     for (int x = 0; x < kPartWords; ++x) {
         w[x] &= ~kReady;
         if (x < kSegs) cs0 += w[x]; else cs1 += w[x];
+        za += w[x] >> 4;
     }
     uint64_t Z = warp_sum_u64(cs0 + cs1);
+    if ((warp_sum_u64(za) >> 57) != 0 && lane == 0 && a.err) atomicOr(a.err, E_MASS);   // mass > 2
     if (lane == 0) TRACE(9, b);
     bool fallback = false;
     if (Z == 0 && use_q) {  // no residual mass while rejecting: the row p_r itself
@@ -664,7 +668,8 @@ __device__ __forceinline__ void issue_item(const VerifyArgs &a, uint8_t *s_tiles
     }
 }
 
-template <bool BF16>
+// CHECK: the consumers also validate the rows' masses (E_MASS; lapssd_set_row_check).
+template <bool BF16, bool CHECK>
 __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_constant__ VerifyArgs a,
                                                                     int32_t B) {
     using E = Elt<BF16>;
@@ -895,7 +900,7 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                     // arithmetic, so the refill's latency overlaps this item's math
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[st]);
-                    uint64_t m = 0;
+                    uint64_t m = 0, hi = 0;
 #if defined(LAPSSD_DIAG) && (LAPSSD_DIAG & 1)
                     if (pv[0].x == 0x7FFFFFFFu && qv[0].y == 1u) m = 1;  // diagnostic build: no residual math
 #else
@@ -907,10 +912,27 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                         const uint4 qm = in ? make_uint4(qv[j].x & qmask.x, qv[j].y & qmask.y, qv[j].z & qmask.z,
                                                          qv[j].w & qmask.w)
                                             : z;
-                        m += E::mass(pm, qm);
+                        const uint64_t x = E::mass(pm, qm);
+                        m += x;
+                        hi |= x;
                     }
 #endif
+                    // (CHECK) Rows of probabilities (entries in [0, 1], row mass ~1) give vector masses
+                    // < 2^61, lane sums < 2^61 and segment sums < 2^62; an invalid row is flagged
+                    // (E_MASS), never wrapped silently into the sums or the ready bit: a lane
+                    // sum cannot wrap unless some vector mass >= 2^61, and the butterfly cannot
+                    // unless >= 5 lanes hold >= 2^58 (then the segment's mass exceeds 1.25).
+                    hi |= m;
+                    bool bad = false;
+                    if (CHECK) {
+                        const unsigned heavy = __ballot_sync(0xFFFFFFFFu, (m >> 58) != 0);
+                        bad = __any_sync(0xFFFFFFFFu, (hi >> 61) != 0) || __popc(heavy) >= 5;
+                    }
                     m = warp_sum_u64(m);
+                    if (CHECK) {
+                        bad |= (m >> 62) != 0;
+                        if (bad && lane == 0 && a.err) atomicOr(a.err, E_MASS);
+                    }
                     if (lane == 0) st_relaxed(&part[((int64_t)b * nc + c) * kPartWords + seg], m | kReady);
                 }
             }
@@ -933,8 +955,10 @@ static int g_verify_grid = 0;  // SM count, set once by verify_prepare
 template <bool BF16>
 static void verify_prepare_t() {
     const size_t smem = (size_t)VerifyCfg<BF16>::kStages * 2 * kTileBytes;
-    cudaFuncSetAttribute(verify_kernel<BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(verify_kernel<BF16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(verify_kernel<BF16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(verify_kernel<BF16, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(verify_kernel<BF16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(verify_kernel<BF16, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 // Once per process, before any launch (see sched_prepare).
@@ -988,7 +1012,8 @@ static cudaError_t launch_verify_t(const VerifyArgs &a, int32_t B, int32_t reser
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = pdl ? attr : nullptr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, verify_kernel<BF16>, a, B);
+    return a.check_rows ? cudaLaunchKernelEx(&cfg, verify_kernel<BF16, true>, a, B)
+                        : cudaLaunchKernelEx(&cfg, verify_kernel<BF16, false>, a, B);
 }
 
 cudaError_t launch_verify_grid(const VerifyArgs &a, int32_t B, int32_t reserve_sms, bool pdl, cudaStream_t s) {

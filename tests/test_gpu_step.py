@@ -380,3 +380,41 @@ def test_step_parity_admission_burst(L, burst):
     pool = synth.make_pool("f2", V=2048, k=4, dtype="bf16", n_buckets=8, variants=3, seed=burst, device="cuda")
     tab = synth.slab_table(tr, 8, 3, R=16, seed=burst)
     run_lockstep(L, dict(BASE, k=4, seed=33), tr, pool, tab, B=32, check_every=2, overlap=True)
+
+
+def test_unnormalised_rows_set_the_mass_flag(L):
+    """Rows that are not probabilities (every entry 0.5: mass V/2) must not wrap silently
+    into the uint64 segment sums: lapssd_check reports ESTATE with flag 256 (E_MASS)."""
+    tr, pool, tab = workload(20, 4096, 4, "bf16", seed=3, drift=False)
+    kw = dict(BASE, k=4, seed=7)
+    B = 4
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=pool.V)
+    h.set_row_check(True)
+    h.laps_select(B)
+    p = torch.full((B, 5, 4096), 0.5, dtype=torch.bfloat16, device="cuda")
+    q = torch.zeros(B, 4, 4096, dtype=torch.bfloat16, device="cuda")
+    d = torch.zeros(B, 4, dtype=torch.int32, device="cuda")
+    h.laps_step(L.Rows(p, q, d, None), B)
+    with pytest.raises(L.LapssdError) as e:
+        h.check()
+    assert "0x100" in str(e.value) or e.value.status == -4
+    # valid rows of the same shape do not set it
+    h2 = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=pool.V)
+    h2.set_row_check(True)
+    h2.laps_select(B)
+    h2.laps_step(L.Rows(torch.full_like(p, 1 / 4096), q, d, None), B)
+    assert h2.check() == 0
+
+
+def test_unnormalised_rows_flagged_without_the_row_check(L):
+    """Without lapssd_set_row_check the finisher's total-mass check still flags a row
+    pair whose residual mass exceeds 2 (rows of 0.25: V/4 per row, no lane wraps)."""
+    tr, pool, tab = workload(20, 4096, 4, "bf16", seed=4, drift=False)
+    h = L.Handle(L.SchedConfig(**dict(BASE, k=4, seed=7)), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=4,
+                 V=4096)
+    h.laps_select(4)
+    p = torch.full((4, 5, 4096), 1 / 512, dtype=torch.bfloat16, device="cuda")   # mass 8 per row
+    h.laps_step(L.Rows(p, torch.zeros(4, 4, 4096, dtype=torch.bfloat16, device="cuda"),
+                       torch.zeros(4, 4, dtype=torch.int32, device="cuda"), None), 4)
+    with pytest.raises(L.LapssdError):
+        h.check()
