@@ -67,16 +67,21 @@ def parse():
     ap.add_argument("--dist-path", action="store_true",
                     help="N=1 only: time the N>1 step (laps_step_dist) with a one-rank NCCL communicator")
     ap.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "verify_dram.json"))
-    ap.add_argument("--workload", choices=["c4", "mc", "logits", "draft", "tree"], default="c4",
+    ap.add_argument("--workload", choices=["c4", "mc", "logits", "draft", "tree", "c2", "c3"], default="c4",
                     help="c4 = configs[3] (the headline); mc = configs[4] Monte-Carlo traces; "
                     "logits = SURVEY 8(f) f1, spec_verify_logits at configs[3] dimensions; "
-                    "draft / tree = SURVEY 8(f) f4, spec_draft_sample / spec_verify_tree")
+                    "draft / tree = SURVEY 8(f) f4, spec_draft_sample / spec_verify_tree; "
+                    "c2 / c3 = configs[1] / configs[2] at full size, run to completion with oracle parity")
     ap.add_argument("--tree-nodes", type=int, default=16, help="f4 tree: nodes per request")
     ap.add_argument("--tree-width", type=int, default=3, help="f4 tree: max children per node")
     ap.add_argument("--mc-traces", type=int, default=8192, help="configs[4]: traces (whole job)")
     ap.add_argument("--mc-n", type=int, default=512, help="configs[4]: requests per trace")
     ap.add_argument("--mc-variants", type=int, default=256, help="configs[4]: slab variants per bucket")
-    ap.add_argument("--mc-policies", default="", help="comma list of policies run to completion "
+    ap.add_argument("--rho", type=float, default=None, help="c2 / c3: offered load (default: the config's)")
+    ap.add_argument("--policy", type=int, default=0, help="c2 / c3: scheduling policy (0 LAPS-SD, 1 FCFS, "
+                    "2 LP-SJF, 3 LAS)")
+    ap.add_argument("--no-parity", action="store_true", help="c2 / c3: skip the oracle run")
+    ap.add_argument("--mc-policies", default="0", help="comma list of policies run to completion "
                     "for mean JCT (e.g. 0,1,2,3; empty: throughput only)")
     return ap.parse_args()
 
@@ -1007,6 +1012,99 @@ def run_f4(args):
         dist.destroy_process_group()
 
 
+def run_c23(args):
+    """configs[1] (1,024 requests, Poisson, Beta(4,2), V=32,000, k=4, fp32, B=64) or
+    configs[2] (4,096 requests, drifting acceptance, V=32,000, k=6, bf16, B=64), full size
+    on one GPU: the whole trace through laps_step to completion (eager calls: the run's
+    length depends on the outcome), then the same trace through the oracle (its OpenMP
+    build) and every request's final state compared bit for bit.  value = verified draft
+    tokens per second of the GPU run; the line also carries the mean JCT."""
+    import paper_2505_17074_b200 as L
+    name = "c2" if args.workload == "c2" else "c3"
+    c = synth.CONFIGS[name]
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    rho = args.rho or c["rho"]
+    tr = synth.make_config_trace(name, rho=rho)
+    pool = synth.make_pool("f2", V=c["V"], k=c["k"], dtype=c["dtype"], n_buckets=64, variants=c["variants"],
+                           seed=c["seed"], device=dev)
+    tab = synth.slab_table(tr, 64, c["variants"], R=32, seed=c["seed"])
+    kw = dict(K=c["K"], s1_up_us=4 * (c["k"] * 1000 + 10_000), M=2.0, gamma=5, delta=0.05, k=c["k"],
+              t_ssm_us=1000, t_llm_us=10_000, policy=args.policy, seed=c["seed"])
+    B = c["B"]
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=c["V"], overlap=True)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device=dev))
+    h.laps_select(B)
+    cnt = h.count
+    # warm-up of the kernels on a throwaway handle (same shapes)
+    hw = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=c["V"], overlap=True)
+    hw.laps_select(B)
+    for _ in range(max(args.warmup, 3)):
+        hw.laps_step(rows, B)
+    torch.cuda.synchronize()
+    del hw
+    clocks = Clocks(0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = 0
+    clocks.start()
+    e0.record()
+    while True:
+        for _ in range(64):                  # 64 steps between host checks of completion
+            h.laps_step(rows, B)
+        steps += 64
+        done = h.state()["done"]
+        if done.all() or steps > 10_000_000:
+            break
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    st = h.state()
+    assert h.check() == 0
+    verified = int(st["rounds"].sum())
+    jct = (st["C_us"] - tr.arrival_us).astype(np.float64)
+    out = {"metric": METRIC, "value": verified * c["k"] / (ms * 1e-3), "unit": UNIT, "n_gpus": 1,
+           "steps": steps, "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None,
+           "dtype": f"{c['dtype']} rows; fp32 residual + exact Q4.60 integer CDF; fp64 scheduler",
+           "data": "synthetic",
+           "config": {"workload": f"configs[{1 if name == 'c2' else 2}] at full size: {c['n']} requests, "
+                                  f"Poisson arrivals at rho={rho}, B={B}, V={c['V']}, k={c['k']}, {c['dtype']}, "
+                                  f"{'drifting ' if c['drift'] else ''}Beta(4,2) acceptance, policy {args.policy}, "
+                                  "run to completion (steps include the idle tail's host checks)",
+                      "n": c["n"], "B": B, "V": c["V"], "k": c["k"], "rho": rho, "policy": args.policy,
+                      "l2": f"{pool.S * (2 * c['k'] + 1) * c['V'] * (2 if c['dtype'] == 'bf16' else 4) / 1e9:.1f} "
+                            "GB slab pool"},
+           "verified_per_step": verified / steps, "clocks": clk,
+           "jct": {"mean_ms": float(jct.mean() / 1e3), "p99_ms": float(np.percentile(jct, 99) / 1e3),
+                   "sim_makespan_s": float(st["now_us"] / 1e6), "perceptible_frac": float(st["perceptible"].mean())}}
+    if not args.no_parity:
+        import oracle
+        P = pool.numpy()
+        P["slab_tab"], P["R"] = tab, tab.shape[1]
+        sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, parallel=True)
+        sel, _ = sim.select(B)
+        t0 = time.perf_counter()
+        n_o = 0
+        while not sim.state()["done"].all():
+            sim.step(P, sel)
+            n_o += 1
+        el = time.perf_counter() - t0
+        o = sim.state()
+        fields = ("acc_tok", "acc_draft", "rounds", "E_us", "T_total_us", "C_us", "x_us", "level", "perceptible",
+                  "pinned", "key")
+        diff = [f for f in fields if not (np.asarray(st[f]) == np.asarray(o[f])).all()]
+        out["parity"] = {"oracle_steps": n_o, "fields_compared": list(fields) + ["A (bits)", "now_us"],
+                         "mismatched": diff + ([] if (st["A"].view(np.uint64) == o["A"].view(np.uint64)).all()
+                                               else ["A"]) + ([] if st["now_us"] == o["now_us"] else ["now_us"]),
+                         "bit_exact": not diff and st["now_us"] == o["now_us"]
+                         and bool((st["A"].view(np.uint64) == o["A"].view(np.uint64)).all())}
+        out["cpu_baseline"] = {"value": int(o["rounds"].sum()) * c["k"] / el, "unit": UNIT, "cores": omp_threads(),
+                               "kind": "oracle", "sample": f"the whole trace ({n_o} steps), oracle/lapssd_oracle.c "
+                               f"-fopenmp build, {el:.1f} s", "host": host_info()}
+    print(json.dumps(out), flush=True)
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle, as it stands, timed on this host's cores on the
     same config / metric; each step a bounded sample (a smaller batch) of the workload."""
@@ -1066,6 +1164,8 @@ def main():
         run_logits(args)
     elif args.workload in ("draft", "tree"):
         run_f4(args)
+    elif args.workload in ("c2", "c3"):
+        run_c23(args)
     elif args.workload == "mc":
         run_mc(args)
     else:
