@@ -65,7 +65,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-path", action="store_true",
-                    help="N=1 only: time the N>1 step (laps_step_dist) with a one-rank NCCL communicator")
+                    help="N=1 only: time the NCCL form of the N>1 step (laps_step_dist) with a one-rank communicator")
+    ap.add_argument("--peer-path", action="store_true",
+                    help="N=1 only: time the N>1 step (laps_step_peer, exchange fused over peer memory) with one rank")
+    ap.add_argument("--nccl-exchange", action="store_true",
+                    help="N>1: laps_step_dist (candidates -> ncclAllGather -> merge kernel) instead of laps_step_peer")
     ap.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "verify_dram.json"))
     ap.add_argument("--workload", choices=["c4", "mc", "logits", "draft", "tree", "c2", "c3"], default="c4",
                     help="c4 = configs[3] (the headline); mc = configs[4] Monte-Carlo traces; "
@@ -216,14 +220,27 @@ def run_ours(args):
     tab_d = torch.as_tensor(tab, device=dev)
     rows = L.Rows(pool.p, pool.q, pool.draft, tab_d)
     comm = cand = None
+    peer = False
     Cn = min(B, args.n_per_gpu)
     W = 2 * Cn + 1                             # candidate block: keys, switch costs, next arrival
     if world > 1:
-        comm = L.nccl_comm()
         cand = torch.zeros((world + 1) * W, dtype=torch.int64, device=dev)
         h.laps_candidates(Cn, cand[:W])
         dist.all_gather_into_tensor(cand[W:], cand[:W])
         h.laps_merge(cand[W:], Cn, B)
+        if args.nccl_exchange:
+            comm = L.nccl_comm()
+        else:   # the exchange fused into the select kernel over NVLink peer memory
+            h.set_peers(Cn)
+            peer = True
+    elif args.peer_path:
+        cand = torch.zeros(2 * W, dtype=torch.int64, device=dev)
+        h.laps_candidates(Cn, cand[:W])
+        cand[W:].copy_(cand[:W])
+        h.laps_merge(cand[W:], Cn, B)
+        h.set_peers(Cn)
+        peer = True
+        args.no_profile = True
     elif args.dist_path:
         # the N>1 step (laps_step_dist: candidates + ncclAllGather + merge) on one rank, to
         # time its cost on the one GPU available; a one-rank gloo group only carries the
@@ -247,7 +264,9 @@ def run_ours(args):
     scratch_row = args.warmup + args.steps
 
     def step(t):
-        if comm is not None:
+        if peer:
+            h.laps_step_peer(rows, B)
+        elif comm is not None:
             h.laps_step_dist(comm, rows, B, Cn, cand)
         else:
             h.laps_step(rows, B, n_accept=hist[t])
@@ -345,8 +364,12 @@ def run_ours(args):
                       "B_per_gpu": B_local, "B_global": B, "V": args.V, "k": args.k,
                       "pool": f"F2 zipf, {pool.S} slabs x {(2 * args.k + 1) * args.V * 2 / 1e6:.2f} MB",
                       "l2": "inputs larger than L2 (4.5 GB slab pool, ~255 MB of rows per step)",
-                      "parallelism": f"dp{world}: requests sharded by id mod {world}" + ("; laps_step_dist path" if comm is not None and world == 1 else "")
-                      + ("; global top-B via NCCL all-gather of candidate keys" if world > 1 else "")},
+                      "parallelism": f"dp{world}: requests sharded by id mod {world}"
+                      + ("; laps_step_dist path" if comm is not None and world == 1 else "")
+                      + ("; laps_step_peer path" if peer and world == 1 else "")
+                      + ("; global top-B via NCCL all-gather of candidate keys" if world > 1 and comm is not None else "")
+                      + ("; global top-B exchanged inside the select kernel over NVLink peer memory (laps_step_peer)"
+                         if world > 1 and peer else "")},
            "verified_per_step": verified / args.steps, "gpu_launches": launches, "clocks": clk}
     if device_error:
         out["device_error"] = device_error

@@ -363,6 +363,24 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
  * together have the results of laps_step_dist.  Errors: EINVAL, ECUDA. */
 lapssd_status laps_step_candidates(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t C,
                                    int32_t *sel_inout, uint64_t *cand_out, lapssd_stream stream);
+/* laps_step_peer -- the multi-GPU step with the exchange FUSED into the select kernel
+ * over peer memory (NVLink / NVSwitch; no collective launch): the verify kernel as in
+ * laps_step, and beside it the side select builds this rank's candidate block (C keys,
+ * their switch-in costs, its next arrival), stores it into slot `rank` of EVERY rank's
+ * exchange buffer through peer pointers and publishes it with a system-scope release of
+ * the step's tag, waits (acquire, with a watchdog: flags 16 | 512) for all world blocks in
+ * its own buffer, ranks the keys among the world sorted lists and commits this rank's
+ * prefix of the global top-B -- the results of laps_step_dist.  Setup, once per handle:
+ * every rank allocates a ZERO-FILLED device buffer of lapssd_peer_buffer_bytes(world, C)
+ * bytes, the buffers are mapped into every process (CUDA IPC; the binding uses torch's),
+ * and lapssd_set_peers(h, peer_bufs, C, stream) passes the world device pointers valid in
+ * this process (peer_bufs[rank] = its own buffer; [host] array).  The first batch comes
+ * from laps_candidates + an all-gather + laps_merge.  C as below; rows pooled; B_global
+ * <= 4096.  All ranks call laps_step_peer in lockstep.  Errors: EINVAL, ECUDA. */
+size_t lapssd_peer_buffer_bytes(int32_t world, int32_t C);
+lapssd_status lapssd_set_peers(lapssd_handle *h, void *const *peer_bufs, int32_t C, lapssd_stream stream);
+lapssd_status laps_step_peer(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t *sel_inout,
+                             int32_t *count_out, lapssd_stream stream);
 /* C must be the same on every rank and world*C <= 16384: the caller passes
  * C = min(B_global, max over ranks of n_local).  sel_inout has B_global slots.
  * NCCL plumbing without torch internals: rank 0 calls lapssd_nccl_unique_id, the
@@ -397,7 +415,8 @@ lapssd_status lapssd_read_state(lapssd_handle *h, lapssd_state_view *host_out,
  * of a completed request, 2 a row with no probability mass, 4 a slot naming a bad
  * request / slab, 8 a descriptor that does not match the batch, 16 a device-side
  * watchdog expired (results invalid) with 32 / 64 / 128 naming the wait (verify
- * finisher / select merge / verify snapshot), 256 a row pair whose residual mass exceeds 2
+ * finisher / select merge / verify snapshot; 512 with 16: the wait for the peers' candidate
+ * blocks, laps_step_peer), 256 a row pair whose residual mass exceeds 2
  * (rows that are not probabilities: the integer sums are invalid, never silently wrapped);
  * lapssd_last_error() then reports the step and slot of the first expiry. */
 lapssd_status lapssd_check(lapssd_handle *h, uint32_t *flags_out);

@@ -86,6 +86,9 @@ def _load():
         "laps_merge": ([vp, vp, i32, i32, vp, vp, vp], i32),
         "laps_step_dist": ([vp, vp, vp, i32, i32, vp, vp, vp, vp], i32),
         "laps_step_candidates": ([vp, vp, i32, i32, vp, vp, vp], i32),
+        "lapssd_peer_buffer_bytes": ([i32, i32], sz),
+        "lapssd_set_peers": ([vp, vp, i32, vp], i32),
+        "laps_step_peer": ([vp, vp, i32, vp, vp, vp], i32),
         "lapssd_nccl_unique_id": ([vp], i32),
         "lapssd_nccl_comm_init": ([vp, i32, vp, i32], i32),
         "lapssd_nccl_comm_destroy": ([vp], i32),
@@ -369,6 +372,32 @@ class Handle:
         _check("laps_step_candidates", _lib.laps_step_candidates(self.h, C.byref(rows.c), B_global, Cn,
                                                                  _dptr(sel), _dptr(cand_out), _stream(stream)))
         return sel
+
+    def set_peers(self, Cn, group=None, stream=None):
+        """Peer-memory exchange for laps_step_peer: a zero-filled buffer of
+        lapssd_peer_buffer_bytes(world, Cn) per rank, mapped into every process with torch's
+        CUDA IPC (torch.multiprocessing.reductions over torch.distributed), then
+        lapssd_set_peers.  world == 1 needs no process group."""
+        nbytes = int(_lib.lapssd_peer_buffer_bytes(self.world, Cn))
+        own = torch.zeros((nbytes + 7) // 8, dtype=torch.int64, device=self.sel.device)
+        bufs = [own]
+        if self.world > 1:
+            import torch.distributed as dist
+            from torch.multiprocessing.reductions import reduce_tensor
+            objs = [None] * self.world
+            dist.all_gather_object(objs, reduce_tensor(own), group=group)
+            bufs = [own if g == self.rank else fn(*args) for g, (fn, args) in enumerate(objs)]
+            dist.barrier(group=group)
+        self._peer_bufs = bufs                    # keep the mappings alive
+        ptrs = (C.c_void_p * self.world)(*[b.data_ptr() for b in bufs])
+        _check("lapssd_set_peers", _lib.lapssd_set_peers(self.h, ptrs, Cn, _stream(stream)))
+
+    def laps_step_peer(self, rows: Rows, B_global, sel=None, count=None, stream=None):
+        sel = self.sel if sel is None else sel
+        count = self.count if count is None else count
+        _check("laps_step_peer", _lib.laps_step_peer(self.h, C.byref(rows.c), B_global, _dptr(sel), _dptr(count),
+                                                     _stream(stream)))
+        return sel, count
 
     # -- snapshot -----------------------------------------------------------------
     def state(self, stream=None) -> dict:

@@ -113,6 +113,8 @@ struct lapssd_handle {
     uint32_t *snap = nullptr;    // verify CTAs that have read sel/desc (incremental select)
     uint64_t *fin_key = nullptr; // per-slot published keys (~key, 0 = none) of fin[] (incremental select)
     WaitList wl{};               // the side select's persistent waiting list (wl.valid: host-tracked)
+    uint64_t **peer_ptrs = nullptr;  // [device] laps_step_peer: every rank's exchange buffer (kMaxPeers)
+    int32_t peer_C = 0;          // 0: no peers set
     cudaStream_t side = nullptr; // side stream for the presort, fork/join events
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaStream_t last_stream;
@@ -172,6 +174,7 @@ static void carve_handle(Carver &cv, lapssd_handle *h, int32_t n, int32_t gamma,
     h->wl.fresh_key = cv.take<uint64_t>((size_t)max_batch);
     h->wl.meta = cv.take<int32_t>(4);
     h->wl.valid = 0;
+    h->peer_ptrs = cv.take<uint64_t *>(64);
 }
 
 static lapssd_status check_config(const lapssd_config *c) {
@@ -857,6 +860,93 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
     if (!allgather) return fail(LAPSSD_ENCCL, "ncclAllGather not found");
     return step_dist(h, nccl_comm, allgather, rows, B_global, C, sel_inout, count_out, cand_scratch,
                      (cudaStream_t)stream, "laps_step_dist");
+}
+
+size_t lapssd_peer_buffer_bytes(int32_t world, int32_t C) {
+    if (world < 1 || world > 64 || C < 1) return 0;
+    return (size_t)2 * world * (2 * (size_t)C + 2) * sizeof(uint64_t);
+}
+
+lapssd_status lapssd_set_peers(lapssd_handle *h, void *const *peer_bufs, int32_t C, lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || !peer_bufs || C < 1) return fail(LAPSSD_EINVAL, "handle / peer_bufs / C");
+    if (h->sc.world > 64) return fail(LAPSSD_EINVAL, "world > 64");
+    if ((int64_t)h->sc.world * C > sort_capacity()) return fail(LAPSSD_EINVAL, "world*C exceeds %d", sort_capacity());
+    for (int32_t g = 0; g < h->sc.world; ++g)
+        if (!peer_bufs[g] || ((uintptr_t)peer_bufs[g] & 7)) return fail(LAPSSD_EINVAL, "peer buffer %d", g);
+    h->peer_C = C;
+    return cuda_status(cudaMemcpyAsync(h->peer_ptrs, peer_bufs, sizeof(void *) * h->sc.world, cudaMemcpyHostToDevice,
+                                       (cudaStream_t)stream),
+                       "lapssd_set_peers");
+}
+
+lapssd_status laps_step_peer(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t *sel_inout,
+                             int32_t *count_out, lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || B_global < 1 || B_global > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B_global");
+    if (!h->peer_C) return fail(LAPSSD_EINVAL, "no peers set (lapssd_set_peers)");
+    int bp = 1;
+    while (bp < B_global) bp <<= 1;
+    if (!rows || !rows->slab_tab || bp > 4096 || h->peer_C > B_global)
+        return fail(LAPSSD_EINVAL, "laps_step_peer needs pooled rows, B_global <= 4096 and C <= B_global");
+    VerifyArgs a;
+    lapssd_status st = fill_step_verify(h, rows, B_global, sel_inout, nullptr, nullptr, a);
+    if (st != LAPSSD_OK) return st;
+    a.count_dev = &h->st.g->count;   // this rank's slots are [0, count) of the B_global
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last_stream = s;
+    if (!h->desc_valid) {
+        st = cuda_status(launch_accept(a.rows, sel_inout, &h->st, &h->sc, nullptr, nullptr, nullptr, h->sc.seed, 0,
+                                       B_global, h->desc, s), "accept");
+        if (st != LAPSSD_OK) return st;
+    }
+    // as laps_step: after a peer step on the same stream the side stream is chained (its
+    // select follows the previous select, which committed everything this one reads)
+    cudaStreamCaptureStatus cap_s = cudaStreamCaptureStatusNone, cap_side = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap_s);
+    cudaStreamIsCapturing(h->side, &cap_side);
+    static const bool no_chain = getenv("LAPSSD_NO_SIDE_CHAIN") != nullptr;
+    const bool capturing = cap_s == cudaStreamCaptureStatusActive;
+    const bool fork = no_chain || !h->side_chained || h->chain_stream != s || cap_s != cap_side ||
+                      capturing != h->chain_captured || !h->desc_valid;
+    h->side_chained = false;
+    cudaError_t ce = cudaSuccess;
+    if (fork) {
+        ce = cudaEventRecord(h->ev_fork, s);
+        if (ce != cudaSuccess) return cuda_status(ce, "laps_step_peer fork");
+    }
+    h->desc_valid = false;
+    a.fin = h->fin;
+    a.fin_key = h->fin_key;
+    a.snap = h->snap;
+    a.part1 = h->part + (size_t)h->max_batch * h->n_chunks * kPartWords;
+    a.work1 = h->work + 2;
+    a.vstep = &h->st.g->vstep;
+    static const bool no_pdl = getenv("LAPSSD_NO_PDL") != nullptr;
+    st = cuda_status(launch_verify_grid(a, B_global, 1, h->overlap && !no_pdl, s), "laps_step_peer verify");
+    if (st != LAPSSD_OK) return st;
+    if (fork) {
+        ce = cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+        if (ce != cudaSuccess) return cuda_status(ce, "laps_step_peer fork wait");
+    }
+    static const bool no_wl = getenv("LAPSSD_NO_WAITLIST") != nullptr;
+    const WaitList *wl = no_wl ? nullptr : &h->wl;
+    const PeerArgs pa{h->peer_ptrs, h->peer_C};
+    st = cuda_status(launch_select_side(h->st, h->sc, a.rows, sel_inout, h->desc, B_global, h->pre, h->fin,
+                                        h->fin_key, h->snap, (uint32_t)verify_grid(B_global, a.n_chunks, 1), count_out,
+                                        h->side, nullptr, 0, wl, &pa),
+                     "laps_step_peer select");
+    if (st != LAPSSD_OK) return st;
+    h->wl.valid = wl != nullptr && bp <= 1024;
+    ce = cudaEventRecord(h->ev_join, h->side);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_peer join");
+    ce = cudaStreamWaitEvent(s, h->ev_join, 0);
+    if (ce != cudaSuccess) return cuda_status(ce, "laps_step_peer join wait");
+    h->desc_valid = true;
+    h->side_chained = true;
+    h->chain_stream = s;
+    h->chain_captured = capturing;
+    return LAPSSD_OK;
 }
 
 lapssd_status laps_step_candidates(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t C,

@@ -39,6 +39,7 @@ enum : uint32_t {
     E_TO_MERGE = 64u,      // ... the side select's wait for the verified slots' records
     E_TO_SNAP = 128u,      // ... the side select's wait for the verify CTAs' snapshots
     E_MASS = 256u,         // a row pair with residual mass > 2 (not probability rows): sums invalid
+    E_TO_PEER = 512u,      // ... (with E_TIMEOUT) the side select's wait for the peers' candidate blocks
 };
 
 // Watchdog for device-side spin waits: true once `t0` is more than 2 s in the past.
@@ -604,10 +605,17 @@ struct WaitList {
     int32_t *meta;         // [4] length, current buffer, fresh count, pad (nullptr: no list)
     int32_t valid;         // the list describes the state (else the side select rebuilds it)
 };
+// laps_step_peer: every rank's exchange buffer as mapped in this process (device array of
+// world pointers; bufs[rank] is this rank's own), C candidates per rank.
+struct PeerArgs {
+    uint64_t *const *bufs;   // nullptr: no peer exchange
+    int32_t C;
+};
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
                                int32_t B, PreSelect *pre, const SelRec *fin, uint64_t *fin_key, uint32_t *snap,
                                uint32_t snap_target, int32_t *count_out, cudaStream_t s,
-                               uint64_t *cand_out = nullptr, int32_t C = 0, const WaitList *wl = nullptr);
+                               uint64_t *cand_out = nullptr, int32_t C = 0, const WaitList *wl = nullptr,
+                               const PeerArgs *peer = nullptr);
 // Monte-Carlo replicas (mc.cu): T traces over one concatenated request SoA.
 struct McDev {
     const int64_t *off;         // [T+1] request offsets of the traces

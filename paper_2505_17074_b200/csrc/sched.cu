@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
                                                                    PreSelect *pre, const SelRec *fin, uint64_t *fin_key,
                                                                    uint32_t *snap, uint32_t snap_target,
                                                                    int32_t *count_out, uint64_t *cand_out,
-                                                                   int32_t C, const WaitList wl) {
+                                                                   int32_t C, const WaitList wl, const PeerArgs peer) {
     extern __shared__ uint64_t s_buf[];
     STRACE(8);
 #ifdef LAPSSD_TRACE
@@ -361,6 +361,8 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     uint64_t *s_kw = s_adm + kAdmCap;                     // [bp] verified, not reselected: waiting keys
     uint64_t *s_S = s_kw + bp;                            // [bp + kAdmCap] merge(A suffix, Kw)
     int *s_hist = reinterpret_cast<int *>(s_S + bp + kAdmCap);   // [bp + kAdmCap + 1] rank histogram
+    // peer exchange (laps_step_peer): the G candidate lists, after the waiting-list regions
+    uint64_t *s_lists = s_buf + side_r0_words(n, bp) + (use_wl ? side_wl_words(bp) : 0);
     if (threadIdx.x == 0) s_cursor0 = st.g->cursor;
     // ---------------- phase 1: presort of every request outside the batch
     for (int w = threadIdx.x; w < (n + 31) / 32; w += T) s_member[w] = 0;
@@ -653,11 +655,94 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     ITRACE(100000);
     SSTEP(3);
     // ---------------- commit
-    int valid = 0;
-    for (int b = threadIdx.x; b < B; b += T) valid += (L[b] >> 63) == 0;
-    if (valid) atomicAdd(&s_count, valid);
-    __syncthreads();
-    const int cnt = s_count;
+    __shared__ int s_gcount;
+    __shared__ unsigned long long s_gsw, s_gnext;
+    if (peer.bufs) {
+        // multi-GPU (a8) fused over peer memory (laps_step_peer): this rank's candidate
+        // block -- its C best keys, their switch-in costs, its next arrival -- is stored
+        // into slot `rank` of every rank's exchange buffer over NVLink (UVA peer pointers),
+        // published by a system-scope release of the step's tag; then this CTA waits for
+        // all G tags in its own buffer, ranks every key among the G sorted lists (its
+        // index plus a binary search in each other list: the global top-B is a prefix of
+        // each list) and commits THIS rank's prefix -- the same result as all-gather +
+        // merge_kernel, in one kernel and without a collective launch.
+        const int G = sc.world, Cp = peer.C, W2 = 2 * Cp + 2;
+        const uint64_t tag = (uint64_t)st.g->vstep + 1;
+        const int par = (int)(tag & 1);
+        const uint32_t seq0 = st.g->sel_seq;
+        for (int g = 0; g < G; ++g) {
+            uint64_t *dst = peer.bufs[g] + ((size_t)par * G + sc.rank) * W2;
+            for (int c = threadIdx.x; c < Cp; c += T) {
+                const uint64_t key = c < bp ? L[c] : ~0ull;
+                const bool ok = (key >> 63) == 0;
+                dst[c] = ok ? key : ~0ull;
+                dst[Cp + c] = ok ? (uint64_t)switch_in_cost(st, sc, (int32_t)((uint32_t)(key & 0xFFFFFFull) /
+                                                                             (uint32_t)sc.world), seq0)
+                                 : 0ull;
+            }
+            if (threadIdx.x == 0) dst[2 * Cp] = s_cursor < n ? (uint64_t)st.arrival[s_cursor] : ~0ull;
+        }
+        // the CTA barrier orders every thread's block stores before the release stores of
+        // the tags (PTX release is cumulative over what happens-before it, barrier included)
+        __syncthreads();
+        if (threadIdx.x < G) {
+            uint64_t *tg = peer.bufs[threadIdx.x] + ((size_t)par * G + sc.rank) * W2 + 2 * Cp + 1;
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(tg), "l"(tag) : "memory");
+        }
+        if (threadIdx.x < G) {   // wait for every rank's block of this step (own buffer)
+            const uint64_t *tg = peer.bufs[sc.rank] + ((size_t)par * G + threadIdx.x) * W2 + 2 * Cp + 1;
+            const unsigned long long t0 = gtimer();
+            for (;;) {
+                uint64_t v;
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(tg) : "memory");
+                if (v == tag) break;
+                if (waited_too_long(t0)) { atomicOr(&st.g->err, E_TIMEOUT | E_TO_PEER); break; }
+                __nanosleep(64);
+            }
+        }
+        if (threadIdx.x == 0) { s_count = 0; s_gcount = 0; s_gsw = 0; s_gnext = ~0ull; }
+        __syncthreads();
+        const uint64_t *own = peer.bufs[sc.rank] + (size_t)par * G * W2;
+        for (int x = threadIdx.x; x < G * Cp; x += T) s_lists[x] = __ldcg(own + (size_t)(x / Cp) * W2 + (x % Cp));
+        for (int g = threadIdx.x; g < G; g += T)
+            atomicMin(&s_gnext, (unsigned long long)__ldcg(own + (size_t)g * W2 + 2 * Cp));
+        __syncthreads();
+        int mine = 0, gsel = 0;
+        unsigned long long gsw = 0;
+        for (int x = threadIdx.x; x < G * Cp; x += T) {
+            const int g = x / Cp, c = x % Cp;
+            const uint64_t key = s_lists[x];
+            if (key >> 63) continue;                       // padding (ineligible)
+            int rk = c;
+            for (int h = 0; h < G && rk < B; ++h) {
+                if (h == g) continue;
+                const uint64_t *Lh = s_lists + (size_t)h * Cp;
+                int lo = 0, hi = Cp;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (Lh[mid] < key) lo = mid + 1; else hi = mid;
+                }
+                rk += lo;
+            }
+            if (rk >= B) continue;
+            ++gsel;
+            gsw += __ldcg(own + (size_t)g * W2 + Cp + c);
+            mine += g == sc.rank;
+        }
+        if (mine) atomicAdd(&s_count, mine);
+        if (gsel) atomicAdd(&s_gcount, gsel);
+        if (gsw) atomicAdd(&s_gsw, gsw);
+        __syncthreads();
+    } else {
+        int valid = 0;
+        for (int b = threadIdx.x; b < B; b += T) valid += (L[b] >> 63) == 0;
+        if (valid) atomicAdd(&s_count, valid);
+        __syncthreads();
+        if (threadIdx.x == 0) { s_gcount = s_count; s_gsw = 0; s_gnext = s_cursor < n ? (uint64_t)st.arrival[s_cursor] : ~0ull; }
+        __syncthreads();
+    }
+    const int cnt = s_count;                 // this rank's selected: the first cnt of L
+    const int gcount = s_gcount;             // the global batch
     ITRACE(100001);
     const int64_t now = s_now;
     const uint32_t seq = st.g->sel_seq;
@@ -693,7 +778,8 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
         sel[b] = d.i;
         desc[b] = d;
     }
-    commit_switch(st, sc, sw, cnt, &s_sw_side);
+    // the step lasts one round plus the switch-ins of the GLOBAL batch (AMB-24)
+    commit_switch(st, sc, peer.bufs ? (threadIdx.x == 0 ? (int64_t)s_gsw : 0) : sw, gcount, &s_sw_side);
     __syncthreads();
     ITRACE(100002);
     for (int b = threadIdx.x; b < B; b += T) {   // the verified batch: running flags cleared
@@ -705,13 +791,10 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
     }
     if (threadIdx.x == 0) {
         int64_t nnow = now;
-        if (cnt == 0 && s_cursor < n) {
-            const int64_t nxt = st.arrival[s_cursor];
-            if (nxt > nnow) nnow = nxt;
-        }
+        if (gcount == 0 && s_gnext != ~0ull && (int64_t)s_gnext > nnow) nnow = (int64_t)s_gnext;   // idle: jump
         st.g->now_us = nnow;
         st.g->cursor = s_cursor;
-        st.g->prev_count = cnt;
+        st.g->prev_count = gcount;
         st.g->count = cnt;
         if (count_out) *count_out = cnt;
         st.g->vstep = st.g->vstep + 1;   // the next verify launch streams into the other set
@@ -830,12 +913,15 @@ __global__ void __launch_bounds__(kSideThreads) select_side_kernel(const State s
 cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &rw, int32_t *sel, SlotDesc *desc,
                                int32_t B, PreSelect *pre, const SelRec *fin, uint64_t *fin_key, uint32_t *snap,
                                uint32_t snap_target, int32_t *count_out, cudaStream_t s, uint64_t *cand_out,
-                               int32_t C, const WaitList *wl) {
+                               int32_t C, const WaitList *wl, const PeerArgs *peer) {
     int bp = 1;
     while (bp < B) bp <<= 1;
     WaitList w{};
     if (wl && wl->meta && !cand_out && bp <= 1024) w = *wl;   // else: the per-step presort
-    const size_t smem = (side_r0_words(sc.n, bp) + (w.meta ? side_wl_words(bp) : 0)) * sizeof(uint64_t);
+    PeerArgs pa{};
+    if (peer) pa = *peer;
+    const size_t smem = (side_r0_words(sc.n, bp) + (w.meta ? side_wl_words(bp) : 0) +
+                         (pa.bufs ? (size_t)sc.world * pa.C : 0)) * sizeof(uint64_t);
     // highest launch priority: when an SM frees up, the block scheduler places this one
     // CTA before the waiting CTAs of the next (programmatically launched) verify grid
     static int prio = [] {
@@ -855,7 +941,7 @@ cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &
     cfg.attrs = attr;
     cfg.numAttrs = no_prio ? 0 : 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, select_side_kernel, st, sc, rw, sel, desc, B, pre, fin, fin_key,
-                                             snap, snap_target, count_out, cand_out, C, w);
+                                             snap, snap_target, count_out, cand_out, C, w, pa);
     if (e != cudaSuccess) return e;
     count_launch();
     return cudaGetLastError();

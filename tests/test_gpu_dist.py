@@ -205,3 +205,48 @@ def test_laps_step_dist_one_rank_graph_replay(L, monkeypatch):
         L.nccl_comm_destroy(comm)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("switch", [False, True])
+def test_laps_step_peer_one_rank_lockstep(L, switch):
+    """laps_step_peer (the exchange fused into the select kernel over peer memory) with
+    one rank, step by step against the oracle; then captured in a CUDA graph and replayed."""
+    seed, B, R = 53, 16, 16
+    tr = synth.make_trace(120, seed, arrival="poisson", rate_per_s=60.0, len_mu=np.log(30),
+                          len_sigma=0.6, len_min=4, len_max=200, beta_ab=(4, 2), drift=True)
+    pool = synth.make_pool("f2", V=4096, k=4, dtype="bf16", n_buckets=8, variants=3, seed=seed, device="cuda")
+    tab = synth.slab_table(tr, 8, 3, R=R, seed=seed)
+    kw = dict(K=4, s1_up_us=56 * MS, gamma=5, delta=0.05, k=4, t_ssm_us=1 * MS, t_llm_us=10 * MS, seed=23)
+    pr = None
+    if switch:
+        kw.update(switch_c0_us=2 * MS, switch_c1_us=12)
+        pr = synth.prompt_lengths(tr.n, seed)
+    P = pool.numpy()
+    P["slab_tab"], P["R"] = tab, R
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, prompt=pr)
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=4096, prompt=pr,
+                 overlap=True)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
+    Cn = B
+    W = 2 * Cn + 1
+    cand = torch.zeros(2 * W, dtype=torch.int64, device="cuda")
+    h.laps_candidates(Cn, cand[:W])
+    cand[W:].copy_(cand[:W])
+    h.laps_merge(cand[W:], Cn, B)
+    h.set_peers(Cn)
+    sel_o, _ = sim.select(B)
+    for step in range(400):
+        sel_g = h.sel[:B].cpu().numpy()
+        assert (sel_g == sel_o).all(), f"step {step}: batch differs"
+        if sim.state()["done"].all():
+            break
+        h.laps_step_peer(rows, B)
+        sim.step(P, sel_o)
+        if step % 4 == 0:
+            g, o = h.state(), sim.state()
+            for f in ("acc_tok", "acc_draft", "rounds", "E_us", "C_us", "level", "perceptible", "pinned", "key",
+                      "switch_us"):
+                assert (np.asarray(g[f]) == np.asarray(o[f])).all(), f"step {step}: {f}"
+            assert g["now_us"] == o["now_us"] and g["switch_total_us"] == o["switch_total_us"]
+    assert sim.state()["done"].all()
+    assert h.check() == 0

@@ -95,6 +95,10 @@ def test_two_processes_gloo_exchange_equal_single_rank(policy, switch, tmp_path)
     seed, B = 0x6D00 + policy, 6
     mp.start_processes(_worker, args=(_free_port(), policy, switch, seed, B, str(tmp_path)), nprocs=G,
                        start_method="spawn", join=True)
+    _compare_with_oracle(tmp_path, policy, switch, seed, B)
+
+
+def _compare_with_oracle(tmp_path, policy, switch, seed, B):
     tr, tab, kw, pr = _setup(seed, switch)
     kw["policy"] = policy
     pool = synth.make_pool("f2", V=2048, k=4, dtype="bf16", n_buckets=8, variants=3, seed=seed, device="cuda")
@@ -120,3 +124,59 @@ def test_two_processes_gloo_exchange_equal_single_rank(policy, switch, tmp_path)
         assert int(r["now_us"]) == o["now_us"]
         assert int(r["switch_total_us"]) == o["switch_total_us"]
     assert (o["switch_total_us"] > 0) == switch
+
+
+def _peer_worker(rank, port, policy, switch, seed, B, out_dir):
+    """As _worker, but every step is laps_step_peer: the candidate blocks travel through
+    peer memory (torch CUDA IPC between the two processes) inside the select kernel."""
+    import torch.distributed as dist
+
+    import paper_2505_17074_b200 as L
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=G)
+    torch.cuda.set_device(0)
+    tr, tab, kw, pr = _setup(seed, switch)
+    kw["policy"] = policy
+    pool = synth.make_pool("f2", V=2048, k=4, dtype="bf16", n_buckets=8, variants=3, seed=seed, device="cuda")
+    sh = tr.shard(rank, G)
+    h = L.Handle(L.SchedConfig(**kw), sh.arrival_us, sh.L_true, sh.L_pred, max_batch=B, V=2048, rank=rank,
+                 world=G, prompt=pr[rank::G] if pr is not None else None)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(np.ascontiguousarray(tab[rank::G]), device="cuda"))
+    Cn = B
+    W = 2 * Cn + 1
+    cand = torch.zeros(W, dtype=torch.int64, device="cuda")
+    h.laps_candidates(Cn, cand)
+    parts = [torch.zeros(W, dtype=torch.int64) for _ in range(G)]
+    dist.all_gather(parts, cand.cpu())
+    h.laps_merge(torch.cat(parts).cuda(), Cn, B)
+    h.set_peers(Cn)
+    batches = []
+    for step in range(5000):
+        sel = h.sel[:B].cpu().numpy()
+        batches.append(sorted(int(i) * G + rank for i in sel if i >= 0))
+        done = torch.tensor([int(h.state()["done"].all())])
+        dist.all_reduce(done)
+        if int(done) == G:
+            break
+        h.laps_step_peer(rows, B)
+    torch.cuda.synchronize()
+    st = h.state()
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), steps=len(batches),
+             batches=np.array([np.array(b + [-1] * (B - len(b))) for b in batches]),
+             **{f: st[f] for f in ("C_us", "acc_tok", "rounds", "E_us", "x_us", "switch_us", "level",
+                                   "perceptible")},
+             now_us=st["now_us"], switch_total_us=st["switch_total_us"], flags=h.check())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy,switch", [(0, True), (3, False)])
+def test_two_processes_peer_exchange_equal_single_rank(policy, switch, tmp_path):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+    seed, B = 0x6E00 + policy, 6
+    mp.start_processes(_peer_worker, args=(_free_port(), policy, switch, seed, B, str(tmp_path)), nprocs=G,
+                       start_method="spawn", join=True)
+    _compare_with_oracle(tmp_path, policy, switch, seed, B)
