@@ -228,11 +228,25 @@ def run_ours(args):
         h.laps_candidates(Cn, cand[:W])
         dist.all_gather_into_tensor(cand[W:], cand[:W])
         h.laps_merge(cand[W:], Cn, B)
-        if args.nccl_exchange:
-            comm = L.nccl_comm()
-        else:   # the exchange fused into the select kernel over NVLink peer memory
+        if not args.nccl_exchange:   # the exchange fused into the select kernel over NVLink peer memory
             h.set_peers(Cn)
             peer = True
+            # safety net: if the peer exchange does not complete (device watchdog), every
+            # rank falls back to the NCCL form on a fresh handle
+            h.laps_step_peer(rows, B)
+            torch.cuda.synchronize()
+            ok = torch.tensor([1.0 if h.check_flags() == 0 else 0.0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() < 1.0:
+                print("bench: peer exchange failed, falling back to laps_step_dist", file=sys.stderr, flush=True)
+                peer = False
+                h = L.Handle(cfg, local.arrival_us, local.L_true, local.L_pred, max_batch=B, V=args.V,
+                             rank=rank, world=world, overlap=True)
+                h.laps_candidates(Cn, cand[:W])
+                dist.all_gather_into_tensor(cand[W:], cand[:W])
+                h.laps_merge(cand[W:], Cn, B)
+        if not peer:
+            comm = L.nccl_comm()
     elif args.peer_path:
         cand = torch.zeros(2 * W, dtype=torch.int64, device=dev)
         h.laps_candidates(Cn, cand[:W])

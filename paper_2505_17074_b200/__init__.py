@@ -425,6 +425,12 @@ class Handle:
         _check("lapssd_check", rc)
         return flags.value
 
+    def check_flags(self) -> int:
+        """The device flags (0: none), without raising."""
+        flags = C.c_uint32()
+        _lib.lapssd_check(self.h, C.byref(flags))
+        return flags.value
+
 
 def _state_arrays(n, gamma):
     return dict(acc_tok=np.zeros(n, np.int32), acc_draft=np.zeros(n, np.int32),
