@@ -105,6 +105,8 @@ def lib(parallel: bool = False):
         L.orc_verify_many.argtypes = [vp, vp, i32, i64, i32, i32, vp, vp, vp, u64, vp, vp]
         L.orc_exp_hat.argtypes = [C.c_float]
         L.orc_exp_hat.restype = C.c_float
+        L.orc_logits_row.argtypes = [vp, i32, i64, vp, vp]
+        L.orc_logits_row.restype = u64
         L.orc_verify_logits_request.argtypes = [vp, vp, i32, i64, i32, vp, u32, u32, u64, u32, vp,
                                                 C.POINTER(LogitsOut)]
         L.orc_verify_logits_request.restype = i32
@@ -204,6 +206,16 @@ def verify_many(p_rows, q_rows, drafts, req_ids, rounds, seed):
 def exp_hat(d) -> float:
     """AMB-30: e^d on [-28, 0] by the fixed fp32 operation sequence."""
     return float(lib().orc_exp_hat(float(d)))
+
+
+def logits_row(z_row):
+    """AMB-30's quantised softmax of one row: (E [V] uint64, S, m)."""
+    z = np.ascontiguousarray(z_row)
+    V = z.shape[-1]
+    E = np.zeros(V, np.uint64)
+    m = np.zeros(1, np.float32)
+    S = lib().orc_logits_row(_ptr(z), _dtype_code(z), V, _ptr(m), _ptr(E))
+    return E, int(S), float(m[0])
 
 
 def verify_logits_request(zp_rows, zq_rows, draft, req_id, round_idx, seed, trace=0):

@@ -426,6 +426,19 @@ static void row_norm(const void *rows, int32_t dtype, int64_t off, int64_t V, fl
     *S_out = S;
 }
 
+/* The quantised softmax of one row (AMB-30): E[v] and S = sum E (returns S; m_out the
+ * row max).  Used by the pins that compare E / S with the fp64 softmax. */
+uint64_t orc_logits_row(const void *z_row, int32_t dtype, int64_t V, float *m_out, uint64_t *E_out)
+{
+    float m;
+    uint64_t S;
+    row_norm(z_row, dtype, 0, V, &m, &S);
+    if (E_out)
+        for (int64_t v = 0; v < V; v++) E_out[v] = e40(load_logit(z_row, dtype, v), m);
+    if (m_out) *m_out = m;
+    return S;
+}
+
 int32_t orc_verify_logits_request(const void *zp_rows, const void *zq_rows, int32_t dtype,
                                   int64_t V, int32_t k, const int32_t *draft,
                                   uint32_t req_id, uint32_t round_idx, uint64_t seed,

@@ -77,6 +77,10 @@ typedef struct {
 /* e^d on [-28, 0] by a fixed fp32 operation sequence (0 below -28). */
 float orc_exp_hat(float d);
 
+/* The quantised softmax of one row: E[v] = floor(exphat(fl32(z[v] - m)) 2^40) into E_out
+ * (nullable), returns S = sum E, m_out = the row max. */
+uint64_t orc_logits_row(const void *z_row, int32_t dtype, int64_t V, float *m_out, uint64_t *E_out);
+
 /* zp_rows: (k+1) rows of V logits; zq_rows: k rows; dtype as above.  Returns r. */
 int32_t orc_verify_logits_request(const void *zp_rows, const void *zq_rows, int32_t dtype,
                                   int64_t V, int32_t k, const int32_t *draft,

@@ -132,3 +132,43 @@ def test_bf16_logits_and_slab_batch_agree_with_single_requests():
     for b in range(B):
         t1, o = oracle.verify_logits_request(zp[slab[b]], zq[slab[b]], drafts[slab[b]], req[b], rnd[b], seed=95)
         assert (t1 == tok[b]).all() and o.r == r[b]
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.uint16])
+def test_quantised_softmax_within_1e6_of_fp64_softmax_at_large_V(dtype):
+    """AMB-30 against the exact softmax of the STORED logits, at V = 128,256 (configs[3]):
+    every probability >= 1e-5 within 1e-6 relative, total variation < 1e-6, and the
+    residual mass Z / (Sp Sq) of a row pair within 1e-6 relative of the fp64
+    sum_v max(0, p - q) (north_star's tolerance on residual probabilities)."""
+    V = 128256
+    rng = np.random.default_rng(7 if dtype == np.float32 else 8)
+    for trial in range(3):
+        ranks = rng.permutation(V) + 1
+        zp = (-1.1 * np.log(ranks) + rng.normal(0, 1.5, V)).astype(np.float32)
+        zq = (zp + rng.normal(0, 0.8, V)).astype(np.float32)
+        if dtype == np.uint16:   # bf16 bit patterns (round to nearest even)
+            to_bf = lambda x: ((x.view(np.uint32) + 0x7FFF + ((x.view(np.uint32) >> 16) & 1)) >> 16).astype(np.uint16)
+            zp_s, zq_s = to_bf(zp), to_bf(zq)
+            zp_f = (zp_s.astype(np.uint32) << 16).view(np.float32)
+            zq_f = (zq_s.astype(np.uint32) << 16).view(np.float32)
+        else:
+            zp_s, zq_s, zp_f, zq_f = zp, zq, zp, zq
+        ref = []
+        for zs, zf in ((zp_s, zp_f), (zq_s, zq_f)):
+            E, S, m = oracle.logits_row(zs)
+            assert m == zf.max()
+            ph = E.astype(np.float64) / float(S)
+            x = zf.astype(np.float64)
+            p = np.exp(x - x.max())
+            p /= p.sum()
+            big = p >= 1e-5
+            assert (np.abs(ph[big] - p[big]) / p[big]).max() < 1e-6
+            assert np.abs(ph - p).sum() < 1e-6
+            ref.append((E, S, p))
+        (Ep, Sp, p), (Eq, Sq, q) = ref
+        # the integer residual of spec_verify_logits: max(0, Ep Sq - Eq Sp) / (Sp Sq)
+        Ep_o = [int(e) for e in Ep]
+        Eq_o = [int(e) for e in Eq]
+        Z = sum(max(0, a * Sq - b * Sp) for a, b in zip(Ep_o, Eq_o))
+        exact = np.maximum(p - q, 0).sum()
+        assert abs(Z / (Sp * Sq) - exact) / exact < 1e-6
