@@ -828,12 +828,17 @@ def run_logits(args):
            "roofline": {"kernel": "logits_norm_kernel + logits_sample_kernel (spec_verify_logits)",
                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak,
-                        "algorithmic_bytes_per_step": alg, "traffic": 4.3935e9,
+                        "algorithmic_bytes_per_step": alg, "traffic": 4.3698e9,
                         "note": "algorithmic bytes: every logit row once (2k+1 rows: normalisers) + the "
                         "residual row pair (or the bonus row).  traffic: ncu DRAM bytes of one step "
-                        "(profiles/r01f_logits_launches.csv): the normaliser's second pass over each "
-                        "row mostly misses L2, and the kernel also issues ~14 slots per entry for the "
-                        "fixed-op exp (69 % issue-active)"}}
+                        "(profiles/r02_logits_counts.csv): the normaliser's second pass over each "
+                        "row mostly misses L2"}}
+    alu = alu_roofline("logits", {"B": B, "V": V, "k": k}, ms / steps, clk)
+    if alu:   # the binding resource: instruction issue (the fixed-op exp and the 128-bit residual)
+        hbm = out["roofline"]
+        out["roofline"] = dict(alu, kernel=hbm["kernel"],
+                               hbm={x: hbm[x] for x in ("achieved", "peak", "unit", "frac", "algorithmic_bytes_per_step",
+                                                        "traffic")})
     if not args.no_cpu_baseline and rank == 0:
         import oracle
         sl = slabs[0].cpu().numpy()
@@ -892,6 +897,30 @@ def timed_graph(args, step, G, local_rank, dist=None):
         dist.all_reduce(t_, op=dist.ReduceOp.MAX)
         ms = float(t_[0])
     return ms, reps * G, clk, launches
+
+
+def alu_roofline(key, workload, ms_per_step, clk):
+    """Issue-rate roofline of an ALU-bound kernel: its executed warp instructions per step
+    (ncu, profiles/alu_counts.json, used only for THIS build and this workload) over the
+    step time, against 148 SMs x 4 sub-partitions x 1 warp instruction per clock at the
+    median SM clock of the timed region.  None if no matching capture is on file."""
+    path = os.path.join(ROOT, "profiles", "alu_counts.json")
+    if not os.path.exists(path):
+        return None
+    try:
+        d = json.load(open(path))
+    except (OSError, ValueError):
+        return None
+    e = d.get(key)
+    if not e or d.get("build_digest") != build_digest() or e.get("workload") != workload:
+        return None
+    mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965
+    peak = 148 * 4 * mhz * 1e6 / 1e9                  # G warp instructions / s
+    achieved = e["warp_inst_per_step"] / (ms_per_step * 1e-3) / 1e9
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "G warp-instructions/s",
+            "frac": achieved / peak, "warp_inst_per_step": e["warp_inst_per_step"],
+            "peak_source": f"148 SMs x 4 SMSPs x 1 warp instruction/clock at {mhz} MHz (B200_PROFILING.md unit counts)",
+            "inst_source": d.get("source")}
 
 
 def hbm_peak():
@@ -1041,6 +1070,11 @@ def run_f4(args):
            "roofline": {"kernel": kernel, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "algorithmic_bytes_per_step": alg, "traffic": None,
                         "timing": f"{steps} steps as replays of a CUDA graph of {G} steps"}}
+    if args.workload == "tree":   # neither bound is reached: the issue rate beside the HBM one
+        alu = alu_roofline("tree", {"B": B, "V": V, "nodes": args.tree_nodes, "max_children": args.tree_width},
+                           ms / steps, clk)
+        if alu:
+            res["roofline"]["alu"] = {x: alu[x] for x in ("achieved", "peak", "unit", "frac")}
     if cpu:
         res["cpu_baseline"] = cpu
     if rank == 0:
