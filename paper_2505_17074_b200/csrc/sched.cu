@@ -922,6 +922,7 @@ cudaError_t launch_select_side(const State &st, const Sched &sc, const RowsDev &
     if (peer) pa = *peer;
     const size_t smem = (side_r0_words(sc.n, bp) + (w.meta ? side_wl_words(bp) : 0) +
                          (pa.bufs ? (size_t)sc.world * pa.C : 0)) * sizeof(uint64_t);
+    if (smem > 220 * 1024) return cudaErrorInvalidConfiguration;   // shared memory of one CTA (sched_prepare)
     // highest launch priority: when an SM frees up, the block scheduler places this one
     // CTA before the waiting CTAs of the next (programmatically launched) verify grid
     static int prio = [] {
