@@ -28,7 +28,11 @@ constexpr int kRowThreads = 512;        // draft sampling: one row per CTA, 4 CT
 #ifndef LAPSSD_TREE_THREADS
 #define LAPSSD_TREE_THREADS 512
 #endif
-constexpr int kTreeThreads = LAPSSD_TREE_THREADS;   // tree verification: one tree per SM (measured: 256 / 128 slower)
+constexpr int kTreeThreads = LAPSSD_TREE_THREADS;   // tree verification: one CTA per SM
+#ifndef LAPSSD_TREES_PER_CTA
+#define LAPSSD_TREES_PER_CTA 1
+#endif
+constexpr int kTreesPerCta = LAPSSD_TREES_PER_CTA;  // trees per CTA (measured: 2 / 4 / 8 per CTA slower: 0.44 / 0.52 / 1.0 ms)
 constexpr int kTreeMax = 64;            // nodes per tree
 
 __device__ __forceinline__ uint4 ld_nc(const void *ptr) {
@@ -116,16 +120,25 @@ struct StageMassT {
     }
 };
 
-// One pass over a row pair: seg[s] = the masses of segment s, returns Z (block-wide).
+// The threads that work on one row: the whole CTA (draft sampling) or one group of warps
+// of it (tree verification runs several trees per CTA); sync() is a named barrier.
+struct Grp {
+    int tid, nt, bar;
+    __device__ __forceinline__ void sync() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nt) : "memory");
+    }
+};
+
+// One pass over a row pair: seg[s] = the masses of segment s, returns Z (group-wide).
 template <bool BF16, class MassF>
 __device__ uint64_t row_pass(const char *prow, const char *qrow, int64_t V, const MassF &mass, uint64_t *seg,
-                             uint64_t *s_tot) {
+                             uint64_t *s_tot, const Grp &gr) {
     using E = RowElt<BF16>;
     constexpr int J = kSegElems / E::kVec / 32;   // vectors per lane per segment
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = gr.tid & 31, warp = gr.tid >> 5;
     const int nseg = (int)((V + kSegElems - 1) / kSegElems);
     uint64_t mine = 0;
-    const int nwarps = (int)(blockDim.x >> 5);
+    const int nwarps = gr.nt >> 5;
     for (int s = warp; s < nseg; s += nwarps) {
         const int64_t base = (int64_t)s * kSegElems;
         uint4 pv[J], qv[J];
@@ -145,19 +158,19 @@ __device__ uint64_t row_pass(const char *prow, const char *qrow, int64_t V, cons
         if (lane == 0) seg[s] = m;
         mine += m;
     }
-    if (threadIdx.x == 0) *s_tot = 0;
-    __syncthreads();
+    if (gr.tid == 0) *s_tot = 0;
+    gr.sync();
     if (lane == 0 && mine) atomicAdd((unsigned long long *)s_tot, (unsigned long long)mine);
-    __syncthreads();
+    gr.sync();
     const uint64_t Z = *s_tot;
-    __syncthreads();
+    gr.sync();
     return Z;
 }
 
 // row_pass / row_search for a runtime stage: compile-time chains for stages 0..4.
 template <bool BF16>
 __device__ uint64_t stage_pass(const char *prow, const char *qrow, int64_t V, int stage, const uint64_t *Zs,
-                               const int *zb, uint64_t *seg, uint64_t *s_tot);
+                               const int *zb, uint64_t *seg, uint64_t *s_tot, const Grp &gr);
 template <bool BF16>
 __device__ int stage_search(const char *prow, const char *qrow, int64_t V, int stage, const uint64_t *Zs,
                             const int *zb, const uint64_t *seg, uint64_t t);
@@ -168,7 +181,7 @@ __device__ int row_search(const char *prow, const char *qrow, int64_t V, const M
                           uint64_t t) {
     using E = RowElt<BF16>;
     constexpr int J = kSegElems / E::kVec / 32;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;   // one warp
     const int nseg = (int)((V + kSegElems - 1) / kSegElems);
     int sstar = nseg - 1;
     for (int s0 = 0; s0 < nseg; s0 += 32) {
@@ -220,14 +233,14 @@ __device__ int row_search(const char *prow, const char *qrow, int64_t V, const M
 
 template <bool BF16>
 __device__ uint64_t stage_pass(const char *prow, const char *qrow, int64_t V, int stage, const uint64_t *Zs,
-                               const int *zb, uint64_t *seg, uint64_t *s_tot) {
+                               const int *zb, uint64_t *seg, uint64_t *s_tot, const Grp &gr) {
     switch (stage) {
-    case 0: return row_pass<BF16>(prow, nullptr, V, StageMass{0, nullptr, nullptr}, seg, s_tot);
-    case 1: return row_pass<BF16>(prow, qrow, V, StageMassT<1>(Zs, zb), seg, s_tot);
-    case 2: return row_pass<BF16>(prow, qrow, V, StageMassT<2>(Zs, zb), seg, s_tot);
-    case 3: return row_pass<BF16>(prow, qrow, V, StageMassT<3>(Zs, zb), seg, s_tot);
-    case 4: return row_pass<BF16>(prow, qrow, V, StageMassT<4>(Zs, zb), seg, s_tot);
-    default: return row_pass<BF16>(prow, qrow, V, StageMass{stage, Zs, zb}, seg, s_tot);
+    case 0: return row_pass<BF16>(prow, nullptr, V, StageMass{0, nullptr, nullptr}, seg, s_tot, gr);
+    case 1: return row_pass<BF16>(prow, qrow, V, StageMassT<1>(Zs, zb), seg, s_tot, gr);
+    case 2: return row_pass<BF16>(prow, qrow, V, StageMassT<2>(Zs, zb), seg, s_tot, gr);
+    case 3: return row_pass<BF16>(prow, qrow, V, StageMassT<3>(Zs, zb), seg, s_tot, gr);
+    case 4: return row_pass<BF16>(prow, qrow, V, StageMassT<4>(Zs, zb), seg, s_tot, gr);
+    default: return row_pass<BF16>(prow, qrow, V, StageMass{stage, Zs, zb}, seg, s_tot, gr);
     }
 }
 template <bool BF16>
@@ -261,7 +274,8 @@ __global__ void __launch_bounds__(kRowThreads) draft_sample_kernel(const char *q
     const int64_t row = row_idx ? row_idx[r] : r;
     const char *qrow = q + row * V * RowElt<BF16>::kEsz;
     const StageMass m{0, nullptr, nullptr};
-    const uint64_t Z = row_pass<BF16>(qrow, nullptr, V, m, seg, &s_tot);   // (draft: stage 0 = the row)
+    const Grp gr{(int)threadIdx.x, (int)blockDim.x, 0};
+    const uint64_t Z = row_pass<BF16>(qrow, nullptr, V, m, seg, &s_tot, gr);   // (draft: stage 0 = the row)
     if (threadIdx.x >= 32) return;
     int x = 0;
     if (Z) {
@@ -290,21 +304,35 @@ __device__ __forceinline__ bool tree_accept(uint32_t u24, float qx, uint64_t Dx,
     return (u128)u24 * m * Z < ((u128)Dx << sh);
 }
 
+// kTreesPerCta trees per CTA, one group of kTreeThreads / kTreesPerCta threads each (named
+// barrier 1 + group): while one tree waits on a gather, a barrier or its loads, the others
+// issue.
 template <bool BF16>
-__global__ void __launch_bounds__(kTreeThreads, 512 / kTreeThreads) tree_verify_kernel(const char *p, const char *q, int64_t V,
+__global__ void __launch_bounds__(kTreeThreads, 1) tree_verify_kernel(const char *p, const char *q, int64_t V,
                                                                   int32_t n_nodes, const int32_t *parent,
                                                                   const int32_t *token, const uint32_t *req_id,
                                                                   const uint32_t *round_idx, uint64_t seed,
                                                                   uint32_t trace, int32_t *tokens, int32_t *path,
-                                                                  int32_t *n_accept, uint64_t *z_out) {
+                                                                  int32_t *n_accept, uint64_t *z_out, int32_t B) {
     using E = RowElt<BF16>;
-    __shared__ uint64_t seg[kMaxSegs];
-    __shared__ uint64_t s_tot;
-    __shared__ uint64_t s_Zs[kTreeMax + 1];
-    __shared__ int s_zb[kTreeMax + 1];
-    __shared__ int s_par[kTreeMax], s_tok[kTreeMax], s_dep[kTreeMax], s_ch[kTreeMax];
-    __shared__ int s_ok, s_w, s_acc;
-    const int b = blockIdx.x, n = n_nodes;
+    constexpr int GT = kTreeThreads / kTreesPerCta;
+    __shared__ uint64_t seg_all[kTreesPerCta][kMaxSegs];
+    __shared__ uint64_t s_tot_all[kTreesPerCta];
+    __shared__ uint64_t s_Zs_all[kTreesPerCta][kTreeMax + 1];
+    __shared__ int s_zb_all[kTreesPerCta][kTreeMax + 1];
+    __shared__ int s_par_all[kTreesPerCta][kTreeMax], s_tok_all[kTreesPerCta][kTreeMax];
+    __shared__ int s_dep_all[kTreesPerCta][kTreeMax], s_ch_all[kTreesPerCta][kTreeMax];
+    __shared__ int s_ok_all[kTreesPerCta], s_w_all[kTreesPerCta], s_acc_all[kTreesPerCta];
+    const int g = (int)threadIdx.x / GT;
+    const Grp gr{(int)threadIdx.x % GT, GT, 1 + g};
+    const int tid = gr.tid;
+    const int b = blockIdx.x * kTreesPerCta + g, n = n_nodes;
+    if (b >= B) return;
+    uint64_t *seg = seg_all[g];
+    uint64_t *s_Zs = s_Zs_all[g];
+    int *s_zb = s_zb_all[g], *s_par = s_par_all[g], *s_tok = s_tok_all[g], *s_dep = s_dep_all[g], *s_ch = s_ch_all[g];
+    int &s_ok = s_ok_all[g], &s_w = s_w_all[g], &s_acc = s_acc_all[g];
+    uint64_t *s_tot = &s_tot_all[g];
     const uint32_t req = req_id[b], rnd = round_idx[b];
     const int32_t *par_g = parent + (int64_t)b * n;
     const int32_t *tok_g = token + (int64_t)b * n;
@@ -312,14 +340,14 @@ __global__ void __launch_bounds__(kTreeThreads, 512 / kTreeThreads) tree_verify_
     const char *qb = q + (int64_t)b * n * V * E::kEsz;
     int32_t *tok_o = tokens + (int64_t)b * n;
     int32_t *path_o = path ? path + (int64_t)b * n : nullptr;
-    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    for (int c = tid; c < n; c += GT) {
         s_par[c] = par_g[c];
         s_tok[c] = tok_g[c];
         tok_o[c] = -1;
         if (path_o) path_o[c] = -1;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {   // structure: parent before child, tokens in range
+    gr.sync();
+    if (tid == 0) {   // structure: parent before child, tokens in range
         int ok = 1;
         s_dep[0] = 0;
         for (int c = 1; c < n && ok; ++c) {
@@ -330,27 +358,27 @@ __global__ void __launch_bounds__(kTreeThreads, 512 / kTreeThreads) tree_verify_
         }
         s_ok = ok;
     }
-    __syncthreads();
+    gr.sync();
     if (!s_ok) {
-        if (threadIdx.x == 0) { n_accept[b] = -1; if (z_out) z_out[b] = 0; }
+        if (tid == 0) { n_accept[b] = -1; if (z_out) z_out[b] = 0; }
         return;
     }
     int u = 0, nacc = 0;
     for (;;) {
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             int w = 0;
             for (int c = u + 1; c < n; ++c)
                 if (s_par[c] == u) s_ch[w++] = c;
             s_w = w;
         }
-        __syncthreads();
+        gr.sync();
         const int w = s_w;
         const char *prow = pb + (int64_t)u * V * E::kEsz;
         const char *qrow = qb + (int64_t)u * V * E::kEsz;
         int next = -1, stage = 0;
         bool fallback = false;
         for (int i = 0; i < w; ++i) {
-            if (threadIdx.x == 0) {
+            if (tid == 0) {
                 const int x = s_tok[s_ch[i]];
                 const float px = E::get(ld_nc(prow + ((int64_t)x - (x % E::kVec)) * E::kEsz), x % E::kVec);
                 const float qx = E::get(ld_nc(qrow + ((int64_t)x - (x % E::kVec)) * E::kEsz), x % E::kVec);
@@ -372,26 +400,26 @@ __global__ void __launch_bounds__(kTreeThreads, 512 / kTreeThreads) tree_verify_
                 }
                 s_acc = acc;
             }
-            __syncthreads();
+            gr.sync();
             if (s_acc) { next = s_ch[i]; break; }
             // D_{i+1} and its total (the segment sums stay for a final draw from it)
-            const uint64_t Z = stage_pass<BF16>(prow, qrow, V, i + 1, s_Zs, s_zb, seg, &s_tot);
+            const uint64_t Z = stage_pass<BF16>(prow, qrow, V, i + 1, s_Zs, s_zb, seg, s_tot, gr);
             stage = i + 1;
-            if (threadIdx.x == 0) {
+            if (tid == 0) {
                 s_Zs[stage] = Z;
                 s_zb[stage] = 64 - __clzll((long long)Z);
             }
-            __syncthreads();
+            gr.sync();
             if (Z == 0) { fallback = true; break; }   // AMB-20: no residual mass
         }
         if (next >= 0) {
-            if (threadIdx.x == 0) {
+            if (tid == 0) {
                 tok_o[nacc] = s_tok[next];
                 if (path_o) path_o[nacc] = next;
             }
             ++nacc;
             u = next;
-            __syncthreads();
+            gr.sync();
             continue;
         }
         // the emitted token: from D_stage (every child rejected), else from the row p_u
@@ -402,15 +430,15 @@ __global__ void __launch_bounds__(kTreeThreads, 512 / kTreeThreads) tree_verify_
             Z = s_Zs[stage];
         } else {
             st_draw = 0;
-            Z = stage_pass<BF16>(prow, nullptr, V, 0, s_Zs, s_zb, seg, &s_tot);
+            Z = stage_pass<BF16>(prow, nullptr, V, 0, s_Zs, s_zb, seg, s_tot, gr);
         }
-        if (threadIdx.x < 32) {
+        if (tid < 32) {
             int y = 0;
             if (Z) {
                 const uint64_t U = philox_u64(req, rnd, 1u << 8, trace, seed);
                 y = stage_search<BF16>(prow, qrow, V, st_draw, s_Zs, s_zb, seg, __umul64hi(U, Z));
             }
-            if (threadIdx.x == 0) {
+            if (tid == 0) {
                 tok_o[nacc] = y;
                 n_accept[b] = nacc;
                 if (z_out) z_out[b] = Z;
@@ -442,13 +470,13 @@ cudaError_t launch_verify_tree(const void *p, const void *q, int32_t dtype, int6
                                int32_t *path, int32_t *n_accept, uint64_t *z_out, cudaStream_t s) {
     if (B <= 0) return cudaSuccess;
     if (dtype == LAPSSD_BF16)
-        tree_verify_kernel<true><<<B, kTreeThreads, 0, s>>>((const char *)p, (const char *)q, V, n_nodes, parent,
-                                                           token, req, rnd, seed, trace, tokens, path, n_accept,
-                                                           z_out);
+        tree_verify_kernel<true><<<(B + kTreesPerCta - 1) / kTreesPerCta, kTreeThreads, 0, s>>>(
+            (const char *)p, (const char *)q, V, n_nodes, parent, token, req, rnd, seed, trace, tokens, path,
+            n_accept, z_out, B);
     else
-        tree_verify_kernel<false><<<B, kTreeThreads, 0, s>>>((const char *)p, (const char *)q, V, n_nodes, parent,
-                                                            token, req, rnd, seed, trace, tokens, path, n_accept,
-                                                            z_out);
+        tree_verify_kernel<false><<<(B + kTreesPerCta - 1) / kTreesPerCta, kTreeThreads, 0, s>>>(
+            (const char *)p, (const char *)q, V, n_nodes, parent, token, req, rnd, seed, trace, tokens, path,
+            n_accept, z_out, B);
     count_launch();
     return cudaGetLastError();
 }
