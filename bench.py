@@ -4,7 +4,9 @@
 One STEP = one pass of the whole hot path over one batch: spec_verify of every
 selected request (rejection sampling) with the fused LAPS-SD
 state update, then admission + priority keys + top-B selection of the
-next batch -- the C-ABI call laps_step (laps_step_dist for N>1).
+next batch -- the C-ABI call laps_step (laps_step_peer for N>1: the
+candidate exchange fused into the select kernel over NVLink peer memory; laps_step_dist,
+the NCCL form, with --nccl-exchange).
 
 Workload = BASELINE.json configs[3] ("16,384 concurrent requests, V=128,256, k=8,
 bf16, batch 512, sharded over 8 B200"): 2,048 resident requests and B=512 per GPU
@@ -41,7 +43,7 @@ METRIC = "verified draft tokens/s at V=128k,k=8 on 1/2/4/8 B200; % of HBM peak"
 UNIT = "verified draft tokens/s"
 WORKLOAD = ("configs[3]: 16,384 concurrent requests over 8 GPUs -> 2,048 resident + batch 512 "
             "per GPU (weak scaling), V=128,256, k=8, bf16 p/q, Beta(7,3) acceptance, "
-            "L~U[512,4096], all arrive at t=0, global top-B all-gather for N>1")
+            "L~U[512,4096], all arrive at t=0, global top-B exchanged over peer memory for N>1")
 SCHED = dict(K=4, s1_up_us=4 * (8 * 1000 + 10_000), M=2.0, gamma=5, delta=0.05, k=8,
              t_ssm_us=1000, t_llm_us=10_000, placement=0, pin_rule=0)
 
