@@ -486,7 +486,6 @@ __device__ __forceinline__ void sample_slot_warp(const VerifyArgs &a, uint64_t *
     uint64_t *part = part_set + (int64_t)b * nc * kPartWords;
     // chunk sums: cs0 for chunk lane, cs1 for chunk lane + 32 (fp32 tiling only)
     uint64_t cs0 = 0, cs1 = 0;
-#pragma unroll
     uint64_t za = 0;   // Z / 16, which cannot wrap: the row mass check (E_MASS)
 #pragma unroll
     for (int x = 0; x < kPartWords; ++x) {
