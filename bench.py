@@ -387,6 +387,15 @@ def run_ours(args):
                       + ("; global top-B exchanged inside the select kernel over NVLink peer memory (laps_step_peer)"
                          if world > 1 and peer else "")},
            "verified_per_step": verified / args.steps, "gpu_launches": launches, "clocks": clk}
+    if world > 1 or peer or comm is not None:
+        # the a8 exchange: each rank's candidate block of 2C+1 words (+ a tag
+        # word on the peer path) to every rank, once per step
+        blk = (2 * Cn + 2 if peer else 2 * Cn + 1) * 8
+        out["exchange"] = {"path": "laps_step_peer (in-kernel, NVLink peer stores)" if peer else "ncclAllGather",
+                           "bytes_sent_per_rank_per_step": blk * world, "bytes_received_per_rank_per_step": blk * world,
+                           "per_step_at_nvlink5_900GBps_us": blk * world / 900e9 * 1e6,
+                           "note": "latency-bound: the bytes need ~0.1 us of NVLink-5 bandwidth; the step time "
+                                   "above includes the exchange (it runs beside the verify kernel)"}
     if device_error:
         out["device_error"] = device_error
     if world == 1 and not args.no_profile:
