@@ -636,6 +636,29 @@ __device__ __forceinline__ uint32_t slot_word(const VerifyArgs &a, int b) {
     return r < 0 ? 0u : ((uint32_t)dh.y << 5) | (uint32_t)(r + 1);
 }
 
+// L2 prefetch (no shared memory, no completion) of item n's bytes: chunk c of p_r and, if
+// r < k, of q_r, for the slot word `it`.
+template <bool BF16>
+__device__ __forceinline__ void prefetch_item(const VerifyArgs &a, int n, uint32_t it) {
+    using E = Elt<BF16>;
+    using TC = VerifyCfg<BF16>;
+    if (it == 0) return;
+    const int kk = a.rows.k, nc = a.n_chunks;
+    const int64_t V = a.rows.V;
+    const int r = (int)(it & 31u) - 1;
+    const int64_t slab = it >> 5;
+    const int c = n % nc;
+    const int64_t e0 = (int64_t)c * TC::kTileElems;
+    const int64_t ne = V - e0 < TC::kTileElems ? V - e0 : TC::kTileElems;
+    const uint32_t bytes = (uint32_t)(ne * E::kEsz);
+    const char *pr = (const char *)a.rows.p + ((slab * (kk + 1) + r) * V + e0) * E::kEsz;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pr), "r"(bytes) : "memory");
+    if (r < kk) {
+        const char *qr = (const char *)a.rows.q + ((slab * kk + r) * V + e0) * E::kEsz;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qr), "r"(bytes) : "memory");
+    }
+}
+
 // Producer: item n (slot n / nc, chunk n % nc) into ring stage st -- chunk c of p_r and,
 // when r < k, of q_r, as bulk copies completing on full[st]; nothing for an empty slot.
 template <bool BF16>
@@ -784,6 +807,31 @@ __global__ void __launch_bounds__(kVerifyThreads, 1) verify_kernel(const __grid_
                 work[0] = 0;
                 work[1] = 0;
             }
+#ifndef LAPSSD_NO_NEXT_PREFETCH
+#ifndef LAPSSD_NEXT_PREFETCH_ITEMS
+#define LAPSSD_NEXT_PREFETCH_ITEMS 3
+#endif
+            // The stream of this step is over for this CTA.  If the side select has already
+            // committed the NEXT step's batch (laps_step: the step counter advanced), warm L2
+            // with the first items the next launch's CTA of the same index will issue, so HBM
+            // stays busy across the kernel boundary (the next grid's ramp reads from L2).
+            if (a.fin_key && a.vstep) {
+                uint32_t v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.vstep) : "memory");
+                if (v == vstep + 1) {
+                    int nb = B;
+                    if (a.count_dev) {
+                        const int cc = __ldcg(a.count_dev);
+                        nb = cc < 0 ? 0 : cc < B ? cc : B;
+                    }
+                    for (int s2 = 0; s2 < LAPSSD_NEXT_PREFETCH_ITEMS; ++s2) {
+                        const int n2 = (int)blockIdx.x + s2 * grid;
+                        if (n2 >= nb * nc) break;
+                        prefetch_item<BF16>(a, n2, slot_word(a, n2 / nc));
+                    }
+                }
+            }
+#endif
         }
         __syncwarp();
     } else if (finisher) {
