@@ -23,9 +23,11 @@ def L():
     return lib
 
 
-@pytest.mark.parametrize("policy,switch", [(0, False), (2, False), (0, True), (3, True)])
-def test_two_handles_candidates_merge_equal_single_rank(L, policy, switch):
-    seed, B, G, R = 41, 6, 2, 16
+@pytest.mark.parametrize("policy,switch,G", [(0, False, 2), (2, False, 2), (0, True, 2), (3, True, 2),
+                                             (0, True, 4), (0, False, 8), (3, True, 8)])
+def test_two_handles_candidates_merge_equal_single_rank(L, policy, switch, G):
+    """PIN-G on the device: G handles on one GPU as ranks 0..G-1 (G = 2, 4, 8)."""
+    seed, B, R = 41, 6, 16
     tr = synth.make_trace(40, seed, arrival="poisson", rate_per_s=50.0, len_mu=np.log(30), len_sigma=0.6,
                           len_min=4, len_max=200, beta_ab=(3, 2), drift=True)
     pool = synth.make_pool("f2", V=2048, k=4, dtype="bf16", n_buckets=8, variants=3, seed=seed, device="cuda")

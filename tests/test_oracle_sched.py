@@ -337,10 +337,12 @@ def test_fcfs_and_lpsjf_never_preempt():
 
 
 # ---------------------------------------------------------------- multi-rank merge (PIN-G, oracle side)
-@pytest.mark.parametrize("policy", [oracle.POL_LAPSSD, oracle.POL_LAS, oracle.POL_FCFS])
-def test_sharded_global_topB_equals_single_rank(policy):
+@pytest.mark.parametrize("policy,G", [(oracle.POL_LAPSSD, 2), (oracle.POL_LAS, 2), (oracle.POL_FCFS, 2),
+                                      (oracle.POL_LAPSSD, 4), (oracle.POL_LAPSSD, 8), (oracle.POL_LAS, 8)])
+def test_sharded_global_topB_equals_single_rank(policy, G):
+    """PIN-G: sharding over G = 2, 4, 8 ranks gives every request the single-rank result."""
     tr, P = random_workload(48, 21)
-    B, G = 5, 2
+    B = 5
     cfg = oracle.SchedConfig(policy=policy, K=4, s1_up_us=30 * MS, gamma=3, delta=0.05, k=4,
                              t_ssm_us=1 * MS, t_llm_us=10 * MS, seed=8)
     ref, st_ref, orders = run_sim(cfg, tr.arrival_us, tr.L_true, tr.L_pred, P, B)
