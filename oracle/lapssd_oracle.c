@@ -782,7 +782,7 @@ static uint64_t pack_key(const prio *f)
 }
 
 /* qsort has no context pointer in C11; the simulation is single-threaded. */
-static const orc_sim *g_sort_sim;
+static _Thread_local const orc_sim *g_sort_sim;   /* per thread: concurrent simulations (the all-cores baseline) */
 static int cmp_idx(const void *pa, const void *pb)
 {
     prio a = prio_of(g_sort_sim, *(const int32_t *)pa);

@@ -413,3 +413,32 @@ def test_openmp_build_equals_plain_oracle():
     assert (out[0][0] == out[1][0]).all()
     for f in ("C_us", "acc_draft", "E_us", "key"):
         assert (out[0][1][f] == out[1][1][f]).all()
+
+
+def test_concurrent_simulations_in_threads_equal_sequential():
+    """The all-cores Monte-Carlo baseline runs independent traces in Python threads (the
+    oracle's C calls release the GIL): each trace's result equals its sequential run."""
+    import concurrent.futures as cf
+
+    import synth
+    w = synth.make_mc_workload(8, 30, 3, rate_per_s=30.0, len_mu=np.log(20), len_sigma=0.5, len_min=2,
+                               len_max=60, n_buckets=4, variants=2, R=8)
+    pool = synth.make_pool("f2", V=256, k=4, dtype="bf16", n_buckets=4, variants=2, seed=3, device="cpu")
+    P = pool.numpy()
+    cfg = oracle.SchedConfig(k=4, seed=9, s1_up_us=40 * MS)
+
+    def run(t):
+        a, lt, lp, tab = w.trace(t)
+        sim = oracle.Sim(cfg, a, lt, lp, trace=t)
+        Pt = dict(P, slab_tab=np.ascontiguousarray(tab), R=8)
+        sel, _ = sim.select(1)
+        for _ in range(5000):
+            if sim.step(Pt, sel)[0] == 0 and sim.state()["done"].all():
+                break
+        return sim.state()["C_us"]
+
+    seq = [run(t) for t in range(8)]
+    with cf.ThreadPoolExecutor(8) as ex:
+        par = list(ex.map(run, range(8)))
+    for a, b in zip(seq, par):
+        assert (a == b).all()
