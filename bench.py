@@ -256,7 +256,6 @@ def run_ours(args):
         h.laps_merge(cand[W:], Cn, B)
         h.set_peers(Cn)
         peer = True
-        args.no_profile = True
     elif args.dist_path:
         # the N>1 step (laps_step_dist: candidates + ncclAllGather + merge) on one rank, to
         # time its cost on the one GPU available; a one-rank gloo group only carries the
@@ -270,10 +269,10 @@ def run_ours(args):
         h.laps_candidates(Cn, cand[:W])
         cand[W:].copy_(cand[:W])
         h.laps_merge(cand[W:], Cn, B)
-        args.no_profile = True
     else:
         h.laps_select(B)
     G = min(args.graph_steps, args.steps) if args.graph_steps > 0 else 0
+    plain = world == 1 and not peer and comm is None   # laps_step: the library's per-kernel events
     # r of every step: rows [0, warmup) warm-up, [warmup, warmup + steps) the timed steps,
     # the last row scratch (the instrumented replay)
     hist = torch.full((args.warmup + args.steps + 1, B), -1, dtype=torch.int32, device=dev)
@@ -281,9 +280,9 @@ def run_ours(args):
 
     def step(t):
         if peer:
-            h.laps_step_peer(rows, B)
+            h.laps_step_peer(rows, B, n_accept=hist[t])
         elif comm is not None:
-            h.laps_step_dist(comm, rows, B, Cn, cand)
+            h.laps_step_dist(comm, rows, B, Cn, cand, n_accept=hist[t])
         else:
             h.laps_step(rows, B, n_accept=hist[t])
 
@@ -300,7 +299,7 @@ def run_ours(args):
         # enqueue cost is removed; the side stream's fork/join is in the graph), each graph
         # writing its steps' r to their own rows of hist (the roofline's bytes are those of
         # exactly the timed steps)
-        if world == 1:
+        if plain:
             h.profile(0)
         c0 = L.launch_count()
         for g0 in range(0, args.steps, G):
@@ -310,7 +309,7 @@ def run_ours(args):
                     step(args.warmup + t)
             graphs.append(gr)
         launches_per_step = (L.launch_count() - c0) / args.steps
-        if world == 1 and not args.no_profile:
+        if plain and not args.no_profile:
             # a second graph of G steps with the library's per-kernel CUDA events,
             # replayed right after the timed region (events add graph nodes, so they are
             # kept out of the timed replays)
@@ -321,7 +320,7 @@ def run_ours(args):
                     step(scratch_row)
         torch.cuda.synchronize()
         upload_graphs(graphs + ([g_prof] if g_prof is not None else []))
-    elif world == 1 and not args.no_profile:
+    elif plain and not args.no_profile:
         h.profile(args.steps)
     st0 = h.state()
     launches0 = L.launch_count()
@@ -398,13 +397,21 @@ def run_ours(args):
                                    "above includes the exchange (it runs beside the verify kernel)"}
     if device_error:
         out["device_error"] = device_error
-    if world == 1 and not args.no_profile:
-        v_ms, s_ms, p_ms, n_prof = h.profile_read()
-        # algorithmic bytes of exactly the timed steps (their r_b rows of hist)
+    if not args.no_profile:
+        v_ms = s_ms = p_ms = None
+        n_prof = 1
+        if plain:
+            v_ms, s_ms, p_ms, n_prof = h.profile_read()
+        # algorithmic bytes of exactly the timed steps (their r_b rows of hist); at N > 1
+        # each rank's verify launch reads its own slots' rows: the mean over ranks
         n_acc = hist[args.warmup:args.warmup + args.steps].cpu().numpy()
         alg = algorithmic_bytes(n_acc, args.V, args.k)
         per_launch = alg / n_acc.shape[0]
-        avg_v = v_ms / n_prof
+        if dist:
+            pl = torch.tensor([per_launch], dtype=torch.float64, device=dev)
+            dist.all_reduce(pl, op=dist.ReduceOp.SUM)
+            per_launch = float(pl[0]) / world
+        avg_v = v_ms / n_prof if v_ms is not None else None
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
         peak = peaks.get("hbm_gbs")
@@ -429,25 +436,35 @@ def run_ours(args):
                     traffic_note = "ncu capture on file is for another build: not reported"
             except (OSError, ValueError):
                 traffic = None
-        out["roofline"] = {"kernel": "verify_kernel<bf16> (laps_step)", "bound": "hbm",
+        kern = "laps_step" if world == 1 and not peer and comm is None else (
+            "laps_step_peer" if peer else "laps_step_dist")
+        out["roofline"] = {"kernel": f"verify_kernel<bf16> ({kern}; per rank)" if world > 1
+                           else f"verify_kernel<bf16> ({kern})", "bound": "hbm",
                            "achieved": achieved, "peak": peak, "unit": "GB/s",
                            "frac": achieved / peak, "peak_source": peak_src,
                            "frac_of_8TBs": achieved / 8000.0,
                            "algorithmic_bytes_per_launch": per_launch, "traffic": traffic,
                            "traffic_source": traffic_note,
                            "verify_interval_ms": interval_ms,
-                           "verify_ms_avg_instrumented": avg_v, "select_ms_avg": s_ms / n_prof,
-                           "presort_end_ms_avg": p_ms / n_prof,
+                           "verify_ms_avg_instrumented": avg_v,
+                           "select_ms_avg": s_ms / n_prof if s_ms is not None else None,
+                           "presort_end_ms_avg": p_ms / n_prof if p_ms is not None else None,
                            "timing": (f"achieved = algorithmic bytes per verify launch / launch interval in the "
                                       f"timed region ({args.steps} steps as replays of an uninstrumented "
                                       f"CUDA graph of {G} steps, one verify launch per step, CUDA events "
                                       f"around it); per-kernel CUDA events from a second, "
                                       f"instrumented graph of {G} steps replayed right after "
                                       f"({prof_ms / G * 1e3 if prof_ms else 0:.1f} us/step instrumented)"
-                                      if G else "eager laps_step calls, events on every step")}
+                                      if G and plain else
+                                      f"achieved = mean over ranks of the algorithmic bytes per verify launch / "
+                                      f"launch interval (max over ranks) in the timed region" if not plain
+                                      else "eager laps_step calls, events on every step")}
         if not args.no_e2e:
-            out["e2e"] = run_e2e(args, L, local, pool, cfg, dev)
-        if not args.no_cpu_baseline:
+            if plain:
+                out["e2e"] = run_e2e(args, L, local, pool, cfg, dev)
+            elif world > 1 or peer:
+                out["e2e"] = run_e2e_multi(args, L, local, pool, tab, cfg, dev, dist, rank, world, Cn, peer)
+        if not args.no_cpu_baseline and plain:
             out["cpu_baseline"] = run_cpu_baseline(args, local, pool, tab, cfg)
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -512,6 +529,93 @@ def run_e2e(args, L, local, pool, cfg, dev):
             "path": "laps_step C-ABI; batch-layout rows in pinned host memory read in place over PCIe "
                     "(UVA zero-copy bulk copies and gathers: only the bytes the step needs); batch, "
                     "accepted counts and tokens read back to pinned host memory every step"}
+
+
+def run_e2e_multi(args, L, local, pool, tab, cfg, dev, dist, rank, world, Cn, peer, host_slabs=64):
+    """e2e at N > 1: every rank runs the multi-GPU step through the C-ABI (laps_step_peer,
+    or laps_step_dist on the NCCL form) on a fresh handle of its shard, with the slab pool
+    in PINNED HOST memory (the first host_slabs slabs; the table maps every request onto
+    them) read in place over PCIe, and reads back its batch, accepted counts and tokens
+    every step.  Time: CUDA events per rank, the max over ranks; bytes: summed over ranks."""
+    B = args.batch * world
+    k, V = args.k, args.V
+    S = min(host_slabs, pool.S)
+    hp, hq, hd = pool.p[:S].cpu().pin_memory(), pool.q[:S].cpu().pin_memory(), pool.draft[:S].cpu().pin_memory()
+    rows = L.Rows(hp, hq, hd, torch.as_tensor(np.ascontiguousarray(tab % S), device=dev))
+    h = L.Handle(cfg, local.arrival_us, local.L_true, local.L_pred, max_batch=B, V=V, rank=rank, world=world,
+                 overlap=True)
+    W = 2 * Cn + 1
+    cand = torch.zeros((world + 1) * W, dtype=torch.int64, device=dev)
+    h.laps_candidates(Cn, cand[:W])
+    if dist:
+        dist.all_gather_into_tensor(cand[W:], cand[:W])
+    else:
+        cand[W:].copy_(cand[:W])
+    h.laps_merge(cand[W:], Cn, B)
+    comm = None
+    if peer:
+        h.set_peers(Cn)
+    else:
+        comm = L.nccl_comm()
+    tok = torch.empty(B, k + 1, dtype=torch.int32, device=dev)
+    nacc = torch.empty(B, dtype=torch.int32, device=dev)
+    out_sel = torch.empty(B, dtype=torch.int32).pin_memory()
+    out_nacc = torch.empty(B, dtype=torch.int32).pin_memory()
+    out_tok = torch.empty(B, k + 1, dtype=torch.int32).pin_memory()
+    s = torch.cuda.current_stream()
+    h2d = []
+
+    def one():
+        if peer:
+            h.laps_step_peer(rows, B, tokens=tok, n_accept=nacc)
+        else:
+            h.laps_step_dist(comm, rows, B, Cn, cand, tokens=tok, n_accept=nacc)
+        out_sel.copy_(h.sel[:B], non_blocking=True)
+        out_nacc.copy_(nacc, non_blocking=True)
+        out_tok.copy_(tok, non_blocking=True)
+        s.synchronize()
+        r = out_nacc.numpy()
+        r = r[r >= 0]
+        h2d.append(int((np.where(r < k, 2, 1) * V * 2 + 4 * k + 2 * 2 * np.minimum(r + 1, k)).sum()))
+
+    one()
+    h2d.clear()
+    st0 = h.state()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.e2e_steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    verified = int((h.state()["rounds"] - st0["rounds"]).sum())
+    err = h.check_flags()
+    agg = torch.tensor([ms, float(verified), float(np.mean(h2d) if h2d else 0.0), float(err)],
+                       dtype=torch.float64, device=dev)
+    mx, sm = agg.clone(), agg.clone()
+    if dist:
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    if comm is not None:
+        L.nccl_comm_destroy(comm)
+    if dist:
+        dist.barrier()
+    h.close()
+    ms_max = float(mx[0])
+    d2h = (B + B + B * (k + 1)) * 4 * world
+    res = {"value": float(sm[1]) * k / (ms_max * 1e-3), "unit": UNIT,
+           "h2d_bytes_per_step": int(sm[2]), "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+           "ms_per_step": ms_max / args.e2e_steps,
+           "path": f"{'laps_step_peer' if peer else 'laps_step_dist'} C-ABI on every rank; the slab pool "
+                   f"({S} slabs) in pinned host memory read in place over PCIe (UVA: only the bytes the step "
+                   "needs); each rank's batch, accepted counts and tokens read back every step; max over "
+                   "ranks of the CUDA-event time, bytes summed over ranks"}
+    if float(mx[3]) != 0:
+        res["device_error_flags"] = int(mx[3])
+    return res
 
 
 def host_info():

@@ -346,13 +346,16 @@ lapssd_status lapssd_set_row_check(lapssd_handle *h, int32_t enable);
  * ncclComm_t created by the caller) + merge, with the results of that sequence; with
  * pooled rows the candidates / all-gather / merge run on the side stream beside the
  * verify kernel as in laps_step.  NCCL is resolved at run time with
- * dlopen("libnccl.so.2"); if unavailable the call returns ENCCL. */
+ * dlopen("libnccl.so.2"); if unavailable the call returns ENCCL.  tokens_out [device,
+ * B_global x (k+1)] and n_accept_out [device, B_global] (nullable) receive this rank's
+ * slots' results as in laps_step (slots [count, B_global) of this rank: r = -1). */
 lapssd_status laps_candidates(lapssd_handle *h, int32_t C, uint64_t *cand_out,
                               lapssd_stream stream);
 lapssd_status laps_merge(lapssd_handle *h, const uint64_t *all_cand, int32_t C, int32_t B,
                          int32_t *sel_out, int32_t *count_out, lapssd_stream stream);
 lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_rows *rows,
                              int32_t B_global, int32_t C, int32_t *sel_inout, int32_t *count_out,
+                             int32_t *tokens_out, int32_t *n_accept_out,
                              uint64_t *cand_scratch /* [device] (world+1)*(2C+1) words */,
                              lapssd_stream stream);
 /* laps_step_candidates -- laps_step_dist without the collective: verify + update of this
@@ -362,7 +365,8 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
  * rank order) and calls laps_merge(h, all, C, B_global, sel_inout, ...); the two calls
  * together have the results of laps_step_dist.  Errors: EINVAL, ECUDA. */
 lapssd_status laps_step_candidates(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t C,
-                                   int32_t *sel_inout, uint64_t *cand_out, lapssd_stream stream);
+                                   int32_t *sel_inout, int32_t *tokens_out, int32_t *n_accept_out,
+                                   uint64_t *cand_out, lapssd_stream stream);
 /* laps_step_peer -- the multi-GPU step with the exchange FUSED into the select kernel
  * over peer memory (NVLink / NVSwitch; no collective launch): the verify kernel as in
  * laps_step, and beside it the side select builds this rank's candidate block (C keys,
@@ -376,11 +380,13 @@ lapssd_status laps_step_candidates(lapssd_handle *h, const lapssd_rows *rows, in
  * and lapssd_set_peers(h, peer_bufs, C, stream) passes the world device pointers valid in
  * this process (peer_bufs[rank] = its own buffer; [host] array).  The first batch comes
  * from laps_candidates + an all-gather + laps_merge.  C as below; rows pooled; B_global
- * <= 4096.  All ranks call laps_step_peer in lockstep.  Errors: EINVAL, ECUDA. */
+ * <= 4096.  tokens_out / n_accept_out as laps_step_dist.  All ranks call laps_step_peer
+ * in lockstep.  Errors: EINVAL, ECUDA. */
 size_t lapssd_peer_buffer_bytes(int32_t world, int32_t C);
 lapssd_status lapssd_set_peers(lapssd_handle *h, void *const *peer_bufs, int32_t C, lapssd_stream stream);
 lapssd_status laps_step_peer(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t *sel_inout,
-                             int32_t *count_out, lapssd_stream stream);
+                             int32_t *count_out, int32_t *tokens_out, int32_t *n_accept_out,
+                             lapssd_stream stream);
 /* C must be the same on every rank and world*C <= 16384: the caller passes
  * C = min(B_global, max over ranks of n_local).  sel_inout has B_global slots.
  * NCCL plumbing without torch internals: rank 0 calls lapssd_nccl_unique_id, the

@@ -84,11 +84,11 @@ def _load():
         "lapssd_set_row_check": ([vp, i32], i32),
         "laps_candidates": ([vp, i32, vp, vp], i32),
         "laps_merge": ([vp, vp, i32, i32, vp, vp, vp], i32),
-        "laps_step_dist": ([vp, vp, vp, i32, i32, vp, vp, vp, vp], i32),
-        "laps_step_candidates": ([vp, vp, i32, i32, vp, vp, vp], i32),
+        "laps_step_dist": ([vp, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp], i32),
+        "laps_step_candidates": ([vp, vp, i32, i32, vp, vp, vp, vp, vp], i32),
         "lapssd_peer_buffer_bytes": ([i32, i32], sz),
         "lapssd_set_peers": ([vp, vp, i32, vp], i32),
-        "laps_step_peer": ([vp, vp, i32, vp, vp, vp], i32),
+        "laps_step_peer": ([vp, vp, i32, vp, vp, vp, vp, vp], i32),
         "lapssd_nccl_unique_id": ([vp], i32),
         "lapssd_nccl_comm_init": ([vp, i32, vp, i32], i32),
         "lapssd_nccl_comm_destroy": ([vp], i32),
@@ -271,7 +271,8 @@ class SchedConfig:
 
 
 class Rows:
-    """lapssd_rows: pooled (slab_tab given) or batch layout, device tensors."""
+    """lapssd_rows: pooled (slab_tab given) or batch layout; p, q, draft device or pinned host
+    tensors (read in place over UVA), slab_tab a device tensor."""
 
     def __init__(self, p, q, draft, slab_tab=None):
         self.p, self.q, self.draft, self.slab_tab = p, q, draft, slab_tab
@@ -357,20 +358,22 @@ class Handle:
         return sel, count
 
     def laps_step_dist(self, comm, rows: Rows, B_global, Cn, cand_scratch, sel=None, count=None,
-                       stream=None):
+                       tokens=None, n_accept=None, stream=None):
         sel = self.sel if sel is None else sel
         count = self.count if count is None else count
         _check("laps_step_dist", _lib.laps_step_dist(self.h, comm, C.byref(rows.c), B_global, Cn,
-                                                     _dptr(sel), _dptr(count), _dptr(cand_scratch),
-                                                     _stream(stream)))
+                                                     _dptr(sel), _dptr(count), _dptr(tokens), _dptr(n_accept),
+                                                     _dptr(cand_scratch), _stream(stream)))
         return sel, count
 
-    def laps_step_candidates(self, rows: Rows, B_global, Cn, cand_out, sel=None, stream=None):
+    def laps_step_candidates(self, rows: Rows, B_global, Cn, cand_out, sel=None, tokens=None, n_accept=None,
+                             stream=None):
         """verify + update of this rank's slots, then its candidate block (2 Cn + 1 words)
         into cand_out; the caller all-gathers the blocks and calls laps_merge."""
         sel = self.sel if sel is None else sel
         _check("laps_step_candidates", _lib.laps_step_candidates(self.h, C.byref(rows.c), B_global, Cn,
-                                                                 _dptr(sel), _dptr(cand_out), _stream(stream)))
+                                                                 _dptr(sel), _dptr(tokens), _dptr(n_accept),
+                                                                 _dptr(cand_out), _stream(stream)))
         return sel
 
     def set_peers(self, Cn, group=None, stream=None):
@@ -392,11 +395,12 @@ class Handle:
         ptrs = (C.c_void_p * self.world)(*[b.data_ptr() for b in bufs])
         _check("lapssd_set_peers", _lib.lapssd_set_peers(self.h, ptrs, Cn, _stream(stream)))
 
-    def laps_step_peer(self, rows: Rows, B_global, sel=None, count=None, stream=None):
+    def laps_step_peer(self, rows: Rows, B_global, sel=None, count=None, tokens=None, n_accept=None,
+                       stream=None):
         sel = self.sel if sel is None else sel
         count = self.count if count is None else count
         _check("laps_step_peer", _lib.laps_step_peer(self.h, C.byref(rows.c), B_global, _dptr(sel), _dptr(count),
-                                                     _stream(stream)))
+                                                     _dptr(tokens), _dptr(n_accept), _stream(stream)))
         return sel, count
 
     # -- snapshot -----------------------------------------------------------------

@@ -777,9 +777,10 @@ lapssd_status lapssd_nccl_comm_destroy(void *comm) {
 // exchanges the blocks with any collective and calls laps_merge.
 static lapssd_status step_dist(lapssd_handle *h, void *nccl_comm, nccl_allgather_t allgather, const lapssd_rows *rows,
                                int32_t B_global, int32_t C, int32_t *sel_inout, int32_t *count_out,
-                               uint64_t *cand_scratch, cudaStream_t s, const char *who) {
+                               int32_t *tokens_out, int32_t *n_accept_out, uint64_t *cand_scratch, cudaStream_t s,
+                               const char *who) {
     VerifyArgs a;
-    lapssd_status st = fill_step_verify(h, rows, B_global, sel_inout, nullptr, nullptr, a);
+    lapssd_status st = fill_step_verify(h, rows, B_global, sel_inout, tokens_out, n_accept_out, a);
     if (st != LAPSSD_OK) return st;
     a.count_dev = &h->st.g->count;   // this rank's slots are [0, count) of the B_global
     h->last_stream = s;
@@ -848,8 +849,8 @@ static lapssd_status step_dist(lapssd_handle *h, void *nccl_comm, nccl_allgather
 }
 
 lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_rows *rows, int32_t B_global,
-                             int32_t C, int32_t *sel_inout, int32_t *count_out, uint64_t *cand_scratch,
-                             lapssd_stream stream) {
+                             int32_t C, int32_t *sel_inout, int32_t *count_out, int32_t *tokens_out,
+                             int32_t *n_accept_out, uint64_t *cand_scratch, lapssd_stream stream) {
     g_last_error.clear();
     if (h) { h->side_chained = false; h->wl.valid = 0; }
     if (!h || !nccl_comm || !cand_scratch || B_global < 1 || B_global > h->max_batch || C < 1)
@@ -858,8 +859,8 @@ lapssd_status laps_step_dist(lapssd_handle *h, void *nccl_comm, const lapssd_row
         return fail(LAPSSD_EINVAL, "world*C exceeds %d", sort_capacity());
     auto allgather = nccl_sym<nccl_allgather_t>("ncclAllGather");
     if (!allgather) return fail(LAPSSD_ENCCL, "ncclAllGather not found");
-    return step_dist(h, nccl_comm, allgather, rows, B_global, C, sel_inout, count_out, cand_scratch,
-                     (cudaStream_t)stream, "laps_step_dist");
+    return step_dist(h, nccl_comm, allgather, rows, B_global, C, sel_inout, count_out, tokens_out, n_accept_out,
+                     cand_scratch, (cudaStream_t)stream, "laps_step_dist");
 }
 
 size_t lapssd_peer_buffer_bytes(int32_t world, int32_t C) {
@@ -881,7 +882,7 @@ lapssd_status lapssd_set_peers(lapssd_handle *h, void *const *peer_bufs, int32_t
 }
 
 lapssd_status laps_step_peer(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t *sel_inout,
-                             int32_t *count_out, lapssd_stream stream) {
+                             int32_t *count_out, int32_t *tokens_out, int32_t *n_accept_out, lapssd_stream stream) {
     g_last_error.clear();
     if (!h || B_global < 1 || B_global > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B_global");
     if (!h->peer_C) return fail(LAPSSD_EINVAL, "no peers set (lapssd_set_peers)");
@@ -890,7 +891,7 @@ lapssd_status laps_step_peer(lapssd_handle *h, const lapssd_rows *rows, int32_t 
     if (!rows || !rows->slab_tab || bp > 4096 || h->peer_C > B_global)
         return fail(LAPSSD_EINVAL, "laps_step_peer needs pooled rows, B_global <= 4096 and C <= B_global");
     VerifyArgs a;
-    lapssd_status st = fill_step_verify(h, rows, B_global, sel_inout, nullptr, nullptr, a);
+    lapssd_status st = fill_step_verify(h, rows, B_global, sel_inout, tokens_out, n_accept_out, a);
     if (st != LAPSSD_OK) return st;
     a.count_dev = &h->st.g->count;   // this rank's slots are [0, count) of the B_global
     cudaStream_t s = (cudaStream_t)stream;
@@ -950,15 +951,16 @@ lapssd_status laps_step_peer(lapssd_handle *h, const lapssd_rows *rows, int32_t 
 }
 
 lapssd_status laps_step_candidates(lapssd_handle *h, const lapssd_rows *rows, int32_t B_global, int32_t C,
-                                   int32_t *sel_inout, uint64_t *cand_out, lapssd_stream stream) {
+                                   int32_t *sel_inout, int32_t *tokens_out, int32_t *n_accept_out,
+                                   uint64_t *cand_out, lapssd_stream stream) {
     g_last_error.clear();
     if (h) { h->side_chained = false; h->wl.valid = 0; }
     if (!h || !cand_out || B_global < 1 || B_global > h->max_batch || C < 1)
         return fail(LAPSSD_EINVAL, "handle / cand_out / B_global / C");
     if ((int64_t)h->sc.world * C > sort_capacity())
         return fail(LAPSSD_EINVAL, "world*C exceeds %d", sort_capacity());
-    return step_dist(h, nullptr, nullptr, rows, B_global, C, sel_inout, nullptr, cand_out, (cudaStream_t)stream,
-                     "laps_step_candidates");
+    return step_dist(h, nullptr, nullptr, rows, B_global, C, sel_inout, nullptr, tokens_out, n_accept_out,
+                     cand_out, (cudaStream_t)stream, "laps_step_candidates");
 }
 
 // ---------------------------------------------------------------- snapshot / check

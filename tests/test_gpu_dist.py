@@ -132,14 +132,19 @@ def test_laps_step_dist_one_rank_lockstep(L, monkeypatch, switch):
         h.laps_candidates(Cn, cand[:W])
         cand[W:].copy_(cand[:W])
         h.laps_merge(cand[W:], Cn, B)
+        tok = torch.empty(B, 5, dtype=torch.int32, device="cuda")
+        nacc = torch.empty(B, dtype=torch.int32, device="cuda")
         sel_o, _ = sim.select(B)
         for step in range(400):
             sel_g = h.sel[:B].cpu().numpy()
             assert (sel_g == sel_o).all(), f"step {step}: batch differs"
             if sim.state()["done"].all():
                 break
-            h.laps_step_dist(comm, rows, B, Cn, cand)
-            sim.step(P, sel_o)
+            h.laps_step_dist(comm, rows, B, Cn, cand, tokens=tok, n_accept=nacc)
+            _, tok_o, na_o, _ = sim.step(P, sel_o)
+            live = sel_g >= 0
+            assert (nacc.cpu().numpy()[live] == na_o[live]).all(), f"step {step}: r differs"
+            assert (tok.cpu().numpy()[live] == tok_o[live]).all(), f"step {step}: tokens differ"
             if step % 4 == 0:
                 g, o = h.state(), sim.state()
                 for f in ("acc_tok", "acc_draft", "rounds", "E_us", "C_us", "level", "perceptible",
@@ -209,10 +214,11 @@ def test_laps_step_dist_one_rank_graph_replay(L, monkeypatch):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("switch", [False, True])
-def test_laps_step_peer_one_rank_lockstep(L, switch):
+@pytest.mark.parametrize("switch,host", [(False, False), (True, False), (False, True)])
+def test_laps_step_peer_one_rank_lockstep(L, switch, host):
     """laps_step_peer (the exchange fused into the select kernel over peer memory) with
-    one rank, step by step against the oracle; then captured in a CUDA graph and replayed."""
+    one rank, step by step against the oracle; with host=True the slab pool lives in
+    pinned host memory (bench.py's e2e at N > 1)."""
     seed, B, R = 53, 16, 16
     tr = synth.make_trace(120, seed, arrival="poisson", rate_per_s=60.0, len_mu=np.log(30),
                           len_sigma=0.6, len_min=4, len_max=200, beta_ab=(4, 2), drift=True)
@@ -228,7 +234,11 @@ def test_laps_step_peer_one_rank_lockstep(L, switch):
     sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, prompt=pr)
     h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=4096, prompt=pr,
                  overlap=True)
-    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
+    if host:
+        rows = L.Rows(pool.p.cpu().pin_memory(), pool.q.cpu().pin_memory(), pool.draft.cpu().pin_memory(),
+                      torch.as_tensor(tab, device="cuda"))
+    else:
+        rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
     Cn = B
     W = 2 * Cn + 1
     cand = torch.zeros(2 * W, dtype=torch.int64, device="cuda")
@@ -236,14 +246,20 @@ def test_laps_step_peer_one_rank_lockstep(L, switch):
     cand[W:].copy_(cand[:W])
     h.laps_merge(cand[W:], Cn, B)
     h.set_peers(Cn)
+    tok = torch.empty(B, 5, dtype=torch.int32, device="cuda")
+    nacc = torch.empty(B, dtype=torch.int32, device="cuda")
     sel_o, _ = sim.select(B)
     for step in range(400):
         sel_g = h.sel[:B].cpu().numpy()
         assert (sel_g == sel_o).all(), f"step {step}: batch differs"
         if sim.state()["done"].all():
             break
-        h.laps_step_peer(rows, B)
-        sim.step(P, sel_o)
+        h.laps_step_peer(rows, B, tokens=tok, n_accept=nacc)
+        _, tok_o, na_o, _ = sim.step(P, sel_o)
+        live = sel_g >= 0
+        assert (nacc.cpu().numpy()[live] == na_o[live]).all(), f"step {step}: r differs"
+        assert (tok.cpu().numpy()[live] == tok_o[live]).all(), f"step {step}: tokens differ"
+        assert (nacc.cpu().numpy()[~live] == -1).all()
         if step % 4 == 0:
             g, o = h.state(), sim.state()
             for f in ("acc_tok", "acc_draft", "rounds", "E_us", "C_us", "level", "perceptible", "pinned", "key",

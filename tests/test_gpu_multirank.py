@@ -42,6 +42,22 @@ def _setup(seed, switch):
     return tr, tab, kw, pr
 
 
+def _step_results(sel, nacc, tok, rank):
+    """This rank's live slots of one step: [global id, r, tokens...] rows; every slot past
+    the rank's count must report r = -1."""
+    r, t = nacc.cpu().numpy(), tok.cpu().numpy()
+    live = sel >= 0
+    assert (r[~live] == -1).all()
+    return np.concatenate([(sel[live].astype(np.int64) * G + rank)[:, None], r[live, None], t[live]], axis=1)
+
+
+def _pack(rs, B):
+    out = np.full((len(rs), B, 7), -2, dtype=np.int64)
+    for t, a in enumerate(rs):
+        out[t, :len(a)] = a
+    return out
+
+
 def _worker(rank, port, policy, switch, seed, B, out_dir):
     import torch.distributed as dist
 
@@ -68,7 +84,9 @@ def _worker(rank, port, policy, switch, seed, B, out_dir):
 
     h.laps_candidates(Cn, cand)
     exchange()
-    batches = []
+    batches, rs = [], []
+    tok = torch.empty(B, 5, dtype=torch.int32, device="cuda")
+    nacc = torch.empty(B, dtype=torch.int32, device="cuda")
     for step in range(5000):
         sel = h.sel[:B].cpu().numpy()
         batches.append(sorted(int(i) * G + rank for i in sel if i >= 0))
@@ -76,10 +94,11 @@ def _worker(rank, port, policy, switch, seed, B, out_dir):
         dist.all_reduce(done)
         if int(done) == G:
             break
-        h.laps_step_candidates(rows, B, Cn, cand)
+        h.laps_step_candidates(rows, B, Cn, cand, tokens=tok, n_accept=nacc)
+        rs.append(_step_results(sel, nacc, tok, rank))
         exchange()
     st = h.state()
-    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), steps=len(batches),
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), steps=len(batches), rs=_pack(rs, B),
              batches=np.array([np.array(b + [-1] * (B - len(b))) for b in batches]),
              **{f: st[f] for f in ("C_us", "acc_tok", "rounds", "E_us", "x_us", "switch_us", "level",
                                    "perceptible")},
@@ -107,8 +126,11 @@ def _compare_with_oracle(tmp_path, policy, switch, seed, B):
     sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, prompt=pr)
     sel, _ = sim.select(B)
     ref = [sorted(int(i) for i in sel if i >= 0)]
+    ref_r = []   # per step: global id -> (r, tokens)
     while not sim.state()["done"].all():
-        sim.step(P, sel)
+        ids = sel.copy()
+        _, tok_o, na_o, _ = sim.step(P, sel)
+        ref_r.append({int(i): (int(na_o[j]), tok_o[j]) for j, i in enumerate(ids) if i >= 0})
         ref.append(sorted(int(i) for i in sel if i >= 0))
     o = sim.state()
     R = [np.load(os.path.join(tmp_path, f"rank{g}.npz")) for g in range(G)]
@@ -118,6 +140,12 @@ def _compare_with_oracle(tmp_path, policy, switch, seed, B):
     for t in range(n_steps):   # the global batch of every step (PIN-G)
         got = sorted(int(x) for r in R for x in r["batches"][t] if x >= 0)
         assert got == ref[t], f"step {t}: {got} != {ref[t]}"
+    for t in range(n_steps - 1):   # every slot's r and tokens (the verify outputs of each rank)
+        got = {int(row[0]): (int(row[1]), row[2:]) for r in R for row in r["rs"][t] if row[0] >= 0}
+        assert sorted(got) == sorted(ref_r[t]), f"step {t}: slots"
+        for i, (rr, tt) in got.items():
+            ro, to = ref_r[t][i]
+            assert rr == ro and (tt == to).all(), f"step {t} request {i}: r/tokens differ"
     for g, r in enumerate(R):
         for f in ("C_us", "acc_tok", "rounds", "E_us", "x_us", "switch_us", "level", "perceptible"):
             assert (r[f] == np.asarray(o[f])[g::G]).all(), f"rank {g}: {f} differs"
@@ -151,7 +179,9 @@ def _peer_worker(rank, port, policy, switch, seed, B, out_dir):
     dist.all_gather(parts, cand.cpu())
     h.laps_merge(torch.cat(parts).cuda(), Cn, B)
     h.set_peers(Cn)
-    batches = []
+    batches, rs = [], []
+    tok = torch.empty(B, 5, dtype=torch.int32, device="cuda")
+    nacc = torch.empty(B, dtype=torch.int32, device="cuda")
     for step in range(5000):
         sel = h.sel[:B].cpu().numpy()
         batches.append(sorted(int(i) * G + rank for i in sel if i >= 0))
@@ -159,10 +189,11 @@ def _peer_worker(rank, port, policy, switch, seed, B, out_dir):
         dist.all_reduce(done)
         if int(done) == G:
             break
-        h.laps_step_peer(rows, B)
+        h.laps_step_peer(rows, B, tokens=tok, n_accept=nacc)
+        rs.append(_step_results(sel, nacc, tok, rank))
     torch.cuda.synchronize()
     st = h.state()
-    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), steps=len(batches),
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), steps=len(batches), rs=_pack(rs, B),
              batches=np.array([np.array(b + [-1] * (B - len(b))) for b in batches]),
              **{f: st[f] for f in ("C_us", "acc_tok", "rounds", "E_us", "x_us", "switch_us", "level",
                                    "perceptible")},
