@@ -193,9 +193,13 @@ lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V
  *   t = U * (Z >> 64) + floor(U * (Z mod 2^64) / 2^64), y = min{v : sum_{w<=v} R_w > t}.
  * Outputs [device]: tokens[B, k+1] (x_0..x_{r-1}, y, -1...), n_accept[B] = r,
  * z[B, 2] = (Z mod 2^64, Z >> 64) (nullable).
- * workspace: [device] >= spec_verify_logits_workspace_bytes(B, k) bytes, any content.
+ * Only the rows the tests consult are normalised (pair j only if x_0..x_{j-1} were all
+ * accepted, p_k only if all k were): one launch over a persistent grid with a work queue
+ * (the results do not depend on it; LAPSSD_LOGITS_EAGER=1 normalises every row instead).
+ * workspace: [device] >= spec_verify_logits_workspace_bytes(B, k, V, dtype) bytes, any
+ * content (one call at a time per workspace).
  * Errors: EINVAL (k, V, dtype, alignment, B < 0, NULL), ENOMEM (workspace), ECUDA. */
-size_t spec_verify_logits_workspace_bytes(int32_t B, int32_t k);
+size_t spec_verify_logits_workspace_bytes(int32_t B, int32_t k, int64_t V, int32_t dtype);
 lapssd_status spec_verify_logits(const void *zp, const void *zq, int32_t dtype, int64_t V, int32_t k,
                                  const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
                                  const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,

@@ -70,7 +70,7 @@ def _load():
     sigs = {
         "spec_verify_workspace_bytes": ([i32, i64], sz),
         "spec_verify": ([vp, vp, i32, i64, i32, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp, vp, sz, vp], i32),
-        "spec_verify_logits_workspace_bytes": ([i32, i32], sz),
+        "spec_verify_logits_workspace_bytes": ([i32, i32, i64, i32], sz),
         "spec_verify_logits": ([vp, vp, i32, i64, i32, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp, vp, sz, vp], i32),
         "spec_draft_sample": ([vp, i32, i64, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp], i32),
         "spec_verify_tree": ([vp, vp, i32, i64, i32, vp, vp, vp, vp, i32, u64, u32, vp, vp, vp, vp, vp], i32),
@@ -181,6 +181,12 @@ def spec_verify(p, q, draft, req_id, round_idx, seed, *, slab=None, trace=0, tok
     return tokens, n_accept, z
 
 
+def spec_verify_logits_workspace_bytes(B, k, V, dtype) -> int:
+    """Workspace bytes of spec_verify_logits; dtype "bf16" / "f32" or the lapssd code."""
+    code = {"bf16": BF16, "f32": F32}.get(dtype, dtype)
+    return int(_lib.spec_verify_logits_workspace_bytes(B, k, V, code))
+
+
 def spec_verify_logits(zp, zq, draft, req_id, round_idx, seed, *, slab=None, trace=0, tokens=None,
                        n_accept=None, z=None, workspace=None, stream=None):
     """Batched verification from logits (include/lapssd.h spec_verify_logits, SURVEY
@@ -196,7 +202,7 @@ def spec_verify_logits(zp, zq, draft, req_id, round_idx, seed, *, slab=None, tra
         n_accept = torch.empty(B, dtype=torch.int32, device=dev)
     if z is None:
         z = torch.empty(B, 2, dtype=torch.int64, device=dev)
-    ws_bytes = int(_lib.spec_verify_logits_workspace_bytes(B, k))
+    ws_bytes = int(_lib.spec_verify_logits_workspace_bytes(B, k, V, _dtype_code(zp)))
     if workspace is None:
         workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
     rc = _lib.spec_verify_logits(_dptr(zp), _dptr(zq), _dtype_code(zp), V, k, _dptr(draft), _dptr(slab),

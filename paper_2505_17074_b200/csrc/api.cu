@@ -318,12 +318,14 @@ lapssd_status spec_verify(const void *p, const void *q, int32_t dtype, int64_t V
 }
 
 // ---------------------------------------------------------------- f1: verify from logits
-size_t spec_verify_logits_workspace_bytes(int32_t B, int32_t k) {
-    if (B < 0 || k < 1 || k > 16) return 0;
-    const size_t rows = (size_t)(B > 0 ? B : 1) * (size_t)(2 * k + 1);
+size_t spec_verify_logits_workspace_bytes(int32_t B, int32_t k, int64_t V, int32_t dtype) {
+    if (B < 0 || k < 1 || k > 16 || V < 1 || (dtype != LAPSSD_BF16 && dtype != LAPSSD_F32)) return 0;
+    const int32_t Bn = B > 0 ? B : 1;
+    const size_t rows = (size_t)Bn * (size_t)(2 * k + 1);
     Carver cv{nullptr};
     cv.take<float>(rows);
     cv.take<uint64_t>(rows);
+    cv.take<char>(logits_lazy_bytes(Bn, k, V, dtype));
     return align256(cv.off);
 }
 
@@ -339,16 +341,17 @@ lapssd_status spec_verify_logits(const void *zp, const void *zq, int32_t dtype, 
     if (B == 0) return LAPSSD_OK;
     if (!zp || !zq || !draft || !req_id || !round_idx || !tokens || !n_accept || !workspace)
         return fail(LAPSSD_EINVAL, "NULL pointer argument");
-    if (workspace_bytes < spec_verify_logits_workspace_bytes(B, k))
+    if (workspace_bytes < spec_verify_logits_workspace_bytes(B, k, V, dtype))
         return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes,
-                    spec_verify_logits_workspace_bytes(B, k));
+                    spec_verify_logits_workspace_bytes(B, k, V, dtype));
     prepare_all();
     Carver cv{(char *)workspace};
     const size_t rows = (size_t)B * (size_t)(2 * k + 1);
     float *m_ws = cv.take<float>(rows);
     uint64_t *S_ws = cv.take<uint64_t>(rows);
+    char *lazy_ws = cv.take<char>(logits_lazy_bytes(B, k, V, dtype));
     return cuda_status(launch_verify_logits(zp, zq, dtype, V, k, draft, slab, req_id, round_idx, B, seed, trace,
-                                            tokens, n_accept, z, m_ws, S_ws, (cudaStream_t)stream),
+                                            tokens, n_accept, z, m_ws, S_ws, lazy_ws, (cudaStream_t)stream),
                        "spec_verify_logits");
 }
 

@@ -575,7 +575,8 @@ cudaError_t launch_verify_logits(const void *zp, const void *zq, int32_t dtype, 
                                  const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
                                  const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,
                                  int32_t *tokens, int32_t *n_accept, uint64_t *z, float *m_ws, uint64_t *S_ws,
-                                 cudaStream_t s);
+                                 char *lazy_ws, cudaStream_t s);
+size_t logits_lazy_bytes(int32_t B, int32_t k, int64_t V, int32_t dtype);   // the lazy form's workspace
 void verify_logits_prepare();
 // f4 (draft_tree.cu)
 cudaError_t launch_draft_sample(const void *q, int32_t dtype, int64_t V, const int32_t *row_idx,

@@ -33,7 +33,11 @@ typedef unsigned __int128 u128;
 // clamp keeps 2^n normal.
 __device__ __forceinline__ void e40x2(float za, float zb, float ma, float mb, uint64_t &ea, uint64_t &eb) {
     const float2 d0 = __fadd2_rn(make_float2(za, zb), make_float2(-ma, -mb));
+#ifdef LAPSSD_E40_UPPER_CLAMP
     const float2 d = make_float2(fmaxf(fminf(d0.x, 0.0f), -28.5f), fmaxf(fminf(d0.y, 0.0f), -28.5f));
+#else   // z <= m (m is the row max), so fl32(z - m) <= 0: only the lower clamp can act
+    const float2 d = make_float2(fmaxf(d0.x, -28.5f), fmaxf(d0.y, -28.5f));
+#endif
     const float2 x = __fmul2_rn(d, make_float2(0x1.715476p+0f, 0x1.715476p+0f));
     const float2 big = __fadd2_rn(x, make_float2(0x1.8p23f, 0x1.8p23f));
     const float2 nf = __fadd2_rn(big, make_float2(-0x1.8p23f, -0x1.8p23f));
@@ -106,23 +110,31 @@ constexpr int kLogitThreads = LAPSSD_SAMPLE_THREADS;   // sample kernel: one slo
 // pass hits L2, and a 4-8 CTA cluster holding the row in shared memory, were slower).
 constexpr int kNormThreads = 512;
 
+#ifndef LAPSSD_NORM_ILP
+#define LAPSSD_NORM_ILP 4
+#endif
+constexpr int kNormIlp = LAPSSD_NORM_ILP;
+
+// Block-wide max of the logits in vectors [lo, hi) of a row (every thread gets it).
 template <bool BF16>
-__global__ void __launch_bounds__(kNormThreads) logits_norm_kernel(const char *zp, const char *zq,
-                                                                   const int32_t *slab, int64_t V, int32_t k,
-                                                                   float *m_out, uint64_t *S_out) {
+__device__ __forceinline__ float range_max(const uint4 *v4, int64_t lo, int64_t hi) {
     using E = LElt<BF16>;
-    const int rows = 2 * k + 1;
-    const int b = blockIdx.x / rows, ri = blockIdx.x % rows;
-    const int64_t s = slab ? slab[b] : b;
-    const char *row = ri <= k ? zp + ((s * (k + 1) + ri) * V) * E::kEsz
-                              : zq + ((s * k + (ri - k - 1)) * V) * E::kEsz;
-    const uint4 *v4 = reinterpret_cast<const uint4 *>(row);
-    const int64_t nv = V / E::kVec;
-    __shared__ float s_m[kNormThreads / 32];
-    __shared__ uint64_t s_S[kNormThreads / 32];
+    __shared__ float s_m[32];
+    constexpr int U = kNormIlp;
+    const int64_t bd = blockDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     float m = -INFINITY;
-    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    int64_t i = lo + threadIdx.x;
+    for (; i + (U - 1) * bd < hi; i += U * bd) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = v4[i + u * bd];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int e = 0; e < E::kVec; ++e) m = fmaxf(m, E::get(v[u], e));
+    }
+    for (; i < hi; i += bd) {
         const uint4 v = v4[i];
 #pragma unroll
         for (int e = 0; e < E::kVec; ++e) m = fmaxf(m, E::get(v, e));
@@ -133,8 +145,35 @@ __global__ void __launch_bounds__(kNormThreads) logits_norm_kernel(const char *z
     __syncthreads();
     m = s_m[0];
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, s_m[w]);
+    __syncthreads();   // s_m may be reused by the next call
+    return m;
+}
+
+// Block-wide integer mass sum E[v] over vectors [lo, hi) for the row max m (thread 0
+// gets the total).  kNormIlp independent 16-byte loads in flight per thread.
+template <bool BF16>
+__device__ __forceinline__ uint64_t range_sum(const uint4 *v4, int64_t lo, int64_t hi, float m) {
+    using E = LElt<BF16>;
+    __shared__ uint64_t s_S[32];
+    constexpr int U = kNormIlp;
+    const int64_t bd = blockDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint64_t S = 0;
-    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    int64_t i = lo + threadIdx.x;
+    for (; i + (U - 1) * bd < hi; i += U * bd) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = v4[i + u * bd];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int e = 0; e < E::kVec; e += 2) {
+                uint64_t a, c;
+                e40x2(E::get(v[u], e), E::get(v[u], e + 1), m, m, a, c);
+                S += a + c;
+            }
+    }
+    for (; i < hi; i += bd) {
         const uint4 v = v4[i];
 #pragma unroll
         for (int e = 0; e < E::kVec; e += 2) {
@@ -147,12 +186,45 @@ __global__ void __launch_bounds__(kNormThreads) logits_norm_kernel(const char *z
     for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(0xFFFFFFFFu, S, o);
     if (lane == 0) s_S[warp] = S;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t t = 0;
+    uint64_t t = 0;
+    if (threadIdx.x == 0)
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_S[w];
+    __syncthreads();
+    return t;
+}
+
+template <bool BF16>
+__device__ __forceinline__ const uint4 *row_ptr(const char *zp, const char *zq, int64_t s, int64_t V, int32_t k,
+                                                int ri) {
+    using E = LElt<BF16>;
+    return reinterpret_cast<const uint4 *>(ri <= k ? zp + ((s * (k + 1) + ri) * V) * E::kEsz
+                                                   : zq + ((s * k + (ri - k - 1)) * V) * E::kEsz);
+}
+
+// Row ri of slot b (target row ri for ri <= k, else draft row ri - k - 1): the max, then
+// the integer mass; thread 0 stores (m, S) to m_out[b*rows + ri], S_out[b*rows + ri].
+template <bool BF16>
+__device__ __forceinline__ void norm_row(const char *zp, const char *zq, const int32_t *slab, int64_t V, int32_t k,
+                                         int b, int ri, float *m_out, uint64_t *S_out) {
+    using E = LElt<BF16>;
+    const int rows = 2 * k + 1;
+    const int64_t s = slab ? slab[b] : b;
+    const uint4 *v4 = row_ptr<BF16>(zp, zq, s, V, k, ri);
+    const int64_t nv = V / E::kVec;
+    const float m = range_max<BF16>(v4, 0, nv);
+    const uint64_t S = range_sum<BF16>(v4, 0, nv, m);
+    if (threadIdx.x == 0) {
         m_out[(int64_t)b * rows + ri] = m;
-        S_out[(int64_t)b * rows + ri] = t;
+        S_out[(int64_t)b * rows + ri] = S;
     }
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kNormThreads) logits_norm_kernel(const char *zp, const char *zq,
+                                                                   const int32_t *slab, int64_t V, int32_t k,
+                                                                   float *m_out, uint64_t *S_out) {
+    const int rows = 2 * k + 1;
+    norm_row<BF16>(zp, zq, slab, V, k, blockIdx.x / rows, blockIdx.x % rows, m_out, S_out);
 }
 
 // ---------------------------------------------------------------- accept + residual draw
@@ -168,90 +240,103 @@ __device__ __forceinline__ u128 entry_mass(float zp, float zq, float mp, float m
     return x > y ? x - y : 0;
 }
 
+// a1 at position j: reject iff NOT u24_j * Eq_j(x_j) * Sp_j < 2^24 * Ep_j(x_j) * Sq_j.
 template <bool BF16>
-__global__ void __launch_bounds__(kLogitThreads, LAPSSD_SAMPLE_MINB) logits_sample_kernel(
-    const char *zp, const char *zq, const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
-    const uint32_t *round_idx, int64_t V, int32_t k, uint64_t seed, uint32_t trace, const float *m_in,
-    const uint64_t *S_in, int32_t *tokens, int32_t *n_accept, uint64_t *z_out, uint32_t *err) {
+__device__ __forceinline__ bool rejects(const char *zp, const char *zq, const int32_t *dr, int64_t s, int j,
+                                        uint32_t req, uint32_t rnd, int64_t V, int32_t k, uint64_t seed,
+                                        uint32_t trace, const float *m, const uint64_t *S) {
     using E = LElt<BF16>;
-    constexpr int kTile = 32 * kTileVecs * E::kVec;
-    extern __shared__ __align__(16) uint8_t s_raw[];
-    u128 *tile_sum = reinterpret_cast<u128 *>(s_raw);
-    __shared__ int s_r;
-    const int b = blockIdx.x;
-    const int rows = 2 * k + 1;
-    const int64_t s = slab ? slab[b] : b;
-    const uint32_t req = req_id[b], rnd = round_idx[b];
+    const int x = dr[j];
+    const char *prow = zp + ((s * (k + 1) + j) * V) * E::kEsz;
+    const char *qrow = zq + ((s * k + j) * V) * E::kEsz;
+    const float zpx = BF16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t *>(prow)[x] << 16)
+                           : reinterpret_cast<const float *>(prow)[x];
+    const float zqx = BF16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t *>(qrow)[x] << 16)
+                           : reinterpret_cast<const float *>(qrow)[x];
+    const unsigned long long *Su = reinterpret_cast<const unsigned long long *>(S);
+    const uint64_t Ep = e40(zpx, __ldcg(m + j)), Eq = e40(zqx, __ldcg(m + k + 1 + j));
+    const uint4 u = philox4x32_10(make_uint4(req, rnd, (uint32_t)(j >> 2), trace), (uint32_t)seed,
+                                  (uint32_t)(seed >> 32));
+    const uint32_t w = (j & 3) == 0 ? u.x : (j & 3) == 1 ? u.y : (j & 3) == 2 ? u.z : u.w;
+    const uint32_t u24 = w >> 8;
+    return !((u128)u24 * Eq * __ldcg(Su + j) < (((u128)Ep * __ldcg(Su + k + 1 + j)) << 24));
+}
+
+// a2 inputs for slot b with r known: the residual row pair (r < k) or the bonus row p_k.
+struct Resid {
+    const uint4 *pv, *qv;
+    float mp, mq;
+    uint64_t Sp, Sq;
+    bool use_q;
+};
+
+template <bool BF16>
+__device__ __forceinline__ Resid resid_of(const char *zp, const char *zq, int64_t s, int r, int64_t V, int32_t k,
+                                          const float *m, const uint64_t *S) {
+    // (L2 reads: in the lazy kernel other CTAs wrote these rows' (m, S) during this launch)
+    const unsigned long long *Su = reinterpret_cast<const unsigned long long *>(S);
+    Resid q;
+    q.use_q = r < k;
+    q.mp = __ldcg(m + r);
+    q.Sp = __ldcg(Su + r);
+    q.mq = q.use_q ? __ldcg(m + k + 1 + r) : 0.0f;
+    q.Sq = q.use_q ? __ldcg(Su + k + 1 + r) : 0;
+    q.pv = row_ptr<BF16>(zp, zq, s, V, k, r);
+    q.qv = row_ptr<BF16>(zp, zq, s, V, k, k + 1 + (q.use_q ? r : 0));
+    return q;
+}
+
+// Residual mass of tiles [t_lo, t_hi) (one warp per tile, coalesced) into out[tile].
+template <bool BF16>
+__device__ __forceinline__ void tile_pass(const Resid &q, int64_t nv, int t_lo, int t_hi, u128 *out) {
+    using E = LElt<BF16>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const float *m = m_in + (int64_t)b * rows;
-    const uint64_t *S = S_in + (int64_t)b * rows;
-    const int32_t *dr = draft + s * k;
-    // ---- a1: position j on lane j of warp 0 (k <= 16), first rejection by ballot
-    if (warp == 0) {
-        bool reject = false;
-        if (lane < k) {
-            const int x = dr[lane];
-            const char *prow = zp + ((s * (k + 1) + lane) * V) * E::kEsz;
-            const char *qrow = zq + ((s * k + lane) * V) * E::kEsz;
-            const float zpx = BF16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t *>(prow)[x] << 16)
-                                   : reinterpret_cast<const float *>(prow)[x];
-            const float zqx = BF16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t *>(qrow)[x] << 16)
-                                   : reinterpret_cast<const float *>(qrow)[x];
-            const uint64_t Ep = e40(zpx, m[lane]), Eq = e40(zqx, m[k + 1 + lane]);
-            const uint4 u = philox4x32_10(make_uint4(req, rnd, (uint32_t)(lane >> 2), trace), (uint32_t)seed,
-                                          (uint32_t)(seed >> 32));
-            const uint32_t w = (lane & 3) == 0 ? u.x : (lane & 3) == 1 ? u.y : (lane & 3) == 2 ? u.z : u.w;
-            const uint32_t u24 = w >> 8;
-            reject = !((u128)u24 * Eq * S[lane] < (((u128)Ep * S[k + 1 + lane]) << 24));
+    for (int tile = t_lo + warp; tile < t_hi; tile += nwarps) {
+        u128 acc = 0;
+#pragma unroll
+        for (int j = 0; j < kTileVecs; ++j) {
+            const int64_t vi = (int64_t)tile * (32 * kTileVecs) + j * 32 + lane;
+            if (vi < nv) {
+                const uint4 a = q.pv[vi];
+                const uint4 c = q.use_q ? q.qv[vi] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int e = 0; e < E::kVec; ++e)
+                    acc += entry_mass<BF16>(E::get(a, e), E::get(c, e), q.mp, q.mq, q.Sp, q.Sq, q.use_q);
+            }
         }
-        const unsigned msk = __ballot_sync(0xFFFFFFFFu, reject);
-        if (lane == 0) s_r = msk ? __ffs(msk) - 1 : k;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += shfl_xor_u128(acc, o);
+        if (lane == 0) out[tile] = acc;
+    }
+}
+
+// Z = sum of the tile sums; with no residual mass while rejecting, the row p_r itself
+// (AMB-20): the tiles are recomputed with use_q = false.  Block-wide; returns use_q.
+template <bool BF16>
+__device__ __forceinline__ void amb20_fallback(Resid &q, int64_t nv, int n_tiles, u128 *tile_sum) {
+    __shared__ int s_again;
+    if (threadIdx.x == 0) {
+        u128 Z = 0;
+        for (int t = 0; t < n_tiles; ++t) Z += tile_sum[t];
+        s_again = (Z == 0 && q.use_q) ? 1 : 0;
     }
     __syncthreads();
-    const int r = s_r;
-    bool use_q = r < k;
-    const float mp = m[r];
-    const uint64_t Sp = S[r];
-    const float mq = use_q ? m[k + 1 + r] : 0.0f;
-    const uint64_t Sq = use_q ? S[k + 1 + r] : 0;
-    const uint4 *pv = reinterpret_cast<const uint4 *>(zp + ((s * (k + 1) + r) * V) * E::kEsz);
-    const uint4 *qv = reinterpret_cast<const uint4 *>(zq + ((s * k + (use_q ? r : 0)) * V) * E::kEsz);
-    const int64_t nv = V / E::kVec;
-    const int n_tiles = (int)((V + kTile - 1) / kTile);
-    // ---- a2: tile sums of the residual mass, one warp per tile (coalesced)
-    for (int pass = 0; pass < 2; ++pass) {
-        for (int tile = warp; tile < n_tiles; tile += nwarps) {
-            u128 acc = 0;
-#pragma unroll
-            for (int j = 0; j < kTileVecs; ++j) {
-                const int64_t vi = (int64_t)tile * (32 * kTileVecs) + j * 32 + lane;
-                if (vi < nv) {
-                    const uint4 a = pv[vi];
-                    const uint4 c = use_q ? qv[vi] : make_uint4(0, 0, 0, 0);
-#pragma unroll
-                    for (int e = 0; e < E::kVec; ++e)
-                        acc += entry_mass<BF16>(E::get(a, e), E::get(c, e), mp, mq, Sp, Sq, use_q);
-                }
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += shfl_xor_u128(acc, o);
-            if (lane == 0) tile_sum[tile] = acc;
-        }
-        __syncthreads();
-        // total; no residual mass while rejecting: the row p_r itself (AMB-20)
-        __shared__ int s_again;
-        if (threadIdx.x == 0) {
-            u128 Z = 0;
-            for (int t = 0; t < n_tiles; ++t) Z += tile_sum[t];
-            s_again = (Z == 0 && use_q) ? 1 : 0;
-        }
-        __syncthreads();
-        if (!s_again) break;
-        use_q = false;
-        __syncthreads();
+    if (s_again) {
+        q.use_q = false;
+        tile_pass<BF16>(q, nv, 0, n_tiles, tile_sum);
     }
-    if (warp != 0) return;
-    // ---- warp 0: Z, t, the tile holding t, rescan it
+    __syncthreads();
+}
+
+// Warp 0: Z, t = floor(U Z / 2^64), the tile holding t (prefix over tile_sum in shared
+// memory), a rescan of that tile in vocabulary order, then the outputs of slot b.
+template <bool BF16>
+__device__ __forceinline__ void draw_token(const Resid &q, int64_t nv, int n_tiles, const u128 *tile_sum,
+                                           const int32_t *dr, int b, int r, uint32_t req, uint32_t rnd, int32_t k,
+                                           int64_t V, uint64_t seed, uint32_t trace, int32_t *tokens,
+                                           int32_t *n_accept, uint64_t *z_out, uint32_t *err) {
+    using E = LElt<BF16>;
+    const int lane = threadIdx.x & 31;
     u128 Z = 0;
     for (int t0 = 0; t0 < n_tiles; t0 += 32) Z += t0 + lane < n_tiles ? tile_sum[t0 + lane] : (u128)0;
 #pragma unroll
@@ -289,11 +374,11 @@ __global__ void __launch_bounds__(kLogitThreads, LAPSSD_SAMPLE_MINB) logits_samp
             u128 me[E::kVec];
             u128 msum = 0;
             if (vi < nv) {
-                const uint4 a = pv[vi];
-                const uint4 c = use_q ? qv[vi] : make_uint4(0, 0, 0, 0);
+                const uint4 a = q.pv[vi];
+                const uint4 c = q.use_q ? q.qv[vi] : make_uint4(0, 0, 0, 0);
 #pragma unroll
                 for (int e = 0; e < E::kVec; ++e) {
-                    me[e] = entry_mass<BF16>(E::get(a, e), E::get(c, e), mp, mq, Sp, Sq, use_q);
+                    me[e] = entry_mass<BF16>(E::get(a, e), E::get(c, e), q.mp, q.mq, q.Sp, q.Sq, q.use_q);
                     msum += me[e];
                 }
             } else {
@@ -337,19 +422,235 @@ __global__ void __launch_bounds__(kLogitThreads, LAPSSD_SAMPLE_MINB) logits_samp
     }
 }
 
+template <bool BF16>
+__global__ void __launch_bounds__(kLogitThreads, LAPSSD_SAMPLE_MINB) logits_sample_kernel(
+    const char *zp, const char *zq, const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
+    const uint32_t *round_idx, int64_t V, int32_t k, uint64_t seed, uint32_t trace, const float *m_in,
+    const uint64_t *S_in, int32_t *tokens, int32_t *n_accept, uint64_t *z_out, uint32_t *err) {
+    using E = LElt<BF16>;
+    constexpr int kTile = 32 * kTileVecs * E::kVec;
+    extern __shared__ __align__(16) uint8_t s_raw[];
+    u128 *tile_sum = reinterpret_cast<u128 *>(s_raw);
+    __shared__ int s_r;
+    const int b = blockIdx.x;
+    const int rows = 2 * k + 1;
+    const int64_t s = slab ? slab[b] : b;
+    const uint32_t req = req_id[b], rnd = round_idx[b];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float *m = m_in + (int64_t)b * rows;
+    const uint64_t *S = S_in + (int64_t)b * rows;
+    const int32_t *dr = draft + s * k;
+    // ---- a1: position j on lane j of warp 0 (k <= 16), first rejection by ballot
+    if (warp == 0) {
+        const bool reject = lane < k && rejects<BF16>(zp, zq, dr, s, lane, req, rnd, V, k, seed, trace, m, S);
+        const unsigned msk = __ballot_sync(0xFFFFFFFFu, reject);
+        if (lane == 0) s_r = msk ? __ffs(msk) - 1 : k;
+    }
+    __syncthreads();
+    const int r = s_r;
+    Resid q = resid_of<BF16>(zp, zq, s, r, V, k, m, S);
+    const int64_t nv = V / E::kVec;
+    const int n_tiles = (int)((V + kTile - 1) / kTile);
+    tile_pass<BF16>(q, nv, 0, n_tiles, tile_sum);
+    __syncthreads();
+    amb20_fallback<BF16>(q, nv, n_tiles, tile_sum);
+    if (warp == 0)
+        draw_token<BF16>(q, nv, n_tiles, tile_sum, dr, b, r, req, rnd, k, V, seed, trace, tokens, n_accept, z_out,
+                         err);
+}
+
+// ---------------------------------------------------------------- lazy form (one launch)
+// Only the rows the method consults are normalised: position j's pair (p_j, q_j) is needed
+// only if x_0..x_{j-1} were all accepted, and p_k only if all k were (the
+// acceptance tests run in order and stop at the first rejection).  A persistent grid
+// claims row units from a queue in order: units [0, 2B) are the pairs of position 0, later
+// units are published by the CTA that completes a pair and accepts it (the next pair, or
+// p_k after position k-1).  The CTA that completes a pair and rejects it -- or completes
+// p_k -- runs the residual draw of that slot at once (its rows are still in L2).  A unit
+// is a whole row: its two passes (max, then mass) run back to back on one CTA so the
+// second pass hits L2 (measured: splitting rows into parts claimed from the queue -- the
+// mass pass then runs long after the max pass -- was slower, 0.65-1.6 ms against 0.56).
+struct LazyArgs {
+    const char *zp, *zq;
+    const int32_t *draft, *slab;
+    const uint32_t *req_id, *round_idx;
+    int64_t V;
+    int32_t k, B;
+    uint64_t seed;
+    uint32_t trace;
+    float *m;                 // [B rows]
+    uint64_t *S;              // [B rows]
+    uint32_t *units;          // [B rows]: row code + 1 published at [2B, ...) (0 = not yet)
+    uint32_t *cpair;          // [B]: rows of the current pair finished (odd -> even: pair done)
+    uint32_t *ctr;            // [0] next unit to claim, [1] units published past 2B, [2] slots done
+    int32_t *tokens, *n_accept;
+    uint64_t *z_out;
+    uint32_t *err;
+};
+
+#ifndef LAPSSD_LAZY_THREADS
+#define LAPSSD_LAZY_THREADS 512
+#endif
+#ifndef LAPSSD_LAZY_MINB
+#define LAPSSD_LAZY_MINB 2
+#endif
+constexpr int kLazyThreads = LAPSSD_LAZY_THREADS;
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kLazyThreads, LAPSSD_LAZY_MINB) logits_lazy_kernel(const LazyArgs a) {
+    using E = LElt<BF16>;
+    constexpr int kTile = 32 * kTileVecs * E::kVec;
+    extern __shared__ __align__(16) uint8_t s_raw[];
+    u128 *tile_sum = reinterpret_cast<u128 *>(s_raw);
+    __shared__ uint32_t s_code;
+    __shared__ int s_r;
+    const int k = a.k, rows = 2 * k + 1;
+    const int64_t nv = a.V / E::kVec;
+    const int n_tiles = (int)((a.V + kTile - 1) / kTile);
+    const uint32_t cap = (uint32_t)a.B * rows, first = 2u * (uint32_t)a.B;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const uint32_t idx = atomicAdd(a.ctr, 1u);
+            uint32_t code = 0xFFFFFFFFu;   // exit
+            if (idx < first) {
+                code = (idx >> 1) * rows + ((idx & 1) ? k + 1 : 0);
+            } else if (idx < cap) {
+                for (;;) {
+                    const uint32_t u = ld_acquire_u32(a.units + idx);
+                    if (u) { code = u - 1; break; }
+                    if (ld_acquire_u32(a.ctr + 2) >= (uint32_t)a.B) break;
+                    __nanosleep(128);
+                }
+            }
+            s_code = code;
+        }
+        __syncthreads();
+        const uint32_t code = s_code;
+        if (code == 0xFFFFFFFFu) return;
+        const int b = (int)(code / rows), ri = (int)(code % rows);
+        const int64_t s = a.slab ? a.slab[b] : b;
+        const int64_t rowi = (int64_t)b * rows + ri;
+        const uint4 *v4 = row_ptr<BF16>(a.zp, a.zq, s, a.V, k, ri);
+        const float m = range_max<BF16>(v4, 0, nv);
+        const uint64_t S = range_sum<BF16>(v4, 0, nv, m);
+        const uint32_t req = a.req_id[b], rnd = a.round_idx[b];
+        const int32_t *dr = a.draft + s * k;
+        const float *mb = a.m + (int64_t)b * rows;
+        const uint64_t *Sb = a.S + (int64_t)b * rows;
+        if (threadIdx.x == 0) {
+            a.m[rowi] = m;
+            a.S[rowi] = S;
+            int r = -1;
+            if (ri == k) {
+                r = k;   // p_k: every draft accepted
+            } else {
+                __threadfence();
+                if (atomicAdd(a.cpair + b, 1u) & 1) {   // the pair's other row is complete too
+                    __threadfence();
+                    const int j = ri < k ? ri : ri - k - 1;
+                    if (rejects<BF16>(a.zp, a.zq, dr, s, j, req, rnd, a.V, k, a.seed, a.trace, mb, Sb)) {
+                        r = j;
+                    } else {
+                        const bool last = j + 1 == k;
+                        const uint32_t at = first + atomicAdd(a.ctr + 1, last ? 1u : 2u);
+                        const uint32_t c0 = (uint32_t)b * rows + (last ? k : j + 1);
+                        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.units + at), "r"(c0 + 1) : "memory");
+                        if (!last)
+                            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.units + at + 1),
+                                         "r"(c0 + k + 2) : "memory");
+                    }
+                }
+            }
+            s_r = r;
+        }
+        __syncthreads();
+        const int r = s_r;
+        if (r >= 0) {   // the residual draw of slot b, by this CTA
+            Resid q = resid_of<BF16>(a.zp, a.zq, s, r, a.V, k, mb, Sb);
+            tile_pass<BF16>(q, nv, 0, n_tiles, tile_sum);
+            __syncthreads();
+            amb20_fallback<BF16>(q, nv, n_tiles, tile_sum);
+            if (threadIdx.x < 32)
+                draw_token<BF16>(q, nv, n_tiles, tile_sum, dr, b, r, req, rnd, k, a.V, a.seed, a.trace, a.tokens,
+                                 a.n_accept, a.z_out, a.err);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.ctr + 2) : "memory");
+            }
+        }
+        __syncthreads();
+    }
+}
+
 size_t logits_tile_smem(int64_t V, int32_t dtype) {
     const int tile = 32 * kTileVecs * (dtype == LAPSSD_BF16 ? 8 : 4);
     return (size_t)((V + tile - 1) / tile) * sizeof(u128);
+}
+
+// Workspace of the lazy form after (m, S): the queue and counters, zeroed per call.
+size_t logits_lazy_bytes(int32_t B, int32_t k, int64_t, int32_t) {
+    return 256 + ((size_t)B * (2 * k + 1) + (size_t)B + 4) * sizeof(uint32_t);
+}
+
+template <bool BF16>
+static cudaError_t launch_lazy(const void *zp, const void *zq, int64_t V, int32_t k, const int32_t *draft,
+                               const int32_t *slab, const uint32_t *req_id, const uint32_t *round_idx, int32_t B,
+                               uint64_t seed, uint32_t trace, int32_t *tokens, int32_t *n_accept, uint64_t *z,
+                               float *m_ws, uint64_t *S_ws, char *lazy_ws, size_t smem, cudaStream_t s) {
+    static int grid_per_sm = -1, sms = 0;
+    static size_t grid_smem = 0;
+    if (grid_per_sm < 0 || grid_smem != smem) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&grid_per_sm, logits_lazy_kernel<BF16>, kLazyThreads, smem);
+        grid_smem = smem;
+        if (grid_per_sm < 1) grid_per_sm = 1;
+    }
+    const int rows = 2 * k + 1;
+    LazyArgs a{};
+    a.zp = (const char *)zp; a.zq = (const char *)zq;
+    a.draft = draft; a.slab = slab; a.req_id = req_id; a.round_idx = round_idx;
+    a.V = V; a.k = k; a.B = B; a.seed = seed; a.trace = trace;
+    a.m = m_ws; a.S = S_ws;
+    uint32_t *q = (uint32_t *)(((size_t)lazy_ws + 255) & ~(size_t)255);
+    const size_t words = (size_t)B * rows + (size_t)B + 4;
+    a.units = q;
+    a.cpair = q + (size_t)B * rows;
+    a.ctr = a.cpair + B;
+    a.tokens = tokens; a.n_accept = n_accept; a.z_out = z; a.err = nullptr;
+    cudaError_t ce = cudaMemsetAsync(q, 0, words * sizeof(uint32_t), s);
+    if (ce != cudaSuccess) return ce;
+    const int64_t want = (int64_t)B * rows;
+    const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)grid_per_sm * sms);
+    logits_lazy_kernel<BF16><<<grid, kLazyThreads, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
 }
 
 cudaError_t launch_verify_logits(const void *zp, const void *zq, int32_t dtype, int64_t V, int32_t k,
                                  const int32_t *draft, const int32_t *slab, const uint32_t *req_id,
                                  const uint32_t *round_idx, int32_t B, uint64_t seed, uint32_t trace,
                                  int32_t *tokens, int32_t *n_accept, uint64_t *z, float *m_ws, uint64_t *S_ws,
-                                 cudaStream_t s) {
+                                 char *lazy_ws, cudaStream_t s) {
     if (B <= 0) return cudaSuccess;
     const unsigned rows = (unsigned)(2 * k + 1);
     const size_t smem = logits_tile_smem(V, dtype);
+    const bool eager = getenv("LAPSSD_LOGITS_EAGER") != nullptr;   // A/B: every row, two launches
+    if (!eager) {
+        return dtype == LAPSSD_BF16
+                   ? launch_lazy<true>(zp, zq, V, k, draft, slab, req_id, round_idx, B, seed, trace, tokens, n_accept,
+                                       z, m_ws, S_ws, lazy_ws, smem, s)
+                   : launch_lazy<false>(zp, zq, V, k, draft, slab, req_id, round_idx, B, seed, trace, tokens, n_accept,
+                                        z, m_ws, S_ws, lazy_ws, smem, s);
+    }
     if (dtype == LAPSSD_BF16) {
         logits_norm_kernel<true><<<(unsigned)B * rows, kNormThreads, 0, s>>>(
             (const char *)zp, (const char *)zq, slab, V, k, m_ws, S_ws);
@@ -372,6 +673,8 @@ cudaError_t launch_verify_logits(const void *zp, const void *zq, int32_t dtype, 
 void verify_logits_prepare() {
     cudaFuncSetAttribute(logits_sample_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(logits_sample_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(logits_lazy_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(logits_lazy_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
 }
 
 }  // namespace lapssd

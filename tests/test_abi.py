@@ -98,8 +98,9 @@ def test_spec_verify_logits_rejects_bad_arguments():
     assert f(16, 16, L.BF16, 16, 4, None, None, None, None, 1, 0, 0, None, None, None, None, 0, None) == -1
     assert f(16, 16, L.BF16, 16, 4, 16, None, 16, 16, 1, 0, 0, 16, 16, None, 16, 0, None) == -5  # ENOMEM
     assert f(16, 16, L.BF16, 16, 4, None, None, None, None, 0, 0, 0, None, None, None, None, 0, None) == 0
-    assert L._lib.spec_verify_logits_workspace_bytes(512, 8) >= 512 * 17 * 12
-    assert L._lib.spec_verify_logits_workspace_bytes(1, 0) == 0
+    assert L._lib.spec_verify_logits_workspace_bytes(512, 8, 128256, 1) >= 512 * 17 * 12
+    assert L._lib.spec_verify_logits_workspace_bytes(1, 0, 1024, 1) == 0
+    assert L._lib.spec_verify_logits_workspace_bytes(1, 4, 1024, 7) == 0
 
 
 def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):

@@ -83,3 +83,53 @@ def test_spec_verify_logits_special_rows(L):
     assert na[0] == k and na[3] == k          # equal logits: every draft accepted
     assert na[1] == 0 and na[4] == 0          # disjoint: rejected at position 0
     assert not inA[tok_o[1, 0]]
+
+
+def _call(L, pool, slab, req, rnd, seed, ws=None):
+    dev = pool.p.device
+    return L.spec_verify_logits(pool.p, pool.q, pool.draft, torch.as_tensor(req, device=dev),
+                                torch.as_tensor(rnd, device=dev), seed, slab=torch.as_tensor(slab, device=dev),
+                                workspace=ws)
+
+
+def test_lazy_equals_every_row_form_large_batch(L, monkeypatch):
+    """The one-launch lazy form (only the rows the tests consult are normalised; a work
+    queue over a persistent grid) against the two-launch form that normalises every row,
+    at more slots than the grid holds CTAs, and against the oracle on a sample of slots."""
+    pool = synth.make_logits_pool(32000, 8, "bf16", n_buckets=8, variants=2, seed=91, device="cuda")
+    rng = np.random.default_rng(91)
+    B = 700
+    slab = rng.integers(0, pool.S, B).astype(np.int32)
+    req = rng.integers(0, 1 << 20, B).astype(np.int32)
+    rnd = rng.integers(0, 1 << 12, B).astype(np.int32)
+    tok, na, z = [x.cpu().numpy() for x in _call(L, pool, slab, req, rnd, 9)]
+    monkeypatch.setenv("LAPSSD_LOGITS_EAGER", "1")
+    tok_e, na_e, z_e = [x.cpu().numpy() for x in _call(L, pool, slab, req, rnd, 9)]
+    monkeypatch.delenv("LAPSSD_LOGITS_EAGER")
+    assert (na == na_e).all() and (tok == tok_e).all() and (z == z_e).all()
+    assert (na == 8).any() and (na == 0).any()
+    P = pool.numpy()
+    pick = rng.choice(B, 40, replace=False)
+    tok_o, r_o, z_o = oracle.verify_logits_batch(P["p"], P["q"], P["draft"], slab[pick], req[pick], rnd[pick], 9)
+    assert (na[pick] == r_o).all() and (tok[pick] == tok_o).all() and (z[pick].view(np.uint64) == z_o).all()
+
+
+@pytest.mark.parametrize("B,k", [(1, 1), (1, 8), (5, 2), (300, 3)])
+def test_lazy_queue_reused_workspace(L, B, k):
+    """One workspace over several calls (the queue is re-zeroed per call), small and odd
+    batches, and rows with every draft accepted (the bonus row p_k is then the last unit)."""
+    V = 4096
+    pool = synth.make_logits_pool(V, k, "f32", n_buckets=4, variants=2, seed=B + k, device="cuda")
+    ws = torch.empty(L.spec_verify_logits_workspace_bytes(B, k, V, "f32"), dtype=torch.uint8, device="cuda")
+    rng = np.random.default_rng(B * 31 + k)
+    P = pool.numpy()
+    for call in range(3):
+        slab = rng.integers(0, pool.S, B).astype(np.int32)
+        req = rng.integers(0, 1 << 20, B).astype(np.int32)
+        rnd = rng.integers(0, 1 << 12, B).astype(np.int32)
+        tok, na, z = [x.cpu().numpy() for x in _call(L, pool, slab, req, rnd, 100 + call, ws)]
+        pick = np.arange(B) if B <= 40 else rng.choice(B, 40, replace=False)
+        tok_o, r_o, z_o = oracle.verify_logits_batch(P["p"], P["q"], P["draft"], slab[pick], req[pick], rnd[pick],
+                                                     100 + call)
+        assert (na[pick] == r_o).all() and (tok[pick] == tok_o).all()
+        assert (z[pick].view(np.uint64) == z_o).all()
