@@ -38,7 +38,14 @@ __device__ __forceinline__ void e40x2(float za, float zb, float ma, float mb, ui
 #else   // z <= m (m is the row max), so fl32(z - m) <= 0: only the lower clamp can act
     const float2 d = make_float2(fmaxf(d0.x, -28.5f), fmaxf(d0.y, -28.5f));
 #endif
+    // x = fl32(d log2e) as two SCALAR multiplies: ptxas contracts a packed mul.rn.f32x2
+    // followed by add.rn.f32x2 into one FFMA2 (one rounding; even with --fmad=false), which
+    // would round d log2e + 1.5 2^23 once and take rint of the exact product, not of x
+#ifdef LAPSSD_E40_PACKED_MUL   // diagnostic build only: reproduces the contraction
     const float2 x = __fmul2_rn(d, make_float2(0x1.715476p+0f, 0x1.715476p+0f));
+#else
+    const float2 x = make_float2(__fmul_rn(d.x, 0x1.715476p+0f), __fmul_rn(d.y, 0x1.715476p+0f));
+#endif
     const float2 big = __fadd2_rn(x, make_float2(0x1.8p23f, 0x1.8p23f));
     const float2 nf = __fadd2_rn(big, make_float2(-0x1.8p23f, -0x1.8p23f));
     float2 r = __ffma2_rn(nf, make_float2(-0x1.62e4p-1f, -0x1.62e4p-1f), d);

@@ -133,3 +133,41 @@ def test_lazy_queue_reused_workspace(L, B, k):
                                                      100 + call)
         assert (na[pick] == r_o).all() and (tok[pick] == tok_o).all()
         assert (z[pick].view(np.uint64) == z_o).all()
+
+
+# fp32 logit gaps d = z - m for which rint(fl32(d log2e)) != rint(d log2e) (the product
+# rounds onto a half-integer) AND E = floor(exphat(d) 2^40) then differs between the two:
+# found by walking the ulp neighbourhoods of (h + 1/2) / log2e.  AMB-30 rounds the product
+# first; an implementation that fuses d log2e + 1.5 2^23 into one FMA gets other masses.
+_TIE_GAPS = [float.fromhex(h) for h in ("-0x1.a56ef8p+2", "-0x1.fe2804p+2", "-0x1.842994p+3")]
+
+
+def test_logits_rint_of_the_rounded_product(L):
+    """AMB-30's exphat takes n = rint(fl32(d log2e)): rows built from gaps where one fused
+    rounding would change E must give the oracle's r, tokens and Z bit-exactly."""
+    V, k, S = 1024, 2, 4
+    rng = np.random.default_rng(17)
+    zp = np.full((S, k + 1, V), -40.0, np.float32)
+    zq = np.full((S, k, V), -40.0, np.float32)
+    for s_ in range(S):
+        for j in range(k + 1):
+            idx = rng.permutation(V)
+            zp[s_, j, idx[0]] = 0.0
+            for t, g in enumerate(_TIE_GAPS):
+                zp[s_, j, idx[1 + 200 * t:1 + 200 * (t + 1)]] = np.float32(g)
+        for j in range(k):
+            zq[s_, j] = zp[s_, j]
+            zq[s_, j, rng.integers(0, V, 300)] = np.float32(_TIE_GAPS[s_ % 3])
+    draft = rng.integers(0, V, (S, k)).astype(np.int32)
+    draft[:, 0] = np.argmax(zp[:, 0], axis=1)          # a likely accepted first draft
+    B = 16
+    slab = np.arange(B, dtype=np.int32) % S
+    req = np.arange(B, dtype=np.int32) * 7 + 1
+    rnd = np.arange(B, dtype=np.int32)
+    dev = "cuda"
+    tok, na, z = L.spec_verify_logits(torch.as_tensor(zp, device=dev), torch.as_tensor(zq, device=dev),
+                                      torch.as_tensor(draft, device=dev), torch.as_tensor(req, device=dev),
+                                      torch.as_tensor(rnd, device=dev), 11, slab=torch.as_tensor(slab, device=dev))
+    tok_o, r_o, z_o = oracle.verify_logits_batch(zp, zq, draft, slab, req, rnd, 11)
+    assert (na.cpu().numpy() == r_o).all() and (tok.cpu().numpy() == tok_o).all()
+    assert (z.cpu().numpy().view(np.uint64) == z_o).all()
