@@ -18,6 +18,8 @@
 //   per warp pass), the tile holding t found by warp 0, which rescans that tile.
 #include "lapssd_internal.cuh"
 
+#include <cuda_bf16.h>
+
 namespace lapssd {
 
 typedef unsigned __int128 u128;
@@ -122,30 +124,46 @@ constexpr int kNormThreads = 512;
 #endif
 constexpr int kNormIlp = LAPSSD_NORM_ILP;
 
+// Max of the 8 / 4 logits of one vector: bf16 pairs by packed HMNMX2 on the raw words
+// (max is exact in any format), fp32 by FMNMX.
+template <bool BF16> struct VecMax;
+template <> struct VecMax<true> {
+    __nv_bfloat162 m = __nv_bfloat162(__ushort_as_bfloat16(0xFF80), __ushort_as_bfloat16(0xFF80));   // -inf
+    __device__ void add(const uint4 &v) {
+        m = __hmax2(m, __hmax2(__hmax2(*reinterpret_cast<const __nv_bfloat162 *>(&v.x),
+                                       *reinterpret_cast<const __nv_bfloat162 *>(&v.y)),
+                               __hmax2(*reinterpret_cast<const __nv_bfloat162 *>(&v.z),
+                                       *reinterpret_cast<const __nv_bfloat162 *>(&v.w))));
+    }
+    __device__ float get() const { return fmaxf(__bfloat162float(m.x), __bfloat162float(m.y)); }
+};
+template <> struct VecMax<false> {
+    float m = -INFINITY;
+    __device__ void add(const uint4 &v) {
+        m = fmaxf(m, fmaxf(fmaxf(__uint_as_float(v.x), __uint_as_float(v.y)),
+                           fmaxf(__uint_as_float(v.z), __uint_as_float(v.w))));
+    }
+    __device__ float get() const { return m; }
+};
+
 // Block-wide max of the logits in vectors [lo, hi) of a row (every thread gets it).
 template <bool BF16>
 __device__ __forceinline__ float range_max(const uint4 *v4, int64_t lo, int64_t hi) {
-    using E = LElt<BF16>;
     __shared__ float s_m[32];
     constexpr int U = kNormIlp;
     const int64_t bd = blockDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    float m = -INFINITY;
+    VecMax<BF16> acc;
     int64_t i = lo + threadIdx.x;
     for (; i + (U - 1) * bd < hi; i += U * bd) {
         uint4 v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) v[u] = v4[i + u * bd];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int e = 0; e < E::kVec; ++e) m = fmaxf(m, E::get(v[u], e));
+        for (int u = 0; u < U; ++u) acc.add(v[u]);
     }
-    for (; i < hi; i += bd) {
-        const uint4 v = v4[i];
-#pragma unroll
-        for (int e = 0; e < E::kVec; ++e) m = fmaxf(m, E::get(v, e));
-    }
+    for (; i < hi; i += bd) acc.add(v4[i]);
+    float m = acc.get();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
     if (lane == 0) s_m[warp] = m;
@@ -476,7 +494,9 @@ __global__ void __launch_bounds__(kLogitThreads, LAPSSD_SAMPLE_MINB) logits_samp
 // p_k -- runs the residual draw of that slot at once (its rows are still in L2).  A unit
 // is a whole row: its two passes (max, then mass) run back to back on one CTA so the
 // second pass hits L2 (measured: splitting rows into parts claimed from the queue -- the
-// mass pass then runs long after the max pass -- was slower, 0.65-1.6 ms against 0.56).
+// mass pass then runs long after the max pass -- was slower, 0.65-1.6 ms against 0.56;
+// claiming the next available unit ahead, with or without an L2 prefetch of its row, was
+// slower too, 0.59-0.60 ms: the claimant holds it while another CTA sits idle).
 struct LazyArgs {
     const char *zp, *zq;
     const int32_t *draft, *slab;
