@@ -11,11 +11,14 @@
 // a2: R_v = max(0, Ep_v Sq - Eq_v Sp) (r < k) or Ep_v (r = k); t = floor(U Z / 2^64);
 //     y = min{v : sum_{w<=v} R_w > t} (128-bit integers).
 //
-// norm_kernel: one CTA per (slot, row) of the 2k+1 rows: max, then the integer mass
-//   (a second read of the row), ~14 issue slots per entry for the exp (packed fp32x2).
-// sample_kernel: one CTA per slot: the k acceptance tests (one lane each), then the
-//   residual row pair in 1,024-entry tiles (warp-coalesced 16-byte loads, one tile sum
-//   per warp pass), the tile holding t found by warp 0, which rescans that tile.
+// logits_lazy_kernel (the default): one launch over a persistent grid that normalises only
+//   the rows the acceptance tests consult (position j's pair only if x_0..x_{j-1} were
+//   accepted), from a work queue (see "lazy form" below); the residual pass sums
+//   Sq * sum_{P+} Ep - Sp * sum_{P+} Eq with two uint64 sums per lane (P+ decided by an
+//   fp32 screen, the exact 128-bit comparison only where the screen cannot decide).
+// norm_kernel + sample_kernel (LAPSSD_LOGITS_EAGER=1, the A/B form): one CTA per (slot,
+//   row) of all 2k+1 rows (max, then the integer mass), then one CTA per slot for the k
+//   acceptance tests and the residual row pair in 1,024-entry tiles.
 #include "lapssd_internal.cuh"
 
 #include <cuda_bf16.h>
@@ -33,7 +36,8 @@ typedef unsigned __int128 u128;
 // IEEE RN operation of the definition).  d is clamped to [-28.5, 0]: below -28 the
 // definition gives 0, and so does the polynomial there (e^-28 2^40 < 0.77), while the
 // clamp keeps 2^n normal.
-__device__ __forceinline__ void e40x2(float za, float zb, float ma, float mb, uint64_t &ea, uint64_t &eb) {
+// f40x2 returns P 2^(n+40) (exact in fp32, before the truncation); e40x2 truncates it.
+__device__ __forceinline__ float2 f40x2(float za, float zb, float ma, float mb) {
     const float2 d0 = __fadd2_rn(make_float2(za, zb), make_float2(-ma, -mb));
 #ifdef LAPSSD_E40_UPPER_CLAMP
     const float2 d = make_float2(fmaxf(fminf(d0.x, 0.0f), -28.5f), fmaxf(fminf(d0.y, 0.0f), -28.5f));
@@ -62,7 +66,11 @@ __device__ __forceinline__ void e40x2(float za, float zb, float ma, float mb, ui
     p = __ffma2_rn(p, r, make_float2(1.0f, 1.0f));
     const int na = __float_as_int(big.x) - 0x4B400000, nb = __float_as_int(big.y) - 0x4B400000;
     const float2 sc = make_float2(__int_as_float((167 + na) << 23), __int_as_float((167 + nb) << 23));
-    const float2 f = __fmul2_rn(p, sc);   // P 2^(n+40), exact
+    return __fmul2_rn(p, sc);   // P 2^(n+40), exact
+}
+
+__device__ __forceinline__ void e40x2(float za, float zb, float ma, float mb, uint64_t &ea, uint64_t &eb) {
+    const float2 f = f40x2(za, zb, ma, mb);
     ea = __float2ull_rz(f.x);
     eb = __float2ull_rz(f.y);
 }
@@ -293,6 +301,7 @@ struct Resid {
     float mp, mq;
     uint64_t Sp, Sq;
     bool use_q;
+    float invSp, invSq;       // the split-sum pass's float screen (tile_pass_split)
 };
 
 template <bool BF16>
@@ -308,31 +317,109 @@ __device__ __forceinline__ Resid resid_of(const char *zp, const char *zq, int64_
     q.Sq = q.use_q ? __ldcg(Su + k + 1 + r) : 0;
     q.pv = row_ptr<BF16>(zp, zq, s, V, k, r);
     q.qv = row_ptr<BF16>(zp, zq, s, V, k, k + 1 + (q.use_q ? r : 0));
+    // 1/S to within 2^-23 relative (two RN roundings)
+    q.invSp = __frcp_rn(__ull2float_rn(q.Sp));
+    q.invSq = q.use_q ? __frcp_rn(__ull2float_rn(q.Sq)) : 0.0f;
     return q;
 }
 
-// Residual mass of tiles [t_lo, t_hi) (one warp per tile, coalesced) into out[tile].
+// Residual mass of tiles [t_lo, t_hi) for r < k without a 128-bit product per entry:
+// R_v > 0 iff Ep_v Sq > Eq_v Sp, and over the set P+ where it holds
+//   sum R = Sq * sum_{P+} Ep - Sp * sum_{P+} Eq   (exact; both sums < 2^58),
+// so each lane keeps two uint64 sums and the tile's 128-bit mass is formed once.
+// Membership is screened in fp32: Ep = trunc(fp) is exact as a float (an integer below
+// 2^41 with <= 24 significant bits), A = fl(Ep invSp) and B = fl(Eq invSq) are within
+// 2^-23 relative of Ep/Sp and Eq/Sq (invS = 1/S to within 2^-23), so x = fl(A - B) is
+// within (A+B) 2^-22 of Ep/Sp - Eq/Sq: x > m = (A+B) 2^-20 proves R_v > 0 and x < -m
+// proves R_v = 0 (Ep = 0 gives R_v = 0, Eq = 0 < Ep gives R_v > 0).  The entries the
+// screen cannot decide (|p^/q^ - 1| below ~2^-19, or exact ties) are decided afterwards by
+// the exact 128-bit comparison, out of the unrolled loop.
 template <bool BF16>
-__device__ __forceinline__ void tile_pass(const Resid &q, int64_t nv, int t_lo, int t_hi, u128 *out) {
+__device__ __forceinline__ int split_screen(float fp, float fq, const Resid &q) {   // 1 take, 0 skip, 2 exact
+    const float tp = truncf(fp), tq = truncf(fq);
+    const float2 ab = __fmul2_rn(make_float2(tp, tq), make_float2(q.invSp, q.invSq));
+    const float x = __fsub_rn(ab.x, ab.y);
+    const float m = __fmul_rn(__fadd_rn(ab.x, ab.y), 0x1p-20f);
+    if (tp == 0.0f) return 0;
+    if (tq == 0.0f || x > m) return 1;
+    if (x < -m) return 0;
+    return 2;
+}
+
+template <bool BF16>
+__device__ __forceinline__ void tile_pass_split(const Resid &q, int64_t nv, int t_lo, int t_hi, u128 *out) {
     using E = LElt<BF16>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
     for (int tile = t_lo + warp; tile < t_hi; tile += nwarps) {
-        u128 acc = 0;
+        uint64_t sP = 0, sQ = 0;
 #pragma unroll
         for (int j = 0; j < kTileVecs; ++j) {
             const int64_t vi = (int64_t)tile * (32 * kTileVecs) + j * 32 + lane;
             if (vi < nv) {
                 const uint4 a = q.pv[vi];
-                const uint4 c = q.use_q ? q.qv[vi] : make_uint4(0, 0, 0, 0);
+                const uint4 c = q.qv[vi];
+                uint32_t unc = 0;
 #pragma unroll
-                for (int e = 0; e < E::kVec; ++e)
-                    acc += entry_mass<BF16>(E::get(a, e), E::get(c, e), q.mp, q.mq, q.Sp, q.Sq, q.use_q);
+                for (int e = 0; e < E::kVec; ++e) {
+                    const float2 f = f40x2(E::get(a, e), E::get(c, e), q.mp, q.mq);
+                    const int d = split_screen<BF16>(f.x, f.y, q);
+                    if (d == 1) {
+                        sP += __float2ull_rz(f.x);
+                        sQ += __float2ull_rz(f.y);
+                    }
+                    unc |= (uint32_t)(d >> 1) << e;
+                }
+                while (unc) {   // rare: the exact comparison
+                    const int e = __ffs(unc) - 1;
+                    unc &= unc - 1;
+                    const float2 f = f40x2(E::get(a, e), E::get(c, e), q.mp, q.mq);
+                    const uint64_t ep = __float2ull_rz(f.x), eq = __float2ull_rz(f.y);
+                    if ((u128)ep * q.Sq > (u128)eq * q.Sp) {
+                        sP += ep;
+                        sQ += eq;
+                    }
+                }
             }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += shfl_xor_u128(acc, o);
-        if (lane == 0) out[tile] = acc;
+        for (int o = 16; o > 0; o >>= 1) {
+            sP += __shfl_xor_sync(0xFFFFFFFFu, sP, o);
+            sQ += __shfl_xor_sync(0xFFFFFFFFu, sQ, o);
+        }
+        if (lane == 0) out[tile] = (u128)sP * q.Sq - (u128)sQ * q.Sp;
     }
+}
+
+// R_v = Ep_r[v] (the bonus row, or AMB-20's fallback): two entries of p per exp call.
+template <bool BF16>
+__device__ __forceinline__ void tile_pass_p(const Resid &q, int64_t nv, int t_lo, int t_hi, u128 *out) {
+    using E = LElt<BF16>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int tile = t_lo + warp; tile < t_hi; tile += nwarps) {
+        uint64_t sP = 0;
+#pragma unroll
+        for (int j = 0; j < kTileVecs; ++j) {
+            const int64_t vi = (int64_t)tile * (32 * kTileVecs) + j * 32 + lane;
+            if (vi < nv) {
+                const uint4 a = q.pv[vi];
+#pragma unroll
+                for (int e = 0; e < E::kVec; e += 2) {
+                    uint64_t x, y;
+                    e40x2(E::get(a, e), E::get(a, e + 1), q.mp, q.mp, x, y);
+                    sP += x + y;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sP += __shfl_xor_sync(0xFFFFFFFFu, sP, o);
+        if (lane == 0) out[tile] = (u128)sP;
+    }
+}
+
+template <bool BF16>
+__device__ __forceinline__ void tile_pass_fast(const Resid &q, int64_t nv, int t_lo, int t_hi, u128 *out) {
+    if (q.use_q) tile_pass_split<BF16>(q, nv, t_lo, t_hi, out);
+    else tile_pass_p<BF16>(q, nv, t_lo, t_hi, out);
 }
 
 // Z = sum of the tile sums; with no residual mass while rejecting, the row p_r itself
@@ -348,7 +435,7 @@ __device__ __forceinline__ void amb20_fallback(Resid &q, int64_t nv, int n_tiles
     __syncthreads();
     if (s_again) {
         q.use_q = false;
-        tile_pass<BF16>(q, nv, 0, n_tiles, tile_sum);
+        tile_pass_p<BF16>(q, nv, 0, n_tiles, tile_sum);
     }
     __syncthreads();
 }
@@ -476,7 +563,7 @@ __global__ void __launch_bounds__(kLogitThreads, LAPSSD_SAMPLE_MINB) logits_samp
     Resid q = resid_of<BF16>(zp, zq, s, r, V, k, m, S);
     const int64_t nv = V / E::kVec;
     const int n_tiles = (int)((V + kTile - 1) / kTile);
-    tile_pass<BF16>(q, nv, 0, n_tiles, tile_sum);
+    tile_pass_fast<BF16>(q, nv, 0, n_tiles, tile_sum);
     __syncthreads();
     amb20_fallback<BF16>(q, nv, n_tiles, tile_sum);
     if (warp == 0)
@@ -488,15 +575,19 @@ __global__ void __launch_bounds__(kLogitThreads, LAPSSD_SAMPLE_MINB) logits_samp
 // Only the rows the method consults are normalised: position j's pair (p_j, q_j) is needed
 // only if x_0..x_{j-1} were all accepted, and p_k only if all k were (the
 // acceptance tests run in order and stop at the first rejection).  A persistent grid
-// claims row units from a queue in order: units [0, 2B) are the pairs of position 0, later
-// units are published by the CTA that completes a pair and accepts it (the next pair, or
-// p_k after position k-1).  The CTA that completes a pair and rejects it -- or completes
-// p_k -- runs the residual draw of that slot at once (its rows are still in L2).  A unit
-// is a whole row: its two passes (max, then mass) run back to back on one CTA so the
-// second pass hits L2 (measured: splitting rows into parts claimed from the queue -- the
-// mass pass then runs long after the max pass -- was slower, 0.65-1.6 ms against 0.56;
-// claiming the next available unit ahead, with or without an L2 prefetch of its row, was
-// slower too, 0.59-0.60 ms: the claimant holds it while another CTA sits idle).
+// claims units, in this order:
+//  1. filler: the 2B rows of position 0 (claimed one unit AHEAD, so the claim's latency
+//     hides under the current unit);
+//  2. published units, FIFO: the pair j+1 (or p_k) published when test j accepts, and the
+//     residual parts published when a test rejects (or p_k completes): np parts of tp
+//     tiles, each writing its tiles' masses, the last to finish draws the token;
+//     speculatively, while CTAs wait for work, test j's acceptance also publishes the
+//     pair j+2: a slot's chain of tests is a latency chain (one row pass per position),
+//     idle CTAs run it a position ahead, and if test j+1 accepts, test j+2 runs at once.
+// A row unit is one whole row, its two passes (max, then mass) back to back on one CTA so
+// the second pass hits L2.  Each row is claimed once (a per-row flag); test j runs when
+// both rows of position j are done and test j-1 accepted (a per-position counter; the
+// party that completes it runs the test, cascading while the next rows are done).
 struct LazyArgs {
     const char *zp, *zq;
     const int32_t *draft, *slab;
@@ -507,9 +598,15 @@ struct LazyArgs {
     uint32_t trace;
     float *m;                 // [B rows]
     uint64_t *S;              // [B rows]
-    uint32_t *units;          // [B rows]: row code + 1 published at [2B, ...) (0 = not yet)
-    uint32_t *cpair;          // [B]: rows of the current pair finished (odd -> even: pair done)
-    uint32_t *ctr;            // [0] next unit to claim, [1] units published past 2B, [2] slots done
+    uint32_t *units;          // [ucap] published unit code + 1 (0 = not yet)
+    uint32_t *cnt;            // [B (k+1)] position j: rows done + test j-1 accepted
+    uint32_t *rowflag;        // [B rows] row claimed
+    uint32_t *rpart;          // [B]: residual parts finished
+    int32_t *rpos;            // [B]: r + 1 of the slot, 0 while unknown (written before its parts are published)
+    uint32_t *ctr;            // [0] filler claims, [1] units published, [2] slots done, [3] tickets
+    u128 *tsum;               // [B n_tiles] residual tile masses
+    uint32_t ucap;
+    int32_t np, tp;           // residual parts per slot, tiles per part
     int32_t *tokens, *n_accept;
     uint64_t *z_out;
     uint32_t *err;
@@ -521,6 +618,15 @@ struct LazyArgs {
 #ifndef LAPSSD_LAZY_MINB
 #define LAPSSD_LAZY_MINB 2
 #endif
+#ifndef LAPSSD_LAZY_PF      // bytes per L2 bulk prefetch of a row unit's row (0: none)
+#define LAPSSD_LAZY_PF 32768
+#endif
+#ifndef LAPSSD_LAZY_TILES_PER_PART
+#define LAPSSD_LAZY_TILES_PER_PART 64
+#endif
+#ifndef LAPSSD_LAZY_SPEC    // speculative rows when idle (0: off)
+#define LAPSSD_LAZY_SPEC 1
+#endif
 constexpr int kLazyThreads = LAPSSD_LAZY_THREADS;
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
@@ -528,91 +634,242 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
+constexpr uint32_t kExit = 0xFFFFFFFFu;
+
+// Thread 0: the next unit code (row units < B rows, residual parts above), or kExit.  After
+// the filler, one ticket per claim (an atomicAdd, no CAS retries: contended CAS claims
+// serialised to ~1 per us), then a wait for that entry; a row taken already (claimed
+// speculatively) or of a slot already resolved is skipped.
+__device__ __forceinline__ uint32_t lazy_claim(const LazyArgs &a, uint32_t first, uint32_t rows) {
+    const uint32_t k = (uint32_t)a.k, row_units = (uint32_t)a.B * rows;
+    if (ld_acquire_u32(a.ctr) < first) {   // the position-0 filler
+        const uint32_t f = atomicAdd(a.ctr, 1u);
+        if (f < first) return (f >> 1) * rows + ((f & 1) ? k + 1 : 0);
+    }
+    for (;;) {
+        const uint32_t idx = atomicAdd(a.ctr + 3, 1u);
+        uint32_t c = kExit;
+        for (;;) {
+            if (idx < a.ucap) {
+                const uint32_t u = ld_acquire_u32(a.units + idx);
+                if (u) { c = u - 1; break; }
+            }
+            if (ld_acquire_u32(a.ctr + 2) >= (uint32_t)a.B) return kExit;
+            __nanosleep(128);
+        }
+        if (c >= row_units) return c;
+        if (__ldcg(a.rpos + c / rows) == 0 && atomicCAS(a.rowflag + c, 0u, 1u) == 0u) return c;
+    }
+}
+
+// Thread 0: publish n unit codes c0, c0 + step, ...
+__device__ __forceinline__ void lazy_publish(const LazyArgs &a, uint32_t c0, uint32_t step, uint32_t n) {
+    const uint32_t at = atomicAdd(a.ctr + 1, n);
+    for (uint32_t i = 0; i < n; ++i) st_release_u32(a.units + at + i, c0 + i * step + 1);
+}
+
+#ifdef LAPSSD_LAZY_TRACE   // diagnostic build only: per-unit (code, smid, claim, start, end)
+__device__ unsigned long long g_lazy_tr[16384][4];
+__device__ unsigned int g_lazy_n;
+extern "C" int lapssd_lazy_trace_read(unsigned long long *out, unsigned *n) {
+    cudaMemcpyFromSymbol(n, g_lazy_n, sizeof(unsigned));
+    cudaMemcpyFromSymbol(out, g_lazy_tr, sizeof g_lazy_tr);
+    unsigned z = 0;
+    cudaMemcpyToSymbol(g_lazy_n, &z, sizeof z);
+    return 0;
+}
+#endif
+
+// Thread 0: the rows of position j (the pair, or p_k for j = k) not claimed yet.
+__device__ __forceinline__ void publish_position(const LazyArgs &a, int b, int j) {
+    const int k = a.k, rows = 2 * k + 1;
+    const uint32_t c0 = (uint32_t)(b * rows + j);
+    if (__ldcg(a.rowflag + c0) == 0u) lazy_publish(a, c0, 0, 1);
+    if (j < k && __ldcg(a.rowflag + c0 + k + 1) == 0u) lazy_publish(a, c0 + k + 1, 0, 1);
+}
+
+// Thread 0: test j of slot b is due (rows of position j done, test j-1 accepted).  Runs the
+// chain of tests while the next position's rows are already done: acceptance makes
+// position j+1 needed and j+2 speculative, rejection at j (or reaching p_k) publishes the
+// slot's residual parts.
+template <bool BF16>
+__device__ __forceinline__ void run_tests(const LazyArgs &a, int b, int j, int64_t s) {
+    const int k = a.k, rows = 2 * k + 1;
+    for (;;) {
+        __threadfence();
+        int rr = -1;
+        if (j == k) {
+            rr = k;   // p_k: every draft accepted
+        } else if (rejects<BF16>(a.zp, a.zq, a.draft + s * k, s, j, a.req_id[b], a.round_idx[b], a.V, k, a.seed,
+                                 a.trace, a.m + (int64_t)b * rows, a.S + (int64_t)b * rows)) {
+            rr = j;
+        }
+        if (rr >= 0) {
+            a.rpos[b] = rr + 1;
+            lazy_publish(a, (uint32_t)a.B * rows + (uint32_t)b * a.np, 1, (uint32_t)a.np);
+            return;
+        }
+        publish_position(a, b, j + 1);
+#if LAPSSD_LAZY_SPEC
+        // a position ahead as well, but only while CTAs wait for work (tickets ahead of
+        // the published entries): idle SMs shorten the chain, busy ones are not diverted
+        if (j + 2 <= k && ld_acquire_u32(a.ctr + 3) > ld_acquire_u32(a.ctr + 1)) publish_position(a, b, j + 2);
+#endif
+        __threadfence();
+        const uint32_t c = atomicAdd(a.cnt + (int64_t)b * (k + 1) + j + 1, 1u) + 1;
+        if (c != (j + 1 == k ? 2u : 3u)) return;   // the rows of j+1 are not all done yet
+        ++j;
+    }
+}
+
+// Thread 0 of a CTA that completed row ri of slot b: store (m, S), count the row at its
+// position, and run the test if it is due.
+template <bool BF16>
+__device__ __forceinline__ void row_done(const LazyArgs &a, int b, int ri, int64_t s, float m, uint64_t S) {
+    const int k = a.k, rows = 2 * k + 1;
+    const int64_t rowi = (int64_t)b * rows + ri;
+    a.m[rowi] = m;
+    a.S[rowi] = S;
+    const int j = ri <= k ? ri : ri - k - 1;
+    __threadfence();
+    const uint32_t c = atomicAdd(a.cnt + (int64_t)b * (k + 1) + j, 1u) + 1;
+    if (c == (j == 0 || j == k ? 2u : 3u)) run_tests<BF16>(a, b, j, s);
+}
+
+// The CTA loop.  The next position-0 filler unit is claimed AHEAD (thread 0's atomic is in
+// flight while the unit streams), so after a row unit the other threads start the next
+// unit at once while thread 0 finishes the pair logic; only once the filler is exhausted
+// does a CTA claim (and wait) at the end of a unit.
 template <bool BF16>
 __global__ void __launch_bounds__(kLazyThreads, LAPSSD_LAZY_MINB) logits_lazy_kernel(const LazyArgs a) {
     using E = LElt<BF16>;
     constexpr int kTile = 32 * kTileVecs * E::kVec;
     extern __shared__ __align__(16) uint8_t s_raw[];
     u128 *tile_sum = reinterpret_cast<u128 *>(s_raw);
-    __shared__ uint32_t s_code;
-    __shared__ int s_r;
+    __shared__ uint32_t s_code, s_next;
+    __shared__ int s_last;
     const int k = a.k, rows = 2 * k + 1;
     const int64_t nv = a.V / E::kVec;
     const int n_tiles = (int)((a.V + kTile - 1) / kTile);
-    const uint32_t cap = (uint32_t)a.B * rows, first = 2u * (uint32_t)a.B;
+    const uint32_t row_units = (uint32_t)a.B * rows, first = 2u * (uint32_t)a.B;
+    constexpr uint32_t kNone = 0xFFFFFFFEu;
+    bool filler_left = true;   // thread 0's view
+#ifdef LAPSSD_LAZY_TRACE
+    unsigned long long tr_claim = 0, tr_got = 0;
+    if (threadIdx.x == 0) tr_claim = gtimer();
+#endif
+    if (threadIdx.x == 0) s_code = lazy_claim(a, first, (uint32_t)rows);
+    __syncthreads();
+    uint32_t code = s_code;
     for (;;) {
-        if (threadIdx.x == 0) {
-            const uint32_t idx = atomicAdd(a.ctr, 1u);
-            uint32_t code = 0xFFFFFFFFu;   // exit
-            if (idx < first) {
-                code = (idx >> 1) * rows + ((idx & 1) ? k + 1 : 0);
-            } else if (idx < cap) {
-                for (;;) {
-                    const uint32_t u = ld_acquire_u32(a.units + idx);
-                    if (u) { code = u - 1; break; }
-                    if (ld_acquire_u32(a.ctr + 2) >= (uint32_t)a.B) break;
-                    __nanosleep(128);
+        if (code == kExit) return;
+#ifdef LAPSSD_LAZY_TRACE
+        const uint32_t cur = code;
+        if (threadIdx.x == 0) tr_got = gtimer();
+#endif
+        uint32_t nf = first;   // thread 0: the filler unit claimed ahead (first = none)
+        if (threadIdx.x == 0 && filler_left) nf = atomicAdd(a.ctr, 1u);
+        int r = -1;
+        if (code < row_units) {   // ---- a row unit
+            const int b = (int)(code / rows), ri = (int)(code % rows);
+            const int64_t s = a.slab ? a.slab[b] : b;
+            const uint4 *v4 = row_ptr<BF16>(a.zp, a.zq, s, a.V, k, ri);
+#if LAPSSD_LAZY_PF > 0   // the whole row requested into L2 up front (the max pass then reads L2)
+            if ((threadIdx.x >> 5) == (int)(blockDim.x >> 5) - 1) {
+                const int64_t bytes = a.V * E::kEsz;
+                for (int64_t o = (int64_t)(threadIdx.x & 31) * LAPSSD_LAZY_PF; o < bytes; o += 32 * LAPSSD_LAZY_PF) {
+                    const uint32_t n = (uint32_t)(bytes - o < LAPSSD_LAZY_PF ? bytes - o : LAPSSD_LAZY_PF);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const char *)v4 + o), "r"(n)
+                                 : "memory");
                 }
             }
-            s_code = code;
-        }
-        __syncthreads();
-        const uint32_t code = s_code;
-        if (code == 0xFFFFFFFFu) return;
-        const int b = (int)(code / rows), ri = (int)(code % rows);
-        const int64_t s = a.slab ? a.slab[b] : b;
-        const int64_t rowi = (int64_t)b * rows + ri;
-        const uint4 *v4 = row_ptr<BF16>(a.zp, a.zq, s, a.V, k, ri);
-        const float m = range_max<BF16>(v4, 0, nv);
-        const uint64_t S = range_sum<BF16>(v4, 0, nv, m);
-        const uint32_t req = a.req_id[b], rnd = a.round_idx[b];
-        const int32_t *dr = a.draft + s * k;
-        const float *mb = a.m + (int64_t)b * rows;
-        const uint64_t *Sb = a.S + (int64_t)b * rows;
-        if (threadIdx.x == 0) {
-            a.m[rowi] = m;
-            a.S[rowi] = S;
-            int r = -1;
-            if (ri == k) {
-                r = k;   // p_k: every draft accepted
-            } else {
-                __threadfence();
-                if (atomicAdd(a.cpair + b, 1u) & 1) {   // the pair's other row is complete too
-                    __threadfence();
-                    const int j = ri < k ? ri : ri - k - 1;
-                    if (rejects<BF16>(a.zp, a.zq, dr, s, j, req, rnd, a.V, k, a.seed, a.trace, mb, Sb)) {
-                        r = j;
-                    } else {
-                        const bool last = j + 1 == k;
-                        const uint32_t at = first + atomicAdd(a.ctr + 1, last ? 1u : 2u);
-                        const uint32_t c0 = (uint32_t)b * rows + (last ? k : j + 1);
-                        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.units + at), "r"(c0 + 1) : "memory");
-                        if (!last)
-                            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.units + at + 1),
-                                         "r"(c0 + k + 2) : "memory");
-                    }
-                }
+#endif
+            const float m = range_max<BF16>(v4, 0, nv);
+            const uint64_t S = range_sum<BF16>(v4, 0, nv, m);
+            if (threadIdx.x == 0) {
+                filler_left = nf < first;
+                s_next = filler_left ? (nf >> 1) * rows + ((nf & 1) ? k + 1 : 0) : kNone;
             }
-            s_r = r;
-        }
-        __syncthreads();
-        const int r = s_r;
-        if (r >= 0) {   // the residual draw of slot b, by this CTA
-            Resid q = resid_of<BF16>(a.zp, a.zq, s, r, a.V, k, mb, Sb);
-            tile_pass<BF16>(q, nv, 0, n_tiles, tile_sum);
             __syncthreads();
-            amb20_fallback<BF16>(q, nv, n_tiles, tile_sum);
-            if (threadIdx.x < 32)
-                draw_token<BF16>(q, nv, n_tiles, tile_sum, dr, b, r, req, rnd, k, a.V, a.seed, a.trace, a.tokens,
-                                 a.n_accept, a.z_out, a.err);
+            const uint32_t next = s_next;
+            if (threadIdx.x == 0) row_done<BF16>(a, b, ri, s, m, S);
+            if (next != kNone) {
+                code = next;
+#ifdef LAPSSD_LAZY_TRACE
+                goto trace;
+#endif
+                continue;
+            }
+        } else {                  // ---- a residual part
+            const uint32_t pc = code - row_units;
+            const int b = (int)(pc / a.np), part = (int)(pc % a.np);
+            r = __ldcg(a.rpos + b) - 1;
+            const int64_t s = a.slab ? a.slab[b] : b;
+            const float *mb = a.m + (int64_t)b * rows;
+            const uint64_t *Sb = a.S + (int64_t)b * rows;
+            Resid q = resid_of<BF16>(a.zp, a.zq, s, r, a.V, k, mb, Sb);
+            u128 *ts = a.tsum + (int64_t)b * n_tiles;
+            const int t_lo = part * a.tp, t_hi = min(n_tiles, t_lo + a.tp);
+            tile_pass_fast<BF16>(q, nv, t_lo, t_hi, ts);
+            __threadfence();
             __syncthreads();
             if (threadIdx.x == 0) {
-                __threadfence();
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.ctr + 2) : "memory");
+                const bool last = atomicAdd(a.rpart + b, 1u) == (uint32_t)a.np - 1;
+                if (last) __threadfence();
+                s_last = last;
+                filler_left = nf < first;
+                s_next = filler_left ? (nf >> 1) * rows + ((nf & 1) ? k + 1 : 0) : kNone;
+            }
+            __syncthreads();
+            if (s_last) {   // every part is in: Z, the draw, the outputs of slot b
+                for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
+                    const unsigned long long *w = reinterpret_cast<const unsigned long long *>(ts + t);
+                    tile_sum[t] = ((u128)__ldcg(w + 1) << 64) | __ldcg(w);
+                }
+                __syncthreads();
+                amb20_fallback<BF16>(q, nv, n_tiles, tile_sum);
+                if (threadIdx.x < 32)
+                    draw_token<BF16>(q, nv, n_tiles, tile_sum, a.draft + s * k, b, r, a.req_id[b], a.round_idx[b],
+                                     k, a.V, a.seed, a.trace, a.tokens, a.n_accept, a.z_out, a.err);
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.ctr + 2) : "memory");
+                }
+            }
+            const uint32_t next = s_next;
+            if (next != kNone) {
+                __syncthreads();   // s_next / s_last are rewritten by the next unit
+                code = next;
+#ifdef LAPSSD_LAZY_TRACE
+                goto trace;
+#endif
+                continue;
             }
         }
+        // no filler left: claim (and wait for) a published unit
+        if (threadIdx.x == 0) s_code = lazy_claim(a, first, (uint32_t)rows);
         __syncthreads();
+        code = s_code;
+#ifdef LAPSSD_LAZY_TRACE
+    trace:
+        if (threadIdx.x == 0) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            const unsigned i = atomicAdd(&g_lazy_n, 1u);
+            if (i < 16384) {
+                g_lazy_tr[i][0] = ((unsigned long long)smid << 32) | (cur & 0x7FFFFFFFu) | ((unsigned long long)(r >= 0) << 31);
+                g_lazy_tr[i][1] = tr_claim;
+                g_lazy_tr[i][2] = tr_got;
+                g_lazy_tr[i][3] = gtimer();
+            }
+            tr_claim = gtimer();
+        }
+#endif
     }
 }
 
@@ -621,9 +878,23 @@ size_t logits_tile_smem(int64_t V, int32_t dtype) {
     return (size_t)((V + tile - 1) / tile) * sizeof(u128);
 }
 
-// Workspace of the lazy form after (m, S): the queue and counters, zeroed per call.
-size_t logits_lazy_bytes(int32_t B, int32_t k, int64_t, int32_t) {
-    return 256 + ((size_t)B * (2 * k + 1) + (size_t)B + 4) * sizeof(uint32_t);
+static int lazy_parts(int64_t V, int32_t dtype, int *tp) {
+    const int n_tiles = (int)(logits_tile_smem(V, dtype) / sizeof(u128));
+    *tp = LAPSSD_LAZY_TILES_PER_PART;
+    return (n_tiles + *tp - 1) / *tp;
+}
+
+static size_t lazy_words(int32_t B, int32_t k, int np) {
+    const size_t rows = 2 * (size_t)k + 1, ucap = (size_t)B * (2 * rows + np) + 4096;   // a row at most twice (ahead, then needed)
+    return ucap + (size_t)B * ((k + 1) + rows + 2) + 8;
+}
+
+// Workspace of the lazy form after (m, S): the queue and counters (zeroed per call), then
+// the residual tile masses.
+size_t logits_lazy_bytes(int32_t B, int32_t k, int64_t V, int32_t dtype) {
+    int tp;
+    const int np = lazy_parts(V, dtype, &tp);
+    return 512 + lazy_words(B, k, np) * sizeof(uint32_t) + (size_t)B * logits_tile_smem(V, dtype);
 }
 
 template <bool BF16>
@@ -647,11 +918,17 @@ static cudaError_t launch_lazy(const void *zp, const void *zq, int64_t V, int32_
     a.draft = draft; a.slab = slab; a.req_id = req_id; a.round_idx = round_idx;
     a.V = V; a.k = k; a.B = B; a.seed = seed; a.trace = trace;
     a.m = m_ws; a.S = S_ws;
+    a.np = lazy_parts(V, BF16 ? LAPSSD_BF16 : LAPSSD_F32, &a.tp);
     uint32_t *q = (uint32_t *)(((size_t)lazy_ws + 255) & ~(size_t)255);
-    const size_t words = (size_t)B * rows + (size_t)B + 4;
+    const size_t words = lazy_words(B, k, a.np);
+    a.ucap = (uint32_t)((size_t)B * (2 * rows + a.np) + 4096);
     a.units = q;
-    a.cpair = q + (size_t)B * rows;
-    a.ctr = a.cpair + B;
+    a.cnt = q + a.ucap;
+    a.rowflag = a.cnt + (size_t)B * (k + 1);
+    a.rpart = a.rowflag + (size_t)B * rows;
+    a.rpos = (int32_t *)(a.rpart + B);
+    a.ctr = (uint32_t *)(a.rpos + B);
+    a.tsum = (u128 *)(((size_t)(q + words) + 255) & ~(size_t)255);
     a.tokens = tokens; a.n_accept = n_accept; a.z_out = z; a.err = nullptr;
     cudaError_t ce = cudaMemsetAsync(q, 0, words * sizeof(uint32_t), s);
     if (ce != cudaSuccess) return ce;

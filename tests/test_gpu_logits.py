@@ -171,3 +171,42 @@ def test_logits_rint_of_the_rounded_product(L):
     tok_o, r_o, z_o = oracle.verify_logits_batch(zp, zq, draft, slab, req, rnd, 11)
     assert (na.cpu().numpy() == r_o).all() and (tok.cpu().numpy() == tok_o).all()
     assert (z.cpu().numpy().view(np.uint64) == z_o).all()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_residual_near_ties_exact_path(L, dtype):
+    """Draft logits equal to the target's except one unit of the format at the draft token
+    (and at a few other entries): every residual entry is a near-tie p^ ~ q^ that the
+    split-sum pass's fp32 screen cannot decide, so the exact 128-bit comparison decides it;
+    logits span the whole exp range, so the masses E run from 0 to 2^40."""
+    V, k, S = 8192, 4, 24
+    rng = np.random.default_rng(17 if dtype == "bf16" else 18)
+    zp = (rng.random((S, k + 1, V)) * -30.0).astype(np.float32)
+    zp[:, :, 0] = 0.0
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    zp = torch.as_tensor(zp).to(tdt)
+    zq = zp[:, :k].clone()
+    draft = torch.as_tensor(rng.integers(1, V, (S, k)).astype(np.int32))
+    step = 1 if dtype == "bf16" else 1 << 15          # units in the last place to move
+    view = zq.view(torch.int16) if dtype == "bf16" else zq.view(torch.int32)
+    for s in range(S):
+        for j in range(k):
+            x = int(draft[s, j])
+            view[s, j, x] -= step * (1 + s % 3)        # logits are <= 0: a smaller magnitude is larger
+            others = rng.integers(1, V, 4)
+            view[s, j, others[:2]] += step
+            view[s, j, others[2:]] -= step
+    B = 384
+    slab = np.arange(B, dtype=np.int32) % S
+    req = rng.integers(0, 1 << 20, B).astype(np.int32)
+    rnd = rng.integers(0, 1 << 12, B).astype(np.int32)
+    dev = "cuda"
+    tok, na, z = L.spec_verify_logits(zp.to(dev), zq.to(dev), draft.to(dev), torch.as_tensor(req, device=dev),
+                                      torch.as_tensor(rnd, device=dev), 23, slab=torch.as_tensor(slab, device=dev))
+    zp_o, zq_o = synth.to_numpy_rows(zp), synth.to_numpy_rows(zq)
+    tok_o, r_o, z_o = oracle.verify_logits_batch(zp_o, zq_o, draft.numpy(), slab, req, rnd, 23)
+    na = na.cpu().numpy()
+    assert (na == r_o).all()
+    assert (z.cpu().numpy().view(np.uint64) == z_o).all()
+    assert (tok.cpu().numpy() == tok_o).all()
+    assert (na < k).sum() >= 20                       # enough residual draws
