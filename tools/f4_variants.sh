@@ -1,13 +1,13 @@
 #!/bin/bash
-# tree kernel: trees per CTA variants (diagnostic builds under tools/variants/, never the product)
+# tree kernel: CTAs-per-tree (cluster size) variants, diagnostic builds under tools/variants/ (never the product).
 cd "$(dirname "$0")/.."
-mkdir -p tools/variants
-bash tools/gpu_tests.sh f4 | tail -2
-for t in 4 2 8; do
-  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -DLAPSSD_TREES_PER_CTA=$t \
-    -Xcompiler -fPIC -shared -o tools/variants/lib_g$t.so paper_2505_17074_b200/csrc/api.cu paper_2505_17074_b200/csrc/verify.cu \
-    paper_2505_17074_b200/csrc/verify_logits.cu paper_2505_17074_b200/csrc/sched.cu paper_2505_17074_b200/csrc/mc.cu \
-    paper_2505_17074_b200/csrc/draft_tree.cu -ldl
-  LAPSSD_LIBRARY=tools/variants/lib_g$t.so timeout 600 python bench.py --workload tree --steps 60 --warmup 5 --no-cpu-baseline > gpurun_out/f4_tree_g$t.log 2>&1
-  echo "trees/CTA $t"; python tools/bench_summary.py gpurun_out/f4_tree_g$t.log | cut -c 1-150
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_f4.py -x -q > gpurun_out/pytest_f4.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_f4.log
+tail -2 gpurun_out/pytest_f4.log
+timeout 600 python bench.py --workload tree --steps 60 --warmup 5 --no-cpu-baseline > gpurun_out/f4_tree.log 2>&1
+echo "product $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/f4_tree.log)"
+for v in $TREE_VARIANTS; do
+  LAPSSD_LIBRARY=tools/variants/lib_$v.so timeout 900 python -m pytest tests/test_gpu_f4.py -x -q 2>&1 | tail -1
+  LAPSSD_LIBRARY=tools/variants/lib_$v.so timeout 600 python bench.py --workload tree --steps 60 --warmup 5 --no-cpu-baseline > gpurun_out/f4_tree_$v.log 2>&1
+  echo "$v $(grep -o '"ms_per_step": [0-9.]*' gpurun_out/f4_tree_$v.log)"
 done
