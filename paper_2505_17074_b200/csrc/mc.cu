@@ -19,7 +19,10 @@
 
 namespace lapssd {
 
-__global__ void __launch_bounds__(256) mc_step_kernel(const State st, const Sched sc, const McDev mc,
+#ifndef LAPSSD_MC_MINB   // resident 256-thread CTAs per SM the register budget is sized for
+#define LAPSSD_MC_MINB 4
+#endif
+__global__ void __launch_bounds__(256, LAPSSD_MC_MINB) mc_step_kernel(const State st, const Sched sc, const McDev mc,
                                                       const RowsDev rw, const int32_t *n_accept, SlotDesc *desc,
                                                       int32_t *sel_out, int32_t *active) {
     const int lane = threadIdx.x & 31;
