@@ -210,3 +210,31 @@ def test_residual_near_ties_exact_path(L, dtype):
     assert (z.cpu().numpy().view(np.uint64) == z_o).all()
     assert (tok.cpu().numpy() == tok_o).all()
     assert (na < k).sum() >= 20                       # enough residual draws
+
+
+@pytest.mark.parametrize("offset", [7950.0, -7990.0, 9000.0, -30000.0])
+def test_large_row_max_bf16(L, offset):
+    """Row maxima near and beyond the packed floor's range (|m| <= 8000: the floor
+    round_down_bf16(m - 28) is coarse there; beyond it the kernel keeps the fp32 clamp):
+    bf16 logits offset by a constant, spread over the exp cut-off."""
+    V, k, S = 4096, 3, 6
+    rng = np.random.default_rng(int(abs(offset)))
+    base = rng.standard_normal((S, k + 1, V)).astype(np.float32) * 12.0
+    zp = torch.as_tensor(base + offset).to(torch.bfloat16)
+    zq = torch.as_tensor(base[:, :k] + offset + rng.standard_normal((S, k, V)).astype(np.float32) * 2.0).to(
+        torch.bfloat16)
+    qs = torch.softmax(zq.float(), -1).reshape(S * k, V)
+    draft = torch.multinomial(qs, 1, generator=torch.Generator().manual_seed(5)).view(S, k).to(torch.int32)
+    B = 48
+    slab = (np.arange(B) % S).astype(np.int32)
+    req = rng.integers(0, 1 << 20, B).astype(np.int32)
+    rnd = rng.integers(0, 1 << 12, B).astype(np.int32)
+    dev = "cuda"
+    tok, na, z = L.spec_verify_logits(zp.to(dev), zq.to(dev), draft.to(dev), torch.as_tensor(req, device=dev),
+                                      torch.as_tensor(rnd, device=dev), 31, slab=torch.as_tensor(slab, device=dev))
+    tok_o, r_o, z_o = oracle.verify_logits_batch(synth.to_numpy_rows(zp), synth.to_numpy_rows(zq), draft.numpy(),
+                                                 slab, req, rnd, 31)
+    na = na.cpu().numpy()
+    assert (na == r_o).all()
+    assert (z.cpu().numpy().view(np.uint64) == z_o).all()
+    assert (tok.cpu().numpy() == tok_o).all()
