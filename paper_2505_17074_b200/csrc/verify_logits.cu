@@ -624,8 +624,11 @@ struct LazyArgs {
 #ifndef LAPSSD_LAZY_TILES_PER_PART
 #define LAPSSD_LAZY_TILES_PER_PART 64
 #endif
-#ifndef LAPSSD_LAZY_SPEC    // speculative rows when idle (0: off)
-#define LAPSSD_LAZY_SPEC 1
+#ifndef LAPSSD_LAZY_SPEC_IDLE   // speculation d positions ahead only with > (d-1) x this many CTAs waiting
+#define LAPSSD_LAZY_SPEC_IDLE 16
+#endif
+#ifndef LAPSSD_LAZY_SPEC    // speculative rows while CTAs wait: up to this many positions ahead (0: off)
+#define LAPSSD_LAZY_SPEC 2
 #endif
 constexpr int kLazyThreads = LAPSSD_LAZY_THREADS;
 
@@ -717,7 +720,11 @@ __device__ __forceinline__ void run_tests(const LazyArgs &a, int b, int j, int64
 #if LAPSSD_LAZY_SPEC
         // a position ahead as well, but only while CTAs wait for work (tickets ahead of
         // the published entries): idle SMs shorten the chain, busy ones are not diverted
-        if (j + 2 <= k && ld_acquire_u32(a.ctr + 3) > ld_acquire_u32(a.ctr + 1)) publish_position(a, b, j + 2);
+        if (j + 2 <= k) {   // position j+1+d while more than (d-1) LAPSSD_LAZY_SPEC_IDLE CTAs wait
+            const int32_t waiting = (int32_t)(ld_acquire_u32(a.ctr + 3) - ld_acquire_u32(a.ctr + 1));
+            for (int d = 1; d <= LAPSSD_LAZY_SPEC && j + 1 + d <= k; ++d)
+                if (waiting > (d - 1) * LAPSSD_LAZY_SPEC_IDLE) publish_position(a, b, j + 1 + d);
+        }
 #endif
         __threadfence();
         const uint32_t c = atomicAdd(a.cnt + (int64_t)b * (k + 1) + j + 1, 1u) + 1;
@@ -885,7 +892,9 @@ static int lazy_parts(int64_t V, int32_t dtype, int *tp) {
 }
 
 static size_t lazy_words(int32_t B, int32_t k, int np) {
-    const size_t rows = 2 * (size_t)k + 1, ucap = (size_t)B * (2 * rows + np) + 4096;   // a row at most twice (ahead, then needed)
+    // position p is published by test p-1 (needed) and at most by tests p-2 .. p-1-SPEC
+    // (ahead), so a row is published at most 1 + LAPSSD_LAZY_SPEC times
+    const size_t rows = 2 * (size_t)k + 1, ucap = (size_t)B * ((1 + LAPSSD_LAZY_SPEC) * rows + np) + 4096;
     return ucap + (size_t)B * ((k + 1) + rows + 2) + 8;
 }
 
@@ -921,7 +930,7 @@ static cudaError_t launch_lazy(const void *zp, const void *zq, int64_t V, int32_
     a.np = lazy_parts(V, BF16 ? LAPSSD_BF16 : LAPSSD_F32, &a.tp);
     uint32_t *q = (uint32_t *)(((size_t)lazy_ws + 255) & ~(size_t)255);
     const size_t words = lazy_words(B, k, a.np);
-    a.ucap = (uint32_t)((size_t)B * (2 * rows + a.np) + 4096);
+    a.ucap = (uint32_t)((size_t)B * ((1 + LAPSSD_LAZY_SPEC) * rows + a.np) + 4096);
     a.units = q;
     a.cnt = q + a.ucap;
     a.rowflag = a.cnt + (size_t)B * (k + 1);
