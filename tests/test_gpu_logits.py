@@ -238,3 +238,51 @@ def test_large_row_max_bf16(L, offset):
     assert (na == r_o).all()
     assert (z.cpu().numpy().view(np.uint64) == z_o).all()
     assert (tok.cpu().numpy() == tok_o).all()
+
+
+@pytest.mark.parametrize("policy", [0, 3])
+def test_laps_sd_driven_by_logits(L, policy):
+    """The LAPS-SD step from LOGITS through the C-ABI: spec_verify_logits on the batch the
+    handle selected (request id and round as the Philox counter, the round's slab), then
+    laps_update with its r and laps_select -- in lockstep with the oracle (verify_logits ->
+    Sim.update -> Sim.select) over whole traces, every state field compared."""
+    from test_gpu_step import BASE, compare_state
+    V, k, B = 4096, 4, 6
+    tr = synth.make_trace(60, 0x10C1 + policy, arrival="poisson", rate_per_s=80.0, len_mu=np.log(24),
+                          len_sigma=0.6, len_min=2, len_max=96, drift=True)
+    pool = synth.make_logits_pool(V, k, "bf16", n_buckets=8, variants=2, seed=0x10C1, device="cuda")
+    R = 8
+    tab = synth.slab_table(tr, 8, 2, R=R, seed=0x10C1)
+    kw = dict(BASE, k=k, seed=31, policy=policy, switch_c0_us=1_000, switch_c1_us=10)
+    pr = synth.prompt_lengths(tr.n, 0x10C1)
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=V, prompt=pr)
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, prompt=pr)
+    zp, zq, dr = synth.to_numpy_rows(pool.p), synth.to_numpy_rows(pool.q), pool.draft.cpu().numpy()
+    sel_o, _ = sim.select(B)
+    h.laps_select(B)
+    seed = 0x5EED
+    for step in range(4000):
+        sel_g = h.sel[:B].cpu().numpy()
+        assert (sel_g == sel_o).all(), f"step {step}: batch differs"
+        if sim.state()["done"].all():
+            break
+        st = h.state()
+        live = sel_g >= 0
+        ids = np.maximum(sel_g, 0)
+        rounds = np.where(live, st["rounds"][ids], 0).astype(np.int32)
+        slab = np.where(live, tab[ids, rounds % R], 0).astype(np.int32)
+        req = ids.astype(np.int32)
+        _, na, _ = L.spec_verify_logits(pool.p, pool.q, pool.draft, torch.as_tensor(req, device="cuda"),
+                                        torch.as_tensor(rounds, device="cuda"), seed,
+                                        slab=torch.as_tensor(slab, device="cuda"))
+        _, r_o, _ = oracle.verify_logits_batch(zp, zq, dr, slab, req, rounds, seed)
+        assert (na.cpu().numpy()[live] == r_o[live]).all(), f"step {step}: r differs"
+        h.laps_update(h.sel[:B], na)
+        h.laps_select(B)
+        sim.update(sel_o, np.where(live, r_o, 0).astype(np.int32))
+        sel_o, _ = sim.select(B)
+        if step % 4 == 0:
+            compare_state(h.state(), sim.state(), step)
+    assert sim.state()["done"].all()
+    compare_state(h.state(), sim.state(), "end")
+    assert h.check() == 0
