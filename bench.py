@@ -984,12 +984,22 @@ def run_logits(args):
                                  "algorithmic bytes: the logit rows the acceptance tests consult, once each "
                                  "(pairs 0..min(r,k-1), and p_k if r = k); the residual pass re-reads its pair "
                                  "from L2") + "; traffic: ncu DRAM bytes of one step for this build, else null"}}
+    if not eager:   # the work the lazy form avoids, against round 1's every-row definition
+        every = float((2 * k + 1) * row * r.size) / G
+        out["roofline"]["every_row_form"] = {
+            "algorithmic_bytes_per_step": every, "rows_consulted_frac": alg / every,
+            "equivalent_GBps": every / (ms / steps * 1e-3) / 1e9,
+            "note": "the every-row form (round 1: all 2k+1 rows normalised, 1.00 ms per step) reads "
+                    "these bytes; the lazy form reads only the consulted rows, so its fractions are "
+                    "of a smaller amount of work, not a slower kernel"}
     alu = alu_roofline("logits", {"B": B, "V": V, "k": k}, ms / steps, clk)
     if alu:   # the binding resource: instruction issue (the fixed-op exp and the 128-bit residual)
         hbm = out["roofline"]
         out["roofline"] = dict(alu, kernel=hbm["kernel"],
                                hbm={x: hbm[x] for x in ("achieved", "peak", "unit", "frac", "algorithmic_bytes_per_step",
                                                         "traffic")})
+        if "every_row_form" in hbm:
+            out["roofline"]["every_row_form"] = hbm["every_row_form"]
     if not args.no_cpu_baseline and rank == 0:
         import oracle
         sl = slabs[0].cpu().numpy()
