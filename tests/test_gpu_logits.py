@@ -286,3 +286,32 @@ def test_laps_sd_driven_by_logits(L, policy):
     assert sim.state()["done"].all()
     compare_state(h.state(), sim.state(), "end")
     assert h.check() == 0
+
+
+@pytest.mark.parametrize("B,dtype", [(1, "bf16"), (3, "f32"), (64, "bf16")])
+def test_lazy_speculation_long_chains(L, B, dtype):
+    """k = 16 with high-acceptance slabs and few slots: almost every CTA of the persistent
+    grid waits for work, so rows are run one and two positions ahead speculatively (and
+    many of them turn out not to be needed); results against the oracle, and repeated calls
+    on one workspace give identical results."""
+    V, k = 2048, 16
+    pool = synth.make_logits_pool(V, k, dtype, n_buckets=4, variants=2, seed=300 + B, device="cuda")
+    rng = np.random.default_rng(300 + B)
+    hi = np.arange(pool.S)[np.arange(pool.S) // 2 >= 2]   # the two high-acceptance buckets
+    slab = rng.choice(hi, B).astype(np.int32)
+    req = rng.integers(0, 1 << 20, B).astype(np.int32)
+    rnd = rng.integers(0, 1 << 12, B).astype(np.int32)
+    P = pool.numpy()
+    if B == 1:   # a round whose chain is long (the oracle picks it)
+        for c in range(4096):
+            rnd[0] = c
+            if oracle.verify_logits_batch(P["p"], P["q"], P["draft"], slab, req, rnd, 41)[1][0] >= 8:
+                break
+    ws = torch.empty(L.spec_verify_logits_workspace_bytes(B, k, V, dtype), dtype=torch.uint8, device="cuda")
+    outs = [[x.cpu().numpy() for x in _call(L, pool, slab, req, rnd, 41, ws)] for _ in range(3)]
+    for o in outs[1:]:
+        assert all((a == b).all() for a, b in zip(o, outs[0]))
+    tok, na, z = outs[0]
+    tok_o, r_o, z_o = oracle.verify_logits_batch(P["p"], P["q"], P["draft"], slab, req, rnd, 41)
+    assert (na == r_o).all() and (tok == tok_o).all() and (z.view(np.uint64) == z_o).all()
+    assert na.max() >= 4
