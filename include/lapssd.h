@@ -323,6 +323,26 @@ lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t
 lapssd_status laps_step(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel_inout,
                         int32_t *count_out, int32_t *tokens_out, int32_t *n_accept_out,
                         lapssd_stream stream);
+
+/* laps_step_logits -- the LAPS-SD step from LOGITS (SURVEY 8(f) f1 inside the step;
+ * P:57-64, P:200 with the quantised softmax of spec_verify_logits, DESIGN.md AMB-30):
+ * for the batch in sel_inout (as left by laps_select / the previous step), slot b verifies
+ * request i = sel_inout[b] exactly as spec_verify_logits would with req_id = the global
+ * id (i * world + rank), round_idx = the request's round count, slab = rows->slab_tab[i,
+ * slab_round_index(round)] (pooled layout; without a slab table slot b reads slab b),
+ * then runs laps_update with the resulting r and laps_select for the next batch.  rows:
+ * logits in rows->p ((k+1) x V target logits per slab) and rows->q (k x V draft logits),
+ * rows->draft, dtype bf16 / fp32, V <= 2^23.  Outputs [device, nullable: internal
+ * buffers]: tokens_out [B, k+1], n_accept_out [B] (-1 and -1 tokens for empty slots),
+ * count_out as laps_select.  workspace: [device] >= laps_step_logits_workspace_bytes(B,
+ * k, V, dtype) bytes, any content.  One C-ABI call, five launches on the caller's stream
+ * (slot counters, the lazy verify, the empty-slot mask, the update, the select); not
+ * overlapped like laps_step.  Errors: EINVAL (handle, B, rows, k mismatch, NULL),
+ * ENOMEM (workspace), ECUDA. */
+size_t laps_step_logits_workspace_bytes(int32_t B, int32_t k, int64_t V, int32_t dtype);
+lapssd_status laps_step_logits(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel_inout,
+                               int32_t *count_out, int32_t *tokens_out, int32_t *n_accept_out, void *workspace,
+                               size_t workspace_bytes, lapssd_stream stream);
 /* Opt in (enable = 1) or out (0, the default) of overlapping consecutive laps_step /
  * laps_step_dist verify launches (programmatic dependent launch; contract above).
  * Errors: EINVAL (NULL handle). */

@@ -80,6 +80,8 @@ def _load():
         "laps_update": ([vp, vp, vp, i32, vp], i32),
         "laps_select": ([vp, i32, vp, vp, vp], i32),
         "laps_step": ([vp, vp, i32, vp, vp, vp, vp, vp], i32),
+        "laps_step_logits_workspace_bytes": ([i32, i32, i64, i32], sz),
+        "laps_step_logits": ([vp, vp, i32, vp, vp, vp, vp, vp, sz, vp], i32),
         "lapssd_set_step_overlap": ([vp, i32], i32),
         "lapssd_set_row_check": ([vp, i32], i32),
         "laps_candidates": ([vp, i32, vp, vp], i32),
@@ -179,6 +181,12 @@ def spec_verify(p, q, draft, req_id, round_idx, seed, *, slab=None, trace=0, tok
                           workspace.numel(), _stream(stream))
     _check("spec_verify", rc)
     return tokens, n_accept, z
+
+
+def laps_step_logits_workspace_bytes(B, k, V, dtype) -> int:
+    """Workspace bytes of Handle.laps_step_logits; dtype "bf16" / "f32" or the lapssd code."""
+    code = {"bf16": BF16, "f32": F32}.get(dtype, dtype)
+    return int(_lib.laps_step_logits_workspace_bytes(B, k, V, code))
 
 
 def spec_verify_logits_workspace_bytes(B, k, V, dtype) -> int:
@@ -343,6 +351,21 @@ class Handle:
         sel = self.sel if sel is None else sel
         count = self.count if count is None else count
         _check("laps_select", _lib.laps_select(self.h, B, _dptr(sel), _dptr(count), _stream(stream)))
+        return sel, count
+
+    def laps_step_logits(self, rows: Rows, B, sel=None, count=None, tokens=None, n_accept=None, workspace=None,
+                         stream=None):
+        """The LAPS-SD step from logits (include/lapssd.h laps_step_logits): rows.p / rows.q
+        hold target / draft LOGITS.  workspace: a uint8 device tensor of at least
+        laps_step_logits_workspace_bytes(B, k, V, dtype) bytes (allocated if None)."""
+        sel = self.sel if sel is None else sel
+        count = self.count if count is None else count
+        nbytes = int(_lib.laps_step_logits_workspace_bytes(B, rows.k, rows.V, _dtype_code(rows.p)))
+        if workspace is None:
+            workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=sel.device)
+        _check("laps_step_logits", _lib.laps_step_logits(self.h, C.byref(rows.c), B, _dptr(sel), _dptr(count),
+                                                         _dptr(tokens), _dptr(n_accept), _dptr(workspace),
+                                                         workspace.numel(), _stream(stream)))
         return sel, count
 
     def laps_step(self, rows: Rows, B, sel=None, count=None, tokens=None, n_accept=None, stream=None):

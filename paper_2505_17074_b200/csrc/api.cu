@@ -486,6 +486,68 @@ lapssd_status laps_select(lapssd_handle *h, int32_t B, int32_t *sel_out, int32_t
                        "laps_select");
 }
 
+// ---------------------------------------------------------------- f1 in the LAPS-SD step
+size_t laps_step_logits_workspace_bytes(int32_t B, int32_t k, int64_t V, int32_t dtype) {
+    if (!spec_verify_logits_workspace_bytes(B, k, V, dtype)) return 0;
+    const int32_t Bn = B > 0 ? B : 1;
+    const size_t rows = (size_t)Bn * (size_t)(2 * k + 1);
+    Carver cv{nullptr};   // the same carving as laps_step_logits
+    cv.take<float>(rows);
+    cv.take<uint64_t>(rows);
+    cv.take<char>(logits_lazy_bytes(Bn, k, V, dtype));
+    cv.take<uint32_t>((size_t)Bn);
+    cv.take<uint32_t>((size_t)Bn);
+    cv.take<int32_t>((size_t)Bn);
+    return align256(cv.off);
+}
+
+lapssd_status laps_step_logits(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel_inout,
+                               int32_t *count_out, int32_t *tokens_out, int32_t *n_accept_out, void *workspace,
+                               size_t workspace_bytes, lapssd_stream stream) {
+    g_last_error.clear();
+    if (!h || B < 1 || B > h->max_batch) return fail(LAPSSD_EINVAL, "handle / B");
+    if (!rows || !rows->p || !rows->q || !rows->draft) return fail(LAPSSD_EINVAL, "rows: NULL pointer");
+    if (rows->k != h->sc.k) return fail(LAPSSD_EINVAL, "rows.k=%d != config k=%d", rows->k, h->sc.k);
+    if (!rows_ok(rows->dtype, rows->V, rows->k, rows->p, rows->q)) return fail(LAPSSD_EINVAL, "rows: dtype/V/alignment");
+    if (rows->V > (int64_t)1 << 23) return fail(LAPSSD_EINVAL, "V > 2^23 (integer softmax mass would overflow)");
+    if (rows->slab_tab && rows->R < 1) return fail(LAPSSD_EINVAL, "rows.R < 1");
+    if (!sel_inout || !workspace) return fail(LAPSSD_EINVAL, "NULL sel / workspace");
+    const int32_t k = rows->k;
+    if (workspace_bytes < laps_step_logits_workspace_bytes(B, k, rows->V, rows->dtype))
+        return fail(LAPSSD_ENOMEM, "workspace %zu < %zu bytes", workspace_bytes,
+                    laps_step_logits_workspace_bytes(B, k, rows->V, rows->dtype));
+    prepare_all();
+    cudaStream_t s = (cudaStream_t)stream;
+    h->last_stream = s;
+    h->side_chained = false;
+    h->wl.valid = 0;
+    h->desc_valid = false;
+    int32_t *tok = tokens_out ? tokens_out : h->tokens;
+    int32_t *na = n_accept_out ? n_accept_out : h->n_accept;
+    Carver cv{(char *)workspace};
+    const size_t nrow = (size_t)B * (size_t)(2 * k + 1);
+    float *m_ws = cv.take<float>(nrow);
+    uint64_t *S_ws = cv.take<uint64_t>(nrow);
+    char *lazy_ws = cv.take<char>(logits_lazy_bytes(B, k, rows->V, rows->dtype));
+    uint32_t *req = cv.take<uint32_t>((size_t)B);
+    uint32_t *rnd = cv.take<uint32_t>((size_t)B);
+    int32_t *slab = cv.take<int32_t>((size_t)B);
+    lapssd_status st = cuda_status(launch_logits_slots(sel_inout, h->st.rounds, rows->slab_tab, rows->R, h->sc.world,
+                                                       h->sc.rank, B, req, rnd, slab, s), "laps_step_logits slots");
+    if (st != LAPSSD_OK) return st;
+    st = cuda_status(launch_verify_logits(rows->p, rows->q, rows->dtype, rows->V, k, rows->draft, slab, req, rnd, B,
+                                          h->sc.seed, 0, tok, na, nullptr, m_ws, S_ws, lazy_ws, s),
+                     "laps_step_logits verify");
+    if (st != LAPSSD_OK) return st;
+    st = cuda_status(launch_logits_mask(sel_inout, k, B, tok, na, s), "laps_step_logits mask");
+    if (st != LAPSSD_OK) return st;
+    st = cuda_status(launch_update(h->st, h->sc, sel_inout, na, B, s), "laps_step_logits update");
+    if (st != LAPSSD_OK) return st;
+    const RowsDev none{};
+    return cuda_status(launch_select(h->st, h->sc, none, h->desc, B, sel_inout, count_out, s),
+                       "laps_step_logits select");
+}
+
 static lapssd_status fill_step_verify(lapssd_handle *h, const lapssd_rows *rows, int32_t B, int32_t *sel,
                                       int32_t *tokens_out, int32_t *n_accept_out, VerifyArgs &a) {
     if (!rows) return fail(LAPSSD_EINVAL, "rows is NULL");

@@ -577,6 +577,11 @@ cudaError_t launch_verify_logits(const void *zp, const void *zq, int32_t dtype, 
                                  int32_t *tokens, int32_t *n_accept, uint64_t *z, float *m_ws, uint64_t *S_ws,
                                  char *lazy_ws, cudaStream_t s);
 size_t logits_lazy_bytes(int32_t B, int32_t k, int64_t V, int32_t dtype);   // the lazy form's workspace
+cudaError_t launch_logits_slots(const int32_t *sel, const int32_t *rounds, const int32_t *slab_tab, int32_t R,
+                                int32_t world, int32_t rank, int32_t B, uint32_t *req, uint32_t *rnd, int32_t *slab,
+                                cudaStream_t s);
+cudaError_t launch_logits_mask(const int32_t *sel, int32_t k, int32_t B, int32_t *tokens, int32_t *n_accept,
+                               cudaStream_t s);
 void verify_logits_prepare();
 // f4 (draft_tree.cu)
 cudaError_t launch_draft_sample(const void *q, int32_t dtype, int64_t V, const int32_t *row_idx,

@@ -983,6 +983,49 @@ cudaError_t launch_verify_logits(const void *zp, const void *zq, int32_t dtype, 
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- laps_step_logits
+// The Philox counters and slabs of the handle's batch, on the device: slot b verifies
+// request i = sel[b] at its current round (req = global id i * world + rank, as laps_step),
+// with the round's slab from the slab table (or slab b: the batch layout).  Empty slots
+// (sel < 0) verify slab 0 as a dummy and are masked afterwards.
+__global__ void logits_slots_kernel(const int32_t *sel, const int32_t *rounds, const int32_t *slab_tab, int32_t R,
+                                    int32_t world, int32_t rank, int32_t B, uint32_t *req, uint32_t *rnd,
+                                    int32_t *slab) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const int32_t i = sel[b];
+    if (i < 0) {
+        req[b] = 0; rnd[b] = 0; slab[b] = 0;
+        return;
+    }
+    const int32_t t = rounds[i];
+    req[b] = (uint32_t)(i * world + rank);
+    rnd[b] = (uint32_t)t;
+    slab[b] = slab_tab ? slab_tab[(int64_t)i * R + slab_round_index(t, R)] : b;
+}
+
+__global__ void logits_mask_kernel(const int32_t *sel, int32_t k, int32_t B, int32_t *tokens, int32_t *n_accept) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B || sel[b] >= 0) return;
+    n_accept[b] = -1;
+    for (int j = 0; j <= k; ++j) tokens[(int64_t)b * (k + 1) + j] = -1;
+}
+
+cudaError_t launch_logits_slots(const int32_t *sel, const int32_t *rounds, const int32_t *slab_tab, int32_t R,
+                                int32_t world, int32_t rank, int32_t B, uint32_t *req, uint32_t *rnd, int32_t *slab,
+                                cudaStream_t s) {
+    logits_slots_kernel<<<(B + 255) / 256, 256, 0, s>>>(sel, rounds, slab_tab, R, world, rank, B, req, rnd, slab);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_logits_mask(const int32_t *sel, int32_t k, int32_t B, int32_t *tokens, int32_t *n_accept,
+                               cudaStream_t s) {
+    logits_mask_kernel<<<(B + 255) / 256, 256, 0, s>>>(sel, k, B, tokens, n_accept);
+    count_launch();
+    return cudaGetLastError();
+}
+
 void verify_logits_prepare() {
     cudaFuncSetAttribute(logits_sample_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     cudaFuncSetAttribute(logits_sample_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);

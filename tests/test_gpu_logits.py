@@ -315,3 +315,55 @@ def test_lazy_speculation_long_chains(L, B, dtype):
     tok_o, r_o, z_o = oracle.verify_logits_batch(P["p"], P["q"], P["draft"], slab, req, rnd, 41)
     assert (na == r_o).all() and (tok == tok_o).all() and (z.view(np.uint64) == z_o).all()
     assert na.max() >= 4
+
+
+def _slab_round_index(t, R):
+    h = R // 2
+    return t if t < R else (R - 1 if h == 0 else h + (t - h) % h)
+
+
+@pytest.mark.parametrize("policy,dtype", [(0, "bf16"), (3, "bf16"), (0, "f32")])
+def test_laps_step_logits_lockstep(L, policy, dtype):
+    """laps_step_logits (one C-ABI call: the handle's batch verified from logits with its
+    own request ids, rounds and slabs, then update and select) against the oracle
+    (verify_logits on the same slots -> Sim.update -> Sim.select) over whole traces."""
+    from test_gpu_step import BASE, compare_state
+    V, k, B, R = 4096, 4, 6, 8
+    tr = synth.make_trace(60, 0x10D1 + policy, arrival="poisson", rate_per_s=80.0, len_mu=np.log(24),
+                          len_sigma=0.6, len_min=2, len_max=96, drift=True)
+    pool = synth.make_logits_pool(V, k, dtype, n_buckets=8, variants=2, seed=0x10D1, device="cuda")
+    tab = synth.slab_table(tr, 8, 2, R=R, seed=0x10D1)
+    kw = dict(BASE, k=k, seed=37, policy=policy, switch_c0_us=1_000, switch_c1_us=10)
+    pr = synth.prompt_lengths(tr.n, 0x10D1)
+    h = L.Handle(L.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=V, prompt=pr)
+    sim = oracle.Sim(oracle.SchedConfig(**kw), tr.arrival_us, tr.L_true, tr.L_pred, prompt=pr)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device="cuda"))
+    zp, zq, dr = synth.to_numpy_rows(pool.p), synth.to_numpy_rows(pool.q), pool.draft.cpu().numpy()
+    ws = torch.empty(L.laps_step_logits_workspace_bytes(B, k, V, dtype), dtype=torch.uint8, device="cuda")
+    tok = torch.empty(B, k + 1, dtype=torch.int32, device="cuda")
+    na = torch.empty(B, dtype=torch.int32, device="cuda")
+    sel_o, _ = sim.select(B)
+    h.laps_select(B)
+    for step in range(4000):
+        sel_g = h.sel[:B].cpu().numpy()
+        assert (sel_g == sel_o).all(), f"step {step}: batch differs"
+        if sim.state()["done"].all():
+            break
+        rounds_o = sim.state()["rounds"]
+        live = sel_o >= 0
+        ids = np.maximum(sel_o, 0)
+        rnd = np.where(live, rounds_o[ids], 0).astype(np.int32)
+        slab = np.array([tab[i, _slab_round_index(int(rnd[b]), R)] if i >= 0 else 0 for b, i in enumerate(sel_o)],
+                        np.int32)
+        tok_o, r_o, _ = oracle.verify_logits_batch(zp, zq, dr, slab, ids.astype(np.int32), rnd, kw["seed"])
+        h.laps_step_logits(rows, B, tokens=tok, n_accept=na, workspace=ws)
+        na_g, tok_g = na.cpu().numpy(), tok.cpu().numpy()
+        assert (na_g[live] == r_o[live]).all() and (na_g[~live] == -1).all(), f"step {step}: r differs"
+        assert (tok_g[live] == tok_o[live]).all(), f"step {step}: tokens differ"
+        sim.update(sel_o, np.where(live, r_o, 0).astype(np.int32))
+        sel_o, _ = sim.select(B)
+        if step % 4 == 0:
+            compare_state(h.state(), sim.state(), step)
+    assert sim.state()["done"].all()
+    compare_state(h.state(), sim.state(), "end")
+    assert h.check() == 0
