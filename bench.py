@@ -73,7 +73,8 @@ def parse():
     ap.add_argument("--nccl-exchange", action="store_true",
                     help="N>1: laps_step_dist (candidates -> ncclAllGather -> merge kernel) instead of laps_step_peer")
     ap.add_argument("--traffic-file", default=os.path.join(ROOT, "profiles", "verify_dram.json"))
-    ap.add_argument("--workload", choices=["c4", "mc", "logits", "draft", "tree", "c2", "c3"], default="c4",
+    ap.add_argument("--workload", choices=["c4", "mc", "logits", "logits_step", "draft", "tree", "c2", "c3"],
+                    default="c4",
                     help="c4 = configs[3] (the headline); mc = configs[4] Monte-Carlo traces; "
                     "logits = SURVEY 8(f) f1, spec_verify_logits at configs[3] dimensions; "
                     "draft / tree = SURVEY 8(f) f4, spec_draft_sample / spec_verify_tree; "
@@ -883,6 +884,86 @@ def mc_cpu_baseline(args, w, pool, cfg):
             "host": host_info()}
 
 # --------------------------------------------------------------------------- reference arm
+def run_logits_step(args):
+    """f1 inside the LAPS-SD step: Handle.laps_step_logits on the configs[3] workload per GPU
+    (2,048 resident, B = 512, V = 128,256, k = 8), the rows a bf16 LOGITS slab pool with the
+    same bucket / variant structure as the headline's probability pool.  One GPU (the step's
+    select is local; N > 1 would need the global merge)."""
+    import paper_2505_17074_b200 as L
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    B, k, V = args.batch, args.k, args.V
+    tr = synth.make_trace(args.n_per_gpu, synth.CONFIGS["c4"]["seed"], arrival="zero", length="uniform",
+                          len_min=512, len_max=4096, beta_ab=(7, 3))
+    pool = synth.make_logits_pool(V, k, "bf16", n_buckets=args.buckets, variants=args.variants,
+                                  seed=synth.CONFIGS["c4"]["seed"], device=dev)
+    tab = synth.slab_table(tr, args.buckets, args.variants, R=64, seed=synth.CONFIGS["c4"]["seed"])
+    cfg = L.SchedConfig(**SCHED, seed=synth.CONFIGS["c4"]["seed"])
+    h = L.Handle(cfg, tr.arrival_us, tr.L_true, tr.L_pred, max_batch=B, V=V)
+    rows = L.Rows(pool.p, pool.q, pool.draft, torch.as_tensor(tab, device=dev))
+    ws = torch.empty(L.laps_step_logits_workspace_bytes(B, k, V, "bf16"), dtype=torch.uint8, device=dev)
+    G = max(1, min(args.graph_steps or 1, args.steps))
+    tok = torch.empty(G, B, k + 1, dtype=torch.int32, device=dev)
+    na = torch.empty(G, B, dtype=torch.int32, device=dev)
+    h.laps_select(B)
+    for t in range(max(args.warmup, 3)):
+        h.laps_step_logits(rows, B, tokens=tok[t % G], n_accept=na[t % G], workspace=ws)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    lc0 = L.launch_count()
+    with torch.cuda.graph(g):
+        for t in range(G):
+            h.laps_step_logits(rows, B, tokens=tok[t], n_accept=na[t], workspace=ws)
+    launches_per_step = (L.launch_count() - lc0) / G
+    reps = max(1, args.steps // G)
+    g.replay()
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    steps = reps * G
+    r = na.cpu().numpy()
+    verified = float((r >= 0).sum()) / G
+    value = verified * k * steps / (ms * 1e-3)
+    row = V * 2
+    rr = r[r >= 0]
+    alg = float(((2 * np.minimum(rr + 1, k) + (rr == k)) * row).sum()) / G
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs") or 6650.0
+    achieved = alg / (ms / steps * 1e-3) / 1e9
+    assert h.check() == 0
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": steps, "warmup": args.warmup,
+           "ms_per_step": ms / steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "bf16 logits; fixed-op fp32 exp, exact 2^40 integer softmax masses; fp64 scheduler",
+           "data": "synthetic",
+           "config": {"workload": "SURVEY 8(f) f1 inside the step: laps_step_logits on configs[3] per GPU "
+                      "(2,048 resident, batch 512, V=128,256, k=8, Beta(7,3) acceptance, L~U[512,4096], all "
+                      "arrive at t=0), bf16 logits slab pool", "N_resident_per_gpu": args.n_per_gpu,
+                      "B_per_gpu": B, "V": V, "k": k, "pool": f"{pool.S} slabs x {(2 * k + 1) * V * 2 / 1e6:.2f} MB",
+                      "l2": "inputs larger than L2 (4.5 GB pool)", "parallelism": "dp1"},
+           "verified_per_step": verified, "gpu_launches": int(round(launches_per_step * steps)), "clocks": clk,
+           "roofline": {"kernel": "whole step (slot counters, logits_lazy_kernel, mask, update, select)",
+                        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                        "algorithmic_bytes_per_step": alg, "traffic": None,
+                        "note": "bytes: the logit rows the acceptance tests consult, once each; the lazy verify "
+                                "is issue- and chain-bound (see --workload logits for its ALU roofline); the step "
+                                "adds the update and the select, not overlapped"}}
+    print(json.dumps(out), flush=True)
+
+
 def run_logits(args):
     """spec_verify_logits on B=512 slots per GPU per step at configs[3]
     dimensions (V=128,256, k=8, bf16 logits), each step a fresh random draw of slabs from
@@ -1406,6 +1487,8 @@ def main():
         run_reference(args)
     elif args.workload == "logits":
         run_logits(args)
+    elif args.workload == "logits_step":
+        run_logits_step(args)
     elif args.workload in ("draft", "tree"):
         run_f4(args)
     elif args.workload in ("c2", "c3"):

@@ -15,6 +15,7 @@ for i in 1 2 3; do
 done
 timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/final_bench_reference.log 2>&1; echo "rc=$?" >> gpurun_out/final_bench_reference.log
 timeout 300 python bench.py --workload logits > gpurun_out/final_line_logits.log 2>&1
+timeout 600 python bench.py --workload logits_step > gpurun_out/final_line_logits_step.log 2>&1
 timeout 900 python bench.py --workload mc > gpurun_out/final_line_mc.log 2>&1
 timeout 300 python bench.py --workload draft > gpurun_out/final_line_draft.log 2>&1
 timeout 300 python bench.py --workload tree > gpurun_out/final_line_tree.log 2>&1
