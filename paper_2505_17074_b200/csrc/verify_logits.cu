@@ -154,11 +154,11 @@ template <> struct VecMax<false> {
     __device__ float get() const { return m; }
 };
 
-// Block-wide max of the logits in vectors [lo, hi) of a row (every thread gets it).
-template <bool BF16>
-__device__ __forceinline__ float range_max(const uint4 *v4, int64_t lo, int64_t hi) {
+// Block-wide max of the logits in vectors [lo, hi) of a row (every thread gets it); U
+// independent 16-byte loads in flight per thread.
+template <bool BF16, int U>
+__device__ __forceinline__ float range_max_u(const uint4 *v4, int64_t lo, int64_t hi) {
     __shared__ float s_m[32];
-    constexpr int U = kNormIlp;
     const int64_t bd = blockDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     VecMax<BF16> acc;
@@ -181,14 +181,17 @@ __device__ __forceinline__ float range_max(const uint4 *v4, int64_t lo, int64_t 
     __syncthreads();   // s_m may be reused by the next call
     return m;
 }
+template <bool BF16>
+__device__ __forceinline__ float range_max(const uint4 *v4, int64_t lo, int64_t hi) {
+    return range_max_u<BF16, kNormIlp>(v4, lo, hi);
+}
 
 // Block-wide integer mass sum E[v] over vectors [lo, hi) for the row max m (thread 0
-// gets the total).  kNormIlp independent 16-byte loads in flight per thread.
-template <bool BF16>
-__device__ __forceinline__ uint64_t range_sum(const uint4 *v4, int64_t lo, int64_t hi, float m) {
+// gets the total).  U independent 16-byte loads in flight per thread.
+template <bool BF16, int U>
+__device__ __forceinline__ uint64_t range_sum_u(const uint4 *v4, int64_t lo, int64_t hi, float m) {
     using E = LElt<BF16>;
     __shared__ uint64_t s_S[32];
-    constexpr int U = kNormIlp;
     const int64_t bd = blockDim.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint64_t S = 0;
@@ -224,6 +227,10 @@ __device__ __forceinline__ uint64_t range_sum(const uint4 *v4, int64_t lo, int64
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_S[w];
     __syncthreads();
     return t;
+}
+template <bool BF16>
+__device__ __forceinline__ uint64_t range_sum(const uint4 *v4, int64_t lo, int64_t hi, float m) {
+    return range_sum_u<BF16, kNormIlp>(v4, lo, hi, m);
 }
 
 template <bool BF16>
@@ -630,7 +637,11 @@ struct LazyArgs {
 #ifndef LAPSSD_LAZY_SPEC    // speculative rows while CTAs wait: up to this many positions ahead (0: off)
 #define LAPSSD_LAZY_SPEC 2
 #endif
+#ifndef LAPSSD_LAZY_ILP     // loads in flight per thread in the lazy kernel's row passes
+#define LAPSSD_LAZY_ILP 2      // (measured: 1 / 2 / 3 / 4 / 6 / 8 -> 0.477 / 0.461 / 0.465 / 0.469 / 0.463 / 0.467 ms)
+#endif
 constexpr int kLazyThreads = LAPSSD_LAZY_THREADS;
+constexpr int kLazyIlp = LAPSSD_LAZY_ILP;
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
     uint32_t v;
@@ -795,8 +806,8 @@ __global__ void __launch_bounds__(kLazyThreads, LAPSSD_LAZY_MINB) logits_lazy_ke
                 }
             }
 #endif
-            const float m = range_max<BF16>(v4, 0, nv);
-            const uint64_t S = range_sum<BF16>(v4, 0, nv, m);
+            const float m = range_max_u<BF16, kLazyIlp>(v4, 0, nv);
+            const uint64_t S = range_sum_u<BF16, kLazyIlp>(v4, 0, nv, m);
             if (threadIdx.x == 0) {
                 filler_left = nf < first;
                 s_next = filler_left ? (nf >> 1) * rows + ((nf & 1) ? k + 1 : 0) : kNone;
