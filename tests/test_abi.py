@@ -123,3 +123,15 @@ def test_product_never_imports_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "lapssd_oracle" not in text, f
+
+
+def test_laps_step_logits_rejects_bad_arguments():
+    """f1 inside the step: a NULL handle, B < 1, NULL rows -- EINVAL before any launch; the
+    workspace covers spec_verify_logits' plus the slot counters, and rejects what it does."""
+    import paper_2505_17074_b200 as L
+    f = L._lib.laps_step_logits
+    assert f(None, None, 1, None, None, None, None, None, 0, None) == -1
+    assert L._lib.lapssd_last_error().decode()
+    ws = L._lib.laps_step_logits_workspace_bytes
+    assert ws(512, 8, 128256, 1) >= L._lib.spec_verify_logits_workspace_bytes(512, 8, 128256, 1) + 3 * 512 * 4
+    assert ws(1, 0, 1024, 1) == 0 and ws(1, 4, 1024, 7) == 0
